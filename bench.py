@@ -1,0 +1,437 @@
+"""bench.py — FAE hot path on B200: hot-batch lookups/s (fwd+bwd+update).
+
+One STEP = one pass of the whole hot path over one
+batch of synthetic input = this rank's dataset shard:
+  fae_profile (sample 5% + loggers) -> fae_threshold (Eq. 1 cutoff, hot set,
+  remap) -> fae_classify (hot/cold inputs, packed hot CSR) -> fae_extract
+  (replicated hot table) -> every hot mini-batch: fae_emb_fwd +
+  fae_emb_bwd_update (+ hot-grad sync over NCCL when N > 1).
+value = hot lookups trained by all ranks / max-over-ranks step time.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config kaggle]
+       python bench.py --impl reference ...   (CPU oracle arm)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import gen  # noqa: E402
+
+METRIC = "hot-batch lookups/sec (fwd+bwd+update) and % of HBM peak at 1/2/4/8 B200"
+UNIT = "lookups/s"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ----------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ----------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+# algorithmic bytes
+# ----------------------------------------------------------------------------
+def fwd_bytes(L, S, D, explicit_off):
+    return 4 * L + (8 * (S + 1) if explicit_off else 0) + 4 * D * L + 4 * D * S
+
+
+# ----------------------------------------------------------------------------
+# CUDA arm
+# ----------------------------------------------------------------------------
+def run_fae(args):
+    import paper_2103_00686_b200 as fae
+    from paper_2103_00686_b200.pipeline import FaePipeline
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = gen.CONFIGS[args.config]
+    R = args.records or cfg.records
+    Tn, D, B = cfg.n_tables, cfg.dim, cfg.batch
+    ds = gen.make_dataset(cfg, n_records=R, device=dev, record_base=rank * R)
+    pipe = FaePipeline(cfg.rows, D, B, cfg.pool, max_pool=max(cfg.pool_hi, 1), device=local,
+                       max_world=world)
+    if world > 1:
+        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(fae.fae_get_nccl_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        fae.fae_comm_init(pipe.ctx, bytes(idt.cpu().numpy().tobytes()), rank, world)
+    W = gen.make_weights(sum(cfg.rows), D, device=dev)
+    S_max = B * Tn
+    dy_bytes = S_max * D * 4
+    n_dy = max(1, math.ceil((256 << 20) / dy_bytes))      # > L2: honest dY reads
+    dY = gen.make_dy(n_dy * S_max, D, device=dev).view(n_dy, S_max, D)
+    Y = torch.empty(S_max, D, device=dev)
+    mode = fae.BUDGET_EXACT if cfg.budget_bytes else fae.FIXED_T
+    state = {}
+
+    def one_step(timing=None):
+        prep = pipe.preprocess(ds.idx, ds.off, R, x_pct=5.0, seed=args.seed, mode=mode,
+                               t=cfg.t, budget_bytes=cfg.budget_bytes,
+                               small_table_bytes=cfg.small_bytes, bufs=state.get("prep"))
+        state["prep"] = prep
+        W_hot = pipe.extract(W, prep)
+        nb = prep.packed["n_hot_batches"]
+        if dist is not None:
+            t = torch.tensor([nb], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            nb_all = int(t)
+        else:
+            nb_all = nb
+        for i in range(nb_all):
+            if i < nb:
+                idx, off, n_bags = pipe.batch_args(prep, i)
+            else:
+                idx, off, n_bags = prep.hot_idx[:0], None, 0
+            if timing is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+            fae.fae_emb_fwd(pipe.ctx, W_hot, idx, off, pipe.pool, n_bags, Y[:n_bags])
+            if timing is not None:
+                e1.record()
+                timing.append((e0, e1, idx.numel() if off is None else None, n_bags))
+            fae.fae_emb_bwd_update(pipe.ctx, W_hot, idx, off, pipe.pool, n_bags,
+                                   dY[i % n_dy, :n_bags], args.lr)
+        return prep.packed["n_hot_lookups"], prep
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    pipe.ctx.check()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    clocks.start()
+    l0 = pipe.ctx.launches
+    timing = []
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    wall0 = time.perf_counter()
+    t0.record()
+    hot_lookups = 0
+    prep = None
+    for _ in range(args.steps):
+        n, prep = one_step(timing)
+        hot_lookups += n
+    t1.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    ck = clocks.stop()
+    pipe.ctx.check()
+    ms = t0.elapsed_time(t1)
+    launches = pipe.ctx.launches - l0
+    fwd_ms = [a.elapsed_time(b) for a, b, _, _ in timing]
+    # per-launch algorithmic bytes of the fwd kernel
+    fb = []
+    for (a, b, L, S) in timing:
+        Lx = L if L is not None else 0
+        fb.append(fwd_bytes(Lx, S, D, cfg.pool == 0))
+    tot = torch.tensor([ms, float(hot_lookups)], dtype=torch.float64, device=dev)
+    if dist is not None:
+        mx = tot.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = tot.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms_max, lookups_all = float(mx[0]), float(sm[1])
+    else:
+        ms_max, lookups_all = ms, float(hot_lookups)
+    peak, kind = peaks()
+    res = None
+    if rank == 0:
+        avg_fwd_s = (sum(fwd_ms) / max(len(fwd_ms), 1)) / 1e3
+        avg_fwd_b = sum(fb) / max(len(fb), 1)
+        achieved = avg_fwd_b / avg_fwd_s / 1e9 if avg_fwd_s > 0 else 0.0
+        res = {
+            "metric": METRIC, "value": lookups_all / (ms_max / 1e3), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded Zipf s=1.1, Feistel-scattered rows; gen/)",
+            "config": {"workload": f"{cfg.name}-shaped", "records_per_gpu": R,
+                       "tables": Tn, "rows_total": sum(cfg.rows), "dim": D,
+                       "batch_per_gpu": B, "pooling": cfg.pool or f"U{{{cfg.pool_lo}..{cfg.pool_hi}}}",
+                       "threshold": ({"budget_bytes": cfg.budget_bytes} if cfg.budget_bytes else {"t": cfg.t}),
+                       "x_pct": 5.0, "lr": args.lr,
+                       "hot_rows": prep.thresh["H_total"], "hot_records": prep.packed["n_hot"],
+                       "hot_batches_per_step": prep.packed["n_hot_batches"],
+                       "l2": "inputs > L2 (dataset %.1f GB, dY pool %d MB)" % (
+                           ds.idx.numel() * 4 / 1e9, n_dy * dy_bytes >> 20),
+                       "parallelism": f"dp{world}"},
+            "gpu_launches": launches,
+            "roofline": {"kernel": "k_emb_fwd", "bound": "hbm", "achieved": achieved,
+                         "peak": peak, "peak_kind": kind, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "bytes_per_launch": avg_fwd_b, "avg_launch_us": avg_fwd_s * 1e6},
+            "clocks": ck,
+            "wall_s": wall,
+        }
+    return res, (pipe, ds, W, cfg, R, dist, rank, world, dev)
+
+
+def run_e2e(args, ctxs):
+    """Same metric through the public API with HOST inputs: the dataset is
+    copied from pinned host memory each step; the full tables stay in pinned
+    host memory (the CPU master copy) and fae_extract pulls only the
+    hot rows across PCIe; the trained hot table is read back each step."""
+    import paper_2103_00686_b200 as fae
+    pipe, ds, W, cfg, R, dist, rank, world, dev = ctxs
+    idx_h = ds.idx.cpu().pin_memory()
+    off_h = ds.off.cpu().pin_memory() if ds.off is not None else None
+    W_h = W.cpu().pin_memory()
+    D, B, Tn = cfg.dim, cfg.batch, cfg.n_tables
+    idx_d = torch.empty_like(ds.idx)
+    off_d = torch.empty_like(ds.off) if ds.off is not None else None
+    S_max = B * Tn
+    dY = gen.make_dy(S_max, D, device=dev)
+    Y = torch.empty(S_max, D, device=dev)
+    mode = fae.BUDGET_EXACT if cfg.budget_bytes else fae.FIXED_T
+    st = {}
+
+    def step():
+        idx_d.copy_(idx_h, non_blocking=True)
+        if off_h is not None:
+            off_d.copy_(off_h, non_blocking=True)
+        prep = pipe.preprocess(idx_d, off_d, R, x_pct=5.0, seed=args.seed, mode=mode, t=cfg.t,
+                               budget_bytes=cfg.budget_bytes, small_table_bytes=cfg.small_bytes,
+                               bufs=st.get("prep"))
+        st["prep"] = prep
+        W_hot = pipe.extract(W_h, prep)
+        nb = prep.packed["n_hot_batches"]
+        for i in range(nb):
+            idx, off, n_bags = pipe.batch_args(prep, i)
+            fae.fae_emb_fwd(pipe.ctx, W_hot, idx, off, pipe.pool, n_bags, Y[:n_bags])
+            fae.fae_emb_bwd_update(pipe.ctx, W_hot, idx, off, pipe.pool, n_bags, dY[:n_bags], args.lr)
+        out = W_hot.cpu()
+        h2d = idx_h.numel() * 4 + (off_h.numel() * 8 if off_h is not None else 0) + W_hot.numel() * 4
+        return prep.packed["n_hot_lookups"], h2d, out.numel() * 4
+
+    step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    n = h2d = d2h = 0
+    ksteps = max(1, min(args.steps, 2))
+    for _ in range(ksteps):
+        a, b, c = step()
+        n += a
+        h2d, d2h = b, c
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    tot = torch.tensor([dt, float(n)], dtype=torch.float64, device=dev)
+    if dist is not None:
+        mx = tot.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = tot.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        dt, n = float(mx[0]), float(sm[1])
+    return {"value": n / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "steps": ksteps}
+
+
+# ----------------------------------------------------------------------------
+# CPU oracle arm (cpu_baseline and --impl reference)
+# ----------------------------------------------------------------------------
+def oracle_step(cfg, R_s, max_batches, seed, lr, ds=None, W=None):
+    """The oracle, as it stands, over a bounded sample of the workload:
+    the full a1-a10 pipeline on the first R_s records, training at most
+    max_batches hot batches.  Returns (hot lookups trained, seconds)."""
+    import numpy as np
+    import oracle
+    t0 = time.perf_counter()
+    x = 5.0
+    samp = oracle.sample(R_s, x, seed)
+    counts, T, _ = oracle.histogram(ds.rows, ds.idx, ds.off, ds.fixed_pool, R_s, samp)
+    small = cfg.small_bytes
+    if cfg.budget_bytes:
+        r = oracle.budget_exact(ds.rows, cfg.dim, small, counts, T, x, cfg.budget_bytes)
+        kmin = r["kmin"]
+    else:
+        kmin = oracle.kmin_fixed_t(ds.rows, cfg.dim, small, T, cfg.t, x)
+    hot = oracle.tag_rows(ds.rows, cfg.dim, small, counts, kmin)
+    rm, base, H = oracle.remap(ds.rows, hot)
+    flag = oracle.classify(ds.rows, ds.idx, ds.off, ds.fixed_pool, R_s, rm)
+    pk = oracle.pack(ds.rows, ds.idx, ds.off, ds.fixed_pool, R_s, rm, flag)
+    W_hot = oracle.extract(W, rm, H)
+    B, Tn = cfg.batch, cfg.n_tables
+    nb = min(max_batches, -(-pk["n_hot"] // B))
+    slot = np.full(max(H, 1), -1, np.int32)
+    done = 0
+    for i in range(nb):
+        r0, r1 = i * B, min((i + 1) * B, pk["n_hot"])
+        n_bags = (r1 - r0) * Tn
+        if ds.off is None:
+            P = ds.fixed_pool
+            bi = pk["hot_idx"][r0 * Tn * P: r1 * Tn * P]
+            off = None
+        else:
+            P = 0
+            off = pk["hot_off"][r0 * Tn: r1 * Tn + 1]
+            bi = pk["hot_idx"]
+        dY = gen.make_dy(n_bags, cfg.dim, seed=1000 + i).numpy()
+        oracle.emb_fwd(W_hot, bi, off, P, n_bags)
+        W_hot, _ = oracle.emb_bwd_sgd(W_hot, bi, off, P, n_bags, dY, lr, slot)
+        done += (r1 - r0) * Tn * (P if P else 0) if off is None else int(off[-1] - off[0])
+    return done, time.perf_counter() - t0
+
+
+def oracle_sample_setup(cfg, R_s):
+    ds = gen.make_dataset(cfg, n_records=R_s)
+    W = gen.make_weights(sum(cfg.rows), cfg.dim).numpy()
+    return ds, W
+
+
+def cpu_baseline(cfg, args):
+    R_s = min(args.cpu_records, cfg.records)
+    ds, W = oracle_sample_setup(cfg, R_s)
+    n, dt = oracle_step(cfg, R_s, args.cpu_batches, args.seed, args.lr, ds, W)
+    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"full a1-a10 oracle pipeline on the first {R_s} records of the "
+                      f"{cfg.name}-shaped workload, <= {args.cpu_batches} hot batches trained "
+                      f"({n} hot lookups in {dt:.1f} s, single-threaded C, fp64)"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    cfg = gen.CONFIGS[args.config]
+    R_s = min(args.cpu_records, cfg.records)
+    ds, W = oracle_sample_setup(cfg, R_s)
+    for _ in range(args.warmup):
+        oracle_step(cfg, R_s, args.cpu_batches, args.seed, args.lr, ds, W)
+    n_tot, t_tot = 0, 0.0
+    for _ in range(args.steps):
+        n, dt = oracle_step(cfg, R_s, args.cpu_batches, args.seed, args.lr, ds, W)
+        n_tot += n
+        t_tot += dt
+    v = n_tot / t_tot
+    samp = (f"full a1-a10 oracle pipeline on the first {R_s} records, <= {args.cpu_batches} "
+            f"hot batches per step, single-threaded C fp64")
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_tot * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Zipf s=1.1; gen/)",
+            "config": {"workload": f"{cfg.name}-shaped", "records_per_step": R_s},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": samp},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="kaggle", choices=sorted(gen.CONFIGS))
+    ap.add_argument("--records", type=int, default=0, help="records per GPU (default: config)")
+    ap.add_argument("--impl", default="fae", choices=["fae", "reference"])
+    ap.add_argument("--lr", type=float, default=0.01)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--cpu-records", type=int, default=100_000)
+    ap.add_argument("--cpu-batches", type=int, default=16)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        r = run_reference(args)
+        if r is not None:
+            print(json.dumps(r), flush=True)
+        return
+    res, ctxs = run_fae(args)
+    if not args.no_e2e:
+        e2e = run_e2e(args, ctxs)
+        if res is not None:
+            res["e2e"] = e2e
+    rank = int(os.environ.get("RANK", "0"))
+    if rank == 0:
+        cfg = gen.CONFIGS[args.config]
+        if not args.no_cpu and res["n_gpus"] == 1:
+            res["cpu_baseline"] = cpu_baseline(cfg, args)
+        print(json.dumps(res), flush=True)
+    dist = ctxs[5]
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -191,13 +191,15 @@ class Dataset:
 
 def make_dataset(cfg: Config, n_records: Optional[int] = None,
                  seed: int = BASE_SEED, device="cpu",
-                 chunk: int = 1 << 26) -> Dataset:
+                 chunk: int = 1 << 26, record_base: int = 0) -> Dataset:
     """Synthetic Zipf-skewed categorical stream shaped like `cfg`.
 
     Table z draws from Zipf(cfg.zipf_s) with its own seed (seed + z), tables
     independent.  Fixed pooling: lookup q = (r*Tn + z)*P + p uses counter q.
     Variable pooling: bag b = r*Tn + z has P_b ~ U{pool_lo..pool_hi} drawn from
-    seed + 777; its lookups use counters off[b]..off[b+1)-1."""
+    seed + 777; its lookups use counters off[b]..off[b+1)-1.
+    record_base: global id of local record 0 (a rank's shard of a larger
+    dataset draws exactly the records the unsharded dataset would hold)."""
     R = cfg.records if n_records is None else n_records
     Tn = cfg.n_tables
     dev = torch.device(device)
@@ -208,7 +210,7 @@ def make_dataset(cfg: Config, n_records: Optional[int] = None,
         for z, n in enumerate(cfg.rows):
             for r0 in range(0, R, max(1, chunk // P)):
                 r1 = min(R, r0 + max(1, chunk // P))
-                rr = torch.arange(r0, r1, device=dev, dtype=torch.int64)
+                rr = torch.arange(r0, r1, device=dev, dtype=torch.int64) + record_base
                 ctr = ((rr * Tn + z) * P).unsqueeze(1) + \
                     torch.arange(P, device=dev, dtype=torch.int64)
                 view[r0:r1, z, :] = zipf_rows(n, cfg.zipf_s, seed + z,
@@ -217,17 +219,24 @@ def make_dataset(cfg: Config, n_records: Optional[int] = None,
     # variable pooling
     nb = R * Tn
     span = cfg.pool_hi - cfg.pool_lo + 1
-    b = torch.arange(nb, device=dev, dtype=torch.int64)
+    b = torch.arange(nb, device=dev, dtype=torch.int64) + record_base * Tn
     sizes = cfg.pool_lo + _srl(counter_hash(seed + 777, b), 11) % span
     off = torch.zeros(nb + 1, dtype=torch.int64, device=dev)
     torch.cumsum(sizes, 0, out=off[1:])
     L = int(off[-1])
+    # counters of a shard continue the global stream: offset by the lookups
+    # of the records before record_base (closed form unavailable -> prefix)
+    q_base = 0
+    if record_base:
+        bp = torch.arange(record_base * Tn, device=dev, dtype=torch.int64)
+        q_base = int((cfg.pool_lo + _srl(counter_hash(seed + 777, bp), 11) % span).sum())
     idx = torch.empty(L, dtype=torch.int32, device=dev)
     for q0 in range(0, L, chunk):
         q1 = min(L, q0 + chunk)
         q = torch.arange(q0, q1, device=dev, dtype=torch.int64)
         bag = torch.searchsorted(off, q, right=True) - 1
         z = bag % Tn
+        q = q + q_base
         out = torch.empty(q1 - q0, dtype=torch.int64, device=dev)
         for zz, n in enumerate(cfg.rows):
             m = z == zz

@@ -1,0 +1,309 @@
+/*
+ * fae.h — C ABI of the B200-native FAE hot path (libfae.so).
+ *
+ * FAE = "Frequently Accessed Embeddings", Adnan et al., "Accelerating
+ * Recommendation System Training by Leveraging Popular Choices",
+ * arXiv 2103.00686.  Citations "P:Lnnn" are PAPER.md line numbers with the
+ * section / equation they fall in; "Rnn" are the readings in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - Plain C, no exceptions across the ABI; every call returns fae_status.
+ *    Host-side argument validation happens before any launch; the message is
+ *    retrievable with fae_last_error().
+ *  - Pointers marked "device" are CUDA device pointers on the ctx's device
+ *    (torch tensors' data_ptr()); "host" pointers are ordinary host memory.
+ *    The caller owns every input and output buffer.  The ctx owns only its
+ *    scratch workspace and the current hot set (bitmap + rank directory).
+ *  - Work is enqueued on the ctx stream (fae_set_stream).  Calls that return
+ *    host values (fae_profile, fae_threshold, fae_classify, fae_check,
+ *    fae_sync_hot_grads' count) synchronise that stream; the step calls
+ *    fae_emb_fwd / fae_emb_bwd_update do not, allocate nothing, and are
+ *    CUDA-graph capturable (world == 1).
+ *  - Device-side errors (an index outside its table, a non-finite update)
+ *    are latched in the ctx and reported by the next synchronising call or
+ *    fae_check() as FAE_ERR_INDEX_RANGE / FAE_ERR_NONFINITE.
+ *  - One ctx per GPU / rank; a ctx is not thread-safe.
+ *
+ * Data layout:
+ *  - Tables z = 0..Tn-1 with N_z rows of D fp32 values, concatenated in table
+ *    order: global row g = rowbase_z + j, rowbase_z = sum_{z'<z} N_z'.
+ *  - Sparse inputs: sample-major CSR.  Record r, table z is bag b = r*Tn + z.
+ *    idx[] holds int32 LOCAL row ids (j in [0, N_z)).  Bag b's lookups are
+ *    idx[off[b] .. off[b+1]) when off != NULL (int64 absolute positions),
+ *    else idx[b*P .. (b+1)*P) with P = fixed_pool.
+ *  - Hot ids: the compact replicated hot table W_hot[H_total][D] holds the
+ *    hot rows in global-row order (R16): hot_id(g) = #{hot g' < g}.
+ */
+#ifndef FAE_H
+#define FAE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum fae_status {
+    FAE_OK = 0,
+    FAE_ERR_INVALID_ARG = 1,       /* bad argument (message in fae_last_error) */
+    FAE_ERR_CAPACITY = 2,          /* exceeds a capacity fixed at fae_create   */
+    FAE_ERR_BUDGET_INFEASIBLE = 3, /* small tables alone exceed the budget     */
+    FAE_ERR_INDEX_RANGE = 4,       /* an index outside its table (latched)     */
+    FAE_ERR_NONFINITE = 5,         /* non-finite gradient/update (latched)     */
+    FAE_ERR_CUDA = 6,              /* CUDA runtime error                        */
+    FAE_ERR_NCCL = 7,              /* NCCL error / async error                  */
+    FAE_ERR_NOT_INIT = 8           /* NULL ctx, or comm needed but not inited  */
+} fae_status;
+
+typedef struct fae_ctx fae_ctx;
+
+/* Capacities, fixed at create time: all workspace is allocated by fae_create
+ * (profile/classify scratch grows on demand inside those one-off calls). */
+typedef struct fae_config {
+    int32_t device;             /* CUDA device ordinal                          */
+    int32_t max_tables;         /* Tn capacity (<= 4096)                        */
+    int64_t max_rows;           /* sum_z N_z capacity (hot-set bitmap)          */
+    int64_t max_batch_lookups;  /* L capacity of one step (< 2^30)              */
+    int64_t max_batch_bags;     /* S capacity of one step                       */
+    int32_t max_dim;            /* D capacity                                   */
+    int32_t max_world;          /* ranks capacity for fae_sync_hot_grads        */
+} fae_config;
+
+/* Table schema (host). */
+typedef struct fae_tables {
+    int32_t n_tables;
+    const int64_t* rows;        /* host [n_tables]: N_z                         */
+    int32_t dim;                /* D (fp32 elements per row)                    */
+} fae_tables;
+
+/* Sparse-input CSR (D1).  For a record shard on rank g of a
+ * sharded dataset, record_base is the global id of local record 0 and
+ * n_records_global the total over ranks (sampling keys use global ids, so a
+ * sharded profile equals the unsharded one).  Single GPU: 0 and n_records. */
+typedef struct fae_csr {
+    const int32_t* idx;         /* device [n_lookups] local row ids             */
+    const int64_t* off;         /* device [n_records*n_tables+1] or NULL        */
+    int32_t fixed_pool;         /* lookups per bag when off == NULL (>= 0)      */
+    int64_t n_records;          /* records in this shard                        */
+    int64_t n_lookups;          /* off[n_records*n_tables] or n_records*Tn*P    */
+    int64_t record_base;        /* global id of local record 0                  */
+    int64_t n_records_global;   /* records over all ranks                       */
+} fae_csr;
+
+/* --------------------------------------------------------------------------
+ * Lifecycle
+ * ------------------------------------------------------------------------ */
+fae_status fae_create(const fae_config* cfg, fae_ctx** out);
+void fae_destroy(fae_ctx* ctx);
+/* stream: a cudaStream_t passed as void* (NULL = legacy default stream). */
+fae_status fae_set_stream(fae_ctx* ctx, void* stream);
+const char* fae_last_error(const fae_ctx* ctx);
+/* Synchronise the ctx stream and report (and clear) latched device errors. */
+fae_status fae_check(fae_ctx* ctx);
+/* NCCL bootstrap: rank 0 calls fae_get_nccl_id, the caller broadcasts the
+ * 128 bytes (torch.distributed), every rank calls fae_comm_init.  world == 1
+ * needs no comm. */
+fae_status fae_get_nccl_id(void* id128);
+fae_status fae_comm_init(fae_ctx* ctx, const void* id128, int32_t rank,
+                         int32_t world);
+/* Number of kernels this ctx has launched so far (bench evidence). */
+int64_t fae_kernel_launches(const fae_ctx* ctx);
+
+/* --------------------------------------------------------------------------
+ * fae_profile — input sampler + embedding logger (a1 + a2).
+ *  P:L358-363 (§4.1.1): sample x% of the dataset D -> D-hat; uniform without
+ *    replacement (R6): the k = floor(R*x/100) records with the smallest
+ *    (key(seed, i), i), key(seed, i) = splitmix64(seed + (i+1)*0x9E3779B97F4A7C15),
+ *    i = global record id; original order kept.
+ *  P:L380-388 (§4.1.2 "Embedding Logger"): k_z[j] = number of sampled lookups
+ *    equal to row j of table z (duplicates count each time).
+ *  T_z = lookups into table z over ALL records (R3).
+ * Arguments:
+ *  counts       device uint32 [sum N_z], overwritten (concatenated loggers).
+ *  T_host       host int64 [n_tables], out.
+ *  sampled_ids  device int64 [>= k] local record ids of the sample, ascending
+ *               (optional, NULL to skip).
+ *  n_sampled    host out: k (this shard's share when sharded).
+ * With a comm (world > 1) every rank passes its record shard; the selection
+ * is global, counts and T are summed over ranks (exact, ncclAllReduce).
+ * Errors: INVALID_ARG if x not in (0, 100] or schema mismatch; INDEX_RANGE
+ * (latched) if a sampled index >= N_z; CAPACITY if n_tables > max_tables or
+ * sum N_z > max_rows.
+ * ------------------------------------------------------------------------ */
+fae_status fae_profile(fae_ctx* ctx, const fae_tables* tabs,
+                       const fae_csr* data, double x_pct, uint64_t seed,
+                       uint32_t* counts, int64_t* T_host,
+                       int64_t* sampled_ids, int64_t* n_sampled);
+
+/* --------------------------------------------------------------------------
+ * fae_threshold — threshold knob, embedding classifier and hot-row remap
+ * (a3 + a4).
+ *  Small-table rule: N_z*D*4 < small_table_bytes => all hot.
+ *  FIXED_T (Eq. 1): H_z = ((t*T_z)*x)/100 in IEEE double (R21);
+ *    large row hot iff k >= H_z (Eq. 2's >=, R1), i.e. k >= kmin_z =
+ *    max(1, ceil(H_z)) (R25).
+ *  BUDGET_EXACT ("top h entries that fit L", in Eq. 1 form, R10):
+ *    with T_ref = max_large T_z and integer K >= 1, kmin_z = max(1,
+ *    ceil(K*T_z/T_ref)); bytes(K) = sum_small N_z*D*4 + sum_large D*4*
+ *    #{j: k_z[j] >= kmin_z}; the smallest K with bytes(K) <= budget.
+ *    t_final = K / (T_ref*x/100).  budget_slack = 1 when K = 1 fits.
+ *  ESTIMATE (want_estimate, Eqs. 2-4) at the final cutoff, per
+ *    large table: n chunks of m rows with the smallest (key(chunk_seed ^ z,
+ *    c), c), C_i (Eq. 2), ybar (Eq. 3), s (n-1 denominator, R8), CI with the
+ *    finite-population factor (Eq. 4) and caller-supplied t_quantile (R9);
+ *    est rows = ybar*N_z/m, bounds clamped to [0, N_z]; tables with fewer
+ *    than n full chunks are scanned exactly (est_exact = 1).
+ *  Remap (R16): hot_id(g) = #{hot g' < g}; base_z = hot_id of
+ *    table z's first row; H_total = number of hot rows.
+ * The resulting hot set is kept in the ctx (1 bit/row + rank directory,
+ * 2 bits/row in HBM) and used by fae_classify / fae_extract.
+ * Arguments:
+ *  counts     device uint32 [sum N_z] from fae_profile.
+ *  T_host     host int64 [n_tables].
+ *  remap_out  device int32 [sum N_z], optional: hot id or -1 per row.
+ *  res        host struct with caller-owned host arrays (NULL to skip each).
+ * Errors: INVALID_ARG (t not in (0,1], bad mode, x not in (0,100], n < 2 or
+ * m < 1); BUDGET_INFEASIBLE; CAPACITY.
+ * ------------------------------------------------------------------------ */
+typedef enum fae_thresh_mode {
+    FAE_THRESH_FIXED_T = 0,
+    FAE_THRESH_BUDGET_EXACT = 1
+} fae_thresh_mode;
+
+typedef struct fae_thresh_req {
+    int32_t mode;               /* fae_thresh_mode                            */
+    double t;                   /* FIXED_T threshold, fraction in (0, 1] (R2) */
+    int64_t budget_bytes;       /* BUDGET_EXACT: L                           */
+    int64_t small_table_bytes;  /* default 1 << 20 (R11)                     */
+    int32_t want_estimate;      /* compute Eqs. 2-4 at the final cutoff      */
+    int32_t n_chunks;           /* n (35)                             */
+    int32_t chunk_rows;         /* m (1024)                           */
+    double t_quantile;          /* t_{alpha/2}, n-1 dof: 3.6007 @ 99.9% (R9) */
+    uint64_t chunk_seed;
+} fae_thresh_req;
+
+typedef struct fae_thresh_result {
+    /* per-table host arrays [n_tables] (each may be NULL) */
+    int64_t* kmin;              /* cutoff used (0 for small tables)          */
+    int64_t* hot_rows;          /* exact hot rows per table                  */
+    int64_t* base;              /* [n_tables + 1] hot-id base per table      */
+    int32_t* is_small;
+    double* est_mean;           /* ybar                                      */
+    double* est_sd;             /* s                                         */
+    double* est_lo;             /* CI lower bound, rows                      */
+    double* est_hi;             /* CI upper bound, rows                      */
+    double* est_rows;           /* point estimate, rows                      */
+    int32_t* est_exact;         /* 1 if full-scan fallback                   */
+    /* scalars (out) */
+    int64_t H_total;
+    int64_t hot_bytes;          /* H_total * D * 4                           */
+    double t_final;
+    uint64_t K;                 /* BUDGET_EXACT integer cutoff (0 otherwise) */
+    int32_t budget_slack;
+} fae_thresh_result;
+
+fae_status fae_threshold(fae_ctx* ctx, const fae_tables* tabs,
+                         const uint32_t* counts, const int64_t* T_host,
+                         double x_pct, const fae_thresh_req* req,
+                         int32_t* remap_out, fae_thresh_result* res);
+
+/* --------------------------------------------------------------------------
+ * fae_classify — input classifier + mini-batch bundling (a5 + a6).
+ *  P:L476-479 (§4.2): a sparse input is hot iff ALL its lookups hit hot rows
+ *    (empty bags are vacuously hot, R19).
+ *  bundle hot and cold inputs into all-hot / all-cold
+ *    mini-batches.  hot_ids / cold_ids are ascending local record ids (R17);
+ *    hot batch i = hot_ids[i*B, min((i+1)*B, n_hot)), trailing partial batch
+ *    kept (R18).  The remapped hot CSR lists, for each hot record in order,
+ *    for z = 0..Tn-1, the bag's hot ids in bag order; with explicit offsets
+ *    hot_off[n_hot*Tn + 1] holds its absolute bag offsets (fixed pooling:
+ *    implicit, hot_off unused).
+ * Uses the hot set of the last fae_threshold on this ctx.
+ * Arguments (fae_packed, device buffers caller-sized):
+ *  hot_ids, cold_ids  int64 [>= n_records] each.
+ *  hot_idx            int32 [>= n_lookups].
+ *  hot_off            int64 [>= n_records*Tn + 1] (offsets input only).
+ *  batch              B >= 1 (INVALID_ARG otherwise; B larger than a kind's
+ *                     count gives one partial batch, not an error).
+ *  shuffle_seed       must be 0 (stable order); other values INVALID_ARG.
+ * Outputs (host fields): n_hot, n_cold, n_hot_lookups, n_hot_batches,
+ * n_cold_batches.  Errors: NOT_INIT if no hot set; INDEX_RANGE (latched).
+ * ------------------------------------------------------------------------ */
+typedef struct fae_packed {
+    int64_t* hot_ids;
+    int64_t* cold_ids;
+    int32_t* hot_idx;
+    int64_t* hot_off;
+    int64_t n_hot;
+    int64_t n_cold;
+    int64_t n_hot_lookups;
+    int64_t n_hot_batches;
+    int64_t n_cold_batches;
+} fae_packed;
+
+fae_status fae_classify(fae_ctx* ctx, const fae_tables* tabs,
+                        const fae_csr* data, int32_t batch,
+                        uint64_t shuffle_seed, fae_packed* out);
+
+/* --------------------------------------------------------------------------
+ * fae_extract — embedding replicator (a7: "extracts hot
+ * embedding entries and creates embedding bags replicated across GPUs"):
+ *   W_hot[hot_id(g), :] = W[g, :] for every hot global row g (bit copy).
+ *  W      [sum N_z][dim] fp32: device memory, or pinned host memory mapped
+ *         into the device address space (only hot rows cross the link).
+ *  W_hot  device [H_total][dim].
+ * ------------------------------------------------------------------------ */
+fae_status fae_extract(fae_ctx* ctx, const float* W, int32_t dim,
+                       float* W_hot);
+
+/* --------------------------------------------------------------------------
+ * fae_emb_fwd — hot embedding-bag forward (a8; sum
+ * pooling, R12):
+ *   Y[b, :] = sum_{p in bag b} W_hot[idx[p], :]           (fp32)
+ *  W_hot  device [H][D];  idx device int32 hot ids in [0, H).
+ *  off    device int64 [n_bags+1] absolute positions into idx, or NULL for
+ *         fixed pooling (bag b = idx[b*P .. (b+1)*P)).
+ *  Y      device [n_bags][D] (sample-major [B][Tn][D]).
+ * D % 4 == 0, D <= max_dim, and D/4 a power of two or a multiple of 32.
+ * Empty bag -> zero row.  Asynchronous; graph-capturable.
+ * ------------------------------------------------------------------------ */
+fae_status fae_emb_fwd(fae_ctx* ctx, const float* W_hot, int64_t H, int32_t D,
+                       const int32_t* idx, const int64_t* off,
+                       int32_t fixed_pool, int64_t n_bags, float* Y);
+
+/* --------------------------------------------------------------------------
+ * fae_emb_bwd_update — hot embedding backward + SGD (a9 + a10 [+ a11]):
+ *   G[r, :] = sum_{p : idx[p] = r} dY[bag(p), :]   (sort-and-segment)
+ *   W_hot[r, :] -= lr * G[r, :]  for every touched r; untouched rows are not
+ *   written (bit-identical).  P:L230, L803 ("massively-parallel SGD"), plain
+ *   SGD (R13), sum semantics (R14: the caller pre-scales dY for a mean).
+ * With a comm of world > 1 the sparse G is summed over ranks first (a11,
+ * P:L298-301), deterministically, so every replica applies identical bits.
+ * Same argument conventions as fae_emb_fwd; dY device [n_bags][D].
+ * n_lookups must fit max_batch_lookups.  Asynchronous; graph-capturable
+ * when world == 1.
+ * ------------------------------------------------------------------------ */
+fae_status fae_emb_bwd_update(fae_ctx* ctx, float* W_hot, int64_t H,
+                              int32_t D, const int32_t* idx,
+                              const int64_t* off, int32_t fixed_pool,
+                              int64_t n_bags, const float* dY, float lr);
+
+/* --------------------------------------------------------------------------
+ * fae_sync_hot_grads — hot-gradient synchronisation across GPUs (a11,
+ * "hot embeddings are synchronized using the AllReduce
+ * collectives over the fast NVlink"; P:L217-220 aggregated gradients).
+ * In:  rows device int32 [cap] sorted ascending, unique; vals device fp32
+ *      [cap][D]; *count_host = local U.
+ * Out: rows/vals = the global sparse sum over ranks (sorted by row, summed
+ *      in rank order: identical bits on every rank); *count_host = global U.
+ * Errors: NOT_INIT without comm (world 1 is the identity); CAPACITY if the
+ * global U or world*max(U) exceeds cap or the ctx capacity; NCCL.
+ * ------------------------------------------------------------------------ */
+fae_status fae_sync_hot_grads(fae_ctx* ctx, int32_t* rows, float* vals,
+                              int64_t* count_host, int64_t cap, int32_t D);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FAE_H */

@@ -1,0 +1,370 @@
+// classify.cu — input classifier, mini-batch bundling and replicator extract
+// (SURVEY §8(a) a5, a6, a7).
+//
+//  a5  P:L476-479 (§4.2): an input is hot iff all its lookups hit hot rows.
+//  a6  P:L493-496: bundle hot / cold inputs into all-hot / all-cold batches;
+//      emit the hot CSR in hot ids so hot batches run entirely on the GPU.
+//  a7  P:L317, L502: extract the hot rows into the replicated hot table.
+//
+// B200 design: ONE pass over the sparse inputs.  Each CTA owns a tile of
+// records; for every lookup it does one 128-bit rank-directory load (bit +
+// hot id together, L2-resident), keeps the hot ids in shared memory, decides
+// the records' class with a block vote, gets its output offsets from a
+// decoupled look-back scan, and writes hot_ids / cold_ids / the hot CSR with
+// coalesced stores.  The dataset (Kaggle-shaped: 4.7 GB) is read exactly once.
+#include <algorithm>
+
+#include "fae_internal.cuh"
+
+namespace fae {
+
+fae_status validate_schema(Ctx* c, const fae_tables* t, const char* who);
+fae_status validate_csr(Ctx* c, const fae_tables* t, const fae_csr* d, const char* who);
+
+constexpr int kClsThreads = 256;
+constexpr int kClsItems = 8192;      // lookups per tile kept in smem (fixed pooling)
+constexpr int kRecBits = 28;         // look-back packing: records | lookups << 28
+constexpr uint64_t kRecMask = (1ull << kRecBits) - 1;
+
+// Fixed pooling, Tn*P <= kClsItems.  TR records per tile.
+__global__ void __launch_bounds__(kClsThreads)
+k_classify_fixed(const int32_t* __restrict__ idx, int64_t n_rec, int Tn, int P, int TR,
+                 const int64_t* __restrict__ rowbase, const uint4* __restrict__ dir,
+                 int64_t* __restrict__ hot_ids, int64_t* __restrict__ cold_ids,
+                 int32_t* __restrict__ hot_idx, uint64_t* __restrict__ status,
+                 uint32_t* __restrict__ ctr, int64_t* __restrict__ result, uint32_t* err,
+                 const int64_t* __restrict__ rows) {
+    extern __shared__ int64_t s_dyn[];
+    int64_t* s_rb = s_dyn;                               // [Tn+1]
+    int64_t* s_rows = s_dyn + (Tn + 1);                  // [Tn]
+    int32_t* s_hid = (int32_t*)(s_dyn + 2 * Tn + 1);     // [kClsItems]
+    __shared__ int s_cold[kClsThreads];
+    __shared__ int s_list[kClsThreads];
+    __shared__ int s_wsum[kClsThreads / 32];
+    __shared__ int s_tile;
+    __shared__ uint64_t s_ex;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int z = tid; z <= Tn; z += blockDim.x) s_rb[z] = rowbase[z];
+    for (int z = tid; z < Tn; z += blockDim.x) s_rows[z] = rows[z];
+    if (tid < TR) s_cold[tid] = 0;
+    if (tid == 0) s_tile = (int)atomicAdd(ctr, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t r0 = tile * TR;
+    if (r0 >= n_rec && tile != 0) return;
+    const int nrec = (int)std::min<int64_t>(TR, std::max<int64_t>(0, n_rec - r0));
+    const int TnP = Tn * P;
+    const int nitems = nrec * TnP;
+    const int32_t* src = idx + r0 * (int64_t)TnP;
+    for (int q = tid; q < nitems; q += kClsThreads) {
+        const int rl = q / TnP;
+        const int qq = q - rl * TnP;
+        const int z = qq / P;
+        const int32_t j = __ldg(src + q);
+        int32_t hid = -1;
+        if (j < 0 || (int64_t)j >= s_rows[z]) {
+            atomicOr(err, kErrIndex);
+            s_cold[rl] = 1;
+        } else {
+            const int64_t g = s_rb[z] + j;
+            uint32_t rk;
+            if (hs_test(__ldg(dir + (g >> 6)), g, &rk)) hid = (int32_t)rk;
+            else s_cold[rl] = 1;
+        }
+        s_hid[q] = hid;
+    }
+    __syncthreads();
+    const bool hot = tid < nrec && !s_cold[tid];
+    const uint32_t bal = __ballot_sync(0xffffffffu, hot);
+    if (lane == 0) s_wsum[warp] = __popc(bal);
+    __syncthreads();
+    int wp = 0, tot = 0;
+    for (int w = 0; w < kClsThreads / 32; w++) {
+        if (w < warp) wp += s_wsum[w];
+        tot += s_wsum[w];
+    }
+    const int rank = wp + __popc(bal & lanemask_lt());
+    if (tid == 0) {
+        s_ex = lookback_u64(status, tile, (uint64_t)tot);
+        const int64_t last = n_rec > 0 ? (n_rec - 1) / TR : 0;
+        if (tile == last) {
+            result[0] = (int64_t)(s_ex + tot);
+        }
+    }
+    __syncthreads();
+    const int64_t ex = (int64_t)s_ex;
+    if (tid < nrec) {
+        if (hot) {
+            hot_ids[ex + rank] = r0 + tid;
+            s_list[rank] = tid;
+        } else {
+            cold_ids[(r0 - ex) + (tid - rank)] = r0 + tid;
+        }
+    }
+    __syncthreads();
+    int32_t* dst = hot_idx + ex * (int64_t)TnP;
+    const int nout = tot * TnP;
+    for (int jx = tid; jx < nout; jx += kClsThreads) {
+        const int k = jx / TnP;
+        const int qq = jx - k * TnP;
+        dst[jx] = s_hid[s_list[k] * TnP + qq];
+    }
+}
+
+// General (offsets or large Tn*P): warp per record, hot ids recomputed in the
+// write phase (L1/L2 hits).  Look-back value = records | lookups << 28.
+constexpr int kGenRec = 64;   // records per tile
+__global__ void __launch_bounds__(kClsThreads)
+k_classify_general(const int32_t* __restrict__ idx, const int64_t* __restrict__ off, int P,
+                   int64_t n_rec, int Tn, const int64_t* __restrict__ rowbase,
+                   const int64_t* __restrict__ rows, const uint4* __restrict__ dir,
+                   int64_t* __restrict__ hot_ids, int64_t* __restrict__ cold_ids,
+                   int32_t* __restrict__ hot_idx, int64_t* __restrict__ hot_off,
+                   uint64_t* __restrict__ status, uint32_t* __restrict__ ctr,
+                   int64_t* __restrict__ result, uint32_t* err) {
+    extern __shared__ int64_t s_dyn[];
+    int64_t* s_rb = s_dyn;
+    int64_t* s_rows = s_dyn + (Tn + 1);
+    __shared__ int s_hot[kGenRec];
+    __shared__ int64_t s_len[kGenRec];
+    __shared__ int s_rank[kGenRec];
+    __shared__ int64_t s_lpre[kGenRec];
+    __shared__ int s_tile;
+    __shared__ uint64_t s_ex;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = kClsThreads / 32;
+    for (int z = tid; z <= Tn; z += blockDim.x) s_rb[z] = rowbase[z];
+    for (int z = tid; z < Tn; z += blockDim.x) s_rows[z] = rows[z];
+    if (tid == 0) s_tile = (int)atomicAdd(ctr, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t r0 = tile * kGenRec;
+    if (r0 >= n_rec && tile != 0) return;
+    const int nrec = (int)std::min<int64_t>(kGenRec, std::max<int64_t>(0, n_rec - r0));
+    auto bag_lo = [&](int64_t b) -> int64_t { return off ? off[b] : b * (int64_t)P; };
+    for (int rl = warp; rl < nrec; rl += NW) {
+        const int64_t r = r0 + rl;
+        bool cold = false;
+        for (int z = 0; z < Tn; z++) {
+            const int64_t lo = bag_lo(r * Tn + z), hi = bag_lo(r * Tn + z + 1);
+            for (int64_t p = lo + lane; p < hi; p += 32) {
+                const int32_t j = __ldg(idx + p);
+                if (j < 0 || (int64_t)j >= s_rows[z]) {
+                    atomicOr(err, kErrIndex);
+                    cold = true;
+                } else {
+                    const int64_t g = s_rb[z] + j;
+                    uint32_t rk;
+                    if (!hs_test(__ldg(dir + (g >> 6)), g, &rk)) cold = true;
+                }
+            }
+        }
+        cold = __any_sync(0xffffffffu, cold);
+        if (lane == 0) {
+            s_hot[rl] = !cold;
+            s_len[rl] = bag_lo((r + 1) * Tn) - bag_lo(r * Tn);
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+        // scan over the tile's records of (hot, hot lookups), 2 records per lane
+        uint64_t v0 = 0, v1 = 0;
+        const int a = 2 * lane, b = 2 * lane + 1;
+        if (a < nrec && s_hot[a]) v0 = 1ull | ((uint64_t)s_len[a] << kRecBits);
+        if (b < nrec && s_hot[b]) v1 = 1ull | ((uint64_t)s_len[b] << kRecBits);
+        const uint64_t pair = v0 + v1;
+        uint64_t x = pair;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        const uint64_t tot = __shfl_sync(0xffffffffu, x, 31);
+        if (lane == 0) {
+            s_ex = lookback_u64(status, tile, tot);
+            const int64_t last = n_rec > 0 ? (n_rec - 1) / kGenRec : 0;
+            if (tile == last) {
+                const uint64_t inc = s_ex + tot;
+                result[0] = (int64_t)(inc & kRecMask);
+                result[1] = (int64_t)(inc >> kRecBits);
+                if (off && hot_off) hot_off[(inc & kRecMask) * Tn] = (int64_t)(inc >> kRecBits);
+            }
+        }
+        const uint64_t ex0 = x - pair;
+        if (a < nrec) {
+            s_rank[a] = (int)(ex0 & kRecMask);
+            s_lpre[a] = (int64_t)(ex0 >> kRecBits);
+        }
+        if (b < nrec) {
+            const uint64_t ex1 = ex0 + v0;
+            s_rank[b] = (int)(ex1 & kRecMask);
+            s_lpre[b] = (int64_t)(ex1 >> kRecBits);
+        }
+    }
+    __syncthreads();
+    const int64_t ex_rec = (int64_t)(s_ex & kRecMask);
+    const int64_t ex_lk = (int64_t)(s_ex >> kRecBits);
+    for (int rl = warp; rl < nrec; rl += NW) {
+        const int64_t r = r0 + rl;
+        if (!s_hot[rl]) {
+            if (lane == 0) cold_ids[(r0 - ex_rec) + (rl - s_rank[rl])] = r;
+            continue;
+        }
+        const int64_t h = ex_rec + s_rank[rl];
+        if (lane == 0) hot_ids[h] = r;
+        int64_t out = ex_lk + s_lpre[rl];
+        const int64_t rbase = bag_lo(r * Tn);
+        for (int z = 0; z < Tn; z++) {
+            const int64_t lo = bag_lo(r * Tn + z), hi = bag_lo(r * Tn + z + 1);
+            if (off && hot_off && lane == 0) hot_off[h * Tn + z] = out + (lo - rbase);
+            for (int64_t p = lo + lane; p < hi; p += 32) {
+                const int64_t g = s_rb[z] + __ldg(idx + p);
+                uint32_t rk;
+                hs_test(__ldg(dir + (g >> 6)), g, &rk);
+                hot_idx[out + (p - rbase)] = (int32_t)rk;
+            }
+        }
+    }
+}
+
+// extract: warp per 64-row word; lane l owns bits l (lo) and l (hi)
+template <int NV4>
+__global__ void __launch_bounds__(256)
+k_extract(const uint4* __restrict__ dir, int64_t total, const float* __restrict__ W, int D,
+          float* __restrict__ W_hot) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wpb = blockDim.x >> 5;
+    const int64_t words = (total + 63) >> 6;
+    for (int64_t w = blockIdx.x * wpb + (threadIdx.x >> 5); w < words; w += (int64_t)gridDim.x * wpb) {
+        const uint4 e = dir[w];
+        const uint32_t lo = e.x, hi = e.y;
+        const uint32_t lt = lanemask_lt();
+        const int nd4 = D / 4;
+        if ((lo >> lane) & 1u) {
+            const int64_t g = w * 64 + lane;
+            const int64_t hid = (int64_t)e.z + __popc(lo & lt);
+            const float4* s = reinterpret_cast<const float4*>(W + g * D);
+            float4* d = reinterpret_cast<float4*>(W_hot + hid * D);
+            for (int k = 0; k < nd4; k++) d[k] = s[k];
+        }
+        if ((hi >> lane) & 1u) {
+            const int64_t g = w * 64 + 32 + lane;
+            const int64_t hid = (int64_t)e.z + __popc(lo) + __popc(hi & lt);
+            const float4* s = reinterpret_cast<const float4*>(W + g * D);
+            float4* d = reinterpret_cast<float4*>(W_hot + hid * D);
+            for (int k = 0; k < nd4; k++) d[k] = s[k];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_extract_scalar(const uint4* __restrict__ dir, int64_t total, const float* __restrict__ W, int D,
+                 float* __restrict__ W_hot) {
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t rk;
+        if (hs_test(dir[g >> 6], g, &rk))
+            for (int d = 0; d < D; d++) W_hot[(int64_t)rk * D + d] = W[g * D + d];
+    }
+}
+
+static int sms(Ctx* c) {
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, c->device);
+    return n;
+}
+
+}  // namespace fae
+
+using namespace fae;
+
+extern "C" fae_status fae_classify(fae_ctx* h, const fae_tables* tabs, const fae_csr* data, int32_t batch,
+                                   uint64_t shuffle_seed, fae_packed* out) {
+    if (!h) return FAE_ERR_NOT_INIT;
+    Ctx* c = &h->c;
+    fae_status st = validate_schema(c, tabs, "fae_classify");
+    if (st != FAE_OK) return st;
+    st = validate_csr(c, tabs, data, "fae_classify");
+    if (st != FAE_OK) return st;
+    if (!out || !out->hot_ids || !out->cold_ids || (!out->hot_idx && data->n_lookups > 0))
+        return set_err(c, FAE_ERR_INVALID_ARG, "fae_classify: null output buffer");
+    if (data->off && !out->hot_off) return set_err(c, FAE_ERR_INVALID_ARG, "fae_classify: hot_off required with offsets");
+    if (batch < 1) return set_err(c, FAE_ERR_INVALID_ARG, "fae_classify: batch must be >= 1");
+    if (shuffle_seed != 0) return set_err(c, FAE_ERR_INVALID_ARG, "fae_classify: only the stable order (shuffle_seed 0) is implemented");
+    HotSet& hs = c->hs;
+    if (!hs.valid) return set_err(c, FAE_ERR_NOT_INIT, "fae_classify: no hot set (call fae_threshold first)");
+    const int Tn = tabs->n_tables;
+    if (Tn != hs.n_tables) return set_err(c, FAE_ERR_INVALID_ARG, "fae_classify: schema differs from the hot set's");
+    for (int z = 0; z < Tn; z++)
+        if (tabs->rows[z] != hs.rows[z]) return set_err(c, FAE_ERR_INVALID_ARG, "fae_classify: schema differs from the hot set's");
+    const int64_t n = data->n_records;
+    if (n >= (int64_t)kRecMask || data->n_lookups >= (1ll << 34))
+        return set_err(c, FAE_ERR_CAPACITY, "fae_classify: > 2^28 records or > 2^34 lookups per shard");
+    FAE_CUDA(c, cudaMemcpyAsync(c->d_rows_tmp, tabs->rows, sizeof(int64_t) * Tn, cudaMemcpyHostToDevice, c->stream));
+    const int P = data->fixed_pool;
+    const bool fast = !data->off && (int64_t)Tn * P <= kClsItems && Tn * P > 0;
+    const int TR = fast ? std::min(kClsThreads, std::max(1, kClsItems / (Tn * P))) : kGenRec;
+    const int64_t tiles = std::max<int64_t>(1, cdiv(n, TR));
+    size_t o = 0;
+    auto take = [&](size_t b) { size_t r = o; o = (o + b + 255) / 256 * 256; return r; };
+    const size_t o_st = take(sizeof(uint64_t) * tiles);
+    const size_t o_ctr = take(sizeof(uint32_t) * 4);
+    const size_t o_res = take(sizeof(int64_t) * 4);
+    char* sc = (char*)scratch(c, o);
+    if (!sc) return set_err(c, FAE_ERR_CUDA, "fae_classify: scratch allocation failed");
+    uint64_t* d_st = (uint64_t*)(sc + o_st);
+    uint32_t* d_ctr = (uint32_t*)(sc + o_ctr);
+    int64_t* d_res = (int64_t*)(sc + o_res);
+    FAE_CUDA(c, cudaMemsetAsync(sc, 0, o, c->stream));
+    const size_t rb_smem = sizeof(int64_t) * (2 * Tn + 1);
+    if (fast) {
+        const size_t smem = rb_smem + sizeof(int32_t) * kClsItems;
+        if (smem > 48 * 1024)
+            FAE_CUDA(c, cudaFuncSetAttribute(k_classify_fixed, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_classify_fixed<<<(unsigned)tiles, kClsThreads, smem, c->stream>>>(
+            data->idx, n, Tn, P, TR, hs.d_rowbase, hs.dir, out->hot_ids, out->cold_ids, out->hot_idx, d_st, d_ctr,
+            d_res, c->d_err, c->d_rows_tmp);
+        FAE_LAUNCHED(c);
+    } else {
+        if (rb_smem > 48 * 1024)
+            FAE_CUDA(c, cudaFuncSetAttribute(k_classify_general, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rb_smem));
+        k_classify_general<<<(unsigned)tiles, kClsThreads, rb_smem, c->stream>>>(
+            data->idx, data->off, P, n, Tn, hs.d_rowbase, c->d_rows_tmp, hs.dir, out->hot_ids, out->cold_ids,
+            out->hot_idx, data->off ? out->hot_off : nullptr, d_st, d_ctr, d_res, c->d_err);
+        FAE_LAUNCHED(c);
+    }
+    int64_t res[2] = {0, 0};
+    FAE_CUDA(c, cudaMemcpyAsync(res, d_res, sizeof(int64_t) * 2, cudaMemcpyDeviceToHost, c->stream));
+    st = read_latched(c);
+    const int64_t nh = res[0];
+    out->n_hot = nh;
+    out->n_cold = n - nh;
+    out->n_hot_lookups = fast ? nh * (int64_t)Tn * P : res[1];
+    out->n_hot_batches = cdiv(nh, batch);
+    out->n_cold_batches = cdiv(n - nh, batch);
+    if (n == 0 && data->off && out->hot_off) {
+        int64_t zero = 0;
+        FAE_CUDA(c, cudaMemcpy(out->hot_off, &zero, sizeof(int64_t), cudaMemcpyHostToDevice));
+    }
+    return st;
+}
+
+extern "C" fae_status fae_extract(fae_ctx* h, const float* W, int32_t dim, float* W_hot) {
+    if (!h) return FAE_ERR_NOT_INIT;
+    Ctx* c = &h->c;
+    HotSet& hs = c->hs;
+    if (!hs.valid) return set_err(c, FAE_ERR_NOT_INIT, "fae_extract: no hot set");
+    if (!W || (!W_hot && hs.H_total > 0) || dim < 1) return set_err(c, FAE_ERR_INVALID_ARG, "fae_extract: bad arguments");
+    if (hs.H_total == 0) return FAE_OK;
+    const int64_t total = hs.total_rows;
+    const bool vec = dim % 4 == 0 && (((uintptr_t)W | (uintptr_t)W_hot) & 15) == 0;
+    if (vec) {
+        const int64_t words = cdiv(total, 64);
+        const int64_t g = std::max<int64_t>(1, std::min<int64_t>(cdiv(words, 8), (int64_t)sms(c) * 16));
+        k_extract<1><<<(unsigned)g, 256, 0, c->stream>>>(hs.dir, total, W, dim, W_hot);
+    } else {
+        const int64_t g = std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), (int64_t)sms(c) * 8));
+        k_extract_scalar<<<(unsigned)g, 256, 0, c->stream>>>(hs.dir, total, W, dim, W_hot);
+    }
+    FAE_LAUNCHED(c);
+    return FAE_OK;
+}

@@ -1,0 +1,222 @@
+// fae_internal.cuh — private declarations of libfae (B200 / sm_100a).
+// Nothing here is shared with oracle/ (the oracle is an independent C file).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/fae.h"
+
+namespace fae {
+
+constexpr int kMaxTables = 4096;
+constexpr int kSortBits = 8;           // radix digit width
+constexpr int kSortBins = 1 << kSortBits;
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 4;          // keys per thread per tile
+constexpr int kSortTile = kSortThreads * kSortItems;
+constexpr int kMaxSortPasses = 4;      // 32-bit keys
+constexpr int kPiece = 16;             // max lookups per reduction piece
+
+// error latch bits (device word)
+constexpr uint32_t kErrIndex = 1u;
+constexpr uint32_t kErrNonfinite = 2u;
+constexpr uint32_t kErrOverflow = 4u;
+
+// Look-back status words: 2 flag bits on top of the value.
+constexpr uint64_t kFlagAgg = 1ull << 62;
+constexpr uint64_t kFlagPre = 2ull << 62;
+constexpr uint64_t kValMask = (1ull << 62) - 1;
+
+// Step workspace: everything fae_emb_bwd_update needs, allocated at create.
+struct StepWs {
+    int64_t cap_L = 0;                  // lookups capacity
+    uint32_t* keys[2] = {nullptr, nullptr};
+    int32_t* vals[2] = {nullptr, nullptr};
+    // zeroed region (one memset per call): digit histograms, tile counters,
+    // look-back status words, scalars.
+    void* zero_base = nullptr;
+    size_t zero_bytes = 0;
+    uint32_t* ghist = nullptr;          // [kMaxSortPasses][256]
+    uint32_t* tile_ctr = nullptr;       // [8]
+    uint32_t* sort_status = nullptr;    // [kMaxSortPasses][tiles][256]
+    uint64_t* piece_status = nullptr;   // [tiles]
+    int64_t* scalars = nullptr;         // [0]=n_valid [1]=n_pieces [2]=n_segs
+    // not zeroed per call
+    int32_t* piece_start = nullptr;     // [cap_P + 1]
+    int32_t* piece_seg = nullptr;       // [cap_P]
+    int32_t* seg_first = nullptr;       // [cap_L + 1]
+    int32_t* seg_row = nullptr;         // [cap_L]
+    uint32_t* seg_cnt = nullptr;        // [cap_L], kept zero by the finisher
+    float* partial = nullptr;           // [cap_P][max_dim]
+    float* grad = nullptr;              // [cap_L][max_dim] emitted sparse G
+    int64_t cap_P = 0;
+    int64_t n_sort_tiles = 0;
+    int64_t n_piece_tiles = 0;
+};
+
+// Hot set produced by fae_threshold: 16-byte entries per 64 rows
+// {bits lo, bits hi, exclusive hot-rank prefix, unused}.
+struct HotSet {
+    bool valid = false;
+    int32_t n_tables = 0;
+    int32_t dim = 0;
+    int64_t total_rows = 0;
+    int64_t H_total = 0;
+    std::vector<int64_t> rows, rowbase, base;   // host copies
+    uint4* dir = nullptr;                       // device [ceil(total/64)]
+    int64_t dir_cap = 0;
+    int64_t* d_rowbase = nullptr;               // device [n_tables + 1]
+};
+
+struct Ctx {
+    fae_config cfg{};
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    uint32_t* d_err = nullptr;                  // latched device error bits
+    int64_t launches = 0;
+    StepWs ws;
+    HotSet hs;
+    // grow-on-demand scratch for the one-off calls
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    int64_t* d_rowbase_tmp = nullptr;           // [max_tables+1]
+    int64_t* d_rows_tmp = nullptr;              // [max_tables]
+    // NCCL
+    ncclComm_t comm = nullptr;
+    int rank = 0, world = 1;
+    // sync scratch
+    int32_t* g_rows = nullptr;                  // [max_world * cap_L]
+    float* g_vals = nullptr;                    // [max_world * cap_L * max_dim]
+    int32_t* g_counts = nullptr;                // [max_world]
+    int64_t g_cap = 0;
+};
+
+// ---------------------------------------------------------------------------
+// host helpers
+// ---------------------------------------------------------------------------
+fae_status set_err(Ctx* c, fae_status st, const std::string& msg);
+fae_status cuda_err(Ctx* c, cudaError_t e, const char* where);
+void* scratch(Ctx* c, size_t bytes);   // ctx-owned, grows; nullptr on failure
+fae_status read_latched(Ctx* c);       // sync + read/clear device error word
+
+#define FAE_CUDA(c, expr)                                                   \
+    do {                                                                    \
+        cudaError_t e_ = (expr);                                            \
+        if (e_ != cudaSuccess) return ::fae::cuda_err((c), e_, #expr);      \
+    } while (0)
+
+#define FAE_LAUNCHED(c)                                                     \
+    do {                                                                    \
+        (c)->launches++;                                                    \
+        cudaError_t e_ = cudaGetLastError();                                \
+        if (e_ != cudaSuccess) return ::fae::cuda_err((c), e_, "launch");   \
+    } while (0)
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// step internals (step.cu), used by sync
+fae_status bwd_group_and_reduce(Ctx* c, float* W_hot, int64_t H, int32_t D,
+                                const uint32_t* keys_in_or_null,
+                                const int32_t* idx, const int64_t* off,
+                                int32_t fixed_pool, int64_t n_bags,
+                                int64_t n_hint, const float* src, float lr,
+                                bool emit);
+fae_status sync_merge_apply(Ctx* c, const int32_t* rows, const float* vals, int64_t U, int32_t D,
+                            float* W, int64_t H, float lr, int32_t* out_rows, float* out_vals,
+                            int64_t* out_count, int64_t out_cap);
+fae_status step_ws_alloc(Ctx* c);
+void step_ws_free(Ctx* c);
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+}
+
+__device__ __forceinline__ uint64_t hash_key(uint64_t seed, uint64_t i) {
+    return mix64(seed + (i + 1) * 0x9E3779B97F4A7C15ull);
+}
+
+__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Decoupled look-back (single thread): publish this tile's aggregate, walk
+// back to the nearest inclusive prefix, publish the inclusive prefix, return
+// the exclusive prefix.  Values are < 2^62 and may be packed sums of
+// non-overflowing fields.
+__device__ __forceinline__ uint64_t lookback_u64(uint64_t* status, int64_t tile,
+                                                 uint64_t agg) {
+    if (tile == 0) {
+        st_relaxed_u64(&status[0], kFlagPre | agg);
+        return 0;
+    }
+    st_relaxed_u64(&status[tile], kFlagAgg | agg);
+    uint64_t excl = 0;
+    int64_t t = tile - 1;
+    while (true) {
+        uint64_t s;
+        do {
+            s = ld_relaxed_u64(&status[t]);
+        } while ((s >> 62) == 0);
+        excl += s & kValMask;
+        if ((s >> 62) == 2) break;
+        --t;
+    }
+    st_relaxed_u64(&status[tile], kFlagPre | (excl + agg));
+    return excl;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Hot-set rank query: e = dir[g >> 6]; bit and rank of global row g.
+__device__ __forceinline__ bool hs_test(const uint4& e, int64_t g, uint32_t* rank) {
+    const uint32_t b = (uint32_t)(g & 63);
+    const uint32_t lo = e.x, hi = e.y;
+    bool bit;
+    uint32_t below;
+    if (b < 32) {
+        bit = (lo >> b) & 1u;
+        below = __popc(lo & ((1u << b) - 1u));
+    } else {
+        bit = (hi >> (b - 32)) & 1u;
+        below = __popc(lo) + __popc(hi & ((1u << (b - 32)) - 1u));
+    }
+    *rank = e.z + below;
+    return bit;
+}
+
+}  // namespace fae
+
+struct fae_ctx {
+    fae::Ctx c;
+};

@@ -1,0 +1,772 @@
+// step.cu — the hot mini-batch embedding step.
+//
+//  a8  fae_emb_fwd         Y[b] = sum_{p in bag b} W_hot[idx[p]]
+//  a9  fae_emb_bwd_update  G[r] = sum_{p: idx[p]=r} dY[bag(p)]      (sort-and-segment)
+//  a10                     W_hot[r] -= lr * G[r]
+//  a11 fae_sync_hot_grads  G_global = sum over ranks
+//
+// Kernels (no tensor cores: gather/scatter, HBM/L2 bound):
+//  k_emb_fwd      sub-warp group of D/4 lanes per bag, 128-bit row loads,
+//                 4 independent rows in flight per lane, streaming Y stores.
+//  k_bwd_prep     (hot id, bag) pairs + all radix-digit histograms, one pass.
+//  k_sort_pass    onesweep LSD radix pass: warp match_any ranking, per-digit
+//                 decoupled look-back, stable scatter; ceil(log2(H+1)/8) passes.
+//  k_pieces       run-length segments of equal hot id split into <= kPiece
+//                 pieces (decoupled look-back over (pieces, segments)).
+//  k_seg_reduce   one D/4-lane group per piece sums its dY rows; single-piece
+//                 segments apply SGD directly, multi-piece segments combine
+//                 their partials in piece order (last-arriver), so the sum
+//                 order is fixed: results are deterministic run to run and
+//                 identical on every rank.
+#include <algorithm>
+
+#include "fae_internal.cuh"
+
+namespace fae {
+
+// ---------------------------------------------------------------------------
+// a8 forward
+// ---------------------------------------------------------------------------
+template <int LPB, int NV>
+__global__ void __launch_bounds__(256)
+k_emb_fwd(const float* __restrict__ W, int64_t H, int D,
+          const int32_t* __restrict__ idx, const int64_t* __restrict__ off,
+          int P, int64_t n_bags, float* __restrict__ Y, uint32_t* err) {
+    const int lane = threadIdx.x % LPB;
+    const int64_t gpb = blockDim.x / LPB;
+    const int64_t stride = (int64_t)gridDim.x * gpb;
+    for (int64_t b = blockIdx.x * gpb + threadIdx.x / LPB; b < n_bags; b += stride) {
+        int64_t lo, hi;
+        if (off) {
+            lo = off[b];
+            hi = off[b + 1];
+        } else {
+            lo = b * P;
+            hi = lo + P;
+        }
+        float4 acc[NV];
+#pragma unroll
+        for (int k = 0; k < NV; k++) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        int64_t p = lo;
+        for (; p + 4 <= hi; p += 4) {
+            int32_t r[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                r[u] = __ldg(idx + p + u);
+                if ((uint32_t)r[u] >= (uint64_t)H) {
+                    atomicOr(err, kErrIndex);
+                    r[u] = -1;
+                }
+            }
+            float4 v[4][NV];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const float4* row = reinterpret_cast<const float4*>(W + (int64_t)(r[u] < 0 ? 0 : r[u]) * D) + lane;
+#pragma unroll
+                for (int k = 0; k < NV; k++) {
+                    v[u][k] = r[u] < 0 ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldg(row + k * LPB);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NV; k++) {
+                acc[k].x += (v[0][k].x + v[1][k].x) + (v[2][k].x + v[3][k].x);
+                acc[k].y += (v[0][k].y + v[1][k].y) + (v[2][k].y + v[3][k].y);
+                acc[k].z += (v[0][k].z + v[1][k].z) + (v[2][k].z + v[3][k].z);
+                acc[k].w += (v[0][k].w + v[1][k].w) + (v[2][k].w + v[3][k].w);
+            }
+        }
+        for (; p < hi; ++p) {
+            int32_t r = __ldg(idx + p);
+            if ((uint32_t)r >= (uint64_t)H) {
+                atomicOr(err, kErrIndex);
+                continue;
+            }
+            const float4* row = reinterpret_cast<const float4*>(W + (int64_t)r * D) + lane;
+#pragma unroll
+            for (int k = 0; k < NV; k++) {
+                float4 v = __ldg(row + k * LPB);
+                acc[k].x += v.x;
+                acc[k].y += v.y;
+                acc[k].z += v.z;
+                acc[k].w += v.w;
+            }
+        }
+        float4* y = reinterpret_cast<float4*>(Y + b * D) + lane;
+#pragma unroll
+        for (int k = 0; k < NV; k++) __stcs(y + k * LPB, acc[k]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// a9 backward: pairs + digit histograms
+// scalars: [0] n_valid, [1] n_pieces, [2] n_segs, [3] n_items
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int32_t find_bag(const int64_t* __restrict__ off, int64_t n_bags, int64_t pos) {
+    // largest b in [0, n_bags) with off[b] <= pos
+    int64_t lo = 0, hi = n_bags - 1;
+    while (lo < hi) {
+        int64_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(off + mid) <= pos) lo = mid;
+        else hi = mid - 1;
+    }
+    return (int32_t)lo;
+}
+
+__global__ void __launch_bounds__(256)
+k_bwd_prep(const int32_t* __restrict__ idx, const int64_t* __restrict__ off, int P,
+           int64_t n_bags, int64_t H, int passes, uint32_t* __restrict__ keys,
+           int32_t* __restrict__ vals, uint32_t* __restrict__ ghist,
+           int64_t* __restrict__ scalars, uint32_t* err) {
+    __shared__ uint32_t sh[kMaxSortPasses][kSortBins];
+    for (int i = threadIdx.x; i < kMaxSortPasses * kSortBins; i += blockDim.x) (&sh[0][0])[i] = 0;
+    __syncthreads();
+    const int64_t base = off ? off[0] : 0;
+    const int64_t n = off ? off[n_bags] - base : n_bags * (int64_t)P;
+    if (blockIdx.x == 0 && threadIdx.x == 0) scalars[3] = n;
+    int nvalid = 0;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t r = __ldg(idx + base + p);
+        const int32_t bag = off ? find_bag(off, n_bags, base + p) : (int32_t)(p / P);
+        uint32_t key;
+        if ((uint32_t)r >= (uint64_t)H) {
+            atomicOr(err, kErrIndex);
+            key = (uint32_t)H;
+        } else {
+            key = (uint32_t)r;
+            nvalid++;
+        }
+        keys[p] = key;
+        vals[p] = bag;
+        for (int ps = 0; ps < passes; ps++) atomicAdd(&sh[ps][(key >> (kSortBits * ps)) & (kSortBins - 1)], 1u);
+    }
+    // warp reduce nvalid
+    for (int o = 16; o; o >>= 1) nvalid += __shfl_xor_sync(0xffffffffu, nvalid, o);
+    if ((threadIdx.x & 31) == 0 && nvalid) atomicAdd((unsigned long long*)&scalars[0], (unsigned long long)nvalid);
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * kSortBins; i += blockDim.x) {
+        uint32_t v = (&sh[0][0])[i];
+        if (v) atomicAdd(&ghist[i], v);
+    }
+}
+
+// Merge prep for a11: gathered per-rank lists (padded to cap per rank).
+__global__ void __launch_bounds__(256)
+k_merge_prep(const int32_t* __restrict__ g_rows, const int32_t* __restrict__ g_counts,
+             int world, int64_t cap, int64_t H, int passes, uint32_t* __restrict__ keys,
+             int32_t* __restrict__ vals, uint32_t* __restrict__ ghist,
+             int64_t* __restrict__ scalars) {
+    __shared__ uint32_t sh[kMaxSortPasses][kSortBins];
+    for (int i = threadIdx.x; i < kMaxSortPasses * kSortBins; i += blockDim.x) (&sh[0][0])[i] = 0;
+    __syncthreads();
+    const int64_t n = (int64_t)world * cap;
+    if (blockIdx.x == 0 && threadIdx.x == 0) scalars[3] = n;
+    int nvalid = 0;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int rk = (int)(p / cap);
+        const int64_t j = p - (int64_t)rk * cap;
+        uint32_t key = (uint32_t)H;
+        if (j < g_counts[rk]) {
+            const int32_t r = g_rows[p];
+            if ((uint32_t)r < (uint64_t)H) {
+                key = (uint32_t)r;
+                nvalid++;
+            }
+        }
+        keys[p] = key;
+        vals[p] = (int32_t)p;
+        for (int ps = 0; ps < passes; ps++) atomicAdd(&sh[ps][(key >> (kSortBits * ps)) & (kSortBins - 1)], 1u);
+    }
+    for (int o = 16; o; o >>= 1) nvalid += __shfl_xor_sync(0xffffffffu, nvalid, o);
+    if ((threadIdx.x & 31) == 0 && nvalid) atomicAdd((unsigned long long*)&scalars[0], (unsigned long long)nvalid);
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * kSortBins; i += blockDim.x) {
+        uint32_t v = (&sh[0][0])[i];
+        if (v) atomicAdd(&ghist[i], v);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// onesweep LSD radix pass (stable)
+// status word: bits 31..30 flag (1 aggregate, 2 inclusive), bits 29..0 count
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSortThreads)
+k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
+            uint32_t* __restrict__ kout, int32_t* __restrict__ vout,
+            const int64_t* __restrict__ scalars, int shift,
+            const uint32_t* __restrict__ ghist, uint32_t* __restrict__ status,
+            uint32_t* __restrict__ tile_ctr) {
+    constexpr int NW = kSortThreads / 32;
+    __shared__ uint32_t s_w[NW][kSortBins];
+    __shared__ uint32_t s_goff[kSortBins];
+    __shared__ uint32_t s_wsum[NW];
+    __shared__ int s_tile;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_tile = (int)atomicAdd(tile_ctr, 1u);
+    for (int i = tid; i < NW * kSortBins; i += kSortThreads) (&s_w[0][0])[i] = 0;
+    const int64_t n = scalars[3];
+    __syncthreads();
+    const int tile = s_tile;
+    const int64_t tbase = (int64_t)tile * kSortTile;
+    if (tbase >= n) return;
+    // global digit starts: exclusive scan of ghist over 256 digits
+    {
+        uint32_t v = ghist[tid];
+        uint32_t x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_wsum[warp] = x;
+        __syncthreads();
+        uint32_t wp = 0;
+        for (int w = 0; w < warp; w++) wp += s_wsum[w];
+        s_goff[tid] = wp + x - v;
+    }
+    const int64_t wbase = tbase + (int64_t)warp * 32 * kSortItems;
+    uint32_t k[kSortItems];
+    int32_t v[kSortItems];
+    uint32_t rk[kSortItems];
+#pragma unroll
+    for (int j = 0; j < kSortItems; j++) {
+        const int64_t i = wbase + j * 32 + lane;
+        const bool ok = i < n;
+        k[j] = ok ? kin[i] : 0u;
+        v[j] = ok ? vin[i] : 0;
+        const uint32_t d = ok ? ((k[j] >> shift) & (kSortBins - 1)) : kSortBins;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t lt = __popc(peers & lanemask_lt());
+        uint32_t cnt = 0;
+        if (ok) cnt = s_w[warp][d];
+        __syncwarp();
+        if (ok && lt == 0) s_w[warp][d] = cnt + __popc(peers);
+        __syncwarp();
+        rk[j] = cnt + lt;
+    }
+    __syncthreads();
+    {
+        const int d = tid;  // kSortThreads == kSortBins
+        uint32_t tot = 0;
+#pragma unroll
+        for (int w = 0; w < NW; w++) {
+            const uint32_t c = s_w[w][d];
+            s_w[w][d] = tot;
+            tot += c;
+        }
+        uint32_t excl = 0;
+        uint32_t* st = status + (int64_t)tile * kSortBins + d;
+        if (tile == 0) {
+            st_relaxed_u32(st, (2u << 30) | tot);
+        } else {
+            st_relaxed_u32(st, (1u << 30) | tot);
+            int t = tile - 1;
+            while (true) {
+                uint32_t s;
+                do {
+                    s = ld_relaxed_u32(status + (int64_t)t * kSortBins + d);
+                } while ((s >> 30) == 0);
+                excl += s & 0x3FFFFFFFu;
+                if ((s >> 30) == 2) break;
+                --t;
+            }
+            st_relaxed_u32(st, (2u << 30) | (excl + tot));
+        }
+        s_goff[d] += excl;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kSortItems; j++) {
+        const int64_t i = wbase + j * 32 + lane;
+        if (i < n) {
+            const uint32_t d = (k[j] >> shift) & (kSortBins - 1);
+            const uint32_t pos = s_goff[d] + s_w[warp][d] + rk[j];
+            kout[pos] = k[j];
+            vout[pos] = v[j];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// pieces: segment heads and piece starts over the sorted keys
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kSortThreads)
+k_pieces(const uint32_t* __restrict__ keys, int64_t* __restrict__ scalars,
+         uint64_t* __restrict__ status, uint32_t* __restrict__ tile_ctr,
+         int32_t* __restrict__ piece_start, int32_t* __restrict__ piece_seg,
+         int32_t* __restrict__ seg_first, int32_t* __restrict__ seg_row) {
+    constexpr int NW = kSortThreads / 32;
+    __shared__ uint64_t s_wsum[NW];
+    __shared__ uint64_t s_texcl;
+    __shared__ int s_tile;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_tile = (int)atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const int tile = s_tile;
+    const int64_t nv = scalars[0];
+    const int64_t tbase = (int64_t)tile * kSortTile;
+    if (tbase >= nv && !(tile == 0 && nv == 0)) return;
+    const int64_t i0 = tbase + (int64_t)tid * kSortItems;
+    uint32_t kk[kSortItems + 1];
+    kk[0] = (i0 > 0 && i0 - 1 < nv) ? keys[i0 - 1] : 0xFFFFFFFFu;
+#pragma unroll
+    for (int j = 0; j < kSortItems; j++) kk[j + 1] = (i0 + j < nv) ? keys[i0 + j] : 0xFFFFFFFFu;
+    uint32_t np = 0, ns = 0;
+#pragma unroll
+    for (int j = 0; j < kSortItems; j++) {
+        const int64_t i = i0 + j;
+        if (i < nv) {
+            const bool head = (i == 0) || (kk[j + 1] != kk[j]);
+            const bool ps = head || (i % kPiece == 0);
+            ns += head;
+            np += ps;
+        }
+    }
+    const uint64_t mine = ((uint64_t)np << 31) | ns;
+    uint64_t x = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+        uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wsum[warp] = x;
+    __syncthreads();
+    uint64_t wp = 0, tot = 0;
+    for (int w = 0; w < NW; w++) {
+        if (w < warp) wp += s_wsum[w];
+        tot += s_wsum[w];
+    }
+    if (tid == 0) {
+        const uint64_t ex = lookback_u64(status, tile, tot);
+        s_texcl = ex;
+        const int64_t last_tile = nv > 0 ? (nv - 1) / kSortTile : 0;
+        if (tile == last_tile) {
+            const uint64_t inc = ex + tot;
+            const int64_t P_total = (int64_t)(inc >> 31);
+            const int64_t S_total = (int64_t)(inc & 0x7FFFFFFFu);
+            scalars[1] = P_total;
+            scalars[2] = S_total;
+            piece_start[P_total] = (int32_t)nv;
+            seg_first[S_total] = (int32_t)P_total;
+        }
+    }
+    __syncthreads();
+    const uint64_t ex = s_texcl + wp + x - mine;
+    int64_t pb = (int64_t)(ex >> 31);
+    int64_t sb = (int64_t)(ex & 0x7FFFFFFFu);
+#pragma unroll
+    for (int j = 0; j < kSortItems; j++) {
+        const int64_t i = i0 + j;
+        if (i < nv) {
+            const bool head = (i == 0) || (kk[j + 1] != kk[j]);
+            const bool ps = head || (i % kPiece == 0);
+            if (head) {
+                seg_first[sb] = (int32_t)pb;
+                seg_row[sb] = (int32_t)kk[j + 1];
+                sb++;
+            }
+            if (ps) {
+                piece_start[pb] = (int32_t)i;
+                piece_seg[pb] = (int32_t)(sb - 1);
+                pb++;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// segment reduce + SGD (or emit)
+// ---------------------------------------------------------------------------
+template <int LPB, int NV>
+__device__ __forceinline__ void finish_segment(int32_t s, const float4 (&g)[NV], int lane,
+                                               const int32_t* __restrict__ seg_row, float* W,
+                                               int D, float lr, bool emit, float* grad_out,
+                                               uint32_t* err) {
+    if (emit) {
+        float4* o = reinterpret_cast<float4*>(grad_out + (int64_t)s * D) + lane;
+#pragma unroll
+        for (int k = 0; k < NV; k++) o[k * LPB] = g[k];
+        return;
+    }
+    const int32_t row = seg_row[s];
+    float4* w = reinterpret_cast<float4*>(W + (int64_t)row * D) + lane;
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < NV; k++) {
+        float4 x = w[k * LPB];
+        x.x = __fmaf_rn(-lr, g[k].x, x.x);
+        x.y = __fmaf_rn(-lr, g[k].y, x.y);
+        x.z = __fmaf_rn(-lr, g[k].z, x.z);
+        x.w = __fmaf_rn(-lr, g[k].w, x.w);
+        bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
+        w[k * LPB] = x;
+    }
+    if (bad) atomicOr(err, kErrNonfinite);
+}
+
+template <int LPB, int NV>
+__global__ void __launch_bounds__(256)
+k_seg_reduce(const int32_t* __restrict__ vals, const int64_t* __restrict__ scalars,
+             const int32_t* __restrict__ piece_start, const int32_t* __restrict__ piece_seg,
+             const int32_t* __restrict__ seg_first, const int32_t* __restrict__ seg_row,
+             const float* __restrict__ src, int D, float* W, float lr, float* partial,
+             uint32_t* seg_cnt, int emit, float* grad_out, uint32_t* err) {
+    const int lane = threadIdx.x % LPB;
+    const int gw = (threadIdx.x & 31) / LPB;  // group index in warp
+    const uint32_t gmask = (LPB == 32) ? 0xffffffffu : (((1u << LPB) - 1u) << (gw * LPB));
+    const int leader = (threadIdx.x & 31) & ~(LPB - 1);
+    const int64_t gpb = blockDim.x / LPB;
+    const int64_t stride = (int64_t)gridDim.x * gpb;
+    const int64_t n_pieces = scalars[1];
+    for (int64_t pi = blockIdx.x * gpb + threadIdx.x / LPB; pi < n_pieces; pi += stride) {
+        const int32_t i0 = piece_start[pi], i1 = piece_start[pi + 1];
+        const int32_t s = piece_seg[pi];
+        const int32_t f0 = seg_first[s], f1 = seg_first[s + 1];
+        float4 g[NV];
+#pragma unroll
+        for (int k = 0; k < NV; k++) g[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        int32_t i = i0;
+        for (; i + 4 <= i1; i += 4) {
+            float4 v[4][NV];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const float4* row = reinterpret_cast<const float4*>(src + (int64_t)__ldg(vals + i + u) * D) + lane;
+#pragma unroll
+                for (int k = 0; k < NV; k++) v[u][k] = __ldg(row + k * LPB);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+#pragma unroll
+                for (int k = 0; k < NV; k++) {
+                    g[k].x += v[u][k].x;
+                    g[k].y += v[u][k].y;
+                    g[k].z += v[u][k].z;
+                    g[k].w += v[u][k].w;
+                }
+        }
+        for (; i < i1; i++) {
+            const float4* row = reinterpret_cast<const float4*>(src + (int64_t)__ldg(vals + i) * D) + lane;
+#pragma unroll
+            for (int k = 0; k < NV; k++) {
+                const float4 v = __ldg(row + k * LPB);
+                g[k].x += v.x;
+                g[k].y += v.y;
+                g[k].z += v.z;
+                g[k].w += v.w;
+            }
+        }
+        if (f1 - f0 == 1) {
+            finish_segment<LPB, NV>(s, g, lane, seg_row, W, D, lr, emit, grad_out, err);
+            continue;
+        }
+        // multi-piece segment: publish partial, last arriver combines in order
+        float4* pp = reinterpret_cast<float4*>(partial + pi * D) + lane;
+#pragma unroll
+        for (int k = 0; k < NV; k++) __stcg(pp + k * LPB, g[k]);
+        __threadfence();
+        __syncwarp(gmask);
+        uint32_t old = 0;
+        if ((threadIdx.x & 31) == leader) old = atomicAdd(&seg_cnt[s], 1u);
+        old = __shfl_sync(gmask, old, leader);
+        if (old != (uint32_t)(f1 - f0 - 1)) continue;
+        __threadfence();
+        float4 tot[NV];
+#pragma unroll
+        for (int k = 0; k < NV; k++) tot[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        // blocked sum: groups of 16 partials summed sequentially, then added
+        for (int32_t q0 = f0; q0 < f1; q0 += 16) {
+            float4 blk[NV];
+#pragma unroll
+            for (int k = 0; k < NV; k++) blk[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            const int32_t q1 = min(f1, q0 + 16);
+            for (int32_t q = q0; q < q1; q++) {
+                const float4* rp = reinterpret_cast<const float4*>(partial + (int64_t)q * D) + lane;
+#pragma unroll
+                for (int k = 0; k < NV; k++) {
+                    const float4 v = __ldcg(rp + k * LPB);
+                    blk[k].x += v.x;
+                    blk[k].y += v.y;
+                    blk[k].z += v.z;
+                    blk[k].w += v.w;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NV; k++) {
+                tot[k].x += blk[k].x;
+                tot[k].y += blk[k].y;
+                tot[k].z += blk[k].z;
+                tot[k].w += blk[k].w;
+            }
+        }
+        finish_segment<LPB, NV>(s, tot, lane, seg_row, W, D, lr, emit, grad_out, err);
+        if ((threadIdx.x & 31) == leader) seg_cnt[s] = 0u;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static int sm_count(Ctx* c) {
+    static int cached[64] = {0};
+    int d = c->device;
+    if (d >= 0 && d < 64 && cached[d]) return cached[d];
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    if (d >= 0 && d < 64) cached[d] = n;
+    return n;
+}
+
+static bool dim_ok(int D) {
+    if (D < 4 || D % 4) return false;
+    const int q = D / 4;
+    if (q <= 32) return (q & (q - 1)) == 0;
+    return q % 32 == 0;
+}
+
+template <int LPB, int NV>
+static void launch_fwd(Ctx* c, const float* W, int64_t H, int D, const int32_t* idx,
+                       const int64_t* off, int P, int64_t n_bags, float* Y) {
+    const int threads = 256;
+    const int64_t gpb = threads / LPB;
+    int64_t blocks = cdiv(n_bags, gpb);
+    const int64_t maxb = (int64_t)sm_count(c) * 16;
+    if (blocks > maxb) blocks = maxb;
+    if (blocks < 1) blocks = 1;
+    k_emb_fwd<LPB, NV><<<(unsigned)blocks, threads, 0, c->stream>>>(W, H, D, idx, off, P, n_bags, Y, c->d_err);
+}
+
+#define FAE_DISPATCH_D(D, FN, ...)                                             \
+    do {                                                                       \
+        switch ((D) / 4) {                                                     \
+            case 1: FN<1, 1>(__VA_ARGS__); break;                              \
+            case 2: FN<2, 1>(__VA_ARGS__); break;                              \
+            case 4: FN<4, 1>(__VA_ARGS__); break;                              \
+            case 8: FN<8, 1>(__VA_ARGS__); break;                              \
+            case 16: FN<16, 1>(__VA_ARGS__); break;                            \
+            case 32: FN<32, 1>(__VA_ARGS__); break;                            \
+            case 64: FN<32, 2>(__VA_ARGS__); break;                            \
+            case 96: FN<32, 3>(__VA_ARGS__); break;                            \
+            case 128: FN<32, 4>(__VA_ARGS__); break;                           \
+            default: return set_err(c, FAE_ERR_INVALID_ARG, "unsupported dim"); \
+        }                                                                      \
+    } while (0)
+
+template <int LPB, int NV>
+static void launch_reduce(Ctx* c, int64_t n_items_hint, const float* src, int D, float* W,
+                          float lr, bool emit) {
+    StepWs& w = c->ws;
+    const int threads = 256;
+    const int64_t gpb = threads / LPB;
+    const int64_t pieces_hint = n_items_hint + n_items_hint / kPiece + 1;
+    int64_t blocks = cdiv(pieces_hint, gpb);
+    const int64_t maxb = (int64_t)sm_count(c) * 16;
+    if (blocks > maxb) blocks = maxb;
+    if (blocks < 1) blocks = 1;
+    k_seg_reduce<LPB, NV><<<(unsigned)blocks, threads, 0, c->stream>>>(
+        w.vals[0], w.scalars, w.piece_start, w.piece_seg, w.seg_first, w.seg_row, src, D, W, lr,
+        w.partial, w.seg_cnt, emit ? 1 : 0, w.grad, c->d_err);
+}
+
+static int key_bits(int64_t H) {
+    // keys in [0, H] (H marks invalid lookups)
+    int b = 1;
+    while (b < 32 && ((uint64_t)1 << b) <= (uint64_t)H) b++;
+    return b;
+}
+
+// Sort (keys, vals) already in ws.keys[0]/vals[0] (prep done), then pieces and
+// reduce.  Result of the sort lands back in buffer 0 (even passes) — we track
+// which buffer holds it and swap pointers so vals[0] is sorted on exit.
+static fae_status sort_pieces_reduce(Ctx* c, int64_t n_hint, int64_t H, int D, const float* src,
+                                     float* W, float lr, bool emit) {
+    StepWs& w = c->ws;
+    const int passes = (key_bits(H) + kSortBits - 1) / kSortBits;
+    const int64_t tiles = std::max<int64_t>(1, cdiv(n_hint, kSortTile));
+    for (int ps = 0; ps < passes; ps++) {
+        const int s = ps & 1;
+        k_sort_pass<<<(unsigned)tiles, kSortThreads, 0, c->stream>>>(
+            w.keys[s], w.vals[s], w.keys[s ^ 1], w.vals[s ^ 1], w.scalars, ps * kSortBits,
+            w.ghist + ps * kSortBins, w.sort_status + (int64_t)ps * w.n_sort_tiles * kSortBins,
+            w.tile_ctr + ps);
+        FAE_LAUNCHED(c);
+    }
+    if (passes & 1) {
+        std::swap(w.keys[0], w.keys[1]);
+        std::swap(w.vals[0], w.vals[1]);
+    }
+    k_pieces<<<(unsigned)tiles, kSortThreads, 0, c->stream>>>(
+        w.keys[0], w.scalars, w.piece_status, w.tile_ctr + 4, w.piece_start, w.piece_seg,
+        w.seg_first, w.seg_row);
+    FAE_LAUNCHED(c);
+    FAE_DISPATCH_D(D, launch_reduce, c, n_hint, src, D, W, lr, emit);
+    FAE_LAUNCHED(c);
+    return FAE_OK;
+}
+
+static fae_status zero_ws(Ctx* c, int64_t n_hint) {
+    StepWs& w = c->ws;
+    // ghist, counters, scalars and the used look-back status prefix
+    const int64_t tiles = std::max<int64_t>(1, cdiv(n_hint, kSortTile));
+    FAE_CUDA(c, cudaMemsetAsync(w.ghist, 0, sizeof(uint32_t) * kMaxSortPasses * kSortBins, c->stream));
+    FAE_CUDA(c, cudaMemsetAsync(w.tile_ctr, 0, sizeof(uint32_t) * 8, c->stream));
+    FAE_CUDA(c, cudaMemsetAsync(w.scalars, 0, sizeof(int64_t) * 8, c->stream));
+    FAE_CUDA(c, cudaMemsetAsync(w.piece_status, 0, sizeof(uint64_t) * tiles, c->stream));
+    for (int ps = 0; ps < kMaxSortPasses; ps++)
+        FAE_CUDA(c, cudaMemsetAsync(w.sort_status + (int64_t)ps * w.n_sort_tiles * kSortBins, 0,
+                                    sizeof(uint32_t) * tiles * kSortBins, c->stream));
+    return FAE_OK;
+}
+
+fae_status bwd_group_and_reduce(Ctx* c, float* W_hot, int64_t H, int32_t D,
+                                const uint32_t* /*unused*/, const int32_t* idx,
+                                const int64_t* off, int32_t P, int64_t n_bags, int64_t n_hint,
+                                const float* dY, float lr, bool emit) {
+    StepWs& w = c->ws;
+    fae_status st = zero_ws(c, n_hint);
+    if (st != FAE_OK) return st;
+    const int passes = (key_bits(H) + kSortBits - 1) / kSortBits;
+    int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(cdiv(n_hint, 256), (int64_t)sm_count(c) * 8));
+    k_bwd_prep<<<(unsigned)blocks, 256, 0, c->stream>>>(idx, off, P, n_bags, H, passes, w.keys[0],
+                                                        w.vals[0], w.ghist, w.scalars, c->d_err);
+    FAE_LAUNCHED(c);
+    return sort_pieces_reduce(c, n_hint, H, D, dY, W_hot, lr, emit);
+}
+
+static fae_status validate_step(Ctx* c, const float* W, int64_t H, int32_t D, const int32_t* idx,
+                                const int64_t* off, int32_t P, int64_t n_bags, const float* X,
+                                const char* who) {
+    if (!W || ((!X || !idx) && n_bags > 0)) return set_err(c, FAE_ERR_INVALID_ARG, std::string(who) + ": null pointer");
+    if (H < 0 || H >= (1ll << 31) - 1) return set_err(c, FAE_ERR_INVALID_ARG, std::string(who) + ": H out of range");
+    if (!dim_ok(D) || D > c->cfg.max_dim) return set_err(c, FAE_ERR_INVALID_ARG, std::string(who) + ": unsupported dim");
+    if (n_bags < 0 || (!off && P < 0)) return set_err(c, FAE_ERR_INVALID_ARG, std::string(who) + ": bad sizes");
+    if (n_bags > c->cfg.max_batch_bags) return set_err(c, FAE_ERR_CAPACITY, std::string(who) + ": n_bags > max_batch_bags");
+    if (!off && n_bags * (int64_t)P > c->cfg.max_batch_lookups)
+        return set_err(c, FAE_ERR_CAPACITY, std::string(who) + ": lookups > max_batch_lookups");
+    if (n_bags > 0 && (((uintptr_t)W | (uintptr_t)X) & 15)) return set_err(c, FAE_ERR_INVALID_ARG, std::string(who) + ": W/Y must be 16-byte aligned");
+    return FAE_OK;
+}
+
+}  // namespace fae
+
+using namespace fae;
+
+extern "C" {
+
+fae_status fae_emb_fwd(fae_ctx* h, const float* W_hot, int64_t H, int32_t D, const int32_t* idx,
+                       const int64_t* off, int32_t fixed_pool, int64_t n_bags, float* Y) {
+    if (!h) return FAE_ERR_NOT_INIT;
+    Ctx* c = &h->c;
+    fae_status st = validate_step(c, W_hot, H, D, idx, off, fixed_pool, n_bags, Y, "fae_emb_fwd");
+    if (st != FAE_OK) return st;
+    if (n_bags == 0) return FAE_OK;
+    FAE_DISPATCH_D(D, launch_fwd, c, W_hot, H, D, idx, off, fixed_pool, n_bags, Y);
+    FAE_LAUNCHED(c);
+    return FAE_OK;
+}
+
+fae_status fae_emb_bwd_update(fae_ctx* h, float* W_hot, int64_t H, int32_t D, const int32_t* idx,
+                              const int64_t* off, int32_t fixed_pool, int64_t n_bags,
+                              const float* dY, float lr) {
+    if (!h) return FAE_ERR_NOT_INIT;
+    Ctx* c = &h->c;
+    fae_status st = validate_step(c, W_hot, H, D, idx, off, fixed_pool, n_bags, dY, "fae_emb_bwd_update");
+    if (st != FAE_OK) return st;
+    if (!(lr == lr)) return set_err(c, FAE_ERR_INVALID_ARG, "fae_emb_bwd_update: lr is NaN");
+    const int64_t n_hint = off ? c->cfg.max_batch_lookups : n_bags * (int64_t)fixed_pool;
+    const bool multi = c->world > 1;
+    if (n_bags == 0 && !multi) return FAE_OK;
+    st = bwd_group_and_reduce(c, W_hot, H, D, nullptr, idx, off, fixed_pool, n_bags, n_hint, dY, lr, multi);
+    if (st != FAE_OK || !multi) return st;
+    // a11: exchange the local sparse gradient, merge deterministically, apply
+    int64_t U = 0;
+    FAE_CUDA(c, cudaMemcpyAsync(&U, c->ws.scalars + 2, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    FAE_CUDA(c, cudaStreamSynchronize(c->stream));
+    // rows are ws.seg_row[0..U), grads ws.grad[0..U)
+    return sync_merge_apply(c, c->ws.seg_row, c->ws.grad, U, D, W_hot, H, lr, nullptr, nullptr, nullptr, 0);
+}
+
+}  // extern "C"
+
+namespace fae {
+
+// Gather every rank's sorted (row, G) list, merge in rank order and either
+// apply SGD to W (W != nullptr) or write the merged list to out_rows/out_vals.
+fae_status sync_merge_apply(Ctx* c, const int32_t* rows, const float* vals, int64_t U, int32_t D,
+                            float* W, int64_t H, float lr, int32_t* out_rows, float* out_vals,
+                            int64_t* out_count, int64_t out_cap) {
+    if (!c->comm) return set_err(c, FAE_ERR_NOT_INIT, "sync: no communicator");
+    const int world = c->world;
+    if (U > c->g_cap) return set_err(c, FAE_ERR_CAPACITY, "sync: local U exceeds capacity");
+    // 1. counts
+    int32_t Ui = (int32_t)U;
+    FAE_CUDA(c, cudaMemcpyAsync(c->g_counts + c->rank, &Ui, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+    ncclResult_t r = ncclAllGather(c->g_counts + c->rank, c->g_counts, 1, ncclInt32, c->comm, c->stream);
+    if (r != ncclSuccess) return set_err(c, FAE_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+    std::vector<int32_t> counts(world);
+    FAE_CUDA(c, cudaMemcpyAsync(counts.data(), c->g_counts, sizeof(int32_t) * world, cudaMemcpyDeviceToHost, c->stream));
+    FAE_CUDA(c, cudaStreamSynchronize(c->stream));
+    int64_t cap = 0;
+    for (int i = 0; i < world; i++) cap = std::max<int64_t>(cap, counts[i]);
+    if (cap == 0) {
+        if (out_count) *out_count = 0;
+        return FAE_OK;
+    }
+    if (cap * world > c->ws.cap_L) return set_err(c, FAE_ERR_CAPACITY, "sync: gathered size exceeds workspace");
+    // 2. padded payloads (rows, vals) — grouped all-gathers
+    int32_t* my_rows = c->g_rows + (int64_t)c->rank * cap;
+    float* my_vals = c->g_vals + (int64_t)c->rank * cap * D;
+    if (U > 0) {
+        FAE_CUDA(c, cudaMemcpyAsync(my_rows, rows, sizeof(int32_t) * U, cudaMemcpyDeviceToDevice, c->stream));
+        FAE_CUDA(c, cudaMemcpyAsync(my_vals, vals, sizeof(float) * U * D, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    ncclGroupStart();
+    ncclAllGather(my_rows, c->g_rows, cap, ncclInt32, c->comm, c->stream);
+    ncclAllGather(my_vals, c->g_vals, cap * D, ncclFloat32, c->comm, c->stream);
+    r = ncclGroupEnd();
+    if (r != ncclSuccess) return set_err(c, FAE_ERR_NCCL, std::string("ncclAllGather payload: ") + ncclGetErrorString(r));
+    // 3. deterministic merge: stable sort by row over the rank-ordered
+    //    concatenation, segment sums in fixed order, then SGD or emit.
+    const int64_t n = cap * world;
+    fae_status st = zero_ws(c, n);
+    if (st != FAE_OK) return st;
+    int64_t Hk = H;
+    if (!W) {
+        // emit mode: key range from the rows themselves (< 2^31)
+        Hk = (1ll << 31) - 2;
+    }
+    const int passes = (key_bits(Hk) + kSortBits - 1) / kSortBits;
+    int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), (int64_t)sm_count(c) * 8));
+    k_merge_prep<<<(unsigned)blocks, 256, 0, c->stream>>>(c->g_rows, c->g_counts, world, cap, Hk, passes,
+                                                          c->ws.keys[0], c->ws.vals[0], c->ws.ghist,
+                                                          c->ws.scalars);
+    FAE_LAUNCHED(c);
+    st = sort_pieces_reduce(c, n, Hk, D, c->g_vals, W, lr, W == nullptr);
+    if (st != FAE_OK) return st;
+    if (!W) {
+        int64_t Ug = 0;
+        FAE_CUDA(c, cudaMemcpyAsync(&Ug, c->ws.scalars + 2, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+        FAE_CUDA(c, cudaStreamSynchronize(c->stream));
+        if (Ug > out_cap) return set_err(c, FAE_ERR_CAPACITY, "sync: global U exceeds cap");
+        FAE_CUDA(c, cudaMemcpyAsync(out_rows, c->ws.seg_row, sizeof(int32_t) * Ug, cudaMemcpyDeviceToDevice, c->stream));
+        FAE_CUDA(c, cudaMemcpyAsync(out_vals, c->ws.grad, sizeof(float) * Ug * D, cudaMemcpyDeviceToDevice, c->stream));
+        FAE_CUDA(c, cudaStreamSynchronize(c->stream));
+        *out_count = Ug;
+    }
+    ncclResult_t ae;
+    if (ncclCommGetAsyncError(c->comm, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress)
+        return set_err(c, FAE_ERR_NCCL, std::string("nccl async: ") + ncclGetErrorString(ae));
+    return FAE_OK;
+}
+
+}  // namespace fae
+
+extern "C" fae_status fae_sync_hot_grads(fae_ctx* h, int32_t* rows, float* vals, int64_t* count_host,
+                                         int64_t cap, int32_t D) {
+    if (!h) return FAE_ERR_NOT_INIT;
+    Ctx* c = &h->c;
+    if (!rows || !vals || !count_host || cap < 0 || !dim_ok(D) || D > c->cfg.max_dim)
+        return set_err(c, FAE_ERR_INVALID_ARG, "fae_sync_hot_grads: bad arguments");
+    if (*count_host < 0 || *count_host > cap)
+        return set_err(c, FAE_ERR_INVALID_ARG, "fae_sync_hot_grads: count outside [0, cap]");
+    if (c->world == 1 && !c->comm) return FAE_OK;   // identity
+    return sync_merge_apply(c, rows, vals, *count_host, D, nullptr, 0, 0.f, rows, vals, count_host, cap);
+}

@@ -1,0 +1,112 @@
+"""Orchestration of the FAE hot path over the C ABI (no arithmetic here).
+
+One `FaePipeline` per GPU.  It allocates the device buffers a run needs and
+calls, in the paper's order:
+
+  fae_profile   -> per-table loggers k and T             (a1, a2)
+  fae_threshold -> hot set + remap                        (a3, a4)
+  fae_classify  -> hot/cold ids + remapped hot CSR        (a5, a6)
+  fae_extract   -> replicated hot table W_hot             (a7)
+  per hot batch: fae_emb_fwd, fae_emb_bwd_update          (a8-a11)
+
+Everything numeric happens inside libfae.so kernels.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import List, Optional
+
+import torch
+
+from . import (BUDGET_EXACT, FIXED_T, Ctx, fae_classify, fae_create,
+               fae_emb_bwd_update, fae_emb_fwd, fae_extract, fae_profile,
+               fae_threshold)
+
+
+@dataclasses.dataclass
+class Prepared:
+    counts: torch.Tensor
+    T: List[int]
+    n_sampled: int
+    thresh: dict
+    hot_ids: torch.Tensor
+    cold_ids: torch.Tensor
+    hot_idx: torch.Tensor
+    hot_off: Optional[torch.Tensor]
+    packed: dict
+
+
+class FaePipeline:
+    def __init__(self, rows: List[int], dim: int, batch: int, pool: int,
+                 max_pool: int = 1, device: int = 0, max_world: int = 1,
+                 ctx: Optional[Ctx] = None):
+        self.rows = [int(r) for r in rows]
+        self.Tn = len(rows)
+        self.dim = dim
+        self.batch = batch
+        self.pool = pool                      # 0 => offsets
+        self.device = device
+        max_lookups = batch * self.Tn * max(pool, max_pool, 1)
+        self.ctx = ctx or fae_create(device, max_tables=max(self.Tn, 1),
+                                     max_rows=sum(self.rows),
+                                     max_batch_lookups=max_lookups,
+                                     max_batch_bags=batch * self.Tn,
+                                     max_dim=max(dim, 4), max_world=max_world)
+        self.dev = torch.device("cuda", device)
+
+    # ---------------------------------------------------------------- a1-a7
+    def preprocess(self, idx: torch.Tensor, off: Optional[torch.Tensor],
+                   n_records: int, x_pct: float = 5.0, seed: int = 1,
+                   mode: int = FIXED_T, t: float = 1e-7,
+                   budget_bytes: int = 0, small_table_bytes: int = 1 << 20,
+                   want_estimate: bool = False,
+                   bufs: Optional[Prepared] = None) -> Prepared:
+        dev = self.dev
+        counts = bufs.counts if bufs else torch.empty(sum(self.rows), dtype=torch.int32, device=dev)
+        T, ns = fae_profile(self.ctx, self.rows, self.dim, idx, off, self.pool,
+                            n_records, x_pct, seed, counts)
+        th = fae_threshold(self.ctx, self.rows, self.dim, counts, T, x_pct,
+                           mode=mode, t=t, budget_bytes=budget_bytes,
+                           small_table_bytes=small_table_bytes,
+                           want_estimate=want_estimate)
+        if bufs is None:
+            hot_ids = torch.empty(max(n_records, 1), dtype=torch.int64, device=dev)
+            cold_ids = torch.empty(max(n_records, 1), dtype=torch.int64, device=dev)
+            hot_idx = torch.empty(max(idx.numel(), 1), dtype=torch.int32, device=dev)
+            hot_off = (torch.empty(n_records * self.Tn + 1, dtype=torch.int64, device=dev)
+                       if off is not None else None)
+        else:
+            hot_ids, cold_ids, hot_idx, hot_off = bufs.hot_ids, bufs.cold_ids, bufs.hot_idx, bufs.hot_off
+        pk = fae_classify(self.ctx, self.rows, self.dim, idx, off, self.pool,
+                          n_records, self.batch, hot_ids, cold_ids, hot_idx, hot_off)
+        return Prepared(counts, T, ns, th, hot_ids, cold_ids, hot_idx, hot_off, pk)
+
+    def extract(self, W: torch.Tensor, prep: Prepared) -> torch.Tensor:
+        """Replicated hot table [H_total, D] (buffer reused across calls)."""
+        H = prep.thresh["H_total"]
+        buf = getattr(self, "_whot", None)
+        if buf is None or buf.shape[0] < max(H, 1):
+            buf = torch.empty(max(H, 1), self.dim, dtype=torch.float32, device=self.dev)
+            self._whot = buf
+        fae_extract(self.ctx, W, buf)
+        return buf[:H]
+
+    # ---------------------------------------------------------------- a8-a11
+    def batch_args(self, prep: Prepared, i: int):
+        """(idx, off, n_bags) views of hot batch i (no copies)."""
+        B, Tn = self.batch, self.Tn
+        nh = prep.packed["n_hot"]
+        r0, r1 = i * B, min((i + 1) * B, nh)
+        n_bags = (r1 - r0) * Tn
+        if self.pool > 0:
+            P = self.pool
+            return prep.hot_idx[r0 * Tn * P: r1 * Tn * P], None, n_bags
+        return prep.hot_idx, prep.hot_off[r0 * Tn: r1 * Tn + 1], n_bags
+
+    def step(self, W_hot, prep: Prepared, i: int, Y, dY, lr: float):
+        idx, off, n_bags = self.batch_args(prep, i)
+        fae_emb_fwd(self.ctx, W_hot, idx, off, self.pool, n_bags, Y)
+        fae_emb_bwd_update(self.ctx, W_hot, idx, off, self.pool, n_bags, dY, lr)
+
+
+__all__ = ["FaePipeline", "Prepared", "FIXED_T", "BUDGET_EXACT"]

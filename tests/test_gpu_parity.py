@@ -1,0 +1,341 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle.
+
+Integer stages (sample, histogram, threshold, remap, classify, pack,
+extract) must be bit-exact.  fp32 stages (pooled Y, updated W_hot) must be
+within |gpu - oracle| <= 1e-6 + 1e-5 * |oracle| (BASELINE.json north_star).
+Inputs are the seeded generators of gen/, identical bits on both sides.
+"""
+import numpy as np
+import pytest
+import torch
+
+import gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+ATOL, RTOL = 1e-6, 1e-5
+
+
+def fae():
+    import paper_2103_00686_b200 as m
+    return m
+
+
+def close(gpu, ref):
+    gpu = np.asarray(gpu, np.float64)
+    ref = np.asarray(ref, np.float64)
+    err = np.abs(gpu - ref)
+    bound = ATOL + RTOL * np.abs(ref)
+    return bool(np.all(err <= bound)), float((err - bound).max(initial=-1))
+
+
+@pytest.fixture(scope="module")
+def dev():
+    return torch.device("cuda", 0)
+
+
+def mkctx(rows, dim, batch_lookups, batch_bags, world=1):
+    return fae().fae_create(0, max_tables=len(rows), max_rows=sum(rows),
+                            max_batch_lookups=batch_lookups,
+                            max_batch_bags=batch_bags, max_dim=max(dim, 4),
+                            max_world=world)
+
+
+# ----------------------------------------------------------------------------
+# a8 forward / a9-a10 backward + SGD on hot batches
+# ----------------------------------------------------------------------------
+def _hot_batch(H, n_bags, pool, dim, seed, var=False, zipf=True):
+    g = torch.Generator().manual_seed(seed)
+    if var:
+        sizes = torch.randint(0, 2 * pool + 1, (n_bags,), generator=g)
+        off = torch.zeros(n_bags + 1, dtype=torch.int64)
+        off[1:] = torch.cumsum(sizes, 0)
+        L = int(off[-1])
+    else:
+        off = None
+        L = n_bags * pool
+    if zipf:
+        u = gen.uniform01(seed, torch.arange(L))
+        cdf = gen.zipf_cdf(H, 1.1, "cpu")
+        idx = gen.feistel(torch.searchsorted(cdf, u).clamp(max=H - 1), H, seed).to(torch.int32)
+    else:
+        idx = torch.randint(0, H, (L,), generator=g, dtype=torch.int32)
+    W = gen.make_weights(H, dim, seed=seed + 1)
+    dY = gen.make_dy(n_bags, dim, seed=seed + 2)
+    return W, idx, off, dY
+
+
+CASES = [
+    # (H, n_bags, pool, dim, var)  -- several tiles + ragged tails
+    (1000, 128 * 4, 1, 16, False),          # tiny-shaped hot batch
+    (50_000, 2048 * 26, 1, 16, False),      # Kaggle-shaped hot batch (S = L = 53,248)
+    (200_000, 4096 * 26, 1, 64, False),     # Terabyte-shaped hot batch (L = 106,496, D = 64)
+    (300_000, 1024 * 3, 60, 16, True),      # Alibaba-shaped multi-hot bags (~180k lookups)
+    (777, 333, 3, 32, False),               # ragged
+    (5000, 1000, 7, 128, True),             # D = 128, variable incl. empty bags
+    (4096, 500, 2, 4, False),               # D = 4
+]
+
+
+@pytest.mark.parametrize("H,n_bags,pool,dim,var", CASES)
+def test_fwd_bwd_parity(dev, H, n_bags, pool, dim, var):
+    W, idx, off, dY = _hot_batch(H, n_bags, pool, dim, seed=H + n_bags, var=var)
+    L = idx.numel()
+    ctx = mkctx([H], dim, max(L, 1), n_bags)
+    Wd, idxd, dYd = W.to(dev), idx.to(dev), dY.to(dev)
+    offd = off.to(dev) if off is not None else None
+    P = 0 if var else pool
+    Y = torch.empty(n_bags, dim, device=dev)
+    fae().fae_emb_fwd(ctx, Wd, idxd, offd, P, n_bags, Y)
+    Yref, st = oracle.emb_fwd(W, idx, off, P, n_bags)
+    assert st == 0
+    ok, worst = close(Y.cpu().numpy(), Yref)
+    assert ok, f"fwd worst excess {worst}"
+    if pool == 1 and not var:
+        assert torch.equal(Y.cpu(), W[idx.long()])          # single lookup: bit copy
+    lr = 0.01
+    fae().fae_emb_bwd_update(ctx, Wd, idxd, offd, P, n_bags, dYd, lr)
+    ctx.check()
+    Wref, st = oracle.emb_bwd_sgd(W, idx, off, P, n_bags, dY, lr)
+    Wg = Wd.cpu().numpy()
+    ok, worst = close(Wg, Wref)
+    assert ok, f"bwd worst excess {worst}"
+    touched = np.zeros(H, bool)
+    touched[idx.numpy()] = True
+    assert np.array_equal(Wg[~touched], W.numpy()[~touched])   # untouched: bit-identical
+
+
+def test_bwd_deterministic(dev):
+    W, idx, _, dY = _hot_batch(20_000, 2048 * 26, 1, 16, seed=5)
+    ctx = mkctx([20_000], 16, idx.numel(), 2048 * 26)
+    outs = []
+    for _ in range(3):
+        Wd = W.to(dev)
+        fae().fae_emb_bwd_update(ctx, Wd, idx.to(dev), None, 1, 2048 * 26, dY.to(dev), 0.01)
+        outs.append(Wd.cpu())
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
+
+
+def test_step_edge_cases(dev):
+    m = fae()
+    ctx = mkctx([100], 16, 1000, 1000)
+    W = gen.make_weights(100, 16).to(dev)
+    Y = torch.empty(0, 16, device=dev)
+    m.fae_emb_fwd(ctx, W, torch.empty(0, dtype=torch.int32, device=dev), None, 1, 0, Y)
+    m.fae_emb_bwd_update(ctx, W, torch.empty(0, dtype=torch.int32, device=dev), None, 1, 0,
+                         torch.empty(0, 16, device=dev), 0.1)
+    ctx.check()
+    # lr = 0 leaves W bit-identical
+    W0 = W.clone()
+    idx = torch.randint(0, 100, (64,), dtype=torch.int32, device=dev)
+    m.fae_emb_bwd_update(ctx, W, idx, None, 1, 64, torch.ones(64, 16, device=dev), 0.0)
+    ctx.check()
+    assert torch.equal(W, W0)
+    # out-of-range index is latched
+    bad = torch.tensor([0, 5, 100], dtype=torch.int32, device=dev)
+    Y = torch.empty(3, 16, device=dev)
+    m.fae_emb_fwd(ctx, W, bad, None, 1, 3, Y)
+    with pytest.raises(m.FaeError) as e:
+        ctx.check()
+    assert e.value.name == "INDEX_RANGE"
+    # unsupported dim / capacity
+    with pytest.raises(m.FaeError):
+        m.fae_emb_fwd(ctx, torch.zeros(10, 12, device=dev), idx, None, 1, 64,
+                      torch.empty(64, 12, device=dev))
+    with pytest.raises(m.FaeError) as e:
+        m.fae_emb_fwd(ctx, W, torch.zeros(2000, dtype=torch.int32, device=dev), None, 1, 2000,
+                      torch.empty(2000, 16, device=dev))
+    assert e.value.name == "CAPACITY"
+
+
+# ----------------------------------------------------------------------------
+# a1-a7 preprocessing
+# ----------------------------------------------------------------------------
+def _prep_ref(ds, x, seed, mode, t=None, budget=None, small=0):
+    samp = oracle.sample(ds.n_records, x, seed)
+    counts, T, st = oracle.histogram(ds.rows, ds.idx, ds.off, ds.fixed_pool, ds.n_records, samp)
+    assert st == 0
+    if mode == "t":
+        kmin = oracle.kmin_fixed_t(ds.rows, 16, small, T, t, x)
+        extra = {}
+    else:
+        r = oracle.budget_exact(ds.rows, 16, small, counts, T, x, budget)
+        kmin, extra = r["kmin"], r
+    hot = oracle.tag_rows(ds.rows, 16, small, counts, kmin)
+    rm, base, H = oracle.remap(ds.rows, hot)
+    flag = oracle.classify(ds.rows, ds.idx, ds.off, ds.fixed_pool, ds.n_records, rm)
+    pk = oracle.pack(ds.rows, ds.idx, ds.off, ds.fixed_pool, ds.n_records, rm, flag)
+    return dict(samp=samp, counts=counts, T=T, kmin=kmin, hot=hot, remap=rm, base=base,
+                H=H, flag=flag, pack=pk, extra=extra)
+
+
+PREP_CASES = [
+    ("tiny", 10_000, 5.0, "t", 1e-3, 0),
+    ("tiny", 10_000, 5.0, "t", 1e-2, 0),
+    ("tiny", 10_000, 5.0, "t", 3e-2, 0),
+    ("tiny", 10_000, 100.0, "t", 3e-3, 0),
+    ("tiny", 10_000, 5.0, "b", 64 * 300, 0),
+    ("kaggle", 60_000, 5.0, "t", 1e-7, 1 << 20),
+    ("kaggle", 60_000, 5.0, "b", 512 << 20, 1 << 20),
+    ("kaggle", 60_000, 5.0, "b", 20 << 20, 1 << 20),
+    ("alibaba", 3_000, 5.0, "t", 1e-5, 1 << 20),
+]
+
+
+@pytest.mark.parametrize("cfg,R,x,mode,arg,small", PREP_CASES)
+def test_preprocess_parity(dev, cfg, R, x, mode, arg, small):
+    m = fae()
+    c = gen.CONFIGS[cfg]
+    ds = gen.make_dataset(c, n_records=R, seed=11)
+    seed = 77
+    ref = _prep_ref(ds, x, seed, mode, t=arg if mode == "t" else None,
+                    budget=arg if mode == "b" else None, small=small)
+    ctx = mkctx(ds.rows, 16, c.batch * c.n_tables * max(c.pool, c.pool_hi, 1), c.batch * c.n_tables)
+    dd = ds.to(dev)
+    counts = torch.empty(sum(ds.rows), dtype=torch.int32, device=dev)
+    samp = torch.empty(max(R, 1), dtype=torch.int64, device=dev)
+    T, ns = m.fae_profile(ctx, ds.rows, 16, dd.idx, dd.off, ds.fixed_pool, R, x, seed, counts, samp)
+    assert ns == len(ref["samp"])
+    assert np.array_equal(samp[:ns].cpu().numpy(), ref["samp"])
+    assert T == list(ref["T"])
+    assert np.array_equal(counts.cpu().numpy().view(np.uint32), ref["counts"])
+    remap = torch.empty(sum(ds.rows), dtype=torch.int32, device=dev)
+    if mode == "t":
+        th = m.fae_threshold(ctx, ds.rows, 16, counts, T, x, mode=m.FIXED_T, t=arg,
+                             small_table_bytes=small, remap_out=remap)
+    else:
+        th = m.fae_threshold(ctx, ds.rows, 16, counts, T, x, mode=m.BUDGET_EXACT, budget_bytes=arg,
+                             small_table_bytes=small, remap_out=remap)
+        assert th["K"] == ref["extra"]["K"]
+        assert th["t_final"] == ref["extra"]["t_final"]
+        assert th["budget_slack"] == ref["extra"]["slack"]
+    assert th["kmin"] == [int(v) for v in ref["kmin"]]
+    assert th["H_total"] == ref["H"]
+    assert th["base"] == [int(v) for v in ref["base"]]
+    assert np.array_equal(remap.cpu().numpy(), ref["remap"])
+    hot_ids = torch.empty(R, dtype=torch.int64, device=dev)
+    cold_ids = torch.empty(R, dtype=torch.int64, device=dev)
+    hot_idx = torch.empty(max(ds.n_lookups, 1), dtype=torch.int32, device=dev)
+    hot_off = torch.empty(R * ds.n_tables + 1, dtype=torch.int64, device=dev) if ds.off is not None else None
+    pk = m.fae_classify(ctx, ds.rows, 16, dd.idx, dd.off, ds.fixed_pool, R, c.batch,
+                        hot_ids, cold_ids, hot_idx, hot_off)
+    rp = ref["pack"]
+    assert pk["n_hot"] == rp["n_hot"] and pk["n_cold"] == rp["n_cold"]
+    assert pk["n_hot_lookups"] == rp["n_hot_lookups"]
+    assert np.array_equal(hot_ids[:pk["n_hot"]].cpu().numpy(), rp["hot_ids"])
+    assert np.array_equal(cold_ids[:pk["n_cold"]].cpu().numpy(), rp["cold_ids"])
+    assert np.array_equal(hot_idx[:pk["n_hot_lookups"]].cpu().numpy(), rp["hot_idx"])
+    if hot_off is not None:
+        assert np.array_equal(hot_off[:pk["n_hot"] * ds.n_tables + 1].cpu().numpy(), rp["hot_off"])
+    # a7 extract: bit copy
+    W = gen.make_weights(sum(ds.rows), 16)
+    W_hot = torch.empty(max(th["H_total"], 1), 16, device=dev)
+    m.fae_extract(ctx, W.to(dev), W_hot)
+    ctx.check()
+    assert np.array_equal(W_hot[:th["H_total"]].cpu().numpy(), oracle.extract(W, ref["remap"], ref["H"]))
+
+
+def test_estimate_parity(dev):
+    m = fae()
+    c = gen.CONFIGS["kaggle"]
+    ds = gen.make_dataset(c, n_records=200_000, seed=3)
+    x, seed = 5.0, 9
+    ctx = mkctx(ds.rows, 16, 2048 * 26, 2048 * 26)
+    dd = ds.to(dev)
+    counts = torch.empty(sum(ds.rows), dtype=torch.int32, device=dev)
+    T, ns = m.fae_profile(ctx, ds.rows, 16, dd.idx, None, 1, ds.n_records, x, seed, counts)
+    th = m.fae_threshold(ctx, ds.rows, 16, counts, T, x, mode=m.FIXED_T, t=1e-7,
+                         want_estimate=True, chunk_seed=1234, t_quantile=3.6007)
+    cnt = counts.cpu().numpy().view(np.uint32)
+    base = np.concatenate([[0], np.cumsum(ds.rows)])
+    for z, n in enumerate(ds.rows):
+        if th["is_small"][z]:
+            continue
+        e = oracle.estimate(cnt[base[z]:base[z + 1]], th["kmin"][z], 35, 1024, 1234 ^ z, 3.6007)
+        assert th["est_mean"][z] == e["ybar"]
+        assert th["est_sd"][z] == e["s"]
+        assert th["est_lo"][z] == e["lo"] and th["est_hi"][z] == e["hi"]
+        assert th["est_rows"][z] == e["est"]
+        assert bool(th["est_exact"][z]) == e["exact"]
+
+
+def test_preprocess_errors(dev):
+    m = fae()
+    ds = gen.make_dataset(gen.CONFIGS["tiny"], n_records=100)
+    dd = ds.to(dev)
+    ctx = mkctx(ds.rows, 16, 1000, 1000)
+    counts = torch.empty(sum(ds.rows), dtype=torch.int32, device=dev)
+    for bad_x in (0.0, -1.0, 100.5):
+        with pytest.raises(m.FaeError) as e:
+            m.fae_profile(ctx, ds.rows, 16, dd.idx, None, 1, 100, bad_x, 1, counts)
+        assert e.value.name == "INVALID_ARG"
+    T, _ = m.fae_profile(ctx, ds.rows, 16, dd.idx, None, 1, 100, 100.0, 1, counts)
+    with pytest.raises(m.FaeError) as e:
+        m.fae_threshold(ctx, ds.rows, 16, counts, T, 5.0, mode=m.FIXED_T, t=0.0)
+    assert e.value.name == "INVALID_ARG"
+    with pytest.raises(m.FaeError) as e:
+        m.fae_threshold(ctx, ds.rows, 16, counts, T, 5.0, mode=m.BUDGET_EXACT, budget_bytes=10,
+                        small_table_bytes=1 << 20)
+    assert e.value.name == "BUDGET_INFEASIBLE"
+    bad = dd.idx.clone()
+    bad[7] = 5000
+    with pytest.raises(m.FaeError) as e:
+        m.fae_profile(ctx, ds.rows, 16, bad, None, 1, 100, 100.0, 1, counts)
+    assert e.value.name == "INDEX_RANGE"
+    with pytest.raises(m.FaeError) as e:
+        m.fae_classify(ctx, ds.rows, 16, dd.idx, None, 1, 100, 0,
+                       torch.empty(100, dtype=torch.int64, device=dev),
+                       torch.empty(100, dtype=torch.int64, device=dev),
+                       torch.empty(400, dtype=torch.int32, device=dev))
+    assert e.value.name == "INVALID_ARG"
+
+
+def test_sync_identity_world1(dev):
+    """fae_sync_hot_grads over a 1-rank NCCL comm runs the gather + merge path
+    and must return the input list unchanged (sorted, unique)."""
+    m = fae()
+    ctx = mkctx([1000], 16, 4096, 4096, world=1)
+    m.fae_comm_init(ctx, m.fae_get_nccl_id(), 0, 1)
+    rows = torch.tensor(sorted(np.random.default_rng(0).choice(1000, 300, replace=False)),
+                        dtype=torch.int32, device=dev)
+    vals = gen.make_dy(300, 16).to(dev)
+    r0, v0 = rows.clone(), vals.clone()
+    cap_rows = torch.zeros(4096, dtype=torch.int32, device=dev)
+    cap_vals = torch.zeros(4096, 16, device=dev)
+    cap_rows[:300] = rows
+    cap_vals[:300] = vals
+    n = m.fae_sync_hot_grads(ctx, cap_rows, cap_vals, 300)
+    assert n == 300
+    assert torch.equal(cap_rows[:300], r0) and torch.equal(cap_vals[:300], v0)
+
+
+def test_pipeline_end_to_end_kaggle(dev):
+    """Kaggle-shaped: full a1-a10 over 100k records, first 3 hot batches
+    trained; W_hot after 3 sequential SGD steps vs the oracle."""
+    from paper_2103_00686_b200.pipeline import FaePipeline
+    c = gen.CONFIGS["kaggle"]
+    R = 100_000
+    ds = gen.make_dataset(c, n_records=R, seed=21)
+    dd = ds.to(dev)
+    pipe = FaePipeline(ds.rows, 16, c.batch, 1)
+    prep = pipe.preprocess(dd.idx, None, R, x_pct=5.0, seed=3, t=1e-6)
+    W = gen.make_weights(sum(ds.rows), 16)
+    W_hot = pipe.extract(W.to(dev), prep)
+    ref = _prep_ref(ds, 5.0, 3, "t", t=1e-6, small=1 << 20)
+    Wref = oracle.extract(W, ref["remap"], ref["H"])
+    lr = 0.05
+    Y = torch.empty(c.batch * 26, 16, device=dev)
+    hot_idx = ref["pack"]["hot_idx"]
+    for i in range(min(3, prep.packed["n_hot_batches"])):
+        idx, off, n_bags = pipe.batch_args(prep, i)
+        dY = gen.make_dy(n_bags, 16, seed=100 + i)
+        pipe.step(W_hot, prep, i, Y[:n_bags], dY.to(dev), lr)
+        bi = hot_idx[i * c.batch * 26:(i * c.batch * 26) + n_bags]
+        Yref, _ = oracle.emb_fwd(Wref, bi, None, 1, n_bags)
+        ok, worst = close(Y[:n_bags].cpu().numpy(), Yref)
+        assert ok, worst
+        Wref, _ = oracle.emb_bwd_sgd(Wref, bi, None, 1, n_bags, dY, lr)
+    pipe.ctx.check()
+    ok, worst = close(W_hot.cpu().numpy(), Wref)
+    assert ok, worst
