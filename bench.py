@@ -103,7 +103,20 @@ class Clocks:
 # algorithmic bytes
 # ----------------------------------------------------------------------------
 def fwd_bytes(L, S, D, explicit_off):
+    """a8 per batch: idx (4L) [+ offsets 8(S+1)] + row gathers 4DL + Y 4DS."""
     return 4 * L + (8 * (S + 1) if explicit_off else 0) + 4 * D * L + 4 * D * S
+
+
+def red_bytes(L, S, U, D):
+    """a9+a10 per batch with the grouping precomputed: sorted bag ids (4L),
+    piece/segment records (~16U + 12L/16), dY rows 4DL, W rows read+write 8DU."""
+    return 4 * L + 16 * U + 12 * (L / 16.0) + 4 * D * L + 8 * D * U
+
+
+def pipe_stats(pipe):
+    import paper_2103_00686_b200 as fae
+    gi = fae.fae_group_info(pipe.ctx)
+    return {"segs_per_batch": gi["segments"] / max(gi["n_batches"], 1), **gi}
 
 
 # ----------------------------------------------------------------------------
@@ -143,34 +156,19 @@ def run_fae(args):
     mode = fae.BUDGET_EXACT if cfg.budget_bytes else fae.FIXED_T
     state = {}
 
-    def one_step(timing=None):
+    def one_step():
         prep = pipe.preprocess(ds.idx, ds.off, R, x_pct=5.0, seed=args.seed, mode=mode,
                                t=cfg.t, budget_bytes=cfg.budget_bytes,
                                small_table_bytes=cfg.small_bytes, bufs=state.get("prep"))
         state["prep"] = prep
+        pipe.group(prep)
         W_hot = pipe.extract(W, prep)
         nb = prep.packed["n_hot_batches"]
         if dist is not None:
             t = torch.tensor([nb], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            nb_all = int(t)
-        else:
-            nb_all = nb
-        for i in range(nb_all):
-            if i < nb:
-                idx, off, n_bags = pipe.batch_args(prep, i)
-            else:
-                idx, off, n_bags = prep.hot_idx[:0], None, 0
-            if timing is not None:
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record()
-            fae.fae_emb_fwd(pipe.ctx, W_hot, idx, off, pipe.pool, n_bags, Y[:n_bags])
-            if timing is not None:
-                e1.record()
-                timing.append((e0, e1, idx.numel() if off is None else None, n_bags))
-            fae.fae_emb_bwd_update(pipe.ctx, W_hot, idx, off, pipe.pool, n_bags,
-                                   dY[i % n_dy, :n_bags], args.lr)
+            nb = int(t)
+        pipe.train(W_hot, 0, nb, dY, Y, args.lr)
         return prep.packed["n_hot_lookups"], prep
 
     for _ in range(args.warmup):
@@ -183,7 +181,7 @@ def run_fae(args):
     clocks = Clocks(local)
     clocks.start()
     l0 = pipe.ctx.launches
-    timing = []
+    fae.fae_set_kernel_timing(pipe.ctx, True)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     wall0 = time.perf_counter()
@@ -191,7 +189,7 @@ def run_fae(args):
     hot_lookups = 0
     prep = None
     for _ in range(args.steps):
-        n, prep = one_step(timing)
+        n, prep = one_step()
         hot_lookups += n
     t1.record()
     torch.cuda.synchronize()
@@ -200,12 +198,8 @@ def run_fae(args):
     pipe.ctx.check()
     ms = t0.elapsed_time(t1)
     launches = pipe.ctx.launches - l0
-    fwd_ms = [a.elapsed_time(b) for a, b, _, _ in timing]
-    # per-launch algorithmic bytes of the fwd kernel
-    fb = []
-    for (a, b, L, S) in timing:
-        Lx = L if L is not None else 0
-        fb.append(fwd_bytes(Lx, S, D, cfg.pool == 0))
+    kt = fae.fae_get_kernel_timing(pipe.ctx)
+    fae.fae_set_kernel_timing(pipe.ctx, False)
     tot = torch.tensor([ms, float(hot_lookups)], dtype=torch.float64, device=dev)
     if dist is not None:
         mx = tot.clone()
@@ -218,9 +212,19 @@ def run_fae(args):
     peak, kind = peaks()
     res = None
     if rank == 0:
-        avg_fwd_s = (sum(fwd_ms) / max(len(fwd_ms), 1)) / 1e3
-        avg_fwd_b = sum(fb) / max(len(fb), 1)
-        achieved = avg_fwd_b / avg_fwd_s / 1e9 if avg_fwd_s > 0 else 0.0
+        # dominant kernel of the step, timed live (event nodes in the graph)
+        kname = max(("fwd", "reduce"), key=lambda k: kt[k][0])
+        kms, kn = kt[kname]
+        avg_s = (kms / max(kn, 1)) / 1e3
+        L_b = prep.packed["n_hot_lookups"] / max(prep.packed["n_hot_batches"], 1)
+        S_b = prep.packed["n_hot"] * Tn / max(prep.packed["n_hot_batches"], 1)
+        gi = pipe_stats(pipe)
+        U_b = gi["segs_per_batch"]
+        if kname == "fwd":
+            kb = fwd_bytes(L_b, S_b, D, cfg.pool == 0)
+        else:
+            kb = red_bytes(L_b, S_b, U_b, D)
+        achieved = kb / avg_s / 1e9 if avg_s > 0 else 0.0
         res = {
             "metric": METRIC, "value": lookups_all / (ms_max / 1e3), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -234,18 +238,23 @@ def run_fae(args):
                        "x_pct": 5.0, "lr": args.lr,
                        "hot_rows": prep.thresh["H_total"], "hot_records": prep.packed["n_hot"],
                        "hot_batches_per_step": prep.packed["n_hot_batches"],
+                       "hot_lookups_per_step": prep.packed["n_hot_lookups"],
+                       "distinct_rows_per_batch": U_b,
                        "l2": "inputs > L2 (dataset %.1f GB, dY pool %d MB)" % (
                            ds.idx.numel() * 4 / 1e9, n_dy * dy_bytes >> 20),
                        "parallelism": f"dp{world}"},
             "gpu_launches": launches,
-            "roofline": {"kernel": "k_emb_fwd", "bound": "hbm", "achieved": achieved,
+            "roofline": {"kernel": {"fwd": "k_grp_fwd", "reduce": "k_grp_reduce"}[kname],
+                         "bound": "hbm", "achieved": achieved,
                          "peak": peak, "peak_kind": kind, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
-                         "bytes_per_launch": avg_fwd_b, "avg_launch_us": avg_fwd_s * 1e6},
+                         "bytes_per_launch": kb, "avg_launch_us": avg_s * 1e6,
+                         "kernels_us": {k: (kt[k][0] / max(kt[k][1], 1)) * 1e3 for k in kt},
+                         "launches_timed": kn},
             "clocks": ck,
             "wall_s": wall,
         }
-    return res, (pipe, ds, W, cfg, R, dist, rank, world, dev)
+    return res, (pipe, ds, W, cfg, R, dist, rank, world, dev, dY, Y)
 
 
 def run_e2e(args, ctxs):
@@ -254,16 +263,13 @@ def run_e2e(args, ctxs):
     host memory (the CPU master copy) and fae_extract pulls only the
     hot rows across PCIe; the trained hot table is read back each step."""
     import paper_2103_00686_b200 as fae
-    pipe, ds, W, cfg, R, dist, rank, world, dev = ctxs
+    pipe, ds, W, cfg, R, dist, rank, world, dev, dY, Y = ctxs
     idx_h = ds.idx.cpu().pin_memory()
     off_h = ds.off.cpu().pin_memory() if ds.off is not None else None
     W_h = W.cpu().pin_memory()
     D, B, Tn = cfg.dim, cfg.batch, cfg.n_tables
     idx_d = torch.empty_like(ds.idx)
     off_d = torch.empty_like(ds.off) if ds.off is not None else None
-    S_max = B * Tn
-    dY = gen.make_dy(S_max, D, device=dev)
-    Y = torch.empty(S_max, D, device=dev)
     mode = fae.BUDGET_EXACT if cfg.budget_bytes else fae.FIXED_T
     st = {}
 
@@ -275,12 +281,14 @@ def run_e2e(args, ctxs):
                                budget_bytes=cfg.budget_bytes, small_table_bytes=cfg.small_bytes,
                                bufs=st.get("prep"))
         st["prep"] = prep
+        pipe.group(prep)
         W_hot = pipe.extract(W_h, prep)
         nb = prep.packed["n_hot_batches"]
-        for i in range(nb):
-            idx, off, n_bags = pipe.batch_args(prep, i)
-            fae.fae_emb_fwd(pipe.ctx, W_hot, idx, off, pipe.pool, n_bags, Y[:n_bags])
-            fae.fae_emb_bwd_update(pipe.ctx, W_hot, idx, off, pipe.pool, n_bags, dY[:n_bags], args.lr)
+        if dist is not None:
+            t = torch.tensor([nb], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            nb = int(t)
+        pipe.train(W_hot, 0, nb, dY, Y, args.lr)
         out = W_hot.cpu()
         h2d = idx_h.numel() * 4 + (off_h.numel() * 8 if off_h is not None else 0) + W_hot.numel() * 4
         return prep.packed["n_hot_lookups"], h2d, out.numel() * 4

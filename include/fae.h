@@ -303,6 +303,57 @@ fae_status fae_emb_bwd_update(fae_ctx* ctx, float* W_hot, int64_t H,
 fae_status fae_sync_hot_grads(fae_ctx* ctx, int32_t* rows, float* vals,
                               int64_t* count_host, int64_t cap, int32_t D);
 
+/* --------------------------------------------------------------------------
+ * fae_group_batches — the backward's sort-and-segment (a9) for EVERY hot
+ * batch of a packed dataset, computed once.  The hot CSR is static for the
+ * whole run (the paper pre-processes once and stores the FAE format,
+ * P:L262, L496), so grouping each batch's lookups by hot id is hoisted out of
+ * the training step.  Per batch: a stable sort of (hot id, bag) and the
+ * run-length segments of equal hot id (split into pieces of <= 16 lookups).
+ * The grouping is kept in the ctx and refers to pk->hot_idx / pk->hot_off,
+ * which must stay valid and unchanged until the next fae_group_batches.
+ *  pk          the fae_packed filled by fae_classify (device hot_idx, hot_off;
+ *              host n_hot, n_hot_lookups).
+ *  fixed_pool  P of the input (0 = explicit offsets, hot_off used).
+ *  batch       B (records per hot batch).
+ *  H           rows of the hot table (hot ids must be < H).
+ * Errors: INVALID_ARG, CAPACITY (>= 2^31 hot lookups), INDEX_RANGE.
+ * ------------------------------------------------------------------------ */
+fae_status fae_group_batches(fae_ctx* ctx, const fae_tables* tabs,
+                             const fae_packed* pk, int32_t fixed_pool,
+                             int32_t batch, int64_t H);
+
+/* --------------------------------------------------------------------------
+ * fae_train_hot_batches — the hot mini-batch training loop over grouped
+ * batches [first, first + n): for each batch i in order,
+ *   Y = fwd(batch i)                                  (a8, as fae_emb_fwd)
+ *   W_hot[r] -= lr * sum_{p: idx[p]=r} dY_i[bag(p)]   (a9 + a10 [+ a11])
+ * with dY_i = dY + (i % n_dy) * (B*Tn) * D (device [n_dy][B*Tn][D]; the
+ * upstream gradient of each step, e.g. written by the MLP backward) and Y
+ * device [B*Tn][D] (overwritten every step).  Sequential SGD semantics:
+ * batch i+1 sees the rows batch i updated.  World 1: replays a captured
+ * CUDA graph of 2 kernels per step (no host work per step).  World > 1: the
+ * sparse gradient is exchanged every step (fae_sync_hot_grads semantics).
+ * H must equal the H given to fae_group_batches.
+ * ------------------------------------------------------------------------ */
+fae_status fae_train_hot_batches(fae_ctx* ctx, float* W_hot, int64_t H,
+                                 int32_t D, int64_t first, int64_t n,
+                                 const float* dY, int64_t n_dy, float* Y,
+                                 float lr);
+
+/* --------------------------------------------------------------------------
+ * Live kernel timing of fae_train_hot_batches (bench evidence): when enabled,
+ * the replayed graphs carry CUDA event nodes around each step's two kernels
+ * and the ctx accumulates their durations.  ms[0]/n[0]: forward kernel
+ * (k_grp_fwd), ms[1]/n[1]: segment-reduce + SGD kernel (k_grp_reduce).
+ * Enabling resets the totals.
+ * ------------------------------------------------------------------------ */
+fae_status fae_set_kernel_timing(fae_ctx* ctx, int32_t enable);
+/* Grouping summary: info[6] = {n_batches, hot lookups, pieces, segments
+ * (distinct hot rows summed over batches), max pieces, max bags per batch}. */
+fae_status fae_group_info(const fae_ctx* ctx, int64_t* info);
+fae_status fae_get_kernel_timing(const fae_ctx* ctx, double* ms, int64_t* n);
+
 #ifdef __cplusplus
 }
 #endif

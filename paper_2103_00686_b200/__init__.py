@@ -29,7 +29,8 @@ EXPORTS = ["fae_create", "fae_destroy", "fae_set_stream", "fae_last_error",
            "fae_check", "fae_get_nccl_id", "fae_comm_init",
            "fae_kernel_launches", "fae_profile", "fae_threshold",
            "fae_classify", "fae_extract", "fae_emb_fwd", "fae_emb_bwd_update",
-           "fae_sync_hot_grads"]
+           "fae_sync_hot_grads", "fae_group_batches", "fae_train_hot_batches",
+           "fae_set_kernel_timing", "fae_get_kernel_timing", "fae_group_info"]
 
 
 class FaeError(RuntimeError):
@@ -112,6 +113,13 @@ def lib():
             "fae_emb_bwd_update": ([P, P, c_i64, c_i32, P, P, c_i32, c_i64, P,
                                     ctypes.c_float], c_i32),
             "fae_sync_hot_grads": ([P, P, P, P, c_i64, c_i32], c_i32),
+            "fae_group_batches": ([P, ctypes.POINTER(FaeTables), ctypes.POINTER(FaePacked),
+                                   c_i32, c_i32, c_i64], c_i32),
+            "fae_train_hot_batches": ([P, P, c_i64, c_i32, c_i64, c_i64, P, c_i64, P,
+                                       ctypes.c_float], c_i32),
+            "fae_set_kernel_timing": ([P, c_i32], c_i32),
+            "fae_get_kernel_timing": ([P, P, P], c_i32),
+            "fae_group_info": ([P, P], c_i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -304,3 +312,45 @@ def fae_sync_hot_grads(ctx: Ctx, rows: torch.Tensor, vals: torch.Tensor,
     ctx._ok(lib().fae_sync_hot_grads(ctx.h, _p(rows), _p(vals), ctypes.byref(cnt),
                                      int(rows.numel()), int(vals.shape[1])))
     return int(cnt.value)
+
+
+def fae_group_batches(ctx: Ctx, rows, dim: int, hot_idx: torch.Tensor,
+                      hot_off: Optional[torch.Tensor], n_hot: int,
+                      n_hot_lookups: int, fixed_pool: int, batch: int, H: int):
+    """a9's sort-and-segment for every hot batch, once (kept in the ctx;
+    hot_idx / hot_off must stay alive and unchanged)."""
+    tabs, keep = _tables(rows, dim)
+    pk = FaePacked(_p(hot_idx), None, _p(hot_idx), _p(hot_off), int(n_hot), 0,
+                   int(n_hot_lookups), 0, 0)
+    ctx._ok(lib().fae_group_batches(ctx.h, ctypes.byref(tabs), ctypes.byref(pk),
+                                    int(fixed_pool), int(batch), int(H)))
+    del keep
+
+
+def fae_train_hot_batches(ctx: Ctx, W_hot: torch.Tensor, first: int, n: int,
+                          dY: torch.Tensor, Y: torch.Tensor, lr: float):
+    """a8-a10 (+a11) over grouped hot batches [first, first+n); dY is
+    [n_dy, B*Tn, D] (batch i uses dY[i % n_dy]), Y is [B*Tn, D]."""
+    n_dy = int(dY.shape[0]) if dY.dim() == 3 else 1
+    ctx._ok(lib().fae_train_hot_batches(ctx.h, _p(W_hot), int(W_hot.shape[0]),
+                                        int(W_hot.shape[1]), int(first), int(n),
+                                        _p(dY), n_dy, _p(Y), ctypes.c_float(lr)))
+
+
+def fae_set_kernel_timing(ctx: Ctx, enable: bool):
+    ctx._ok(lib().fae_set_kernel_timing(ctx.h, int(bool(enable))))
+
+
+def fae_get_kernel_timing(ctx: Ctx) -> dict:
+    """{'fwd': (total_ms, launches), 'reduce': (total_ms, launches)}."""
+    ms = (c_dbl * 2)()
+    n = (c_i64 * 2)()
+    ctx._ok(lib().fae_get_kernel_timing(ctx.h, ctypes.cast(ms, c_ptr), ctypes.cast(n, c_ptr)))
+    return {"fwd": (ms[0], n[0]), "reduce": (ms[1], n[1])}
+
+
+def fae_group_info(ctx: Ctx) -> dict:
+    info = (c_i64 * 6)()
+    ctx._ok(lib().fae_group_info(ctx.h, ctypes.cast(info, c_ptr)))
+    keys = ("n_batches", "lookups", "pieces", "segments", "max_pieces", "max_bags")
+    return dict(zip(keys, [int(v) for v in info]))

@@ -73,6 +73,48 @@ struct HotSet {
     int64_t* d_rowbase = nullptr;               // device [n_tables + 1]
 };
 
+// Grouping of a packed dataset's hot batches (fae_group_batches): the
+// backward's sort-and-segment result per batch, computed once.
+struct BatchDesc {
+    int64_t lk0, lk1;      // lookups [lk0, lk1) of hot_idx (global positions)
+    int64_t bag0;          // global bag index of the batch's first bag
+    int64_t pb0, pb1;      // pieces [pb0, pb1)
+    int64_t sb0, sb1;      // segments [sb0, sb1)
+    int32_t n_bags, pad;
+};
+
+struct Group {
+    bool valid = false;
+    int64_t n_batches = 0, L_total = 0, P_total = 0, S_total = 0;
+    int32_t Tn = 0, P = 0, B = 0;
+    int64_t H = 0;
+    int64_t max_bags = 0, max_lookups = 0, max_pieces = 0, max_segs = 0;
+    const int32_t* hot_idx = nullptr;
+    const int64_t* hot_off = nullptr;
+    int32_t* perm = nullptr;          // [L_total] local bag index, grouped by hot id
+    int64_t* piece_start = nullptr;   // [P_total + 1] global positions
+    int32_t* piece_seg = nullptr;     // [P_total]
+    int32_t* seg_first = nullptr;     // [S_total + 1]
+    int32_t* seg_row = nullptr;       // [S_total]
+    uint32_t* seg_cnt = nullptr;      // [S_total], kept zero
+    BatchDesc* desc = nullptr;        // device [n_batches]
+    std::vector<BatchDesc> hdesc;     // host copy
+    int64_t cap_L = 0, cap_P = 0, cap_S = 0, cap_B = 0;
+    // epoch runner
+    int64_t* cursor = nullptr;        // device: batches done in this run
+    int64_t* run = nullptr;           // device: [0] first batch, [1] n batches
+    uint32_t* done_ctr = nullptr;     // device: finished CTAs of the reduce
+    float* partial = nullptr;         // [max_pieces][max_dim]
+    cudaGraphExec_t graph = nullptr;
+    int graph_steps = 0;
+    uint64_t graph_key = 0;
+    // timed variant: 2 graph instances, each with 3 events per step
+    // (before fwd, between fwd and reduce, after reduce)
+    cudaGraphExec_t tgraph[2] = {nullptr, nullptr};
+    cudaEvent_t tev[2][3 * 64] = {};
+    uint64_t tgraph_key = 0;
+};
+
 struct Ctx {
     fae_config cfg{};
     int device = 0;
@@ -95,6 +137,11 @@ struct Ctx {
     float* g_vals = nullptr;                    // [max_world * cap_L * max_dim]
     int32_t* g_counts = nullptr;                // [max_world]
     int64_t g_cap = 0;
+    Group grp;
+    // kernel timing (fae_set_kernel_timing): accumulated over timed calls
+    bool timing = false;
+    double t_ms[2] = {0.0, 0.0};      // [0] fwd kernel, [1] reduce kernel
+    int64_t t_n[2] = {0, 0};
 };
 
 // ---------------------------------------------------------------------------

@@ -1,0 +1,227 @@
+// kern_common.cuh — device bodies shared by the standalone step calls
+// (step.cu) and the graph-replayed epoch runner (epoch.cu).
+#pragma once
+
+#include "fae_internal.cuh"
+
+namespace fae {
+
+// a8: Y[b] = sum_{p in bag b} W[idx[p]] for bags [0, n_bags) (grid-stride over
+// bags, LPB lanes per bag, NV float4 per lane, 4 rows in flight per lane).
+template <int LPB, int NV>
+__device__ __forceinline__ void fwd_bags(const float* __restrict__ W, int64_t H, int D,
+                                         const int32_t* __restrict__ idx,
+                                         const int64_t* __restrict__ off, int P, int64_t n_bags,
+                                         float* __restrict__ Y, uint32_t* err) {
+    const int lane = threadIdx.x % LPB;
+    const int64_t gpb = blockDim.x / LPB;
+    const int64_t stride = (int64_t)gridDim.x * gpb;
+    for (int64_t b = blockIdx.x * gpb + threadIdx.x / LPB; b < n_bags; b += stride) {
+        int64_t lo, hi;
+        if (off) {
+            lo = off[b];
+            hi = off[b + 1];
+        } else {
+            lo = b * P;
+            hi = lo + P;
+        }
+        float4 acc[NV];
+#pragma unroll
+        for (int k = 0; k < NV; k++) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        int64_t p = lo;
+        for (; p + 4 <= hi; p += 4) {
+            int32_t r[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                r[u] = __ldg(idx + p + u);
+                if ((uint32_t)r[u] >= (uint64_t)H) {
+                    atomicOr(err, kErrIndex);
+                    r[u] = -1;
+                }
+            }
+            float4 v[4][NV];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const float4* row = reinterpret_cast<const float4*>(W + (int64_t)(r[u] < 0 ? 0 : r[u]) * D) + lane;
+#pragma unroll
+                for (int k = 0; k < NV; k++)
+                    v[u][k] = r[u] < 0 ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldg(row + k * LPB);
+            }
+#pragma unroll
+            for (int k = 0; k < NV; k++) {
+                acc[k].x += (v[0][k].x + v[1][k].x) + (v[2][k].x + v[3][k].x);
+                acc[k].y += (v[0][k].y + v[1][k].y) + (v[2][k].y + v[3][k].y);
+                acc[k].z += (v[0][k].z + v[1][k].z) + (v[2][k].z + v[3][k].z);
+                acc[k].w += (v[0][k].w + v[1][k].w) + (v[2][k].w + v[3][k].w);
+            }
+        }
+        for (; p < hi; ++p) {
+            const int32_t r = __ldg(idx + p);
+            if ((uint32_t)r >= (uint64_t)H) {
+                atomicOr(err, kErrIndex);
+                continue;
+            }
+            const float4* row = reinterpret_cast<const float4*>(W + (int64_t)r * D) + lane;
+#pragma unroll
+            for (int k = 0; k < NV; k++) {
+                const float4 v = __ldg(row + k * LPB);
+                acc[k].x += v.x;
+                acc[k].y += v.y;
+                acc[k].z += v.z;
+                acc[k].w += v.w;
+            }
+        }
+        float4* y = reinterpret_cast<float4*>(Y + b * D) + lane;
+#pragma unroll
+        for (int k = 0; k < NV; k++) __stcs(y + k * LPB, acc[k]);
+    }
+}
+
+// a10 (or emit for a11): apply W[row] -= lr * G, or write G to grad_out.
+template <int LPB, int NV>
+__device__ __forceinline__ void finish_segment(int64_t s, int64_t s_out, const float4 (&g)[NV],
+                                               int lane, const int32_t* __restrict__ seg_row,
+                                               float* W, int D, float lr, bool emit,
+                                               float* grad_out, uint32_t* err) {
+    if (emit) {
+        float4* o = reinterpret_cast<float4*>(grad_out + s_out * D) + lane;
+#pragma unroll
+        for (int k = 0; k < NV; k++) o[k * LPB] = g[k];
+        return;
+    }
+    const int32_t row = seg_row[s];
+    float4* w = reinterpret_cast<float4*>(W + (int64_t)row * D) + lane;
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < NV; k++) {
+        float4 x = w[k * LPB];
+        x.x = __fmaf_rn(-lr, g[k].x, x.x);
+        x.y = __fmaf_rn(-lr, g[k].y, x.y);
+        x.z = __fmaf_rn(-lr, g[k].z, x.z);
+        x.w = __fmaf_rn(-lr, g[k].w, x.w);
+        bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
+        w[k * LPB] = x;
+    }
+    if (bad) atomicOr(err, kErrNonfinite);
+}
+
+__device__ __forceinline__ void add4(float4& a, const float4& b) {
+    a.x += b.x;
+    a.y += b.y;
+    a.z += b.z;
+    a.w += b.w;
+}
+
+// a9 + a10 over pieces [p_begin, p_end): each LPB-lane group sums the src rows
+// vals[i] for positions i in [piece_start[pi], piece_start[pi+1]) in order.
+// Single-piece segments finish directly; multi-piece segments publish their
+// partial (partial[pi - p_begin]) and the last arriver of the segment sums the
+// partials in piece order (blocks of 16), so the summation order is fixed.
+template <int LPB, int NV, typename PosT>
+__device__ __forceinline__ void reduce_pieces(
+    int64_t p_begin, int64_t p_end, int64_t s_out_base, int64_t /*unused*/,
+    const int32_t* __restrict__ vals, const PosT* __restrict__ piece_start,
+    const int32_t* __restrict__ piece_seg, const int32_t* __restrict__ seg_first,
+    const int32_t* __restrict__ seg_row, const float* __restrict__ src, int D, float* W,
+    float lr, float* partial, uint32_t* seg_cnt, int emit, float* grad_out, uint32_t* err) {
+    const int lane = threadIdx.x % LPB;
+    const int gw = (threadIdx.x & 31) / LPB;
+    const uint32_t gmask = (LPB == 32) ? 0xffffffffu : (((1u << LPB) - 1u) << (gw * LPB));
+    const int leader = (threadIdx.x & 31) & ~(LPB - 1);
+    const int64_t gpb = blockDim.x / LPB;
+    const int64_t stride = (int64_t)gridDim.x * gpb;
+    for (int64_t pi = p_begin + blockIdx.x * gpb + threadIdx.x / LPB; pi < p_end; pi += stride) {
+        const int64_t i0 = piece_start[pi], i1 = piece_start[pi + 1];
+        const int64_t s = piece_seg[pi];
+        const int64_t f0 = seg_first[s], f1 = seg_first[s + 1];
+        float4 g[NV];
+#pragma unroll
+        for (int k = 0; k < NV; k++) g[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        int64_t i = i0;
+        for (; i + 4 <= i1; i += 4) {
+            float4 v[4][NV];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const float4* row = reinterpret_cast<const float4*>(src + (int64_t)__ldg(vals + i + u) * D) + lane;
+#pragma unroll
+                for (int k = 0; k < NV; k++) v[u][k] = __ldg(row + k * LPB);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+#pragma unroll
+                for (int k = 0; k < NV; k++) add4(g[k], v[u][k]);
+        }
+        for (; i < i1; i++) {
+            const float4* row = reinterpret_cast<const float4*>(src + (int64_t)__ldg(vals + i) * D) + lane;
+#pragma unroll
+            for (int k = 0; k < NV; k++) add4(g[k], __ldg(row + k * LPB));
+        }
+        if (f1 - f0 == 1) {
+            finish_segment<LPB, NV>(s, s - s_out_base, g, lane, seg_row, W, D, lr, emit, grad_out, err);
+            continue;
+        }
+        float4* pp = reinterpret_cast<float4*>(partial + (pi - p_begin) * D) + lane;
+#pragma unroll
+        for (int k = 0; k < NV; k++) __stcg(pp + k * LPB, g[k]);
+        __threadfence();
+        __syncwarp(gmask);
+        uint32_t old = 0;
+        if ((threadIdx.x & 31) == leader) old = atomicAdd(&seg_cnt[s], 1u);
+        old = __shfl_sync(gmask, old, leader);
+        if (old != (uint32_t)(f1 - f0 - 1)) continue;
+        __threadfence();
+        float4 tot[NV];
+#pragma unroll
+        for (int k = 0; k < NV; k++) tot[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int64_t q0 = f0; q0 < f1; q0 += 16) {
+            float4 blk[NV];
+#pragma unroll
+            for (int k = 0; k < NV; k++) blk[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            const int64_t q1 = q0 + 16 < f1 ? q0 + 16 : f1;
+            for (int64_t q = q0; q < q1; q++) {
+                const float4* rp = reinterpret_cast<const float4*>(partial + (q - p_begin) * D) + lane;
+#pragma unroll
+                for (int k = 0; k < NV; k++) add4(blk[k], __ldcg(rp + k * LPB));
+            }
+#pragma unroll
+            for (int k = 0; k < NV; k++) add4(tot[k], blk[k]);
+        }
+        finish_segment<LPB, NV>(s, s - s_out_base, tot, lane, seg_row, W, D, lr, emit, grad_out, err);
+        if ((threadIdx.x & 31) == leader) seg_cnt[s] = 0u;
+    }
+}
+
+#define FAE_DISPATCH_D(D, FN, ...)                                             \
+    do {                                                                       \
+        switch ((D) / 4) {                                                     \
+            case 1: FN<1, 1>(__VA_ARGS__); break;                              \
+            case 2: FN<2, 1>(__VA_ARGS__); break;                              \
+            case 4: FN<4, 1>(__VA_ARGS__); break;                              \
+            case 8: FN<8, 1>(__VA_ARGS__); break;                              \
+            case 16: FN<16, 1>(__VA_ARGS__); break;                            \
+            case 32: FN<32, 1>(__VA_ARGS__); break;                            \
+            case 64: FN<32, 2>(__VA_ARGS__); break;                            \
+            case 96: FN<32, 3>(__VA_ARGS__); break;                            \
+            case 128: FN<32, 4>(__VA_ARGS__); break;                           \
+            default: return set_err(c, FAE_ERR_INVALID_ARG, "unsupported dim"); \
+        }                                                                      \
+    } while (0)
+
+inline bool dim_ok(int D) {
+    if (D < 4 || D % 4) return false;
+    const int q = D / 4;
+    if (q <= 32) return (q & (q - 1)) == 0;
+    return q % 32 == 0 && q <= 128;
+}
+
+inline int sm_count(Ctx* c) {
+    static int cached[64] = {0};
+    const int d = c->device;
+    if (d >= 0 && d < 64 && cached[d]) return cached[d];
+    int n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+    if (d >= 0 && d < 64) cached[d] = n;
+    return n;
+}
+
+}  // namespace fae

@@ -20,7 +20,7 @@
 //                 identical on every rank.
 #include <algorithm>
 
-#include "fae_internal.cuh"
+#include "kern_common.cuh"
 
 namespace fae {
 
@@ -32,69 +32,7 @@ __global__ void __launch_bounds__(256)
 k_emb_fwd(const float* __restrict__ W, int64_t H, int D,
           const int32_t* __restrict__ idx, const int64_t* __restrict__ off,
           int P, int64_t n_bags, float* __restrict__ Y, uint32_t* err) {
-    const int lane = threadIdx.x % LPB;
-    const int64_t gpb = blockDim.x / LPB;
-    const int64_t stride = (int64_t)gridDim.x * gpb;
-    for (int64_t b = blockIdx.x * gpb + threadIdx.x / LPB; b < n_bags; b += stride) {
-        int64_t lo, hi;
-        if (off) {
-            lo = off[b];
-            hi = off[b + 1];
-        } else {
-            lo = b * P;
-            hi = lo + P;
-        }
-        float4 acc[NV];
-#pragma unroll
-        for (int k = 0; k < NV; k++) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        int64_t p = lo;
-        for (; p + 4 <= hi; p += 4) {
-            int32_t r[4];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                r[u] = __ldg(idx + p + u);
-                if ((uint32_t)r[u] >= (uint64_t)H) {
-                    atomicOr(err, kErrIndex);
-                    r[u] = -1;
-                }
-            }
-            float4 v[4][NV];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const float4* row = reinterpret_cast<const float4*>(W + (int64_t)(r[u] < 0 ? 0 : r[u]) * D) + lane;
-#pragma unroll
-                for (int k = 0; k < NV; k++) {
-                    v[u][k] = r[u] < 0 ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldg(row + k * LPB);
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < NV; k++) {
-                acc[k].x += (v[0][k].x + v[1][k].x) + (v[2][k].x + v[3][k].x);
-                acc[k].y += (v[0][k].y + v[1][k].y) + (v[2][k].y + v[3][k].y);
-                acc[k].z += (v[0][k].z + v[1][k].z) + (v[2][k].z + v[3][k].z);
-                acc[k].w += (v[0][k].w + v[1][k].w) + (v[2][k].w + v[3][k].w);
-            }
-        }
-        for (; p < hi; ++p) {
-            int32_t r = __ldg(idx + p);
-            if ((uint32_t)r >= (uint64_t)H) {
-                atomicOr(err, kErrIndex);
-                continue;
-            }
-            const float4* row = reinterpret_cast<const float4*>(W + (int64_t)r * D) + lane;
-#pragma unroll
-            for (int k = 0; k < NV; k++) {
-                float4 v = __ldg(row + k * LPB);
-                acc[k].x += v.x;
-                acc[k].y += v.y;
-                acc[k].z += v.z;
-                acc[k].w += v.w;
-            }
-        }
-        float4* y = reinterpret_cast<float4*>(Y + b * D) + lane;
-#pragma unroll
-        for (int k = 0; k < NV; k++) __stcs(y + k * LPB, acc[k]);
-    }
+    fwd_bags<LPB, NV>(W, H, D, idx, off, P, n_bags, Y, err);
 }
 
 // ---------------------------------------------------------------------------
@@ -377,151 +315,19 @@ k_pieces(const uint32_t* __restrict__ keys, int64_t* __restrict__ scalars,
 // segment reduce + SGD (or emit)
 // ---------------------------------------------------------------------------
 template <int LPB, int NV>
-__device__ __forceinline__ void finish_segment(int32_t s, const float4 (&g)[NV], int lane,
-                                               const int32_t* __restrict__ seg_row, float* W,
-                                               int D, float lr, bool emit, float* grad_out,
-                                               uint32_t* err) {
-    if (emit) {
-        float4* o = reinterpret_cast<float4*>(grad_out + (int64_t)s * D) + lane;
-#pragma unroll
-        for (int k = 0; k < NV; k++) o[k * LPB] = g[k];
-        return;
-    }
-    const int32_t row = seg_row[s];
-    float4* w = reinterpret_cast<float4*>(W + (int64_t)row * D) + lane;
-    bool bad = false;
-#pragma unroll
-    for (int k = 0; k < NV; k++) {
-        float4 x = w[k * LPB];
-        x.x = __fmaf_rn(-lr, g[k].x, x.x);
-        x.y = __fmaf_rn(-lr, g[k].y, x.y);
-        x.z = __fmaf_rn(-lr, g[k].z, x.z);
-        x.w = __fmaf_rn(-lr, g[k].w, x.w);
-        bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
-        w[k * LPB] = x;
-    }
-    if (bad) atomicOr(err, kErrNonfinite);
-}
-
-template <int LPB, int NV>
 __global__ void __launch_bounds__(256)
 k_seg_reduce(const int32_t* __restrict__ vals, const int64_t* __restrict__ scalars,
              const int32_t* __restrict__ piece_start, const int32_t* __restrict__ piece_seg,
              const int32_t* __restrict__ seg_first, const int32_t* __restrict__ seg_row,
              const float* __restrict__ src, int D, float* W, float lr, float* partial,
              uint32_t* seg_cnt, int emit, float* grad_out, uint32_t* err) {
-    const int lane = threadIdx.x % LPB;
-    const int gw = (threadIdx.x & 31) / LPB;  // group index in warp
-    const uint32_t gmask = (LPB == 32) ? 0xffffffffu : (((1u << LPB) - 1u) << (gw * LPB));
-    const int leader = (threadIdx.x & 31) & ~(LPB - 1);
-    const int64_t gpb = blockDim.x / LPB;
-    const int64_t stride = (int64_t)gridDim.x * gpb;
-    const int64_t n_pieces = scalars[1];
-    for (int64_t pi = blockIdx.x * gpb + threadIdx.x / LPB; pi < n_pieces; pi += stride) {
-        const int32_t i0 = piece_start[pi], i1 = piece_start[pi + 1];
-        const int32_t s = piece_seg[pi];
-        const int32_t f0 = seg_first[s], f1 = seg_first[s + 1];
-        float4 g[NV];
-#pragma unroll
-        for (int k = 0; k < NV; k++) g[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        int32_t i = i0;
-        for (; i + 4 <= i1; i += 4) {
-            float4 v[4][NV];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const float4* row = reinterpret_cast<const float4*>(src + (int64_t)__ldg(vals + i + u) * D) + lane;
-#pragma unroll
-                for (int k = 0; k < NV; k++) v[u][k] = __ldg(row + k * LPB);
-            }
-#pragma unroll
-            for (int u = 0; u < 4; u++)
-#pragma unroll
-                for (int k = 0; k < NV; k++) {
-                    g[k].x += v[u][k].x;
-                    g[k].y += v[u][k].y;
-                    g[k].z += v[u][k].z;
-                    g[k].w += v[u][k].w;
-                }
-        }
-        for (; i < i1; i++) {
-            const float4* row = reinterpret_cast<const float4*>(src + (int64_t)__ldg(vals + i) * D) + lane;
-#pragma unroll
-            for (int k = 0; k < NV; k++) {
-                const float4 v = __ldg(row + k * LPB);
-                g[k].x += v.x;
-                g[k].y += v.y;
-                g[k].z += v.z;
-                g[k].w += v.w;
-            }
-        }
-        if (f1 - f0 == 1) {
-            finish_segment<LPB, NV>(s, g, lane, seg_row, W, D, lr, emit, grad_out, err);
-            continue;
-        }
-        // multi-piece segment: publish partial, last arriver combines in order
-        float4* pp = reinterpret_cast<float4*>(partial + pi * D) + lane;
-#pragma unroll
-        for (int k = 0; k < NV; k++) __stcg(pp + k * LPB, g[k]);
-        __threadfence();
-        __syncwarp(gmask);
-        uint32_t old = 0;
-        if ((threadIdx.x & 31) == leader) old = atomicAdd(&seg_cnt[s], 1u);
-        old = __shfl_sync(gmask, old, leader);
-        if (old != (uint32_t)(f1 - f0 - 1)) continue;
-        __threadfence();
-        float4 tot[NV];
-#pragma unroll
-        for (int k = 0; k < NV; k++) tot[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        // blocked sum: groups of 16 partials summed sequentially, then added
-        for (int32_t q0 = f0; q0 < f1; q0 += 16) {
-            float4 blk[NV];
-#pragma unroll
-            for (int k = 0; k < NV; k++) blk[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-            const int32_t q1 = min(f1, q0 + 16);
-            for (int32_t q = q0; q < q1; q++) {
-                const float4* rp = reinterpret_cast<const float4*>(partial + (int64_t)q * D) + lane;
-#pragma unroll
-                for (int k = 0; k < NV; k++) {
-                    const float4 v = __ldcg(rp + k * LPB);
-                    blk[k].x += v.x;
-                    blk[k].y += v.y;
-                    blk[k].z += v.z;
-                    blk[k].w += v.w;
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < NV; k++) {
-                tot[k].x += blk[k].x;
-                tot[k].y += blk[k].y;
-                tot[k].z += blk[k].z;
-                tot[k].w += blk[k].w;
-            }
-        }
-        finish_segment<LPB, NV>(s, tot, lane, seg_row, W, D, lr, emit, grad_out, err);
-        if ((threadIdx.x & 31) == leader) seg_cnt[s] = 0u;
-    }
+    reduce_pieces<LPB, NV, int32_t>(0, scalars[1], 0, 0, vals, piece_start, piece_seg, seg_first,
+                                    seg_row, src, D, W, lr, partial, seg_cnt, emit, grad_out, err);
 }
 
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-static int sm_count(Ctx* c) {
-    static int cached[64] = {0};
-    int d = c->device;
-    if (d >= 0 && d < 64 && cached[d]) return cached[d];
-    int n = 148;
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
-    if (d >= 0 && d < 64) cached[d] = n;
-    return n;
-}
-
-static bool dim_ok(int D) {
-    if (D < 4 || D % 4) return false;
-    const int q = D / 4;
-    if (q <= 32) return (q & (q - 1)) == 0;
-    return q % 32 == 0;
-}
-
 template <int LPB, int NV>
 static void launch_fwd(Ctx* c, const float* W, int64_t H, int D, const int32_t* idx,
                        const int64_t* off, int P, int64_t n_bags, float* Y) {
@@ -533,22 +339,6 @@ static void launch_fwd(Ctx* c, const float* W, int64_t H, int D, const int32_t* 
     if (blocks < 1) blocks = 1;
     k_emb_fwd<LPB, NV><<<(unsigned)blocks, threads, 0, c->stream>>>(W, H, D, idx, off, P, n_bags, Y, c->d_err);
 }
-
-#define FAE_DISPATCH_D(D, FN, ...)                                             \
-    do {                                                                       \
-        switch ((D) / 4) {                                                     \
-            case 1: FN<1, 1>(__VA_ARGS__); break;                              \
-            case 2: FN<2, 1>(__VA_ARGS__); break;                              \
-            case 4: FN<4, 1>(__VA_ARGS__); break;                              \
-            case 8: FN<8, 1>(__VA_ARGS__); break;                              \
-            case 16: FN<16, 1>(__VA_ARGS__); break;                            \
-            case 32: FN<32, 1>(__VA_ARGS__); break;                            \
-            case 64: FN<32, 2>(__VA_ARGS__); break;                            \
-            case 96: FN<32, 3>(__VA_ARGS__); break;                            \
-            case 128: FN<32, 4>(__VA_ARGS__); break;                           \
-            default: return set_err(c, FAE_ERR_INVALID_ARG, "unsupported dim"); \
-        }                                                                      \
-    } while (0)
 
 template <int LPB, int NV>
 static void launch_reduce(Ctx* c, int64_t n_items_hint, const float* src, int D, float* W,
@@ -634,7 +424,7 @@ fae_status bwd_group_and_reduce(Ctx* c, float* W_hot, int64_t H, int32_t D,
 static fae_status validate_step(Ctx* c, const float* W, int64_t H, int32_t D, const int32_t* idx,
                                 const int64_t* off, int32_t P, int64_t n_bags, const float* X,
                                 const char* who) {
-    if (!W || ((!X || !idx) && n_bags > 0)) return set_err(c, FAE_ERR_INVALID_ARG, std::string(who) + ": null pointer");
+    if ((!W || !X || !idx) && n_bags > 0) return set_err(c, FAE_ERR_INVALID_ARG, std::string(who) + ": null pointer");
     if (H < 0 || H >= (1ll << 31) - 1) return set_err(c, FAE_ERR_INVALID_ARG, std::string(who) + ": H out of range");
     if (!dim_ok(D) || D > c->cfg.max_dim) return set_err(c, FAE_ERR_INVALID_ARG, std::string(who) + ": unsupported dim");
     if (n_bags < 0 || (!off && P < 0)) return set_err(c, FAE_ERR_INVALID_ARG, std::string(who) + ": bad sizes");

@@ -19,8 +19,8 @@ from typing import List, Optional
 import torch
 
 from . import (BUDGET_EXACT, FIXED_T, Ctx, fae_classify, fae_create,
-               fae_emb_bwd_update, fae_emb_fwd, fae_extract, fae_profile,
-               fae_threshold)
+               fae_emb_bwd_update, fae_emb_fwd, fae_extract, fae_group_batches,
+               fae_profile, fae_threshold, fae_train_hot_batches)
 
 
 @dataclasses.dataclass
@@ -102,6 +102,17 @@ class FaePipeline:
             P = self.pool
             return prep.hot_idx[r0 * Tn * P: r1 * Tn * P], None, n_bags
         return prep.hot_idx, prep.hot_off[r0 * Tn: r1 * Tn + 1], n_bags
+
+    def group(self, prep: Prepared):
+        """Sort-and-segment of every hot batch, once (fae_group_batches)."""
+        pk = prep.packed
+        fae_group_batches(self.ctx, self.rows, self.dim, prep.hot_idx, prep.hot_off,
+                          pk["n_hot"], pk["n_hot_lookups"], self.pool, self.batch,
+                          prep.thresh["H_total"])
+
+    def train(self, W_hot, first: int, n: int, dY, Y, lr: float):
+        """Hot batches [first, first+n) through the graph-replayed loop."""
+        fae_train_hot_batches(self.ctx, W_hot, first, n, dY, Y, lr)
 
     def step(self, W_hot, prep: Prepared, i: int, Y, dY, lr: float):
         idx, off, n_bags = self.batch_args(prep, i)

@@ -339,3 +339,54 @@ def test_pipeline_end_to_end_kaggle(dev):
     pipe.ctx.check()
     ok, worst = close(W_hot.cpu().numpy(), Wref)
     assert ok, worst
+
+
+@pytest.mark.parametrize("cfg,R,t,small", [("kaggle", 100_000, 1e-6, 1 << 20),
+                                           ("alibaba", 20_000, 1e-5, 1 << 20),
+                                           ("tiny", 10_000, 1e-2, 0)])
+def test_grouped_training(dev, cfg, R, t, small):
+    """fae_group_batches + fae_train_hot_batches (graph replay, device cursor)
+    == the standalone per-step calls bit for bit, and == the oracle's
+    sequential SGD within tolerance; includes the ragged last batch."""
+    from paper_2103_00686_b200.pipeline import FaePipeline
+    c = gen.CONFIGS[cfg]
+    ds = gen.make_dataset(c, n_records=R, seed=5)
+    dd = ds.to(dev)
+    pipe = FaePipeline(ds.rows, c.dim, c.batch, c.pool, max_pool=max(c.pool_hi, 1))
+    prep = pipe.preprocess(dd.idx, dd.off, R, x_pct=5.0, seed=2, t=t, small_table_bytes=small)
+    W = gen.make_weights(sum(ds.rows), c.dim)
+    W_hot = pipe.extract(W.to(dev), prep).clone()
+    W_std = W_hot.clone()
+    nbt = prep.packed["n_hot_batches"]
+    nb = min(5, nbt)
+    first = nbt - nb
+    S = c.batch * c.n_tables
+    dY = gen.make_dy(nb * S, c.dim, seed=9).view(nb, S, c.dim).to(dev)
+    lr = 0.05
+    pipe.group(prep)
+    Y = torch.zeros(S, c.dim, device=dev)
+    pipe.train(W_hot, first, nb, dY, Y, lr)
+    pipe.ctx.check()
+    Y2 = torch.zeros(S, c.dim, device=dev)
+    for i in range(nb):
+        _, _, n_bags = pipe.batch_args(prep, first + i)
+        pipe.step(W_std, prep, first + i, Y2[:n_bags], dY[i, :n_bags], lr)
+    pipe.ctx.check()
+    assert torch.equal(W_hot, W_std)
+    assert torch.equal(Y, Y2)
+    # oracle: sequential SGD over the same batches
+    ref = _prep_ref(ds, 5.0, 2, "t", t=t, small=small)
+    Wr = oracle.extract(W, ref["remap"], ref["H"])
+    pk = ref["pack"]
+    Tn = c.n_tables
+    for i in range(nb):
+        b = first + i
+        r0, r1 = b * c.batch, min((b + 1) * c.batch, pk["n_hot"])
+        n_bags = (r1 - r0) * Tn
+        if ds.off is None:
+            bi, off, P = pk["hot_idx"][r0 * Tn * c.pool: r1 * Tn * c.pool], None, c.pool
+        else:
+            bi, off, P = pk["hot_idx"], pk["hot_off"][r0 * Tn: r1 * Tn + 1], 0
+        Wr, _ = oracle.emb_bwd_sgd(Wr, bi, off, P, n_bags, dY[i, :n_bags].cpu(), lr)
+    ok, worst = close(W_hot.cpu().numpy(), Wr)
+    assert ok, worst
