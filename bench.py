@@ -156,19 +156,32 @@ def run_fae(args):
     mode = fae.BUDGET_EXACT if cfg.budget_bytes else fae.FIXED_T
     state = {}
 
+    phases = {}
+
+    def mark(name, t0):
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        phases[name] = phases.get(name, 0.0) + (t1 - t0) * 1e3
+        return t1
+
     def one_step():
+        t = time.perf_counter()
         prep = pipe.preprocess(ds.idx, ds.off, R, x_pct=5.0, seed=args.seed, mode=mode,
                                t=cfg.t, budget_bytes=cfg.budget_bytes,
                                small_table_bytes=cfg.small_bytes, bufs=state.get("prep"))
         state["prep"] = prep
+        t = mark("profile_threshold_classify", t)
         pipe.group(prep)
+        t = mark("group", t)
         W_hot = pipe.extract(W, prep)
+        t = mark("extract", t)
         nb = prep.packed["n_hot_batches"]
         if dist is not None:
-            t = torch.tensor([nb], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            nb = int(t)
+            tt = torch.tensor([nb], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            nb = int(tt)
         pipe.train(W_hot, 0, nb, dY, Y, args.lr)
+        mark("train", t)
         return prep.packed["n_hot_lookups"], prep
 
     for _ in range(args.warmup):
@@ -181,7 +194,8 @@ def run_fae(args):
     clocks = Clocks(local)
     clocks.start()
     l0 = pipe.ctx.launches
-    fae.fae_set_kernel_timing(pipe.ctx, True)
+    phases.clear()
+    fae.fae_set_kernel_timing(pipe.ctx, 1)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     wall0 = time.perf_counter()
@@ -199,7 +213,7 @@ def run_fae(args):
     ms = t0.elapsed_time(t1)
     launches = pipe.ctx.launches - l0
     kt = fae.fae_get_kernel_timing(pipe.ctx)
-    fae.fae_set_kernel_timing(pipe.ctx, False)
+    fae.fae_set_kernel_timing(pipe.ctx, 0)
     tot = torch.tensor([ms, float(hot_lookups)], dtype=torch.float64, device=dev)
     if dist is not None:
         mx = tot.clone()
@@ -214,6 +228,8 @@ def run_fae(args):
     if rank == 0:
         # dominant kernel of the step, timed live (event nodes in the graph)
         kname = max(("fwd", "reduce"), key=lambda k: kt[k][0])
+        overlap = {"steps_overlapped": kt["overlap"][1],
+                   "avg_reduce_entry_lead_us": kt["overlap"][0] / max(kt["overlap"][1], 1) * 1e3}
         kms, kn = kt[kname]
         avg_s = (kms / max(kn, 1)) / 1e3
         L_b = prep.packed["n_hot_lookups"] / max(prep.packed["n_hot_batches"], 1)
@@ -244,15 +260,17 @@ def run_fae(args):
                            ds.idx.numel() * 4 / 1e9, n_dy * dy_bytes >> 20),
                        "parallelism": f"dp{world}"},
             "gpu_launches": launches,
-            "roofline": {"kernel": {"fwd": "k_grp_fwd", "reduce": "k_grp_reduce"}[kname],
+            "roofline": {"kernel": {"fwd": "k_grp_fwd_pdl", "reduce": "k_grp_reduce_pdl"}[kname],
+                         "timing": "in-kernel globaltimer, exclusive share of the step, every launch of the timed region",
                          "bound": "hbm", "achieved": achieved,
                          "peak": peak, "peak_kind": kind, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
                          "bytes_per_launch": kb, "avg_launch_us": avg_s * 1e6,
                          "kernels_us": {k: (kt[k][0] / max(kt[k][1], 1)) * 1e3 for k in kt},
-                         "launches_timed": kn},
+                         "launches_timed": kn, "pdl": overlap},
             "clocks": ck,
             "wall_s": wall,
+            "phases_ms_per_step": {k: v / args.steps for k, v in phases.items()},
         }
     return res, (pipe, ds, W, cfg, R, dist, rank, world, dev, dY, Y)
 

@@ -342,15 +342,23 @@ fae_status fae_train_hot_batches(fae_ctx* ctx, float* W_hot, int64_t H,
                                  float lr);
 
 /* --------------------------------------------------------------------------
- * Live kernel timing of fae_train_hot_batches (bench evidence): when enabled,
- * the replayed graphs carry CUDA event nodes around each step's two kernels
- * and the ctx accumulates their durations.  ms[0]/n[0]: forward kernel
- * (k_grp_fwd), ms[1]/n[1]: segment-reduce + SGD kernel (k_grp_reduce).
- * Enabling resets the totals.
+ * Live kernel timing of fae_train_hot_batches (bench evidence).  enable:
+ *  0 off;
+ *  1 in-kernel %globaltimer stamps (min CTA start / max CTA end per launch):
+ *    keeps the programmatic-dependent-launch overlap; each kernel's time is
+ *    its exclusive share of the step (fwd(s) from the end of reduce(s-1),
+ *    reduce(s) from the end of fwd(s));
+ *  2 CUDA event nodes around each kernel in the graph (serialises kernels).
+ * ms[0]/n[0]: forward kernel (k_grp_fwd_pdl), ms[1]/n[1]: segment-reduce +
+ * SGD kernel (k_grp_reduce_pdl); mode 1 also reports ms[2] = summed lead of
+ * each reduce's entry over its forward's end and n[2] = steps where the
+ * reduce entered before the forward ended (PDL overlap evidence); ms, n
+ * have 3 entries.  Enabling resets the totals.
  * ------------------------------------------------------------------------ */
 fae_status fae_set_kernel_timing(fae_ctx* ctx, int32_t enable);
-/* Grouping summary: info[6] = {n_batches, hot lookups, pieces, segments
- * (distinct hot rows summed over batches), max pieces, max bags per batch}. */
+/* Grouping summary: info[6] = {n_batches, hot lookups, long segments (more
+ * than 16 lookups; one CTA each), segments (distinct hot rows summed over
+ * batches), max long segments per batch, max bags per batch}. */
 fae_status fae_group_info(const fae_ctx* ctx, int64_t* info);
 fae_status fae_get_kernel_timing(const fae_ctx* ctx, double* ms, int64_t* n);
 

@@ -337,20 +337,24 @@ def fae_train_hot_batches(ctx: Ctx, W_hot: torch.Tensor, first: int, n: int,
                                         _p(dY), n_dy, _p(Y), ctypes.c_float(lr)))
 
 
-def fae_set_kernel_timing(ctx: Ctx, enable: bool):
-    ctx._ok(lib().fae_set_kernel_timing(ctx.h, int(bool(enable))))
+def fae_set_kernel_timing(ctx: Ctx, mode: int):
+    """0 off; 1 in-kernel globaltimer stamps (keeps the PDL overlap; each
+    kernel's exclusive share of the step); 2 CUDA event nodes in the graph
+    (serialises the kernels; cross-check)."""
+    ctx._ok(lib().fae_set_kernel_timing(ctx.h, int(mode)))
 
 
 def fae_get_kernel_timing(ctx: Ctx) -> dict:
     """{'fwd': (total_ms, launches), 'reduce': (total_ms, launches)}."""
-    ms = (c_dbl * 2)()
-    n = (c_i64 * 2)()
+    ms = (c_dbl * 3)()
+    n = (c_i64 * 3)()
     ctx._ok(lib().fae_get_kernel_timing(ctx.h, ctypes.cast(ms, c_ptr), ctypes.cast(n, c_ptr)))
-    return {"fwd": (ms[0], n[0]), "reduce": (ms[1], n[1])}
+    return {"fwd": (ms[0], n[0]), "reduce": (ms[1], n[1]),
+            "overlap": (ms[2], n[2])}
 
 
 def fae_group_info(ctx: Ctx) -> dict:
     info = (c_i64 * 6)()
     ctx._ok(lib().fae_group_info(ctx.h, ctypes.cast(info, c_ptr)))
-    keys = ("n_batches", "lookups", "pieces", "segments", "max_pieces", "max_bags")
+    keys = ("n_batches", "lookups", "long_segments", "segments", "max_long", "max_bags")
     return dict(zip(keys, [int(v) for v in info]))

@@ -1,5 +1,6 @@
 // ctx.cu — lifecycle, errors, NCCL bootstrap and step workspace of libfae.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "fae_internal.cuh"
@@ -123,6 +124,12 @@ fae_status fae_create(const fae_config* cfg, fae_ctx** out) {
     Ctx* c = &h->c;
     c->cfg = *cfg;
     c->device = cfg->device;
+    {
+        const char* e = getenv("FAE_NO_PDL");
+        c->no_pdl = e && e[0] == '1';
+        const char* t = getenv("FAE_PDL_TRIG");
+        c->pdl_trig = t ? atoi(t) : 0;
+    }
     cudaError_t e = cudaSetDevice(cfg->device);
     if (e != cudaSuccess) {
         delete h;
@@ -149,6 +156,7 @@ void fae_destroy(fae_ctx* h) {
     else cudaDeviceSynchronize();
     if (c->comm) ncclCommDestroy(c->comm);
     step_ws_free(c);
+    group_free(c);
     cudaFree(c->d_err);
     cudaFree(c->scratch);
     cudaFree(c->d_rowbase_tmp);

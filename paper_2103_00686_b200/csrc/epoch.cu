@@ -24,245 +24,215 @@
 
 namespace fae {
 
-fae_status validate_schema(Ctx* c, const fae_tables* t, const char* who);
-
-constexpr int kGT = 1024;
-constexpr int kGW = kGT / 32;
-constexpr int kGI = 4;
-constexpr int kGChunk = kGT * kGI;
-constexpr int kUnroll = 32;
-
-__device__ __forceinline__ int32_t find_bag64(const int64_t* __restrict__ off, int64_t n_bags,
-                                              int64_t pos) {
-    int64_t lo = 0, hi = n_bags - 1;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi + 1) >> 1;
-        if (off[mid] <= pos) lo = mid;
-        else hi = mid - 1;
+// finish a segment: emit G (a11 exchange) or W[row] -= lr * G (a10)
+template <int LPB, int NV>
+__device__ __forceinline__ void seg_finish(const float4 (&g)[NV], int lane, int32_t row, int32_t seg,
+                                           float* W, int D, float lr, int emit, float* grad_out,
+                                           uint32_t* err) {
+    if (emit) {
+        float4* o = reinterpret_cast<float4*>(grad_out + (int64_t)seg * D) + lane;
+#pragma unroll
+        for (int k = 0; k < NV; k++) o[k * LPB] = g[k];
+        return;
     }
-    return (int32_t)lo;
+    float4* w = reinterpret_cast<float4*>(W + (int64_t)row * D) + lane;
+    bool bad = false;
+#pragma unroll
+    for (int k = 0; k < NV; k++) {
+        float4 x = w[k * LPB];
+        x.x = __fmaf_rn(-lr, g[k].x, x.x);
+        x.y = __fmaf_rn(-lr, g[k].y, x.y);
+        x.z = __fmaf_rn(-lr, g[k].z, x.z);
+        x.w = __fmaf_rn(-lr, g[k].w, x.w);
+        bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
+        w[k * LPB] = x;
+    }
+    if (bad) atomicOr(err, kErrNonfinite);
 }
 
-// block-wide exclusive scan of one uint32 per thread (kGT threads)
-__device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_ws, uint32_t* total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t x = v;
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) s_ws[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t w = lane < kGW ? s_ws[lane] : 0u;
-        uint32_t z = w;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
-            if (lane >= o) z += y;
+// sum of src rows bag[0..n) (n <= kPiece) in position order
+template <int LPB, int NV>
+__device__ __forceinline__ void sum_rows16(const int32_t* __restrict__ perm, int32_t pos, int32_t n,
+                                           const float* __restrict__ src, int D, int lane,
+                                           float4 (&g)[NV]) {
+    constexpr int CH = kPiece / NV > 4 ? kPiece / NV : 4;
+    int32_t bag[kPiece];
+#pragma unroll
+    for (int u = 0; u < kPiece; u++) bag[u] = u < n ? __ldg(perm + pos + u) : -1;
+#pragma unroll
+    for (int k = 0; k < NV; k++) g[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int c0 = 0; c0 < kPiece; c0 += CH) {
+        float4 v[CH][NV];
+#pragma unroll
+        for (int u = 0; u < CH; u++) {
+            const float4* rp = reinterpret_cast<const float4*>(src + (int64_t)(bag[c0 + u] < 0 ? 0 : bag[c0 + u]) * D) + lane;
+#pragma unroll
+            for (int k = 0; k < NV; k++)
+                v[u][k] = bag[c0 + u] < 0 ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldg(rp + k * LPB);
         }
-        if (lane < kGW) s_ws[lane] = z - w;
-        if (lane == 31) s_ws[kGW] = z;
+#pragma unroll
+        for (int u = 0; u < CH; u++)
+#pragma unroll
+            for (int k = 0; k < NV; k++)
+                if (bag[c0 + u] >= 0) add4(g[k], v[u][k]);
     }
-    __syncthreads();
-    const uint32_t r = s_ws[warp] + x - v;
-    *total = s_ws[kGW];
-    __syncthreads();
-    return r;
 }
 
-__global__ void __launch_bounds__(kGT, 1)
-k_group(const int32_t* __restrict__ hot_idx, const int64_t* __restrict__ hot_off, int P,
-        BatchDesc* __restrict__ desc, int64_t n_batches, int64_t H, int passes,
-        uint32_t* __restrict__ kbuf, int32_t* __restrict__ vbuf, int64_t slot_cap,
-        uint32_t* __restrict__ batch_ctr, uint64_t* __restrict__ bstatus,
-        int32_t* __restrict__ perm, int64_t* __restrict__ piece_start,
-        int32_t* __restrict__ piece_seg, int32_t* __restrict__ seg_first,
-        int32_t* __restrict__ seg_row, int64_t* __restrict__ totals, uint32_t* err) {
-    __shared__ uint32_t s_wh[kGW][kSortBins];
-    __shared__ uint32_t s_off[kSortBins];
-    __shared__ uint32_t s_tot[kSortBins];
-    __shared__ uint32_t s_ws[kGW + 1];
-    __shared__ int64_t s_batch;
-    __shared__ uint64_t s_base;
-    __shared__ uint32_t s_run[2];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    uint32_t* kA = kbuf + (int64_t)blockIdx.x * 2 * slot_cap;
-    uint32_t* kB = kA + slot_cap;
-    int32_t* vA = vbuf + (int64_t)blockIdx.x * 2 * slot_cap;
-    int32_t* vB = vA + slot_cap;
-    while (true) {
-        if (tid == 0) s_batch = (int64_t)atomicAdd(batch_ctr, 1u);
-        __syncthreads();
-        const int64_t bi = s_batch;
-        if (bi >= n_batches) break;
-        const BatchDesc d = desc[bi];
-        const int64_t L = d.lk1 - d.lk0;
-        // (hot id, local bag) pairs in CSR order
-        for (int64_t j = tid; j < L; j += kGT) {
-            const int32_t r = hot_idx[d.lk0 + j];
-            uint32_t key;
-            if ((uint32_t)r >= (uint64_t)H) {
-                atomicOr(err, kErrIndex);
-                key = (uint32_t)H;
-            } else {
-                key = (uint32_t)r;
-            }
-            kA[j] = key;
-            vA[j] = hot_off ? find_bag64(hot_off + d.bag0, d.n_bags, d.lk0 + j) : (int32_t)(j / P);
-        }
-        __syncthreads();
-        uint32_t *kin = kA, *kout = kB;
-        int32_t *vin = vA, *vout = vB;
-        for (int ps = 0; ps < passes; ps++) {
-            const int shift = ps * kSortBits;
-            if (tid < kSortBins) s_off[tid] = 0;
-            __syncthreads();
-            for (int64_t j0 = 0; j0 < L; j0 += kGT) {
-                const int64_t j = j0 + tid;
-                const uint32_t dg = j < L ? ((kin[j] >> shift) & (kSortBins - 1)) : (uint32_t)kSortBins + lane;
-                const uint32_t peers = __match_any_sync(0xffffffffu, dg);
-                if (dg < (uint32_t)kSortBins && (__ffs(peers) - 1) == lane) atomicAdd(&s_off[dg], (uint32_t)__popc(peers));
-            }
-            __syncthreads();
-            if (warp < kSortBins / 32) {   // exclusive scan over 256 digits (warps 0..7)
-                const uint32_t v = s_off[tid];
-                uint32_t x = v;
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                    if (lane >= o) x += y;
-                }
-                if (lane == 31) s_ws[warp] = x;
-                s_tot[tid] = x - v;
-            }
-            __syncthreads();
-            if (tid < kSortBins) {
-                uint32_t wp = 0;
-                for (int w = 0; w < (tid >> 5); w++) wp += s_ws[w];
-                s_off[tid] = s_tot[tid] + wp;
-            }
-            __syncthreads();
-            for (int64_t c0 = 0; c0 < L; c0 += kGChunk) {
-                for (int i = tid; i < kGW * kSortBins; i += kGT) (&s_wh[0][0])[i] = 0;
-                __syncthreads();
-                uint32_t k[kGI];
-                int32_t v[kGI];
-                uint32_t rk[kGI];
-                const int64_t wb = c0 + (int64_t)warp * 32 * kGI;
+// ordered combination of piece partials (the standalone path's order): the
+// partials are summed in blocks of CH (sub = p0 + p1 + ...), and the block
+// sums are added to tot in order.
+template <int NV>
+struct PieceSum {
+    float4 tot[NV], sub[NV];
+    int in_blk;
+    __device__ __forceinline__ void init() {
 #pragma unroll
-                for (int r = 0; r < kGI; r++) {
-                    const int64_t i = wb + r * 32 + lane;
-                    const bool ok = i < L;
-                    k[r] = ok ? kin[i] : 0u;
-                    v[r] = ok ? vin[i] : 0;
-                    const uint32_t dg = ok ? ((k[r] >> shift) & (kSortBins - 1)) : (uint32_t)kSortBins;
-                    const uint32_t peers = __match_any_sync(0xffffffffu, dg);
-                    const uint32_t lt = __popc(peers & lanemask_lt());
-                    uint32_t cnt = 0;
-                    if (ok) cnt = s_wh[warp][dg];
-                    __syncwarp();
-                    if (ok && lt == 0) s_wh[warp][dg] = cnt + __popc(peers);
-                    __syncwarp();
-                    rk[r] = cnt + lt;
-                }
-                __syncthreads();
-                if (tid < kSortBins) {
-                    uint32_t tot = 0;
-                    for (int w = 0; w < kGW; w++) {
-                        const uint32_t cc = s_wh[w][tid];
-                        s_wh[w][tid] = tot;
-                        tot += cc;
-                    }
-                    s_tot[tid] = tot;
-                }
-                __syncthreads();
+        for (int k = 0; k < NV; k++) tot[k] = sub[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        in_blk = 0;
+    }
+    template <int CH>
+    __device__ __forceinline__ void add(const float4 (&p)[NV]) {
 #pragma unroll
-                for (int r = 0; r < kGI; r++) {
-                    const int64_t i = wb + r * 32 + lane;
-                    if (i < L) {
-                        const uint32_t dg = (k[r] >> shift) & (kSortBins - 1);
-                        const uint32_t pos = s_off[dg] + s_wh[warp][dg] + rk[r];
-                        kout[pos] = k[r];
-                        vout[pos] = v[r];
-                    }
+        for (int k = 0; k < NV; k++) {
+            if (in_blk == 0) sub[k] = p[k];
+            else add4(sub[k], p[k]);
+        }
+        if (++in_blk == CH) {
+#pragma unroll
+            for (int k = 0; k < NV; k++) add4(tot[k], sub[k]);
+            in_blk = 0;
+        }
+    }
+    __device__ __forceinline__ void flush() {
+        if (in_blk) {
+#pragma unroll
+            for (int k = 0; k < NV; k++) add4(tot[k], sub[k]);
+            in_blk = 0;
+        }
+    }
+};
+
+// a9 + a10 over one grouped batch, no cross-CTA communication.  Block ranges:
+//  short:  one LPB-lane group per segment of <= kPiece lookups;
+//  medium: one warp per segment of <= kMedium lookups: each of the warp's
+//          groups sums a 16-lookup piece, partials combined by shuffles;
+//  long:   one CTA per longer segment: partials combined in shared memory.
+// Pieces start at the segment start and hold 16 lookups; partials combine in
+// piece order (PieceSum), identical to the standalone fae_emb_bwd_update.
+// kPDL: all loads of static data happen before griddepcontrol.wait; only
+// the W read-modify-write waits for the forward of this batch.
+template <int LPB, int NV, bool kPDL>
+__device__ __forceinline__ void reduce_segments(const SegRec* __restrict__ rec, int64_t n_short,
+                                                int64_t n_med, int64_t n_long,
+                                                const int32_t* __restrict__ perm,
+                                                const float* __restrict__ src, int D, float* W,
+                                                float lr, int emit, float* grad_out, uint32_t* err) {
+    constexpr int G = 256 / LPB;     // groups per block
+    constexpr int GW = 32 / LPB;     // groups per warp
+    constexpr int CH = kPiece / NV > 4 ? kPiece / NV : 4;
+    __shared__ float4 s_part[2 * G][NV * LPB];
+    const int lane = threadIdx.x % LPB;
+    const int grp = threadIdx.x / LPB;
+    int64_t b = blockIdx.x;
+    const int64_t short_blocks = (n_short + G - 1) / G;
+    if (b < short_blocks) {
+        const int64_t q = b * G + grp;
+        if (q >= n_short) return;
+        const int4 r = __ldg(reinterpret_cast<const int4*>(rec + q));
+        float4 g[NV];
+        sum_rows16<LPB, NV>(perm, r.x, r.y, src, D, lane, g);
+        if (kPDL) pdl_wait();
+        seg_finish<LPB, NV>(g, lane, r.z, r.w, W, D, lr, emit, grad_out, err);
+        return;
+    }
+    b -= short_blocks;
+    const int64_t med_blocks = (n_med + 7) / 8;
+    if (b < med_blocks) {
+        const int64_t m = b * 8 + (threadIdx.x >> 5);
+        if (m >= n_med) return;
+        const int4 r = __ldg(reinterpret_cast<const int4*>(rec + n_short + m));
+        const int gi = (threadIdx.x & 31) / LPB;
+        PieceSum<NV> ps;
+        ps.init();
+        for (int32_t c0 = 0; c0 < r.y; c0 += GW * kPiece) {
+            const int32_t p0 = c0 + gi * kPiece;
+            const int32_t n = p0 < r.y ? min(kPiece, r.y - p0) : 0;
+            float4 g[NV];
+            sum_rows16<LPB, NV>(perm, r.x + p0, n, src, D, lane, g);
+            const int ng = min(GW, (r.y - c0 + kPiece - 1) / kPiece);
+            for (int j = 0; j < ng; j++) {
+                float4 p[NV];
+#pragma unroll
+                for (int k = 0; k < NV; k++) {
+                    p[k].x = __shfl_sync(0xffffffffu, g[k].x, j * LPB + lane);
+                    p[k].y = __shfl_sync(0xffffffffu, g[k].y, j * LPB + lane);
+                    p[k].z = __shfl_sync(0xffffffffu, g[k].z, j * LPB + lane);
+                    p[k].w = __shfl_sync(0xffffffffu, g[k].w, j * LPB + lane);
                 }
-                __syncthreads();
-                if (tid < kSortBins) s_off[tid] += s_tot[tid];
-                __syncthreads();
+                ps.template add<CH>(p);
             }
-            uint32_t* tk = kin; kin = kout; kout = tk;
-            int32_t* tv = vin; vin = vout; vout = tv;
-            __syncthreads();
         }
-        // count pieces / segments of this batch (invalid keys == H excluded)
-        uint32_t np = 0, ns = 0;
-        for (int64_t j = tid; j < L; j += kGT) {
-            const uint32_t kk = kin[j];
-            if (kk >= (uint64_t)H) continue;
-            const bool head = j == 0 || kin[j - 1] != kk;
-            ns += head;
-            np += head || (j % kPiece == 0);
+        ps.flush();
+        if (gi == 0) {
+            if (kPDL) pdl_wait();
+            seg_finish<LPB, NV>(ps.tot, lane, r.z, r.w, W, D, lr, emit, grad_out, err);
         }
-        uint32_t tnp, tns;
-        block_excl_scan(np, s_ws, &tnp);
-        block_excl_scan(ns, s_ws, &tns);
-        if (tid == 0) {
-            const uint64_t agg = ((uint64_t)tnp << 31) | tns;
-            const uint64_t ex = lookback_u64(bstatus, bi, agg);
-            s_base = ex;
-            const int64_t pb0 = (int64_t)(ex >> 31), sb0 = (int64_t)(ex & 0x7FFFFFFFu);
-            desc[bi].pb0 = pb0;
-            desc[bi].pb1 = pb0 + tnp;
-            desc[bi].sb0 = sb0;
-            desc[bi].sb1 = sb0 + tns;
-            if (bi == n_batches - 1) {
-                totals[0] = pb0 + tnp;
-                totals[1] = sb0 + tns;
-                piece_start[pb0 + tnp] = d.lk1;
-                seg_first[sb0 + tns] = (int32_t)(pb0 + tnp);
-            }
-            s_run[0] = 0;
-            s_run[1] = 0;
+        return;
+    }
+    b -= med_blocks;
+    if (b >= n_long) return;
+    // long segment: one CTA; a pass covers up to 2G pieces (group j takes
+    // pieces j and j + G), the partials go to shared memory, CH-piece block
+    // sums are formed in parallel (one group per block), and group 0 adds
+    // the block sums in order.  2G is a multiple of CH, so blocks never
+    // straddle passes.
+    const int4 r = __ldg(reinterpret_cast<const int4*>(rec + n_short + n_med + b));
+    float4 tot[NV];
+#pragma unroll
+    for (int k = 0; k < NV; k++) tot[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int32_t c0 = 0; c0 < r.y; c0 += 2 * G * kPiece) {
+        const int np = min(2 * G, (r.y - c0 + kPiece - 1) / kPiece);
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int pc = grp + h * G;
+            const int32_t p0 = c0 + pc * kPiece;
+            const int32_t n = pc < np ? min(kPiece, r.y - p0) : 0;
+            float4 g[NV];
+            sum_rows16<LPB, NV>(perm, r.x + p0, n, src, D, lane, g);
+#pragma unroll
+            for (int k = 0; k < NV; k++) s_part[pc][k * LPB + lane] = g[k];
         }
         __syncthreads();
-        const int64_t pbase = (int64_t)(s_base >> 31), sbase = (int64_t)(s_base & 0x7FFFFFFFu);
-        // ordered write pass, kGT positions per round
-        for (int64_t j0 = 0; j0 < L; j0 += kGT) {
-            const int64_t j = j0 + tid;
-            uint32_t kk = 0;
-            bool head = false, ps = false;
-            if (j < L) {
-                kk = kin[j];
-                perm[d.lk0 + j] = vin[j];
-                if (kk < (uint64_t)H) {
-                    head = j == 0 || kin[j - 1] != kk;
-                    ps = head || (j % kPiece == 0);
-                }
-            }
-            uint32_t cps, chd;
-            const uint32_t eps = block_excl_scan(ps ? 1u : 0u, s_ws, &cps);
-            const uint32_t ehd = block_excl_scan(head ? 1u : 0u, s_ws, &chd);
-            const int64_t pidx = pbase + s_run[0] + eps;
-            const int64_t sidx = sbase + s_run[1] + ehd + (head ? 1 : 0) - 1;
-            if (head) {
-                seg_first[sidx] = (int32_t)pidx;
-                seg_row[sidx] = (int32_t)kk;
-            }
-            if (ps) {
-                piece_start[pidx] = d.lk0 + j;
-                piece_seg[pidx] = (int32_t)sidx;
-            }
-            __syncthreads();
-            if (tid == 0) {
-                s_run[0] += cps;
-                s_run[1] += chd;
-            }
-            __syncthreads();
+        const int nblk = (np + CH - 1) / CH;
+        float4 sub[NV];
+        if (grp < nblk) {
+            const int q0 = grp * CH, q1 = min(np, q0 + CH);
+#pragma unroll
+            for (int k = 0; k < NV; k++) sub[k] = s_part[q0][k * LPB + lane];
+            for (int q = q0 + 1; q < q1; q++)
+#pragma unroll
+                for (int k = 0; k < NV; k++) add4(sub[k], s_part[q][k * LPB + lane]);
         }
+        __syncthreads();
+        if (grp < nblk)
+#pragma unroll
+            for (int k = 0; k < NV; k++) s_part[grp][k * LPB + lane] = sub[k];
+        __syncthreads();
+        if (grp == 0)
+            for (int j = 0; j < nblk; j++)
+#pragma unroll
+                for (int k = 0; k < NV; k++) add4(tot[k], s_part[j][k * LPB + lane]);
+        __syncthreads();
+    }
+    if (grp == 0) {
+        if (kPDL) pdl_wait();
+        seg_finish<LPB, NV>(tot, lane, r.z, r.w, W, D, lr, emit, grad_out, err);
     }
 }
 
 // ---------------------------------------------------------------------------
-// epoch runner kernels (batch from the device cursor)
+// world > 1 kernels: batch from the device cursor (host loop per step)
 // run[0] = first batch, run[1] = number of batches in this call
 // ---------------------------------------------------------------------------
 template <int LPB, int NV>
@@ -275,29 +245,25 @@ k_grp_fwd(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ run,
     if (i >= run[1]) return;
     const BatchDesc d = desc[run[0] + i];
     if (hot_off) fwd_bags<LPB, NV>(W, H, D, hot_idx, hot_off + d.bag0, 0, d.n_bags, Y, err);
+    else if (P == 1) fwd_gather1<LPB, NV>(W, H, D, hot_idx + d.lk0, d.n_bags, Y, err);
     else fwd_bags<LPB, NV>(W, H, D, hot_idx + d.lk0, nullptr, P, d.n_bags, Y, err);
 }
 
 template <int LPB, int NV>
 __global__ void __launch_bounds__(256)
 k_grp_reduce(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ run,
-             int64_t* cursor, uint32_t* done_ctr, const int32_t* __restrict__ perm,
-             const int64_t* __restrict__ piece_start, const int32_t* __restrict__ piece_seg,
-             const int32_t* __restrict__ seg_first, const int32_t* __restrict__ seg_row,
-             const float* __restrict__ dY, int64_t n_dy, int64_t dy_stride, int D, float* W,
-             float lr, float* partial, uint32_t* seg_cnt, int emit, float* grad_out,
-             uint32_t* err) {
+             int64_t* cursor, uint32_t* done_ctr, const SegRec* __restrict__ rec,
+             const int32_t* __restrict__ perm, const float* __restrict__ dY, int64_t n_dy,
+             int64_t dy_stride, int D, float* W, float lr, int emit, float* grad_out, uint32_t* err) {
     const int64_t i = *cursor;
     if (i < run[1]) {
         const BatchDesc d = desc[run[0] + i];
-        const float* src = dY + (i % n_dy) * dy_stride;
-        reduce_pieces<LPB, NV, int64_t>(d.pb0, d.pb1, d.sb0, 0, perm, piece_start, piece_seg,
-                                        seg_first, seg_row, src, D, W, lr, partial, seg_cnt, emit,
-                                        grad_out, err);
+        reduce_segments<LPB, NV, false>(rec + d.sb0, d.n_short, d.n_med, (d.sb1 - d.sb0) - d.n_short - d.n_med,
+                                        perm + d.lk0,
+                                        dY + (i % n_dy) * dy_stride, D, W, lr, emit, grad_out, err);
     }
-    // the last CTA to finish advances the cursor (every CTA read it above)
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {   // the last CTA to finish advances the cursor
         __threadfence();
         const uint32_t old = atomicAdd(done_ctr, 1u);
         if (old == gridDim.x - 1) {
@@ -308,21 +274,93 @@ k_grp_reduce(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ run
     }
 }
 
+// World-1 graph kernels: step s of the replay handles batch
+// run[0] + *base + s; *base advances by kUnroll at the end of each replay.
+// Launched with programmatic stream serialization: each kernel triggers its
+// dependents at entry, so the next kernel's prologue overlaps this kernel;
+// griddepcontrol.wait guards W.  stamps (optional, per step): [0] fwd start,
+// [1] fwd end, [2] reduce start, [3] reduce end (globaltimer ns; start = min
+// over CTAs after the wait, end = max).
+template <int LPB, int NV>
+__global__ void __launch_bounds__(256)
+k_grp_fwd_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ run,
+              const int64_t* __restrict__ base, int s, const int32_t* __restrict__ hot_idx,
+              const int64_t* __restrict__ hot_off, int P, const float* __restrict__ W, int64_t H,
+              int D, float* __restrict__ Y, uint32_t* err, unsigned long long* stamps, int trig) {
+    if (!(trig & 2)) pdl_trigger();
+    const int64_t rel = *base + s;
+    if (rel >= run[1]) {
+        if (trig & 2) pdl_trigger();
+        return;
+    }
+    if (stamps && threadIdx.x == 0) atomicMin(&stamps[rel * 8 + 5], (unsigned long long)gtimer());
+    const BatchDesc d = desc[run[0] + rel];
+    if (stamps && threadIdx.x == 0) {
+        pdl_wait();
+        atomicMin(&stamps[rel * 8 + 0], (unsigned long long)gtimer());
+    }
+    if (trig & 2) {
+        pdl_wait();
+        pdl_trigger();
+    }
+    if (hot_off) fwd_bags<LPB, NV, true>(W, H, D, hot_idx, hot_off + d.bag0, 0, d.n_bags, Y, err);
+    else if (P == 1) fwd_gather1<LPB, NV, true>(W, H, D, hot_idx + d.lk0, d.n_bags, Y, err);
+    else fwd_bags<LPB, NV, true>(W, H, D, hot_idx + d.lk0, nullptr, P, d.n_bags, Y, err);
+    if (stamps) {
+        __syncthreads();
+        if (threadIdx.x == 0) atomicMax(&stamps[rel * 8 + 1], (unsigned long long)gtimer());
+    }
+}
+
+template <int LPB, int NV>
+__global__ void __launch_bounds__(256)
+k_grp_reduce_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ run,
+                 int64_t* base, int s, int last_step, uint32_t* done_ctr,
+                 const SegRec* __restrict__ rec, const int32_t* __restrict__ perm,
+                 const float* __restrict__ dY, int64_t n_dy, int64_t dy_stride, int D, float* W,
+                 float lr, uint32_t* err, unsigned long long* stamps, int trig) {
+    if (!(trig & 1)) pdl_trigger();
+    const int64_t b0 = *base;
+    const int64_t rel = b0 + s;
+    if (rel < run[1]) {
+        if (stamps && threadIdx.x == 0) atomicMin(&stamps[rel * 8 + 4], (unsigned long long)gtimer());
+        const BatchDesc d = desc[run[0] + rel];
+        if (stamps && threadIdx.x == 0) {
+            pdl_wait();   // start of the exclusive part: the forward of this batch is done
+            atomicMin(&stamps[rel * 8 + 2], (unsigned long long)gtimer());
+        }
+        reduce_segments<LPB, NV, true>(rec + d.sb0, d.n_short, d.n_med, (d.sb1 - d.sb0) - d.n_short - d.n_med,
+                                       perm + d.lk0,
+                                       dY + (rel % n_dy) * dy_stride, D, W, lr, 0, nullptr, err);
+        if (trig & 1) {
+            pdl_wait();
+            pdl_trigger();
+        }
+        if (stamps) {
+            __syncthreads();
+            if (threadIdx.x == 0) atomicMax(&stamps[rel * 8 + 3], (unsigned long long)gtimer());
+        }
+    }
+    if ((trig & 1) && rel >= run[1]) pdl_trigger();
+    if (last_step) {   // the last CTA of the replay's last kernel advances the base
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            pdl_wait();
+            __threadfence();
+            const uint32_t old = atomicAdd(done_ctr, 1u);
+            if (old == gridDim.x - 1) {
+                *done_ctr = 0u;
+                *base = b0 + last_step;
+                __threadfence();
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // host
 // ---------------------------------------------------------------------------
-template <typename T>
-static fae_status grow(Ctx* c, T** p, int64_t* cap, int64_t need) {
-    if (*cap >= need && *p) return FAE_OK;
-    cudaFree(*p);
-    *p = nullptr;
-    const int64_t n = need + need / 8 + 64;
-    FAE_CUDA(c, cudaMalloc(p, sizeof(T) * n));
-    *cap = n;
-    return FAE_OK;
-}
-
-static void drop_graph(Group& g) {
+void drop_graphs(Group& g) {
     if (g.graph) cudaGraphExecDestroy(g.graph);
     g.graph = nullptr;
     g.graph_key = 0;
@@ -340,14 +378,46 @@ static void launch_grp_step(Ctx* c, cudaStream_t s, float* W, int64_t H, int D, 
     const int threads = 256;
     const int64_t gpb = threads / LPB;
     const int64_t maxb = (int64_t)sm_count(c) * 16;
-    const int64_t fb = std::max<int64_t>(1, std::min<int64_t>(cdiv(g.max_bags, gpb), maxb));
+    const int64_t fu = g.P == 1 ? cdiv(g.max_bags, 4) : g.max_bags;
+    const int64_t fb = std::max<int64_t>(1, std::min<int64_t>(cdiv(fu, gpb), maxb));
     k_grp_fwd<LPB, NV><<<(unsigned)fb, threads, 0, s>>>(g.desc, g.run, g.cursor, g.hot_idx, g.hot_off, g.P,
                                                        W, H, D, Y, c->d_err);
     if (mid) cudaEventRecordWithFlags(mid, s, cudaEventRecordExternal);
-    const int64_t rb = std::max<int64_t>(1, std::min<int64_t>(cdiv(g.max_pieces, gpb), maxb));
-    k_grp_reduce<LPB, NV><<<(unsigned)rb, threads, 0, s>>>(
-        g.desc, g.run, g.cursor, g.done_ctr, g.perm, g.piece_start, g.piece_seg, g.seg_first, g.seg_row,
-        dY, n_dy, g.max_bags * (int64_t)D, D, W, lr, g.partial, g.seg_cnt, emit, c->ws.grad, c->d_err);
+    (void)maxb;
+    const int64_t rb = std::max<int64_t>(1, cdiv(g.max_short, gpb) + cdiv(g.max_med, 8) + g.max_long);
+    k_grp_reduce<LPB, NV><<<(unsigned)rb, threads, 0, s>>>(g.desc, g.run, g.cursor, g.done_ctr, g.rec, g.perm,
+                                                          dY, n_dy, g.max_bags * (int64_t)D, D, W, lr, emit,
+                                                          c->ws.grad, c->d_err);
+}
+
+template <int LPB, int NV>
+static fae_status launch_pdl_step(Ctx* c, cudaStream_t st, int s, float* W, int64_t H, int D,
+                                  const float* dY, int64_t n_dy, float* Y, float lr,
+                                  unsigned long long* stamps) {
+    Group& g = c->grp;
+    const int threads = 256;
+    const int64_t gpb = threads / LPB;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = c->no_pdl ? 0 : 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const int64_t half = (int64_t)sm_count(c) * 4;   // each kernel gets about half of the GPU
+    const int64_t fu = g.P == 1 ? cdiv(g.max_bags, 4) : g.max_bags;
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(fu, gpb), half)));
+    FAE_CUDA(c, cudaLaunchKernelEx(&cfg, k_grp_fwd_pdl<LPB, NV>, (const BatchDesc*)g.desc, (const int64_t*)g.run,
+                                   (const int64_t*)g.cursor, s, g.hot_idx, g.hot_off, (int)g.P, (const float*)W, H, D,
+                                   Y, c->d_err, stamps, c->pdl_trig));
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, cdiv(g.max_short, gpb) + cdiv(g.max_med, 8) + g.max_long));
+    const int last = (s == kUnroll - 1) ? kUnroll : 0;
+    FAE_CUDA(c, cudaLaunchKernelEx(&cfg, k_grp_reduce_pdl<LPB, NV>, (const BatchDesc*)g.desc, (const int64_t*)g.run,
+                                   g.cursor, s, last, g.done_ctr, (const SegRec*)g.rec, (const int32_t*)g.perm,
+                                   dY, n_dy, g.max_bags * (int64_t)D, D, W, lr, c->d_err, stamps, c->pdl_trig));
+    return FAE_OK;
 }
 
 static fae_status launch_step(Ctx* c, cudaStream_t s, float* W, int64_t H, int D, const float* dY,
@@ -356,24 +426,31 @@ static fae_status launch_step(Ctx* c, cudaStream_t s, float* W, int64_t H, int D
     return FAE_OK;
 }
 
-static fae_status launch_step_split(Ctx* c, cudaStream_t s, float* W, int64_t H, int D, const float* dY,
-                                    int64_t n_dy, float* Y, float lr, int emit, cudaEvent_t mid) {
-    return launch_step(c, s, W, H, D, dY, n_dy, Y, lr, emit, mid);
+static fae_status launch_pdl(Ctx* c, cudaStream_t st, int s, float* W, int64_t H, int D, const float* dY,
+                             int64_t n_dy, float* Y, float lr, unsigned long long* stamps) {
+    FAE_DISPATCH_D(D, return launch_pdl_step, c, st, s, W, H, D, dY, n_dy, Y, lr, stamps);
+    return FAE_OK;
 }
 
-// Capture kUnroll steps into an executable graph; with `ev` the graph also
-// records ev[3s], ev[3s+1], ev[3s+2] around step s's two kernels.
+// Capture kUnroll steps into an executable graph; with `ev` (timing mode 2)
+// the graph records ev[3s], ev[3s+1], ev[3s+2] around step s's two kernels
+// (plain launches, no PDL edges).
 static fae_status capture(Ctx* c, cudaGraphExec_t* out, float* W, int64_t H, int D, const float* dY,
-                          int64_t n_dy, float* Y, float lr, cudaEvent_t* ev) {
+                          int64_t n_dy, float* Y, float lr, cudaEvent_t* ev,
+                          unsigned long long* stamps = nullptr) {
     cudaStream_t cs;
     FAE_CUDA(c, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     cudaGraph_t graph;
     FAE_CUDA(c, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
     fae_status st = FAE_OK;
     for (int s = 0; s < kUnroll && st == FAE_OK; s++) {
-        if (ev) cudaEventRecordWithFlags(ev[3 * s], cs, cudaEventRecordExternal);
-        st = launch_step_split(c, cs, W, H, D, dY, n_dy, Y, lr, 0, ev ? ev[3 * s + 1] : nullptr);
-        if (ev) cudaEventRecordWithFlags(ev[3 * s + 2], cs, cudaEventRecordExternal);
+        if (ev) {
+            cudaEventRecordWithFlags(ev[3 * s], cs, cudaEventRecordExternal);
+            st = launch_step(c, cs, W, H, D, dY, n_dy, Y, lr, 0, ev[3 * s + 1]);
+            cudaEventRecordWithFlags(ev[3 * s + 2], cs, cudaEventRecordExternal);
+        } else {
+            st = launch_pdl(c, cs, s, W, H, D, dY, n_dy, Y, lr, stamps);
+        }
     }
     cudaError_t e = cudaStreamEndCapture(cs, &graph);
     if (st != FAE_OK) {
@@ -392,15 +469,29 @@ static fae_status capture(Ctx* c, cudaGraphExec_t* out, float* W, int64_t H, int
     return FAE_OK;
 }
 
+void group_free(Ctx* c) {
+    Group& g = c->grp;
+    drop_graphs(g);
+    for (int v = 0; v < 2; v++)
+        for (int e = 0; e < 3 * kUnroll; e++)
+            if (g.tev[v][e]) cudaEventDestroy(g.tev[v][e]);
+    void* ptrs[] = {g.desc, g.perm, g.rec, g.keys[0], g.keys[1], g.vals, g.seg_start, g.seg_row,
+                    g.tile_start, g.tile_batch, g.sstatus, g.pstatus, g.ghist, g.cursor, g.done_ctr, g.stamps};
+    for (void* p : ptrs) cudaFree(p);
+    g = Group{};
+}
+
 }  // namespace fae
 
 using namespace fae;
 
 extern "C" fae_status fae_set_kernel_timing(fae_ctx* h, int32_t enable) {
     if (!h) return FAE_ERR_NOT_INIT;
-    h->c.timing = enable != 0;
+    h->c.timing = enable;
     h->c.t_ms[0] = h->c.t_ms[1] = 0.0;
     h->c.t_n[0] = h->c.t_n[1] = 0;
+    h->c.t_overlap_n = 0;
+    h->c.t_red_entry_lead_ms = 0.0;
     return FAE_OK;
 }
 
@@ -408,157 +499,10 @@ extern "C" fae_status fae_get_kernel_timing(const fae_ctx* h, double* ms, int64_
     if (!h || !ms || !n) return FAE_ERR_INVALID_ARG;
     ms[0] = h->c.t_ms[0];
     ms[1] = h->c.t_ms[1];
+    ms[2] = h->c.t_red_entry_lead_ms;
     n[0] = h->c.t_n[0];
     n[1] = h->c.t_n[1];
-    return FAE_OK;
-}
-
-extern "C" fae_status fae_group_info(const fae_ctx* h, int64_t* info) {
-    if (!h || !info) return FAE_ERR_INVALID_ARG;
-    const Group& g = h->c.grp;
-    if (!g.valid) return FAE_ERR_NOT_INIT;
-    info[0] = g.n_batches;
-    info[1] = g.L_total;
-    info[2] = g.P_total;
-    info[3] = g.S_total;
-    info[4] = g.max_pieces;
-    info[5] = g.max_bags;
-    return FAE_OK;
-}
-
-extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, const fae_packed* pk,
-                                        int32_t fixed_pool, int32_t batch, int64_t H) {
-    if (!h) return FAE_ERR_NOT_INIT;
-    Ctx* c = &h->c;
-    fae_status st = validate_schema(c, tabs, "fae_group_batches");
-    if (st != FAE_OK) return st;
-    if (!pk || batch < 1 || fixed_pool < 0 || H < 0 || H >= (1ll << 31) - 1)
-        return set_err(c, FAE_ERR_INVALID_ARG, "fae_group_batches: bad arguments");
-    const int Tn = tabs->n_tables;
-    const bool offs = fixed_pool == 0;
-    if (pk->n_hot < 0 || pk->n_hot_lookups < 0 || (pk->n_hot_lookups > 0 && !pk->hot_idx) || (offs && !pk->hot_off))
-        return set_err(c, FAE_ERR_INVALID_ARG, "fae_group_batches: bad packed dataset");
-    if (pk->n_hot_lookups >= (1ll << 31) - 1)
-        return set_err(c, FAE_ERR_CAPACITY, "fae_group_batches: >= 2^31 hot lookups");
-    Group& g = c->grp;
-    drop_graph(g);
-    g.valid = false;
-    const int64_t nb = cdiv(pk->n_hot, batch);
-    g.n_batches = nb;
-    g.Tn = Tn;
-    g.P = fixed_pool;
-    g.B = batch;
-    g.H = H;
-    g.hot_idx = pk->hot_idx;
-    g.hot_off = offs ? pk->hot_off : nullptr;
-    g.L_total = pk->n_hot_lookups;
-    // host batch descriptors
-    g.hdesc.assign(nb, BatchDesc{});
-    std::vector<int64_t> starts(nb + 1, 0);
-    if (offs) {
-        if (nb > 0) {
-            FAE_CUDA(c, cudaMemcpy2DAsync(starts.data(), sizeof(int64_t), pk->hot_off,
-                                          sizeof(int64_t) * batch * (int64_t)Tn, sizeof(int64_t), nb,
-                                          cudaMemcpyDeviceToHost, c->stream));
-            FAE_CUDA(c, cudaMemcpyAsync(&starts[nb], pk->hot_off + pk->n_hot * Tn, sizeof(int64_t),
-                                        cudaMemcpyDeviceToHost, c->stream));
-            FAE_CUDA(c, cudaStreamSynchronize(c->stream));
-        }
-    } else {
-        for (int64_t i = 0; i <= nb; i++)
-            starts[i] = std::min<int64_t>(i * batch, pk->n_hot) * Tn * (int64_t)fixed_pool;
-    }
-    int64_t max_bags = 0, max_lk = 0;
-    for (int64_t i = 0; i < nb; i++) {
-        BatchDesc& d = g.hdesc[i];
-        const int64_t r0 = i * batch, r1 = std::min<int64_t>((i + 1) * batch, pk->n_hot);
-        d.lk0 = starts[i];
-        d.lk1 = starts[i + 1];
-        d.bag0 = r0 * Tn;
-        d.n_bags = (int32_t)((r1 - r0) * Tn);
-        max_bags = std::max<int64_t>(max_bags, d.n_bags);
-        max_lk = std::max<int64_t>(max_lk, d.lk1 - d.lk0);
-    }
-    if (max_lk >= (1ll << 30)) return set_err(c, FAE_ERR_CAPACITY, "fae_group_batches: batch too large");
-    g.max_bags = max_bags;
-    g.max_lookups = max_lk;
-    const int64_t L = g.L_total;
-    const int64_t capP = L + L / kPiece + nb + 2;
-    if ((st = grow(c, &g.perm, &g.cap_L, std::max<int64_t>(L, 1))) != FAE_OK) return st;
-    if (g.cap_P < capP + 1 || !g.piece_start || !g.piece_seg) {
-        cudaFree(g.piece_start);
-        cudaFree(g.piece_seg);
-        g.piece_start = nullptr;
-        g.piece_seg = nullptr;
-        g.cap_P = capP + capP / 8 + 64;
-        FAE_CUDA(c, cudaMalloc(&g.piece_start, sizeof(int64_t) * g.cap_P));
-        FAE_CUDA(c, cudaMalloc(&g.piece_seg, sizeof(int32_t) * g.cap_P));
-    }
-    if (g.cap_S < L + 2 || !g.seg_first) {
-        cudaFree(g.seg_first);
-        cudaFree(g.seg_row);
-        cudaFree(g.seg_cnt);
-        g.seg_first = nullptr;
-        g.seg_row = nullptr;
-        g.seg_cnt = nullptr;
-        g.cap_S = L + 2 + L / 8 + 64;
-        FAE_CUDA(c, cudaMalloc(&g.seg_first, sizeof(int32_t) * g.cap_S));
-        FAE_CUDA(c, cudaMalloc(&g.seg_row, sizeof(int32_t) * g.cap_S));
-        FAE_CUDA(c, cudaMalloc(&g.seg_cnt, sizeof(uint32_t) * g.cap_S));
-        FAE_CUDA(c, cudaMemsetAsync(g.seg_cnt, 0, sizeof(uint32_t) * g.cap_S, c->stream));
-    }
-    if ((st = grow(c, &g.desc, &g.cap_B, std::max<int64_t>(nb, 1))) != FAE_OK) return st;
-    if (!g.cursor) {
-        FAE_CUDA(c, cudaMalloc(&g.cursor, sizeof(int64_t) * 4));
-        g.run = g.cursor + 2;
-        FAE_CUDA(c, cudaMalloc(&g.done_ctr, sizeof(uint32_t) * 4));
-        FAE_CUDA(c, cudaMemset(g.done_ctr, 0, sizeof(uint32_t) * 4));
-    }
-    // scratch: per-CTA (k, v) x 2 slots, batch status, counters
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(nb, sm_count(c)));
-    const int64_t slot = std::max<int64_t>(max_lk, 1);
-    size_t o = 0;
-    auto take = [&](size_t b) { size_t r = o; o = (o + b + 255) / 256 * 256; return r; };
-    const size_t o_k = take(sizeof(uint32_t) * 2 * slot * grid);
-    const size_t o_v = take(sizeof(int32_t) * 2 * slot * grid);
-    const size_t o_st = take(sizeof(uint64_t) * std::max<int64_t>(nb, 1));
-    const size_t o_ctr = take(sizeof(uint32_t) * 4);
-    const size_t o_tot = take(sizeof(int64_t) * 2);
-    char* sc = (char*)scratch(c, o);
-    if (!sc) return set_err(c, FAE_ERR_CUDA, "fae_group_batches: scratch allocation failed");
-    FAE_CUDA(c, cudaMemcpyAsync(g.desc, g.hdesc.data(), sizeof(BatchDesc) * nb, cudaMemcpyHostToDevice, c->stream));
-    FAE_CUDA(c, cudaMemsetAsync(sc + o_st, 0, (o_ctr - o_st) + 256, c->stream));
-    FAE_CUDA(c, cudaMemsetAsync(sc + o_tot, 0, sizeof(int64_t) * 2, c->stream));
-    int bits = 1;
-    while (bits < 32 && ((uint64_t)1 << bits) <= (uint64_t)H) bits++;
-    const int passes = (bits + kSortBits - 1) / kSortBits;
-    if (nb > 0) {
-        k_group<<<grid, kGT, 0, c->stream>>>(g.hot_idx, g.hot_off, fixed_pool, g.desc, nb, H, passes,
-                                             (uint32_t*)(sc + o_k), (int32_t*)(sc + o_v), slot,
-                                             (uint32_t*)(sc + o_ctr), (uint64_t*)(sc + o_st), g.perm,
-                                             g.piece_start, g.piece_seg, g.seg_first, g.seg_row,
-                                             (int64_t*)(sc + o_tot), c->d_err);
-        FAE_LAUNCHED(c);
-    }
-    int64_t tot[2] = {0, 0};
-    FAE_CUDA(c, cudaMemcpyAsync(tot, sc + o_tot, sizeof(tot), cudaMemcpyDeviceToHost, c->stream));
-    FAE_CUDA(c, cudaMemcpyAsync(g.hdesc.data(), g.desc, sizeof(BatchDesc) * nb, cudaMemcpyDeviceToHost, c->stream));
-    st = read_latched(c);
-    if (st != FAE_OK) return st;
-    g.P_total = tot[0];
-    g.S_total = tot[1];
-    int64_t mp = 0, ms = 0;
-    for (const BatchDesc& d : g.hdesc) {
-        mp = std::max<int64_t>(mp, d.pb1 - d.pb0);
-        ms = std::max<int64_t>(ms, d.sb1 - d.sb0);
-    }
-    g.max_pieces = std::max<int64_t>(mp, 1);
-    g.max_segs = ms;
-    cudaFree(g.partial);
-    g.partial = nullptr;
-    FAE_CUDA(c, cudaMalloc(&g.partial, sizeof(float) * g.max_pieces * c->cfg.max_dim));
-    if (ms > c->ws.cap_L) return set_err(c, FAE_ERR_CAPACITY, "fae_group_batches: batch segments exceed ctx capacity");
-    g.valid = true;
+    n[2] = h->c.t_overlap_n;
     return FAE_OK;
 }
 
@@ -612,15 +556,18 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
     memcpy(&lb, &lr, 4);
     mix(lb);
     mix((uint64_t)(uintptr_t)g.perm);
-    mix((uint64_t)(uintptr_t)g.partial);
+    mix((uint64_t)(uintptr_t)g.rec);
     mix((uint64_t)(uintptr_t)g.desc);
-    mix((uint64_t)g.max_pieces);
+    mix((uint64_t)g.max_short);
+    mix((uint64_t)g.max_long);
+    mix((uint64_t)g.max_med);
     mix((uint64_t)g.max_bags);
     mix((uint64_t)(uintptr_t)c->d_err);
     const int64_t reps = cdiv(n, kUnroll);
-    if (c->timing) {
-        // two graph instances with their own events: replay r+1 runs while
-        // the host reads replay r's events (no GPU bubble)
+    if (c->timing == 2) {
+        // event mode (cross-check): event nodes between the kernels (this
+        // serialises the PDL edges); two graph instances so replay r+1 runs
+        // while the host reads replay r's events
         if (g.tgraph_key != key || !g.tgraph[0]) {
             for (int v = 0; v < 2; v++) {
                 if (g.tgraph[v]) cudaGraphExecDestroy(g.tgraph[v]);
@@ -661,15 +608,62 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
         c->launches += 2 * reps * kUnroll;
         return FAE_OK;
     }
+    unsigned long long* stamps = nullptr;
+    if (c->timing == 1) {
+        if (g.stamp_cap < n) {
+            cudaFree(g.stamps);
+            g.stamps = nullptr;
+            g.stamp_cap = n + n / 4 + 64;
+            FAE_CUDA(c, cudaMalloc(&g.stamps, sizeof(unsigned long long) * 8 * g.stamp_cap));
+        }
+        stamps = g.stamps;
+        std::vector<unsigned long long> init(8 * n);
+        for (int64_t i = 0; i < n; i++) {
+            init[8 * i + 0] = ~0ull;
+            init[8 * i + 1] = 0;
+            init[8 * i + 2] = ~0ull;
+            init[8 * i + 3] = 0;
+            init[8 * i + 4] = ~0ull;
+            init[8 * i + 5] = ~0ull;
+            init[8 * i + 6] = 0;
+            init[8 * i + 7] = 0;
+        }
+        FAE_CUDA(c, cudaMemcpyAsync(stamps, init.data(), sizeof(unsigned long long) * 8 * n,
+                                    cudaMemcpyHostToDevice, c->stream));
+        FAE_CUDA(c, cudaStreamSynchronize(c->stream));
+    }
+    mix((uint64_t)(uintptr_t)stamps);
     if (!g.graph || g.graph_key != key) {
         if (g.graph) cudaGraphExecDestroy(g.graph);
         g.graph = nullptr;
-        fae_status st = capture(c, &g.graph, W_hot, H, D, dY, n_dy, Y, lr, nullptr);
+        fae_status st = capture(c, &g.graph, W_hot, H, D, dY, n_dy, Y, lr, nullptr, stamps);
         if (st != FAE_OK) return st;
         g.graph_key = key;
         g.graph_steps = kUnroll;
     }
     for (int64_t r = 0; r < reps; r++) FAE_CUDA(c, cudaGraphLaunch(g.graph, c->stream));
     c->launches += 2 * reps * g.graph_steps;
+    if (stamps) {
+        // exclusive critical-path share of each kernel: fwd(s) from the end of
+        // reduce(s-1) (same replay), reduce(s) from the end of fwd(s)
+        std::vector<unsigned long long> st(8 * n);
+        FAE_CUDA(c, cudaMemcpyAsync(st.data(), stamps, sizeof(unsigned long long) * 8 * n,
+                                    cudaMemcpyDeviceToHost, c->stream));
+        FAE_CUDA(c, cudaStreamSynchronize(c->stream));
+        for (int64_t i = 0; i < n; i++) {
+            const unsigned long long fs = st[8 * i], fe = st[8 * i + 1], rs = st[8 * i + 2], re = st[8 * i + 3];
+            if (fe == 0 || re == 0) continue;
+            // overlap evidence: the reduce entered before the forward ended
+            if (st[8 * i + 4] < fe) c->t_overlap_n++;
+            c->t_red_entry_lead_ms += fe > st[8 * i + 4] ? (double)(fe - st[8 * i + 4]) * 1e-6 : 0.0;
+            unsigned long long f0 = fs;
+            if (i > 0 && (i % kUnroll) != 0 && st[8 * (i - 1) + 3] > f0) f0 = st[8 * (i - 1) + 3];
+            const unsigned long long r0 = rs > fe ? rs : fe;
+            c->t_ms[0] += fe > f0 ? (double)(fe - f0) * 1e-6 : 0.0;
+            c->t_ms[1] += re > r0 ? (double)(re - r0) * 1e-6 : 0.0;
+            c->t_n[0]++;
+            c->t_n[1]++;
+        }
+    }
     return FAE_OK;
 }

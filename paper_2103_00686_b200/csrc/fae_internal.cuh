@@ -21,6 +21,11 @@ constexpr int kSortItems = 4;          // keys per thread per tile
 constexpr int kSortTile = kSortThreads * kSortItems;
 constexpr int kMaxSortPasses = 4;      // 32-bit keys
 constexpr int kPiece = 16;             // max lookups per reduction piece
+constexpr int kUnroll = 128;           // steps per captured epoch graph
+constexpr int kMedium = 128;           // segments of (kPiece, kMedium] lookups: one warp
+constexpr int kGSThreads = 256;        // grouping sort: threads per tile
+constexpr int kGSItems = 16;           // grouping sort: items per thread
+constexpr int kGSTile = kGSThreads * kGSItems;   // 4096 lookups per tile
 
 // error latch bits (device word)
 constexpr uint32_t kErrIndex = 1u;
@@ -78,41 +83,63 @@ struct HotSet {
 struct BatchDesc {
     int64_t lk0, lk1;      // lookups [lk0, lk1) of hot_idx (global positions)
     int64_t bag0;          // global bag index of the batch's first bag
-    int64_t pb0, pb1;      // pieces [pb0, pb1)
-    int64_t sb0, sb1;      // segments [sb0, sb1)
+    int64_t sb0, sb1;      // segments [sb0, sb1) (records: short first)
+    int32_t n_short;       // segments of <= kPiece lookups (records first)
+    int32_t n_med;         // then segments of <= kMedium lookups; then the long ones
     int32_t n_bags, pad;
+};
+
+// One segment (a run of equal hot ids in a grouped batch), batch-local
+// indices, 16 bytes.  Per batch the records are stably partitioned by length:
+// <= kPiece lookups (one lane group each), then <= kMedium (one warp each),
+// then longer (one CTA each).
+struct alignas(16) SegRec {
+    int32_t pos;    // first position of the segment in the batch
+    int32_t len;    // lookups of the segment
+    int32_t row;    // hot id
+    int32_t seg;    // segment index in the batch (ascending hot id)
 };
 
 struct Group {
     bool valid = false;
-    int64_t n_batches = 0, L_total = 0, P_total = 0, S_total = 0;
+    int64_t n_batches = 0, L_total = 0, S_total = 0, n_long_total = 0;
     int32_t Tn = 0, P = 0, B = 0;
     int64_t H = 0;
-    int64_t max_bags = 0, max_lookups = 0, max_pieces = 0, max_segs = 0;
+    int64_t max_bags = 0, max_lookups = 0, max_short = 0, max_med = 0, max_long = 0, max_segs = 0;
     const int32_t* hot_idx = nullptr;
     const int64_t* hot_off = nullptr;
-    int32_t* perm = nullptr;          // [L_total] local bag index, grouped by hot id
-    int64_t* piece_start = nullptr;   // [P_total + 1] global positions
-    int32_t* piece_seg = nullptr;     // [P_total]
-    int32_t* seg_first = nullptr;     // [S_total + 1]
-    int32_t* seg_row = nullptr;       // [S_total]
-    uint32_t* seg_cnt = nullptr;      // [S_total], kept zero
     BatchDesc* desc = nullptr;        // device [n_batches]
     std::vector<BatchDesc> hdesc;     // host copy
-    int64_t cap_L = 0, cap_P = 0, cap_S = 0, cap_B = 0;
+    int64_t cap_B = 0;
+    // grouping result
+    int32_t* perm = nullptr;          // [L_total] local bag index, grouped by hot id
+    SegRec* rec = nullptr;            // [S_total]
+    int64_t cap_L = 0, cap_R = 0;
+    // grouping scratch (kept for reuse)
+    uint32_t* keys[2] = {nullptr, nullptr};
+    int32_t* vals = nullptr;          // [L_total] (second value buffer is perm)
+    int64_t* seg_start = nullptr;     // [cap_S] global position of each segment
+    int32_t* seg_row = nullptr;       // [cap_S] hot id of each segment (ascending per batch)
+    int64_t cap_S = 0;
+    int64_t* tile_start = nullptr;    // [n_tiles + 1] global positions
+    int32_t* tile_batch = nullptr;    // [n_tiles] (bit 31: first tile of its batch)
+    uint32_t* sstatus = nullptr;      // [n_tiles][256] digit look-back
+    uint64_t* pstatus = nullptr;      // [n_tiles] segment look-back
+    uint32_t* ghist = nullptr;        // [n_batches][kMaxSortPasses][256]
+    int64_t cap_T = 0, cap_Hh = 0;
     // epoch runner
-    int64_t* cursor = nullptr;        // device: batches done in this run
-    int64_t* run = nullptr;           // device: [0] first batch, [1] n batches
-    uint32_t* done_ctr = nullptr;     // device: finished CTAs of the reduce
-    float* partial = nullptr;         // [max_pieces][max_dim]
+    int64_t* cursor = nullptr;        // device: [0] base / cursor, [2] first, [3] n
+    int64_t* run = nullptr;
+    uint32_t* done_ctr = nullptr;
+
     cudaGraphExec_t graph = nullptr;
     int graph_steps = 0;
     uint64_t graph_key = 0;
-    // timed variant: 2 graph instances, each with 3 events per step
-    // (before fwd, between fwd and reduce, after reduce)
     cudaGraphExec_t tgraph[2] = {nullptr, nullptr};
-    cudaEvent_t tev[2][3 * 64] = {};
+    cudaEvent_t tev[2][3 * kUnroll] = {};
     uint64_t tgraph_key = 0;
+    unsigned long long* stamps = nullptr;
+    int64_t stamp_cap = 0;
 };
 
 struct Ctx {
@@ -139,9 +166,13 @@ struct Ctx {
     int64_t g_cap = 0;
     Group grp;
     // kernel timing (fae_set_kernel_timing): accumulated over timed calls
-    bool timing = false;
+    int timing = 0;                   // 0 off, 1 in-kernel stamps, 2 graph events
     double t_ms[2] = {0.0, 0.0};      // [0] fwd kernel, [1] reduce kernel
     int64_t t_n[2] = {0, 0};
+    int64_t t_overlap_n = 0;          // steps whose reduce entered before the fwd ended
+    double t_red_entry_lead_ms = 0.0; // sum of (fwd end - reduce entry)
+    bool no_pdl = false;              // FAE_NO_PDL=1: plain serialized launches
+    int pdl_trig = 0;                 // FAE_PDL_TRIG bit0: reduce triggers after its wait, bit1: fwd too
 };
 
 // ---------------------------------------------------------------------------
@@ -178,6 +209,8 @@ fae_status sync_merge_apply(Ctx* c, const int32_t* rows, const float* vals, int6
                             float* W, int64_t H, float lr, int32_t* out_rows, float* out_vals,
                             int64_t* out_count, int64_t out_cap);
 fae_status step_ws_alloc(Ctx* c);
+void group_free(Ctx* c);
+fae_status validate_schema(Ctx* c, const fae_tables* t, const char* who);
 void step_ws_free(Ctx* c);
 
 // ---------------------------------------------------------------------------

@@ -1,0 +1,535 @@
+// group.cu — fae_group_batches: the backward's sort-and-segment (a9) for every
+// hot batch of a packed dataset, in bulk.
+//
+// The hot CSR is static for the whole run (the paper pre-processes once and
+// stores the FAE format), so grouping each hot batch's lookups
+// by hot id is hoisted out of the training step and done for all batches at
+// once, as a SEGMENTED onesweep LSD radix sort over the whole hot CSR:
+//   k_gs_init     tiles of 4096 lookups (never spanning two batches): (hot id,
+//                 local bag) pairs + every pass's per-batch digit histogram
+//   k_gs_pass     one 8-bit digit per pass, ceil(log2(H+1)/8) passes: warp
+//                 match_any ranking, per-digit decoupled look-back restricted
+//                 to the tiles of the same batch, stable scatter inside the
+//                 batch (the last pass writes the bag ids straight to perm)
+//   k_gs_segments runs of equal hot id -> segments; global numbering by a
+//                 decoupled look-back
+//   k_gs_records  one 16-byte SegRec per segment (batch-local indices), per
+//                 batch stably partitioned: short segments (<= kPiece
+//                 lookups, one lane group each) first, long ones (one CTA
+//                 each) after
+// Every pass streams its tile once (HBM-bound); no CTA-serial work per batch.
+#include <algorithm>
+#include <cstring>
+
+#include "kern_common.cuh"
+
+namespace fae {
+
+constexpr int kGSW = kGSThreads / 32;
+
+__device__ __forceinline__ int32_t find_bag_g(const int64_t* __restrict__ off, int64_t n_bags,
+                                              int64_t pos) {
+    int64_t lo = 0, hi = n_bags - 1;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (off[mid] <= pos) lo = mid;
+        else hi = mid - 1;
+    }
+    return (int32_t)lo;
+}
+
+__global__ void __launch_bounds__(kGSThreads)
+k_gs_init(const int32_t* __restrict__ hot_idx, const int64_t* __restrict__ hot_off, int P,
+          const int64_t* __restrict__ tile_start, const int32_t* __restrict__ tile_batch,
+          const BatchDesc* __restrict__ desc, int64_t n_tiles, int64_t H, int passes,
+          uint32_t* __restrict__ keys, int32_t* __restrict__ vals, uint32_t* __restrict__ ghist,
+          uint32_t* err) {
+    __shared__ uint32_t sh[kMaxSortPasses][kSortBins];
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        for (int i = tid; i < kMaxSortPasses * kSortBins; i += kGSThreads) (&sh[0][0])[i] = 0;
+        __syncthreads();
+        const int64_t s0 = tile_start[t], s1 = tile_start[t + 1];
+        const int b = tile_batch[t] & 0x7FFFFFFF;
+        const BatchDesc d = desc[b];
+        for (int64_t j0 = s0; j0 < s1; j0 += kGSThreads) {
+            const int64_t j = j0 + tid;
+            uint32_t key = 0;
+            if (j < s1) {
+                const int32_t r = hot_idx[j];
+                if ((uint32_t)r >= (uint64_t)H) {
+                    atomicOr(err, kErrIndex);
+                    key = (uint32_t)H;
+                } else {
+                    key = (uint32_t)r;
+                }
+                keys[j] = key;
+                vals[j] = hot_off ? find_bag_g(hot_off + d.bag0, d.n_bags, j) : (int32_t)((j - d.lk0) / P);
+            }
+            for (int ps = 0; ps < passes; ps++) {
+                const uint32_t dg = j < s1 ? ((key >> (ps * kSortBits)) & (kSortBins - 1)) : (uint32_t)kSortBins + lane;
+                const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+                if (dg < (uint32_t)kSortBins && (__ffs(peers) - 1) == lane) atomicAdd(&sh[ps][dg], (uint32_t)__popc(peers));
+            }
+        }
+        __syncthreads();
+        for (int i = tid; i < passes * kSortBins; i += kGSThreads) {
+            const uint32_t v = (&sh[0][0])[i];
+            if (v) atomicAdd(&ghist[(int64_t)b * kMaxSortPasses * kSortBins + i], v);
+        }
+        __syncthreads();
+    }
+}
+
+// status word: bits 31..30 flag (1 aggregate, 2 inclusive), 29..0 count
+__global__ void __launch_bounds__(kGSThreads)
+k_gs_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
+          uint32_t* __restrict__ kout, int32_t* __restrict__ vout,
+          const int64_t* __restrict__ tile_start, const int32_t* __restrict__ tile_batch,
+          const BatchDesc* __restrict__ desc, const uint32_t* __restrict__ ghist, int pass,
+          uint32_t* __restrict__ status, uint32_t* __restrict__ tile_ctr) {
+    __shared__ uint32_t s_w[kGSW][kSortBins];
+    __shared__ uint32_t s_goff[kSortBins];
+    __shared__ uint32_t s_ws[kGSW];
+    __shared__ int64_t s_tile;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int shift = pass * kSortBits;
+    if (tid == 0) s_tile = (int64_t)atomicAdd(tile_ctr, 1u);
+    for (int i = tid; i < kGSW * kSortBins; i += kGSThreads) (&s_w[0][0])[i] = 0;
+    __syncthreads();
+    const int64_t t = s_tile;
+    const int64_t s0 = tile_start[t], s1 = tile_start[t + 1];
+    const int32_t tb = tile_batch[t];
+    const int b = tb & 0x7FFFFFFF;
+    const bool first = tb < 0;
+    const int64_t lk0 = desc[b].lk0;
+    {   // batch digit starts: exclusive scan of the batch histogram
+        const uint32_t v = ghist[((int64_t)b * kMaxSortPasses + pass) * kSortBins + tid];
+        uint32_t x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_ws[warp] = x;
+        __syncthreads();
+        uint32_t wp = 0;
+        for (int w = 0; w < warp; w++) wp += s_ws[w];
+        s_goff[tid] = wp + x - v;
+    }
+    const int64_t wb = s0 + (int64_t)warp * 32 * kGSItems;
+    uint32_t k[kGSItems];
+    int32_t v[kGSItems];
+    uint16_t rk[kGSItems];
+#pragma unroll
+    for (int r = 0; r < kGSItems; r++) {
+        const int64_t i = wb + r * 32 + lane;
+        k[r] = i < s1 ? kin[i] : 0u;
+        v[r] = i < s1 ? vin[i] : 0;
+    }
+#pragma unroll
+    for (int r = 0; r < kGSItems; r++) {
+        const bool ok = wb + r * 32 + lane < s1;
+        const uint32_t dg = ok ? ((k[r] >> shift) & (kSortBins - 1)) : (uint32_t)kSortBins;
+        const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+        const uint32_t lt = __popc(peers & lanemask_lt());
+        uint32_t cnt = 0;
+        if (ok) cnt = s_w[warp][dg];
+        __syncwarp();
+        if (ok && lt == 0) s_w[warp][dg] = cnt + __popc(peers);
+        __syncwarp();
+        rk[r] = (uint16_t)(cnt + lt);
+    }
+    __syncthreads();
+    {
+        const int d = tid;   // kGSThreads == kSortBins
+        uint32_t tot = 0;
+#pragma unroll
+        for (int w = 0; w < kGSW; w++) {
+            const uint32_t c = s_w[w][d];
+            s_w[w][d] = tot;
+            tot += c;
+        }
+        uint32_t excl = 0;
+        uint32_t* st = status + t * kSortBins + d;
+        if (first) {
+            st_relaxed_u32(st, (2u << 30) | tot);
+        } else {
+            st_relaxed_u32(st, (1u << 30) | tot);
+            int64_t q = t - 1;
+            while (true) {
+                uint32_t sv;
+                do {
+                    sv = ld_relaxed_u32(status + q * kSortBins + d);
+                } while ((sv >> 30) == 0);
+                excl += sv & 0x3FFFFFFFu;
+                if ((sv >> 30) == 2) break;
+                --q;
+            }
+            st_relaxed_u32(st, (2u << 30) | (excl + tot));
+        }
+        s_goff[d] += excl;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kGSItems; r++) {
+        const int64_t i = wb + r * 32 + lane;
+        if (i < s1) {
+            const uint32_t dg = (k[r] >> shift) & (kSortBins - 1);
+            const int64_t pos = lk0 + s_goff[dg] + s_w[warp][dg] + rk[r];
+            kout[pos] = k[r];
+            vout[pos] = v[r];
+        }
+    }
+}
+
+// segments over the sorted keys; global numbering (look-back)
+__global__ void __launch_bounds__(kGSThreads)
+k_gs_segments(const uint32_t* __restrict__ keys, const int64_t* __restrict__ tile_start,
+              const int32_t* __restrict__ tile_batch, BatchDesc* __restrict__ desc, int64_t n_tiles,
+              int64_t H, int64_t L_total, uint64_t* __restrict__ status, uint32_t* __restrict__ tile_ctr,
+              int64_t* __restrict__ seg_start, int32_t* __restrict__ seg_row, int64_t* __restrict__ totals) {
+    __shared__ uint32_t s_ws[kGSW + 1];
+    __shared__ uint64_t s_ex;
+    __shared__ int64_t s_tile;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_tile = (int64_t)atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const int64_t t = s_tile;
+    const int64_t s0 = tile_start[t], s1 = tile_start[t + 1];
+    const int32_t tb = tile_batch[t];
+    const int b = tb & 0x7FFFFFFF;
+    const int64_t lk0 = desc[b].lk0;
+    const int64_t j0 = s0 + (int64_t)tid * kGSItems;
+    uint32_t kk[kGSItems];
+    uint32_t prev = (j0 > lk0 && j0 - 1 < s1) ? keys[j0 - 1] : 0xFFFFFFFFu;
+    uint32_t fl = 0, cs = 0;
+#pragma unroll
+    for (int r = 0; r < kGSItems; r++) {
+        const int64_t j = j0 + r;
+        kk[r] = 0xFFFFFFFFu;
+        if (j < s1) {
+            kk[r] = keys[j];
+            if (kk[r] < (uint64_t)H && (j == lk0 || prev != kk[r])) {
+                fl |= 1u << r;
+                cs++;
+            }
+            prev = kk[r];
+        }
+    }
+    uint32_t x = cs;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_ws[warp] = x;
+    __syncthreads();
+    uint32_t wp = 0, tot = 0;
+    for (int w = 0; w < kGSW; w++) {
+        if (w < warp) wp += s_ws[w];
+        tot += s_ws[w];
+    }
+    if (tid == 0) {
+        const uint64_t ex = lookback_u64(status, t, tot);
+        s_ex = ex;
+        if (tb < 0) desc[b].sb0 = (int64_t)ex;   // first tile of batch b
+        if (t == n_tiles - 1) {
+            totals[0] = (int64_t)(ex + tot);
+            seg_start[ex + tot] = L_total;
+        }
+    }
+    __syncthreads();
+    int64_t si = (int64_t)s_ex + wp + x - cs;
+#pragma unroll
+    for (int r = 0; r < kGSItems; r++) {
+        if ((fl >> r) & 1u) {
+            seg_start[si] = j0 + r;
+            seg_row[si] = (int32_t)kk[r];
+            si++;
+        }
+    }
+}
+
+// one block per batch (grid-stride over batches): batch-local SegRecs,
+// stably partitioned by length class (<= kPiece, <= kMedium, longer), each
+// class in ascending hot id; desc[b].n_short, n_med
+__global__ void __launch_bounds__(256)
+k_gs_records(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __restrict__ seg_start,
+             const int32_t* __restrict__ seg_row, SegRec* __restrict__ rec) {
+    __shared__ uint32_t s_w[3][8];
+    __shared__ uint32_t s_n[2];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int64_t b = blockIdx.x; b < n_batches; b += gridDim.x) {
+        const BatchDesc d = desc[b];
+        const int64_t S = d.sb1 - d.sb0;
+        auto cls = [&](int64_t q, SegRec& r) -> int {
+            const int64_t s = d.sb0 + q;
+            const int64_t st = seg_start[s];
+            const int64_t e = q + 1 < S ? seg_start[s + 1] : d.lk1;
+            r.pos = (int32_t)(st - d.lk0);
+            r.len = (int32_t)(e - st);
+            r.row = seg_row[s];
+            r.seg = (int32_t)q;
+            return r.len <= kPiece ? 0 : (r.len <= kMedium ? 1 : 2);
+        };
+        // pass 1: class sizes
+        uint32_t n0 = 0, n1 = 0;
+        for (int64_t q = tid; q < S; q += 256) {
+            SegRec r;
+            const int k = cls(q, r);
+            n0 += k == 0;
+            n1 += k == 1;
+        }
+        for (int o = 16; o; o >>= 1) {
+            n0 += __shfl_xor_sync(0xffffffffu, n0, o);
+            n1 += __shfl_xor_sync(0xffffffffu, n1, o);
+        }
+        if (lane == 0) {
+            s_w[0][warp] = n0;
+            s_w[1][warp] = n1;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t t0 = 0, t1 = 0;
+            for (int w = 0; w < 8; w++) {
+                t0 += s_w[0][w];
+                t1 += s_w[1][w];
+            }
+            s_n[0] = t0;
+            s_n[1] = t1;
+            desc[b].n_short = (int32_t)t0;
+            desc[b].n_med = (int32_t)t1;
+        }
+        __syncthreads();
+        const uint32_t base[3] = {0u, s_n[0], s_n[0] + s_n[1]};
+        uint32_t run[3] = {0u, 0u, 0u};
+        // pass 2: stable partition, chunks of 256 segments
+        for (int64_t q0 = 0; q0 < S; q0 += 256) {
+            const int64_t q = q0 + tid;
+            const bool valid = q < S;
+            SegRec r{};
+            const int k = valid ? cls(q, r) : -1;
+            uint32_t bal[3];
+#pragma unroll
+            for (int c = 0; c < 3; c++) bal[c] = __ballot_sync(0xffffffffu, k == c);
+            __syncthreads();
+            if (lane == 0)
+#pragma unroll
+                for (int c = 0; c < 3; c++) s_w[c][warp] = __popc(bal[c]);
+            __syncthreads();
+            uint32_t pre[3] = {0u, 0u, 0u}, tot[3] = {0u, 0u, 0u};
+            for (int w = 0; w < 8; w++)
+#pragma unroll
+                for (int c = 0; c < 3; c++) {
+                    if (w < warp) pre[c] += s_w[c][w];
+                    tot[c] += s_w[c][w];
+                }
+            if (valid) rec[d.sb0 + base[k] + run[k] + pre[k] + __popc(bal[k] & lanemask_lt())] = r;
+#pragma unroll
+            for (int c = 0; c < 3; c++) run[c] += tot[c];
+        }
+        __syncthreads();
+    }
+}
+
+template <typename T>
+static fae_status ensure(Ctx* c, T** p, int64_t* cap, int64_t need) {
+    if (*p && *cap >= need) return FAE_OK;
+    cudaFree(*p);
+    *p = nullptr;
+    const int64_t n = need + need / 8 + 256;
+    FAE_CUDA(c, cudaMalloc(p, sizeof(T) * n));
+    *cap = n;
+    return FAE_OK;
+}
+
+void drop_graphs(Group& g);
+
+}  // namespace fae
+
+using namespace fae;
+
+extern "C" fae_status fae_group_info(const fae_ctx* h, int64_t* info) {
+    if (!h || !info) return FAE_ERR_INVALID_ARG;
+    const Group& g = h->c.grp;
+    if (!g.valid) return FAE_ERR_NOT_INIT;
+    info[0] = g.n_batches;
+    info[1] = g.L_total;
+    info[2] = g.n_long_total;
+    info[3] = g.S_total;
+    info[4] = g.max_long;
+    info[5] = g.max_bags;
+    return FAE_OK;
+}
+
+extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, const fae_packed* pk,
+                                        int32_t fixed_pool, int32_t batch, int64_t H) {
+    if (!h) return FAE_ERR_NOT_INIT;
+    Ctx* c = &h->c;
+    fae_status st = validate_schema(c, tabs, "fae_group_batches");
+    if (st != FAE_OK) return st;
+    if (!pk || batch < 1 || fixed_pool < 0 || H < 0 || H >= (1ll << 31) - 1)
+        return set_err(c, FAE_ERR_INVALID_ARG, "fae_group_batches: bad arguments");
+    const int Tn = tabs->n_tables;
+    const bool offs = fixed_pool == 0;
+    if (pk->n_hot < 0 || pk->n_hot_lookups < 0 || (pk->n_hot_lookups > 0 && !pk->hot_idx) || (offs && !pk->hot_off))
+        return set_err(c, FAE_ERR_INVALID_ARG, "fae_group_batches: bad packed dataset");
+    if (pk->n_hot_lookups >= (1ll << 31) - 1)
+        return set_err(c, FAE_ERR_CAPACITY, "fae_group_batches: >= 2^31 hot lookups");
+    Group& g = c->grp;
+    drop_graphs(g);
+    g.valid = false;
+    const int64_t nb = cdiv(pk->n_hot, batch);
+    g.n_batches = nb;
+    g.Tn = Tn;
+    g.P = fixed_pool;
+    g.B = batch;
+    g.H = H;
+    g.hot_idx = pk->hot_idx;
+    g.hot_off = offs ? pk->hot_off : nullptr;
+    const int64_t L = pk->n_hot_lookups;
+    g.L_total = L;
+    // batch descriptors + tiles (host)
+    g.hdesc.assign(nb, BatchDesc{});
+    std::vector<int64_t> starts(nb + 1, 0);
+    if (offs) {
+        if (nb > 0) {
+            FAE_CUDA(c, cudaMemcpy2DAsync(starts.data(), sizeof(int64_t), pk->hot_off,
+                                          sizeof(int64_t) * batch * (int64_t)Tn, sizeof(int64_t), nb,
+                                          cudaMemcpyDeviceToHost, c->stream));
+            FAE_CUDA(c, cudaMemcpyAsync(&starts[nb], pk->hot_off + pk->n_hot * Tn, sizeof(int64_t),
+                                        cudaMemcpyDeviceToHost, c->stream));
+            FAE_CUDA(c, cudaStreamSynchronize(c->stream));
+        }
+    } else {
+        for (int64_t i = 0; i <= nb; i++)
+            starts[i] = std::min<int64_t>(i * batch, pk->n_hot) * Tn * (int64_t)fixed_pool;
+    }
+    std::vector<int64_t> tstart;
+    std::vector<int32_t> tbatch;
+    tstart.reserve(L / kGSTile + nb + 1);
+    int64_t max_bags = 0, max_lk = 0;
+    for (int64_t i = 0; i < nb; i++) {
+        BatchDesc& d = g.hdesc[i];
+        const int64_t r0 = i * batch, r1 = std::min<int64_t>((i + 1) * batch, pk->n_hot);
+        d.lk0 = starts[i];
+        d.lk1 = starts[i + 1];
+        d.bag0 = r0 * Tn;
+        d.n_bags = (int32_t)((r1 - r0) * Tn);
+        max_bags = std::max<int64_t>(max_bags, d.n_bags);
+        max_lk = std::max<int64_t>(max_lk, d.lk1 - d.lk0);
+        for (int64_t s = d.lk0; s < d.lk1; s += kGSTile) {
+            tstart.push_back(s);
+            tbatch.push_back((int32_t)i | (s == d.lk0 ? (int32_t)0x80000000 : 0));
+        }
+    }
+    if (max_lk >= (1ll << 30)) return set_err(c, FAE_ERR_CAPACITY, "fae_group_batches: batch too large");
+    const int64_t nt = (int64_t)tbatch.size();
+    tstart.push_back(L);
+    g.max_bags = max_bags;
+    g.max_lookups = max_lk;
+    int bits = 1;
+    while (bits < 32 && ((uint64_t)1 << bits) <= (uint64_t)H) bits++;
+    const int passes = (bits + kSortBits - 1) / kSortBits;
+    // buffers
+    int64_t k0cap = g.cap_L, k1cap = g.cap_L, vcap = g.cap_L, pcap = g.cap_L;
+    if ((st = ensure(c, &g.keys[0], &k0cap, std::max<int64_t>(L, 1))) != FAE_OK) return st;
+    if ((st = ensure(c, &g.keys[1], &k1cap, std::max<int64_t>(L, 1))) != FAE_OK) return st;
+    if ((st = ensure(c, &g.vals, &vcap, std::max<int64_t>(L, 1))) != FAE_OK) return st;
+    if ((st = ensure(c, &g.perm, &pcap, std::max<int64_t>(L, 1))) != FAE_OK) return st;
+    g.cap_L = std::min(std::min(k0cap, k1cap), std::min(vcap, pcap));
+    int64_t c3 = g.cap_S, c4 = g.cap_S, c5 = g.cap_S;
+    if ((st = ensure(c, &g.seg_start, &c3, L + 2)) != FAE_OK) return st;
+    if ((st = ensure(c, &g.seg_row, &c4, L + 2)) != FAE_OK) return st;
+    if ((st = ensure(c, &g.rec, &c5, L + 2)) != FAE_OK) return st;
+    g.cap_S = std::min(std::min(c3, c4), c5);
+    if ((st = ensure(c, &g.desc, &g.cap_B, std::max<int64_t>(nb, 1))) != FAE_OK) return st;
+    int64_t t1 = g.cap_T, t2 = g.cap_T, t3 = g.cap_T, t4 = g.cap_T;
+    if ((st = ensure(c, &g.tile_start, &t1, nt + 2)) != FAE_OK) return st;
+    if ((st = ensure(c, &g.tile_batch, &t2, nt + 1)) != FAE_OK) return st;
+    if ((st = ensure(c, &g.sstatus, &t3, (nt + 1) * kSortBins)) != FAE_OK) return st;
+    if ((st = ensure(c, &g.pstatus, &t4, nt + 1)) != FAE_OK) return st;
+    g.cap_T = std::min(std::min(t1, t2), std::min(t3 / kSortBins, t4));
+    if ((st = ensure(c, &g.ghist, &g.cap_Hh, std::max<int64_t>(nb, 1) * kMaxSortPasses * kSortBins)) != FAE_OK)
+        return st;
+    if (!g.cursor) {
+        FAE_CUDA(c, cudaMalloc(&g.cursor, sizeof(int64_t) * 4));
+        g.run = g.cursor + 2;
+        FAE_CUDA(c, cudaMalloc(&g.done_ctr, sizeof(uint32_t) * 16));
+        FAE_CUDA(c, cudaMemset(g.done_ctr, 0, sizeof(uint32_t) * 16));
+    }
+    g.S_total = 0;
+    g.max_short = g.max_med = g.max_long = 0;
+    g.max_segs = 1;
+    g.n_long_total = 0;
+    if (nb > 0) {
+        uint32_t* ctr = g.done_ctr + 8;   // tile counters (kept apart from the runner's)
+        int64_t* totals = (int64_t*)scratch(c, 64);
+        if (!totals) return set_err(c, FAE_ERR_CUDA, "fae_group_batches: scratch allocation failed");
+        FAE_CUDA(c, cudaMemcpyAsync(g.desc, g.hdesc.data(), sizeof(BatchDesc) * nb, cudaMemcpyHostToDevice, c->stream));
+        FAE_CUDA(c, cudaMemcpyAsync(g.tile_start, tstart.data(), sizeof(int64_t) * (nt + 1), cudaMemcpyHostToDevice, c->stream));
+        FAE_CUDA(c, cudaMemcpyAsync(g.tile_batch, tbatch.data(), sizeof(int32_t) * nt, cudaMemcpyHostToDevice, c->stream));
+        FAE_CUDA(c, cudaMemsetAsync(g.ghist, 0, sizeof(uint32_t) * nb * kMaxSortPasses * kSortBins, c->stream));
+        FAE_CUDA(c, cudaMemsetAsync(totals, 0, 64, c->stream));
+        const int64_t gi = std::max<int64_t>(1, std::min<int64_t>(nt, (int64_t)sm_count(c) * 8));
+        k_gs_init<<<(unsigned)gi, kGSThreads, 0, c->stream>>>(g.hot_idx, g.hot_off, fixed_pool, g.tile_start, g.tile_batch,
+                                                             g.desc, nt, H, passes, g.keys[0], g.vals, g.ghist, c->d_err);
+        FAE_LAUNCHED(c);
+        // passes: keys k0 -> k1 -> k0 ...; values vals <-> perm, the last pass lands in perm
+        uint32_t* kin = g.keys[0];
+        uint32_t* kout = g.keys[1];
+        int32_t* vbuf[2] = {g.vals, g.perm};
+        int vin_i = (passes % 2 == 1) ? 0 : 1;
+        if (vin_i == 1)
+            FAE_CUDA(c, cudaMemcpyAsync(g.perm, g.vals, sizeof(int32_t) * L, cudaMemcpyDeviceToDevice, c->stream));
+        for (int ps = 0; ps < passes; ps++) {
+            FAE_CUDA(c, cudaMemsetAsync(g.sstatus, 0, sizeof(uint32_t) * nt * kSortBins, c->stream));
+            FAE_CUDA(c, cudaMemsetAsync(ctr, 0, sizeof(uint32_t), c->stream));
+            k_gs_pass<<<(unsigned)nt, kGSThreads, 0, c->stream>>>(kin, vbuf[vin_i], kout, vbuf[vin_i ^ 1], g.tile_start,
+                                                                  g.tile_batch, g.desc, g.ghist, ps, g.sstatus, ctr);
+            FAE_LAUNCHED(c);
+            std::swap(kin, kout);
+            vin_i ^= 1;
+        }
+        // sorted keys in kin, bag ids in perm
+        FAE_CUDA(c, cudaMemsetAsync(g.pstatus, 0, sizeof(uint64_t) * nt, c->stream));
+        FAE_CUDA(c, cudaMemsetAsync(ctr + 1, 0, sizeof(uint32_t), c->stream));
+        k_gs_segments<<<(unsigned)nt, kGSThreads, 0, c->stream>>>(kin, g.tile_start, g.tile_batch, g.desc, nt, H, L,
+                                                                 g.pstatus, ctr + 1, g.seg_start, g.seg_row, totals);
+        FAE_LAUNCHED(c);
+        int64_t tot = 0;
+        FAE_CUDA(c, cudaMemcpyAsync(&tot, totals, sizeof(tot), cudaMemcpyDeviceToHost, c->stream));
+        FAE_CUDA(c, cudaMemcpyAsync(g.hdesc.data(), g.desc, sizeof(BatchDesc) * nb, cudaMemcpyDeviceToHost, c->stream));
+        st = read_latched(c);
+        if (st != FAE_OK) return st;
+        g.S_total = tot;
+        // batches without lookups have no tile: take the next batch's base
+        int64_t ns = g.S_total;
+        for (int64_t i = nb - 1; i >= 0; i--) {
+            BatchDesc& d = g.hdesc[i];
+            if (d.lk1 == d.lk0) d.sb0 = ns;
+            d.sb1 = ns;
+            ns = d.sb0;
+        }
+        FAE_CUDA(c, cudaMemcpyAsync(g.desc, g.hdesc.data(), sizeof(BatchDesc) * nb, cudaMemcpyHostToDevice, c->stream));
+        const int64_t gr = std::max<int64_t>(1, std::min<int64_t>(nb, (int64_t)sm_count(c) * 8));
+        k_gs_records<<<(unsigned)gr, 256, 0, c->stream>>>(g.desc, nb, g.seg_start, g.seg_row, g.rec);
+        FAE_LAUNCHED(c);
+        FAE_CUDA(c, cudaMemcpyAsync(g.hdesc.data(), g.desc, sizeof(BatchDesc) * nb, cudaMemcpyDeviceToHost, c->stream));
+        st = read_latched(c);
+        if (st != FAE_OK) return st;
+        for (const BatchDesc& d : g.hdesc) {
+            const int64_t S = d.sb1 - d.sb0;
+            const int64_t nl = S - d.n_short - d.n_med;
+            g.max_short = std::max<int64_t>(g.max_short, d.n_short);
+            g.max_med = std::max<int64_t>(g.max_med, d.n_med);
+            g.max_long = std::max<int64_t>(g.max_long, nl);
+            g.max_segs = std::max<int64_t>(g.max_segs, S);
+            g.n_long_total += S - d.n_short;
+        }
+    }
+    if (g.max_segs > c->ws.cap_L) return set_err(c, FAE_ERR_CAPACITY, "fae_group_batches: batch segments exceed ctx capacity");
+    st = read_latched(c);
+    if (st != FAE_OK) return st;
+    g.valid = true;
+    return FAE_OK;
+}

@@ -6,9 +6,21 @@
 
 namespace fae {
 
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // a8: Y[b] = sum_{p in bag b} W[idx[p]] for bags [0, n_bags) (grid-stride over
-// bags, LPB lanes per bag, NV float4 per lane, 4 rows in flight per lane).
-template <int LPB, int NV>
+// bags, LPB lanes per bag, NV float4 per lane).  Lookups go in chunks of 8:
+// the 8 indices are loaded first, then the 8 rows (8 rows in flight per lane);
+// the sum order is fixed: acc += ((r0+r1)+(r2+r3)); acc += ((r4+r5)+(r6+r7)).
+// kPDL: the indices of the first chunk are loaded before griddepcontrol.wait
+// (they are static), the rows of W after it (written by the previous kernel).
+template <int LPB, int NV, bool kPDL = false>
 __device__ __forceinline__ void fwd_bags(const float* __restrict__ W, int64_t H, int D,
                                          const int32_t* __restrict__ idx,
                                          const int64_t* __restrict__ off, int P, int64_t n_bags,
@@ -16,6 +28,7 @@ __device__ __forceinline__ void fwd_bags(const float* __restrict__ W, int64_t H,
     const int lane = threadIdx.x % LPB;
     const int64_t gpb = blockDim.x / LPB;
     const int64_t stride = (int64_t)gridDim.x * gpb;
+    bool waited = !kPDL;
     for (int64_t b = blockIdx.x * gpb + threadIdx.x / LPB; b < n_bags; b += stride) {
         int64_t lo, hi;
         if (off) {
@@ -28,20 +41,23 @@ __device__ __forceinline__ void fwd_bags(const float* __restrict__ W, int64_t H,
         float4 acc[NV];
 #pragma unroll
         for (int k = 0; k < NV; k++) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        int64_t p = lo;
-        for (; p + 4 <= hi; p += 4) {
-            int32_t r[4];
+        for (int64_t p = lo; p < hi; p += 8) {
+            int32_t r[8];
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
-                r[u] = __ldg(idx + p + u);
-                if ((uint32_t)r[u] >= (uint64_t)H) {
+            for (int u = 0; u < 8; u++) {
+                r[u] = p + u < hi ? __ldg(idx + p + u) : -1;
+                if (p + u < hi && (uint32_t)r[u] >= (uint64_t)H) {
                     atomicOr(err, kErrIndex);
                     r[u] = -1;
                 }
             }
-            float4 v[4][NV];
+            if (!waited) {
+                pdl_wait();
+                waited = true;
+            }
+            float4 v[8][NV];
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < 8; u++) {
                 const float4* row = reinterpret_cast<const float4*>(W + (int64_t)(r[u] < 0 ? 0 : r[u]) * D) + lane;
 #pragma unroll
                 for (int k = 0; k < NV; k++)
@@ -49,26 +65,13 @@ __device__ __forceinline__ void fwd_bags(const float* __restrict__ W, int64_t H,
             }
 #pragma unroll
             for (int k = 0; k < NV; k++) {
-                acc[k].x += (v[0][k].x + v[1][k].x) + (v[2][k].x + v[3][k].x);
-                acc[k].y += (v[0][k].y + v[1][k].y) + (v[2][k].y + v[3][k].y);
-                acc[k].z += (v[0][k].z + v[1][k].z) + (v[2][k].z + v[3][k].z);
-                acc[k].w += (v[0][k].w + v[1][k].w) + (v[2][k].w + v[3][k].w);
-            }
-        }
-        for (; p < hi; ++p) {
-            const int32_t r = __ldg(idx + p);
-            if ((uint32_t)r >= (uint64_t)H) {
-                atomicOr(err, kErrIndex);
-                continue;
-            }
-            const float4* row = reinterpret_cast<const float4*>(W + (int64_t)r * D) + lane;
 #pragma unroll
-            for (int k = 0; k < NV; k++) {
-                const float4 v = __ldg(row + k * LPB);
-                acc[k].x += v.x;
-                acc[k].y += v.y;
-                acc[k].z += v.z;
-                acc[k].w += v.w;
+                for (int h = 0; h < 8; h += 4) {
+                    acc[k].x += (v[h][k].x + v[h + 1][k].x) + (v[h + 2][k].x + v[h + 3][k].x);
+                    acc[k].y += (v[h][k].y + v[h + 1][k].y) + (v[h + 2][k].y + v[h + 3][k].y);
+                    acc[k].z += (v[h][k].z + v[h + 1][k].z) + (v[h + 2][k].z + v[h + 3][k].z);
+                    acc[k].w += (v[h][k].w + v[h + 1][k].w) + (v[h + 2][k].w + v[h + 3][k].w);
+                }
             }
         }
         float4* y = reinterpret_cast<float4*>(Y + b * D) + lane;
@@ -77,12 +80,56 @@ __device__ __forceinline__ void fwd_bags(const float* __restrict__ W, int64_t H,
     }
 }
 
+// a8 for single-lookup bags (fixed pooling P = 1): Y[b] = W[idx[b]] — a row
+// gather; each LPB-lane group moves U bags per iteration (U rows in flight).
+template <int LPB, int NV, bool kPDL = false, int U = 4>
+__device__ __forceinline__ void fwd_gather1(const float* __restrict__ W, int64_t H, int D,
+                                            const int32_t* __restrict__ idx, int64_t n_bags,
+                                            float* __restrict__ Y, uint32_t* err) {
+    const int lane = threadIdx.x % LPB;
+    const int64_t gpb = blockDim.x / LPB;
+    const int64_t groups = (int64_t)gridDim.x * gpb;
+    const int64_t g0 = blockIdx.x * gpb + threadIdx.x / LPB;
+    bool waited = !kPDL;
+    for (int64_t b0 = g0 * U; b0 < n_bags; b0 += groups * U) {
+        int32_t r[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            r[u] = b0 + u < n_bags ? __ldg(idx + b0 + u) : -1;
+            if (b0 + u < n_bags && (uint32_t)r[u] >= (uint64_t)H) {
+                atomicOr(err, kErrIndex);
+                r[u] = -2;
+            }
+        }
+        if (!waited) {
+            pdl_wait();
+            waited = true;
+        }
+        float4 v[U][NV];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const float4* row = reinterpret_cast<const float4*>(W + (int64_t)(r[u] < 0 ? 0 : r[u]) * D) + lane;
+#pragma unroll
+            for (int k = 0; k < NV; k++)
+                v[u][k] = r[u] < 0 ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldg(row + k * LPB);
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            if (r[u] == -1) continue;
+            float4* y = reinterpret_cast<float4*>(Y + (b0 + u) * D) + lane;
+#pragma unroll
+            for (int k = 0; k < NV; k++) __stcs(y + k * LPB, v[u][k]);
+        }
+    }
+}
+
 // a10 (or emit for a11): apply W[row] -= lr * G, or write G to grad_out.
-template <int LPB, int NV>
+template <int LPB, int NV, bool kPDL = false>
 __device__ __forceinline__ void finish_segment(int64_t s, int64_t s_out, const float4 (&g)[NV],
                                                int lane, const int32_t* __restrict__ seg_row,
                                                float* W, int D, float lr, bool emit,
                                                float* grad_out, uint32_t* err) {
+    if (kPDL) pdl_wait();   // W is read by the previous kernel (fwd of this batch)
     if (emit) {
         float4* o = reinterpret_cast<float4*>(grad_out + s_out * D) + lane;
 #pragma unroll
@@ -117,13 +164,14 @@ __device__ __forceinline__ void add4(float4& a, const float4& b) {
 // Single-piece segments finish directly; multi-piece segments publish their
 // partial (partial[pi - p_begin]) and the last arriver of the segment sums the
 // partials in piece order (blocks of 16), so the summation order is fixed.
-template <int LPB, int NV, typename PosT>
+template <int LPB, int NV, typename PosT, bool kPDL = false>
 __device__ __forceinline__ void reduce_pieces(
     int64_t p_begin, int64_t p_end, int64_t s_out_base, int64_t /*unused*/,
     const int32_t* __restrict__ vals, const PosT* __restrict__ piece_start,
     const int32_t* __restrict__ piece_seg, const int32_t* __restrict__ seg_first,
     const int32_t* __restrict__ seg_row, const float* __restrict__ src, int D, float* W,
     float lr, float* partial, uint32_t* seg_cnt, int emit, float* grad_out, uint32_t* err) {
+    constexpr int CH = kPiece / NV > 4 ? kPiece / NV : 4;   // rows in flight per lane
     const int lane = threadIdx.x % LPB;
     const int gw = (threadIdx.x & 31) / LPB;
     const uint32_t gmask = (LPB == 32) ? 0xffffffffu : (((1u << LPB) - 1u) << (gw * LPB));
@@ -137,56 +185,69 @@ __device__ __forceinline__ void reduce_pieces(
         float4 g[NV];
 #pragma unroll
         for (int k = 0; k < NV; k++) g[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        int64_t i = i0;
-        for (; i + 4 <= i1; i += 4) {
-            float4 v[4][NV];
+        // phase 1: the piece's (<= kPiece) bag ids; phase 2: their rows, CH at
+        // a time, summed in position order
+        int32_t bag[kPiece];
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const float4* row = reinterpret_cast<const float4*>(src + (int64_t)__ldg(vals + i + u) * D) + lane;
+        for (int u = 0; u < kPiece; u++) bag[u] = i0 + u < i1 ? __ldg(vals + i0 + u) : -1;
 #pragma unroll
-                for (int k = 0; k < NV; k++) v[u][k] = __ldg(row + k * LPB);
+        for (int c0 = 0; c0 < kPiece; c0 += CH) {
+            float4 v[CH][NV];
+#pragma unroll
+            for (int u = 0; u < CH; u++) {
+                const float4* row = reinterpret_cast<const float4*>(src + (int64_t)(bag[c0 + u] < 0 ? 0 : bag[c0 + u]) * D) + lane;
+#pragma unroll
+                for (int k = 0; k < NV; k++)
+                    v[u][k] = bag[c0 + u] < 0 ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldg(row + k * LPB);
             }
 #pragma unroll
-            for (int u = 0; u < 4; u++)
+            for (int u = 0; u < CH; u++)
 #pragma unroll
-                for (int k = 0; k < NV; k++) add4(g[k], v[u][k]);
-        }
-        for (; i < i1; i++) {
-            const float4* row = reinterpret_cast<const float4*>(src + (int64_t)__ldg(vals + i) * D) + lane;
-#pragma unroll
-            for (int k = 0; k < NV; k++) add4(g[k], __ldg(row + k * LPB));
+                for (int k = 0; k < NV; k++)
+                    if (bag[c0 + u] >= 0) add4(g[k], v[u][k]);
         }
         if (f1 - f0 == 1) {
-            finish_segment<LPB, NV>(s, s - s_out_base, g, lane, seg_row, W, D, lr, emit, grad_out, err);
+            finish_segment<LPB, NV, kPDL>(s, s - s_out_base, g, lane, seg_row, W, D, lr, emit, grad_out, err);
             continue;
         }
         float4* pp = reinterpret_cast<float4*>(partial + (pi - p_begin) * D) + lane;
 #pragma unroll
         for (int k = 0; k < NV; k++) __stcg(pp + k * LPB, g[k]);
-        __threadfence();
+        // one fence per group: the group's stores are ordered before the
+        // leader's fence by __syncwarp; the last arriver's leader fences again
+        // before the group reads the partials (L2 loads)
         __syncwarp(gmask);
         uint32_t old = 0;
-        if ((threadIdx.x & 31) == leader) old = atomicAdd(&seg_cnt[s], 1u);
+        if ((threadIdx.x & 31) == leader) {
+            __threadfence();
+            old = atomicAdd(&seg_cnt[s], 1u);
+            if (old == (uint32_t)(f1 - f0 - 1)) __threadfence();
+        }
         old = __shfl_sync(gmask, old, leader);
         if (old != (uint32_t)(f1 - f0 - 1)) continue;
-        __threadfence();
+        __syncwarp(gmask);
         float4 tot[NV];
 #pragma unroll
         for (int k = 0; k < NV; k++) tot[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int64_t q0 = f0; q0 < f1; q0 += 16) {
-            float4 blk[NV];
+        for (int64_t q0 = f0; q0 < f1; q0 += CH) {
+            float4 blk[CH][NV];
 #pragma unroll
-            for (int k = 0; k < NV; k++) blk[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-            const int64_t q1 = q0 + 16 < f1 ? q0 + 16 : f1;
-            for (int64_t q = q0; q < q1; q++) {
-                const float4* rp = reinterpret_cast<const float4*>(partial + (q - p_begin) * D) + lane;
+            for (int u = 0; u < CH; u++) {
+                const float4* rp = reinterpret_cast<const float4*>(partial + (q0 + u - p_begin) * D) + lane;
 #pragma unroll
-                for (int k = 0; k < NV; k++) add4(blk[k], __ldcg(rp + k * LPB));
+                for (int k = 0; k < NV; k++)
+                    blk[u][k] = q0 + u < f1 ? __ldcg(rp + k * LPB) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
+            float4 sub[NV];
 #pragma unroll
-            for (int k = 0; k < NV; k++) add4(tot[k], blk[k]);
+            for (int k = 0; k < NV; k++) {
+                sub[k] = blk[0][k];
+#pragma unroll
+                for (int u = 1; u < CH; u++) add4(sub[k], blk[u][k]);
+                add4(tot[k], sub[k]);
+            }
         }
-        finish_segment<LPB, NV>(s, s - s_out_base, tot, lane, seg_row, W, D, lr, emit, grad_out, err);
+        finish_segment<LPB, NV, kPDL>(s, s - s_out_base, tot, lane, seg_row, W, D, lr, emit, grad_out, err);
         if ((threadIdx.x & 31) == leader) seg_cnt[s] = 0u;
     }
 }

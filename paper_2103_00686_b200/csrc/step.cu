@@ -235,6 +235,8 @@ k_pieces(const uint32_t* __restrict__ keys, int64_t* __restrict__ scalars,
          int32_t* __restrict__ seg_first, int32_t* __restrict__ seg_row) {
     constexpr int NW = kSortThreads / 32;
     __shared__ uint64_t s_wsum[NW];
+    __shared__ int64_t s_wmax[NW];
+    __shared__ int64_t s_carry;
     __shared__ uint64_t s_texcl;
     __shared__ int s_tile;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -249,15 +251,57 @@ k_pieces(const uint32_t* __restrict__ keys, int64_t* __restrict__ scalars,
     kk[0] = (i0 > 0 && i0 - 1 < nv) ? keys[i0 - 1] : 0xFFFFFFFFu;
 #pragma unroll
     for (int j = 0; j < kSortItems; j++) kk[j + 1] = (i0 + j < nv) ? keys[i0 + j] : 0xFFFFFFFFu;
-    uint32_t np = 0, ns = 0;
+    // pieces split relative to the segment start (see k_gs_pieces)
+    if (tid == 0) {
+        int64_t cs = tbase;
+        if (tbase > 0 && tbase < nv && keys[tbase - 1] == keys[tbase]) {
+            const uint32_t kv = keys[tbase];
+            int64_t lo = 0, hi = tbase - 1;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (keys[mid] < kv) lo = mid + 1;
+                else hi = mid;
+            }
+            cs = lo;
+        }
+        s_carry = cs;
+    }
+    int64_t lasthead = -1;
 #pragma unroll
     for (int j = 0; j < kSortItems; j++) {
         const int64_t i = i0 + j;
-        if (i < nv) {
-            const bool head = (i == 0) || (kk[j + 1] != kk[j]);
-            const bool ps = head || (i % kPiece == 0);
-            ns += head;
-            np += ps;
+        if (i < nv && (i == 0 || kk[j + 1] != kk[j])) lasthead = i;
+    }
+    {
+        int64_t xm = lasthead;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, xm, o);
+            if (lane >= o) xm = y > xm ? y : xm;
+        }
+        if (lane == 31) s_wmax[warp] = xm;
+        __syncthreads();
+        int64_t before = -1;
+        for (int w = 0; w < warp; w++) before = s_wmax[w] > before ? s_wmax[w] : before;
+        const int64_t xe = __shfl_up_sync(0xffffffffu, xm, 1);
+        if (lane > 0) before = xe > before ? xe : before;
+        lasthead = before >= 0 ? before : s_carry;
+    }
+    uint32_t np = 0, ns = 0;
+    bool isps[kSortItems], ishd[kSortItems];
+    {
+        int64_t segstart = lasthead;
+#pragma unroll
+        for (int j = 0; j < kSortItems; j++) {
+            const int64_t i = i0 + j;
+            ishd[j] = isps[j] = false;
+            if (i < nv) {
+                const bool head = (i == 0) || (kk[j + 1] != kk[j]);
+                if (head) segstart = i;
+                ishd[j] = head;
+                isps[j] = head || ((i - segstart) % kPiece == 0);
+                ns += ishd[j];
+                np += isps[j];
+            }
         }
     }
     const uint64_t mine = ((uint64_t)np << 31) | ns;
@@ -295,8 +339,8 @@ k_pieces(const uint32_t* __restrict__ keys, int64_t* __restrict__ scalars,
     for (int j = 0; j < kSortItems; j++) {
         const int64_t i = i0 + j;
         if (i < nv) {
-            const bool head = (i == 0) || (kk[j + 1] != kk[j]);
-            const bool ps = head || (i % kPiece == 0);
+            const bool head = ishd[j];
+            const bool ps = isps[j];
             if (head) {
                 seg_first[sb] = (int32_t)pb;
                 seg_row[sb] = (int32_t)kk[j + 1];
