@@ -142,11 +142,8 @@ def run_fae(args):
     pipe = FaePipeline(cfg.rows, D, B, cfg.pool, max_pool=max(cfg.pool_hi, 1), device=local,
                        max_world=world)
     if world > 1:
-        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(fae.fae_get_nccl_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        fae.fae_comm_init(pipe.ctx, bytes(idt.cpu().numpy().tobytes()), rank, world)
+        from paper_2103_00686_b200 import dist as fdist
+        fdist.init_comm(pipe.ctx, dev)
     W = gen.make_weights(sum(cfg.rows), D, device=dev)
     S_max = B * Tn
     dy_bytes = S_max * D * 4
@@ -177,9 +174,8 @@ def run_fae(args):
         t = mark("extract", t)
         nb = prep.packed["n_hot_batches"]
         if dist is not None:
-            tt = torch.tensor([nb], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            nb = int(tt)
+            from paper_2103_00686_b200 import dist as fdist
+            nb = fdist.max_over_ranks(nb, dev)
         pipe.train(W_hot, 0, nb, dY, Y, args.lr)
         mark("train", t)
         return prep.packed["n_hot_lookups"], prep
@@ -303,9 +299,8 @@ def run_e2e(args, ctxs):
         W_hot = pipe.extract(W_h, prep)
         nb = prep.packed["n_hot_batches"]
         if dist is not None:
-            t = torch.tensor([nb], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            nb = int(t)
+            from paper_2103_00686_b200 import dist as fdist
+            nb = fdist.max_over_ranks(nb, dev)
         pipe.train(W_hot, 0, nb, dY, Y, args.lr)
         out = W_hot.cpu()
         h2d = idx_h.numel() * 4 + (off_h.numel() * 8 if off_h is not None else 0) + W_hot.numel() * 4

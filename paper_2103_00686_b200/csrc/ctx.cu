@@ -128,7 +128,11 @@ fae_status fae_create(const fae_config* cfg, fae_ctx** out) {
         const char* e = getenv("FAE_NO_PDL");
         c->no_pdl = e && e[0] == '1';
         const char* t = getenv("FAE_PDL_TRIG");
-        c->pdl_trig = t ? atoi(t) : 0;
+        // default 3: each kernel triggers its dependent only after its own
+        // griddepcontrol.wait, bounding the PDL run-ahead to one kernel
+        c->pdl_trig = t ? atoi(t) : 3;
+        const char* m = getenv("FAE_RED_MB");
+        c->red_mb = m ? atoi(m) : 4;
     }
     cudaError_t e = cudaSetDevice(cfg->device);
     if (e != cudaSuccess) {

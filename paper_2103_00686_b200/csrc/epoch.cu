@@ -18,6 +18,8 @@
 //                        CTA of k_grp_reduce advances, so one captured graph
 //                        serves every batch (no per-step host work).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "kern_common.cuh"
@@ -50,7 +52,8 @@ __device__ __forceinline__ void seg_finish(const float4 (&g)[NV], int lane, int3
     if (bad) atomicOr(err, kErrNonfinite);
 }
 
-// sum of src rows bag[0..n) (n <= kPiece) in position order
+// sum of src rows perm[pos .. pos+n) (n <= kPiece) in position order: all
+// bag ids first, then up to CH rows in flight per lane (sum order unaffected)
 template <int LPB, int NV>
 __device__ __forceinline__ void sum_rows16(const int32_t* __restrict__ perm, int32_t pos, int32_t n,
                                            const float* __restrict__ src, int D, int lane,
@@ -134,9 +137,47 @@ __device__ __forceinline__ void reduce_segments(const SegRec* __restrict__ rec, 
     __shared__ float4 s_part[2 * G][NV * LPB];
     const int lane = threadIdx.x % LPB;
     const int grp = threadIdx.x / LPB;
+    // block order: long segments first (they are the longest units, so they
+    // must not form the tail), then medium, then short
     int64_t b = blockIdx.x;
     const int64_t short_blocks = (n_short + G - 1) / G;
-    if (b < short_blocks) {
+    const int64_t med_blocks = (n_med + 7) / 8;
+    if (b >= n_long) {
+        b -= n_long;
+        if (b < med_blocks) {
+            const int64_t m = b * 8 + (threadIdx.x >> 5);
+            if (m >= n_med) return;
+            const int4 r = __ldg(reinterpret_cast<const int4*>(rec + n_short + m));
+            const int gi = (threadIdx.x & 31) / LPB;
+            PieceSum<NV> ps;
+            ps.init();
+            for (int32_t c0 = 0; c0 < r.y; c0 += GW * kPiece) {
+                const int32_t p0 = c0 + gi * kPiece;
+                const int32_t n = p0 < r.y ? min(kPiece, r.y - p0) : 0;
+                float4 g[NV];
+                sum_rows16<LPB, NV>(perm, r.x + p0, n, src, D, lane, g);
+                const int ng = min(GW, (r.y - c0 + kPiece - 1) / kPiece);
+                for (int j = 0; j < ng; j++) {
+                    float4 p[NV];
+#pragma unroll
+                    for (int k = 0; k < NV; k++) {
+                        p[k].x = __shfl_sync(0xffffffffu, g[k].x, j * LPB + lane);
+                        p[k].y = __shfl_sync(0xffffffffu, g[k].y, j * LPB + lane);
+                        p[k].z = __shfl_sync(0xffffffffu, g[k].z, j * LPB + lane);
+                        p[k].w = __shfl_sync(0xffffffffu, g[k].w, j * LPB + lane);
+                    }
+                    ps.template add<CH>(p);
+                }
+            }
+            ps.flush();
+            if (gi == 0) {
+                if (kPDL) pdl_wait();
+                seg_finish<LPB, NV>(ps.tot, lane, r.z, r.w, W, D, lr, emit, grad_out, err);
+            }
+            return;
+        }
+        b -= med_blocks;
+        if (b >= short_blocks) return;
         const int64_t q = b * G + grp;
         if (q >= n_short) return;
         const int4 r = __ldg(reinterpret_cast<const int4*>(rec + q));
@@ -146,43 +187,7 @@ __device__ __forceinline__ void reduce_segments(const SegRec* __restrict__ rec, 
         seg_finish<LPB, NV>(g, lane, r.z, r.w, W, D, lr, emit, grad_out, err);
         return;
     }
-    b -= short_blocks;
-    const int64_t med_blocks = (n_med + 7) / 8;
-    if (b < med_blocks) {
-        const int64_t m = b * 8 + (threadIdx.x >> 5);
-        if (m >= n_med) return;
-        const int4 r = __ldg(reinterpret_cast<const int4*>(rec + n_short + m));
-        const int gi = (threadIdx.x & 31) / LPB;
-        PieceSum<NV> ps;
-        ps.init();
-        for (int32_t c0 = 0; c0 < r.y; c0 += GW * kPiece) {
-            const int32_t p0 = c0 + gi * kPiece;
-            const int32_t n = p0 < r.y ? min(kPiece, r.y - p0) : 0;
-            float4 g[NV];
-            sum_rows16<LPB, NV>(perm, r.x + p0, n, src, D, lane, g);
-            const int ng = min(GW, (r.y - c0 + kPiece - 1) / kPiece);
-            for (int j = 0; j < ng; j++) {
-                float4 p[NV];
-#pragma unroll
-                for (int k = 0; k < NV; k++) {
-                    p[k].x = __shfl_sync(0xffffffffu, g[k].x, j * LPB + lane);
-                    p[k].y = __shfl_sync(0xffffffffu, g[k].y, j * LPB + lane);
-                    p[k].z = __shfl_sync(0xffffffffu, g[k].z, j * LPB + lane);
-                    p[k].w = __shfl_sync(0xffffffffu, g[k].w, j * LPB + lane);
-                }
-                ps.template add<CH>(p);
-            }
-        }
-        ps.flush();
-        if (gi == 0) {
-            if (kPDL) pdl_wait();
-            seg_finish<LPB, NV>(ps.tot, lane, r.z, r.w, W, D, lr, emit, grad_out, err);
-        }
-        return;
-    }
-    b -= med_blocks;
-    if (b >= n_long) return;
-    // long segment: one CTA; a pass covers up to 2G pieces (group j takes
+    // long segment b: one CTA; a pass covers up to 2G pieces (group j takes
     // pieces j and j + G), the partials go to shared memory, CH-piece block
     // sums are formed in parallel (one group per block), and group 0 adds
     // the block sums in order.  2G is a multiple of CH, so blocks never
@@ -312,8 +317,8 @@ k_grp_fwd_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ ru
     }
 }
 
-template <int LPB, int NV>
-__global__ void __launch_bounds__(256)
+template <int LPB, int NV, int MB>
+__global__ void __launch_bounds__(256, MB)
 k_grp_reduce_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ run,
                  int64_t* base, int s, int last_step, uint32_t* done_ctr,
                  const SegRec* __restrict__ rec, const int32_t* __restrict__ perm,
@@ -329,9 +334,14 @@ k_grp_reduce_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__
             pdl_wait();   // start of the exclusive part: the forward of this batch is done
             atomicMin(&stamps[rel * 8 + 2], (unsigned long long)gtimer());
         }
-        reduce_segments<LPB, NV, true>(rec + d.sb0, d.n_short, d.n_med, (d.sb1 - d.sb0) - d.n_short - d.n_med,
-                                       perm + d.lk0,
+        const int64_t n_long = (d.sb1 - d.sb0) - d.n_short - d.n_med;
+        reduce_segments<LPB, NV, true>(rec + d.sb0, d.n_short, d.n_med, n_long, perm + d.lk0,
                                        dY + (rel % n_dy) * dy_stride, D, W, lr, 0, nullptr, err);
+        if (stamps) {   // per-tier completion: [6] long CTAs, [7] short/medium CTAs
+            __syncthreads();
+            if (threadIdx.x == 0)
+                atomicMax(&stamps[rel * 8 + (blockIdx.x < n_long ? 6 : 7)], (unsigned long long)gtimer());
+        }
         if (trig & 1) {
             pdl_wait();
             pdl_trigger();
@@ -414,7 +424,9 @@ static fae_status launch_pdl_step(Ctx* c, cudaStream_t st, int s, float* W, int6
                                    Y, c->d_err, stamps, c->pdl_trig));
     cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, cdiv(g.max_short, gpb) + cdiv(g.max_med, 8) + g.max_long));
     const int last = (s == kUnroll - 1) ? kUnroll : 0;
-    FAE_CUDA(c, cudaLaunchKernelEx(&cfg, k_grp_reduce_pdl<LPB, NV>, (const BatchDesc*)g.desc, (const int64_t*)g.run,
+    auto kern = c->red_mb >= 8 ? k_grp_reduce_pdl<LPB, NV, 8>
+              : (c->red_mb >= 6 ? k_grp_reduce_pdl<LPB, NV, 6> : k_grp_reduce_pdl<LPB, NV, 4>);
+    FAE_CUDA(c, cudaLaunchKernelEx(&cfg, kern, (const BatchDesc*)g.desc, (const int64_t*)g.run,
                                    g.cursor, s, last, g.done_ctr, (const SegRec*)g.rec, (const int32_t*)g.perm,
                                    dY, n_dy, g.max_bags * (int64_t)D, D, W, lr, c->d_err, stamps, c->pdl_trig));
     return FAE_OK;
@@ -491,6 +503,7 @@ extern "C" fae_status fae_set_kernel_timing(fae_ctx* h, int32_t enable) {
     h->c.t_ms[0] = h->c.t_ms[1] = 0.0;
     h->c.t_n[0] = h->c.t_n[1] = 0;
     h->c.t_overlap_n = 0;
+    h->c.t_tier_ms[0] = h->c.t_tier_ms[1] = 0.0;
     h->c.t_red_entry_lead_ms = 0.0;
     return FAE_OK;
 }
@@ -626,7 +639,7 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
             init[8 * i + 4] = ~0ull;
             init[8 * i + 5] = ~0ull;
             init[8 * i + 6] = 0;
-            init[8 * i + 7] = 0;
+            init[8 * i + 7] = 0;   // tier ends
         }
         FAE_CUDA(c, cudaMemcpyAsync(stamps, init.data(), sizeof(unsigned long long) * 8 * n,
                                     cudaMemcpyHostToDevice, c->stream));
@@ -663,7 +676,12 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
             c->t_ms[1] += re > r0 ? (double)(re - r0) * 1e-6 : 0.0;
             c->t_n[0]++;
             c->t_n[1]++;
+            if (st[8 * i + 6] > fe) c->t_tier_ms[0] += (double)(st[8 * i + 6] - fe) * 1e-6;
+            if (st[8 * i + 7] > fe) c->t_tier_ms[1] += (double)(st[8 * i + 7] - fe) * 1e-6;
         }
+        if (getenv("FAE_VERBOSE") && c->t_n[1] > 0)
+            fprintf(stderr, "[fae_train_hot_batches] avg after fwd end: long CTAs %.2f us, short/medium CTAs %.2f us\n",
+                    c->t_tier_ms[0] / c->t_n[1] * 1e3, c->t_tier_ms[1] / c->t_n[1] * 1e3);
     }
     return FAE_OK;
 }

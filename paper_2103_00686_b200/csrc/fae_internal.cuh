@@ -171,7 +171,9 @@ struct Ctx {
     int64_t t_n[2] = {0, 0};
     int64_t t_overlap_n = 0;          // steps whose reduce entered before the fwd ended
     double t_red_entry_lead_ms = 0.0; // sum of (fwd end - reduce entry)
+    double t_tier_ms[2] = {0.0, 0.0}; // reduce tiers' completion after fwd end
     bool no_pdl = false;              // FAE_NO_PDL=1: plain serialized launches
+    int red_mb = 4;                   // FAE_RED_MB: min resident reduce CTAs per SM (4/6/8)
     int pdl_trig = 0;                 // FAE_PDL_TRIG bit0: reduce triggers after its wait, bit1: fwd too
 };
 

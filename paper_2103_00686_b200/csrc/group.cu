@@ -19,6 +19,9 @@
 //                 each) after
 // Every pass streams its tile once (HBM-bound); no CTA-serial work per batch.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "kern_common.cuh"
@@ -378,6 +381,16 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
     Group& g = c->grp;
     drop_graphs(g);
     g.valid = false;
+    const bool verbose = getenv("FAE_VERBOSE") != nullptr;
+    auto t_last = std::chrono::steady_clock::now();
+    auto stage = [&](const char* name) {
+        if (!verbose) return;
+        cudaStreamSynchronize(c->stream);
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[fae_group_batches] %-10s %9.3f ms\n", name,
+                std::chrono::duration<double, std::milli>(now - t_last).count());
+        t_last = now;
+    };
     const int64_t nb = cdiv(pk->n_hot, batch);
     g.n_batches = nb;
     g.Tn = Tn;
@@ -424,6 +437,7 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
     }
     if (max_lk >= (1ll << 30)) return set_err(c, FAE_ERR_CAPACITY, "fae_group_batches: batch too large");
     const int64_t nt = (int64_t)tbatch.size();
+    stage("host");
     tstart.push_back(L);
     g.max_bags = max_bags;
     g.max_lookups = max_lk;
@@ -443,11 +457,11 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
     if ((st = ensure(c, &g.rec, &c5, L + 2)) != FAE_OK) return st;
     g.cap_S = std::min(std::min(c3, c4), c5);
     if ((st = ensure(c, &g.desc, &g.cap_B, std::max<int64_t>(nb, 1))) != FAE_OK) return st;
-    int64_t t1 = g.cap_T, t2 = g.cap_T, t3 = g.cap_T, t4 = g.cap_T;
+    int64_t t1 = g.cap_T, t2 = g.cap_T, t3 = g.cap_T * kSortBins, t4 = g.cap_T;
     if ((st = ensure(c, &g.tile_start, &t1, nt + 2)) != FAE_OK) return st;
-    if ((st = ensure(c, &g.tile_batch, &t2, nt + 1)) != FAE_OK) return st;
-    if ((st = ensure(c, &g.sstatus, &t3, (nt + 1) * kSortBins)) != FAE_OK) return st;
-    if ((st = ensure(c, &g.pstatus, &t4, nt + 1)) != FAE_OK) return st;
+    if ((st = ensure(c, &g.tile_batch, &t2, nt + 2)) != FAE_OK) return st;
+    if ((st = ensure(c, &g.sstatus, &t3, (nt + 2) * kSortBins)) != FAE_OK) return st;
+    if ((st = ensure(c, &g.pstatus, &t4, nt + 2)) != FAE_OK) return st;
     g.cap_T = std::min(std::min(t1, t2), std::min(t3 / kSortBins, t4));
     if ((st = ensure(c, &g.ghist, &g.cap_Hh, std::max<int64_t>(nb, 1) * kMaxSortPasses * kSortBins)) != FAE_OK)
         return st;
@@ -457,6 +471,7 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
         FAE_CUDA(c, cudaMalloc(&g.done_ctr, sizeof(uint32_t) * 16));
         FAE_CUDA(c, cudaMemset(g.done_ctr, 0, sizeof(uint32_t) * 16));
     }
+    stage("alloc");
     g.S_total = 0;
     g.max_short = g.max_med = g.max_long = 0;
     g.max_segs = 1;
@@ -474,6 +489,7 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
         k_gs_init<<<(unsigned)gi, kGSThreads, 0, c->stream>>>(g.hot_idx, g.hot_off, fixed_pool, g.tile_start, g.tile_batch,
                                                              g.desc, nt, H, passes, g.keys[0], g.vals, g.ghist, c->d_err);
         FAE_LAUNCHED(c);
+        stage("init");
         // passes: keys k0 -> k1 -> k0 ...; values vals <-> perm, the last pass lands in perm
         uint32_t* kin = g.keys[0];
         uint32_t* kout = g.keys[1];
@@ -490,12 +506,14 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
             std::swap(kin, kout);
             vin_i ^= 1;
         }
+        stage("passes");
         // sorted keys in kin, bag ids in perm
         FAE_CUDA(c, cudaMemsetAsync(g.pstatus, 0, sizeof(uint64_t) * nt, c->stream));
         FAE_CUDA(c, cudaMemsetAsync(ctr + 1, 0, sizeof(uint32_t), c->stream));
         k_gs_segments<<<(unsigned)nt, kGSThreads, 0, c->stream>>>(kin, g.tile_start, g.tile_batch, g.desc, nt, H, L,
                                                                  g.pstatus, ctr + 1, g.seg_start, g.seg_row, totals);
         FAE_LAUNCHED(c);
+        stage("segments");
         int64_t tot = 0;
         FAE_CUDA(c, cudaMemcpyAsync(&tot, totals, sizeof(tot), cudaMemcpyDeviceToHost, c->stream));
         FAE_CUDA(c, cudaMemcpyAsync(g.hdesc.data(), g.desc, sizeof(BatchDesc) * nb, cudaMemcpyDeviceToHost, c->stream));
@@ -517,6 +535,7 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
         FAE_CUDA(c, cudaMemcpyAsync(g.hdesc.data(), g.desc, sizeof(BatchDesc) * nb, cudaMemcpyDeviceToHost, c->stream));
         st = read_latched(c);
         if (st != FAE_OK) return st;
+        stage("records");
         for (const BatchDesc& d : g.hdesc) {
             const int64_t S = d.sb1 - d.sb0;
             const int64_t nl = S - d.n_short - d.n_med;
