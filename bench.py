@@ -109,8 +109,8 @@ def fwd_bytes(L, S, D, explicit_off):
 
 def red_bytes(L, S, U, D):
     """a9+a10 per batch with the grouping precomputed: sorted bag ids (4L),
-    piece/segment records (~16U + 12L/16), dY rows 4DL, W rows read+write 8DU."""
-    return 4 * L + 16 * U + 12 * (L / 16.0) + 4 * D * L + 8 * D * U
+    32-byte segment records (32U), dY rows 4DL, W rows read+write 8DU."""
+    return 4 * L + 32 * U + 4 * D * L + 8 * D * U
 
 
 def pipe_stats(pipe):
@@ -223,7 +223,8 @@ def run_fae(args):
     res = None
     if rank == 0:
         # dominant kernel of the step, timed live (event nodes in the graph)
-        kname = max(("fwd", "reduce"), key=lambda k: kt[k][0])
+        fused = kt["fused"]
+        kname = "reduce" if fused else max(("fwd", "reduce"), key=lambda k: kt[k][0])
         overlap = {"steps_overlapped": kt["overlap"][1],
                    "avg_reduce_entry_lead_us": kt["overlap"][0] / max(kt["overlap"][1], 1) * 1e3}
         kms, kn = kt[kname]
@@ -232,7 +233,10 @@ def run_fae(args):
         S_b = prep.packed["n_hot"] * Tn / max(prep.packed["n_hot_batches"], 1)
         gi = pipe_stats(pipe)
         U_b = gi["segs_per_batch"]
-        if kname == "fwd":
+        F_b = gi["free_segments"] / max(gi["n_batches"], 1)
+        if fused:   # backward+SGD of one batch + forward of the next
+            kb = red_bytes(L_b, S_b, U_b, D) + 4 * L_b + 4 * D * S_b + (16 + 4 * D) * F_b
+        elif kname == "fwd":
             kb = fwd_bytes(L_b, S_b, D, cfg.pool == 0)
         else:
             kb = red_bytes(L_b, S_b, U_b, D)
@@ -256,13 +260,13 @@ def run_fae(args):
                            ds.idx.numel() * 4 / 1e9, n_dy * dy_bytes >> 20),
                        "parallelism": f"dp{world}"},
             "gpu_launches": launches,
-            "roofline": {"kernel": {"fwd": "k_grp_fwd_pdl", "reduce": "k_grp_reduce_pdl"}[kname],
+            "roofline": {"kernel": "k_grp_fused_pdl" if fused else {"fwd": "k_grp_fwd_pdl", "reduce": "k_grp_reduce_pdl"}[kname],
                          "timing": "in-kernel globaltimer, exclusive share of the step, every launch of the timed region",
                          "bound": "hbm", "achieved": achieved,
                          "peak": peak, "peak_kind": kind, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
                          "bytes_per_launch": kb, "avg_launch_us": avg_s * 1e6,
-                         "kernels_us": {k: (kt[k][0] / max(kt[k][1], 1)) * 1e3 for k in kt},
+                         "kernels_us": {k: (kt[k][0] / max(kt[k][1], 1)) * 1e3 for k in ("fwd", "reduce")},
                          "launches_timed": kn, "pdl": overlap},
             "clocks": ck,
             "wall_s": wall,

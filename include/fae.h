@@ -352,13 +352,15 @@ fae_status fae_train_hot_batches(fae_ctx* ctx, float* W_hot, int64_t H,
  * ms[0]/n[0]: forward kernel (k_grp_fwd_pdl), ms[1]/n[1]: segment-reduce +
  * SGD kernel (k_grp_reduce_pdl); mode 1 also reports ms[2] = summed lead of
  * each reduce's entry over its forward's end and n[2] = steps where the
- * reduce entered before the forward ended (PDL overlap evidence); ms, n
- * have 3 entries.  Enabling resets the totals.
+ * reduce entered before the forward ended (PDL overlap evidence); n[3] = 1
+ * when the fused single-kernel step ran (its time is in ms[1]/n[1]); ms, n
+ * have 4 entries.  Enabling resets the totals.
  * ------------------------------------------------------------------------ */
 fae_status fae_set_kernel_timing(fae_ctx* ctx, int32_t enable);
-/* Grouping summary: info[6] = {n_batches, hot lookups, long segments (more
- * than 16 lookups; one CTA each), segments (distinct hot rows summed over
- * batches), max long segments per batch, max bags per batch}. */
+/* Grouping summary: info[8] = {n_batches, hot lookups, segments of more
+ * than 16 lookups, segments (distinct hot rows summed over batches), max
+ * long segments per batch, max bags per batch, free segments (rows of a
+ * batch absent from the previous batch, summed), fused step in use}. */
 fae_status fae_group_info(const fae_ctx* ctx, int64_t* info);
 fae_status fae_get_kernel_timing(const fae_ctx* ctx, double* ms, int64_t* n);
 

@@ -346,15 +346,16 @@ def fae_set_kernel_timing(ctx: Ctx, mode: int):
 
 def fae_get_kernel_timing(ctx: Ctx) -> dict:
     """{'fwd': (total_ms, launches), 'reduce': (total_ms, launches)}."""
-    ms = (c_dbl * 3)()
-    n = (c_i64 * 3)()
+    ms = (c_dbl * 4)()
+    n = (c_i64 * 4)()
     ctx._ok(lib().fae_get_kernel_timing(ctx.h, ctypes.cast(ms, c_ptr), ctypes.cast(n, c_ptr)))
     return {"fwd": (ms[0], n[0]), "reduce": (ms[1], n[1]),
-            "overlap": (ms[2], n[2])}
+            "overlap": (ms[2], n[2]), "fused": bool(n[3])}
 
 
 def fae_group_info(ctx: Ctx) -> dict:
-    info = (c_i64 * 6)()
+    info = (c_i64 * 8)()
     ctx._ok(lib().fae_group_info(ctx.h, ctypes.cast(info, c_ptr)))
-    keys = ("n_batches", "lookups", "long_segments", "segments", "max_long", "max_bags")
+    keys = ("n_batches", "lookups", "long_segments", "segments", "max_long", "max_bags",
+            "free_segments", "fused")
     return dict(zip(keys, [int(v) for v in info]))

@@ -131,6 +131,9 @@ fae_status fae_create(const fae_config* cfg, fae_ctx** out) {
         // default 3: each kernel triggers its dependent only after its own
         // griddepcontrol.wait, bounding the PDL run-ahead to one kernel
         c->pdl_trig = t ? atoi(t) : 3;
+        // the fused one-kernel step (bit-identical) is opt-in: FAE_FUSED=1
+        const char* f = getenv("FAE_FUSED");
+        c->no_fused = !(f && f[0] == '1');
         const char* m = getenv("FAE_RED_MB");
         c->red_mb = m ? atoi(m) : 4;
     }

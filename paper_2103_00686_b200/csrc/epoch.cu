@@ -116,6 +116,165 @@ struct PieceSum {
     }
 };
 
+template <int LPB, int NV>
+__device__ __forceinline__ void write_y(const float4 (&v)[NV], const int32_t* __restrict__ perm_b,
+                                        int32_t pos, int32_t len, float* __restrict__ Y, int D,
+                                        int lane, int worker, int n_workers) {
+    int32_t q = worker;
+    for (; q + 3 * n_workers < len; q += 4 * n_workers) {
+        int32_t bg[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) bg[u] = __ldg(perm_b + pos + q + u * n_workers);
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            float4* y = reinterpret_cast<float4*>(Y + (int64_t)bg[u] * D) + lane;
+#pragma unroll
+            for (int k = 0; k < NV; k++) __stcs(y + k * LPB, v[k]);
+        }
+    }
+    for (; q < len; q += n_workers) {
+        float4* y = reinterpret_cast<float4*>(Y + (int64_t)__ldg(perm_b + pos + q) * D) + lane;
+#pragma unroll
+        for (int k = 0; k < NV; k++) __stcs(y + k * LPB, v[k]);
+    }
+}
+
+// Long segments (> kMedium lookups): one CTA per kChunk-lookup chunk.  A
+// chunk's pieces (16 lookups from the segment start) are summed by the
+// CTA's groups (2G pieces per pass), then its CH-piece block sums are formed
+// in shared memory.  Single-chunk segments finish in place; otherwise each
+// chunk publishes its block sums (one fence per CTA) and the last-arriving
+// chunk adds all block sums of the segment in order — the standalone path's
+// order (PieceSum), so results are bit-identical.  lb: block index in the
+// batch's long-chunk range.  kFused: the finisher also writes the new row
+// into Y_b for the linked segment of the next batch.
+template <int LPB, int NV, bool kPDL, bool kFused>
+__device__ __forceinline__ void long_chunk(const SegRec* __restrict__ lrec, int64_t n_long, int64_t lb,
+                                           const int32_t* __restrict__ perm_a,
+                                           const int32_t* __restrict__ perm_b,
+                                           const float* __restrict__ src, int D, float* W, float lr,
+                                           float* lpart, uint32_t* lcnt, int emit, float* grad_out,
+                                           float* Y, uint32_t* err) {
+    constexpr int G = 256 / LPB;
+    constexpr int CH = kPiece / NV > 4 ? kPiece / NV : 4;
+    __shared__ float4 s_part[2 * G][NV * LPB];
+    __shared__ int s_last;
+    const int lane = threadIdx.x % LPB;
+    const int grp = threadIdx.x / LPB;
+    // the segment of this chunk: last k with c0 <= lb
+    int64_t lo = 0, hi = n_long - 1;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (__ldg(&lrec[mid].c0) <= lb) lo = mid;
+        else hi = mid - 1;
+    }
+    const int64_t k = lo;
+    const int4 r = __ldg(reinterpret_cast<const int4*>(lrec + k));          // pos, len, row, seg
+    const int4 r2 = __ldg(reinterpret_cast<const int4*>(lrec + k) + 1);     // npos, nlen, c0, nc
+    const int32_t cidx = (int32_t)(lb - r2.z);
+    const int32_t cbeg = cidx * kChunk, cend = min(r.y, cbeg + kChunk);
+    // block sums of this chunk, in shared memory rows [0, nblk_total)
+    int nblk_total = 0;
+    for (int32_t c0 = cbeg; c0 < cend; c0 += 2 * G * kPiece) {
+        const int np = min(2 * G, (cend - c0 + kPiece - 1) / kPiece);
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int pc = grp + h * G;
+            const int32_t p0 = c0 + pc * kPiece;
+            const int32_t n = pc < np ? min(kPiece, cend - p0) : 0;
+            float4 g[NV];
+            sum_rows16<LPB, NV>(perm_a, r.x + p0, n, src, D, lane, g);
+#pragma unroll
+            for (int kk = 0; kk < NV; kk++) s_part[pc][kk * LPB + lane] = g[kk];
+        }
+        __syncthreads();
+        const int nblk = (np + CH - 1) / CH;
+        float4 sub[NV];
+        if (grp < nblk) {
+            const int q0 = grp * CH, q1 = min(np, q0 + CH);
+#pragma unroll
+            for (int kk = 0; kk < NV; kk++) sub[kk] = s_part[q0][kk * LPB + lane];
+            for (int q = q0 + 1; q < q1; q++)
+#pragma unroll
+                for (int kk = 0; kk < NV; kk++) add4(sub[kk], s_part[q][kk * LPB + lane]);
+        }
+        __syncthreads();
+        if (grp < nblk)
+#pragma unroll
+            for (int kk = 0; kk < NV; kk++) s_part[nblk_total + grp][kk * LPB + lane] = sub[kk];
+        nblk_total += nblk;
+        __syncthreads();
+    }
+    float4 tot[NV];
+#pragma unroll
+    for (int kk = 0; kk < NV; kk++) tot[kk] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r2.w == 1) {
+        if (grp == 0)
+            for (int j = 0; j < nblk_total; j++)
+#pragma unroll
+                for (int kk = 0; kk < NV; kk++) add4(tot[kk], s_part[j][kk * LPB + lane]);
+    } else {
+        // publish this chunk's block sums; the last-arriving chunk combines
+        if (grp < nblk_total) {
+            float4* pp = reinterpret_cast<float4*>(lpart + ((int64_t)lb * 8 + grp) * D) + lane;
+#pragma unroll
+            for (int kk = 0; kk < NV; kk++) __stcg(pp + kk * LPB, s_part[grp][kk * LPB + lane]);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const uint32_t old = atomicAdd(&lcnt[k], 1u);
+            s_last = old == (uint32_t)(r2.w - 1);
+            if (s_last) __threadfence();
+        }
+        __syncthreads();
+        if (!s_last) return;
+        if (grp == 0) {
+            for (int32_t cc = 0; cc < r2.w; cc++) {
+                const int32_t len_c = min(kChunk, r.y - cc * kChunk);
+                const int nb = ((len_c + kPiece - 1) / kPiece + CH - 1) / CH;
+                const int64_t base = (int64_t)(r2.z + cc) * 8;
+                for (int j = 0; j < nb; j++) {
+                    const float4* rp = reinterpret_cast<const float4*>(lpart + (base + j) * D) + lane;
+#pragma unroll
+                    for (int kk = 0; kk < NV; kk++) add4(tot[kk], __ldcg(rp + kk * LPB));
+                }
+            }
+            if (threadIdx.x == 0) lcnt[k] = 0u;
+        }
+    }
+    if (kPDL) pdl_wait();
+    if (grp == 0) {
+        if (emit) {
+            float4* o = reinterpret_cast<float4*>(grad_out + (int64_t)r.w * D) + lane;
+#pragma unroll
+            for (int kk = 0; kk < NV; kk++) o[kk * LPB] = tot[kk];
+        } else {
+            float4* w = reinterpret_cast<float4*>(W + (int64_t)r.z * D) + lane;
+            bool bad = false;
+#pragma unroll
+            for (int kk = 0; kk < NV; kk++) {
+                float4 x = w[kk * LPB];
+                x.x = __fmaf_rn(-lr, tot[kk].x, x.x);
+                x.y = __fmaf_rn(-lr, tot[kk].y, x.y);
+                x.z = __fmaf_rn(-lr, tot[kk].z, x.z);
+                x.w = __fmaf_rn(-lr, tot[kk].w, x.w);
+                bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
+                w[kk * LPB] = x;
+                if (kFused) s_part[0][kk * LPB + lane] = x;
+            }
+            if (bad) atomicOr(err, kErrNonfinite);
+        }
+    }
+    if (kFused && r2.x >= 0) {
+        __syncthreads();
+        float4 v[NV];
+#pragma unroll
+        for (int kk = 0; kk < NV; kk++) v[kk] = s_part[0][kk * LPB + lane];
+        write_y<LPB, NV>(v, perm_b, r2.x, r2.y, Y, D, lane, grp, G);
+    }
+}
+
 // a9 + a10 over one grouped batch, no cross-CTA communication.  Block ranges:
 //  short:  one LPB-lane group per segment of <= kPiece lookups;
 //  medium: one warp per segment of <= kMedium lookups: each of the warp's
@@ -127,10 +286,11 @@ struct PieceSum {
 // the W read-modify-write waits for the forward of this batch.
 template <int LPB, int NV, bool kPDL>
 __device__ __forceinline__ void reduce_segments(const SegRec* __restrict__ rec, int64_t n_short,
-                                                int64_t n_med, int64_t n_long,
+                                                int64_t n_med, int64_t n_long, int64_t n_lchunk,
                                                 const int32_t* __restrict__ perm,
                                                 const float* __restrict__ src, int D, float* W,
-                                                float lr, int emit, float* grad_out, uint32_t* err) {
+                                                float lr, float* lpart, uint32_t* lcnt, int emit,
+                                                float* grad_out, uint32_t* err) {
     constexpr int G = 256 / LPB;     // groups per block
     constexpr int GW = 32 / LPB;     // groups per warp
     constexpr int CH = kPiece / NV > 4 ? kPiece / NV : 4;
@@ -142,8 +302,8 @@ __device__ __forceinline__ void reduce_segments(const SegRec* __restrict__ rec, 
     int64_t b = blockIdx.x;
     const int64_t short_blocks = (n_short + G - 1) / G;
     const int64_t med_blocks = (n_med + 7) / 8;
-    if (b >= n_long) {
-        b -= n_long;
+    if (b >= n_lchunk) {
+        b -= n_lchunk;
         if (b < med_blocks) {
             const int64_t m = b * 8 + (threadIdx.x >> 5);
             if (m >= n_med) return;
@@ -187,52 +347,219 @@ __device__ __forceinline__ void reduce_segments(const SegRec* __restrict__ rec, 
         seg_finish<LPB, NV>(g, lane, r.z, r.w, W, D, lr, emit, grad_out, err);
         return;
     }
-    // long segment b: one CTA; a pass covers up to 2G pieces (group j takes
-    // pieces j and j + G), the partials go to shared memory, CH-piece block
-    // sums are formed in parallel (one group per block), and group 0 adds
-    // the block sums in order.  2G is a multiple of CH, so blocks never
-    // straddle passes.
-    const int4 r = __ldg(reinterpret_cast<const int4*>(rec + n_short + n_med + b));
-    float4 tot[NV];
+    long_chunk<LPB, NV, kPDL, false>(rec + n_short + n_med, n_long, b, perm, nullptr, src, D, W, lr, lpart,
+                                     lcnt, emit, grad_out, nullptr, err);
+}
+
+// ---------------------------------------------------------------------------
+// Fused step (single-lookup bags, world 1): kernel K(i) of a run does the
+// backward + SGD of batch a = i-1 AND the forward of batch b = i.
+//  * the unit that finishes row r of batch a (new W[r] in registers) also
+//    writes Y_b[bag] = new W[r] for every bag of batch b that looks up r
+//    (SegRec.npos/nlen: the same row's segment in batch b);
+//  * rows of batch b absent from batch a (FreeRecs of b) are gathered from W
+//    after griddepcontrol.wait (their last writer is K(i-1) or earlier).
+// Y_b = W (after batch a's update)[idx_b] exactly as the separate forward,
+// and the update of batch a is the same arithmetic as k_grp_reduce_pdl, so
+// results are bit-identical to the two-kernel path.  One kernel boundary per
+// step instead of two.
+// ---------------------------------------------------------------------------
+// W[row] -= lr * g; returns the new row part of this lane in v
+template <int LPB, int NV>
+__device__ __forceinline__ void sgd_row(const float4 (&g)[NV], int lane, int32_t row, float* W, int D,
+                                        float lr, uint32_t* err, float4 (&v)[NV]) {
+    float4* w = reinterpret_cast<float4*>(W + (int64_t)row * D) + lane;
+    bool bad = false;
 #pragma unroll
-    for (int k = 0; k < NV; k++) tot[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int32_t c0 = 0; c0 < r.y; c0 += 2 * G * kPiece) {
-        const int np = min(2 * G, (r.y - c0 + kPiece - 1) / kPiece);
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const int pc = grp + h * G;
-            const int32_t p0 = c0 + pc * kPiece;
-            const int32_t n = pc < np ? min(kPiece, r.y - p0) : 0;
-            float4 g[NV];
-            sum_rows16<LPB, NV>(perm, r.x + p0, n, src, D, lane, g);
-#pragma unroll
-            for (int k = 0; k < NV; k++) s_part[pc][k * LPB + lane] = g[k];
-        }
-        __syncthreads();
-        const int nblk = (np + CH - 1) / CH;
-        float4 sub[NV];
-        if (grp < nblk) {
-            const int q0 = grp * CH, q1 = min(np, q0 + CH);
-#pragma unroll
-            for (int k = 0; k < NV; k++) sub[k] = s_part[q0][k * LPB + lane];
-            for (int q = q0 + 1; q < q1; q++)
-#pragma unroll
-                for (int k = 0; k < NV; k++) add4(sub[k], s_part[q][k * LPB + lane]);
-        }
-        __syncthreads();
-        if (grp < nblk)
-#pragma unroll
-            for (int k = 0; k < NV; k++) s_part[grp][k * LPB + lane] = sub[k];
-        __syncthreads();
-        if (grp == 0)
-            for (int j = 0; j < nblk; j++)
-#pragma unroll
-                for (int k = 0; k < NV; k++) add4(tot[k], s_part[j][k * LPB + lane]);
-        __syncthreads();
+    for (int k = 0; k < NV; k++) {
+        float4 x = w[k * LPB];
+        x.x = __fmaf_rn(-lr, g[k].x, x.x);
+        x.y = __fmaf_rn(-lr, g[k].y, x.y);
+        x.z = __fmaf_rn(-lr, g[k].z, x.z);
+        x.w = __fmaf_rn(-lr, g[k].w, x.w);
+        bad |= !(isfinite(x.x) && isfinite(x.y) && isfinite(x.z) && isfinite(x.w));
+        w[k * LPB] = x;
+        v[k] = x;
     }
-    if (grp == 0) {
-        if (kPDL) pdl_wait();
-        seg_finish<LPB, NV>(tot, lane, r.z, r.w, W, D, lr, emit, grad_out, err);
+    if (bad) atomicOr(err, kErrNonfinite);
+}
+
+template <int LPB, int NV>
+__device__ __forceinline__ void load_row(const float* __restrict__ W, int32_t row, int D, int lane,
+                                         float4 (&v)[NV]) {
+    const float4* w = reinterpret_cast<const float4*>(W + (int64_t)row * D) + lane;
+#pragma unroll
+    for (int k = 0; k < NV; k++) v[k] = w[k * LPB];
+}
+
+// Part R over batch a (blocks [0, red_blocks)) with links into batch b.
+template <int LPB, int NV>
+__device__ __forceinline__ void fused_reduce(const SegRec* __restrict__ rec, int64_t n_short, int64_t n_med,
+                                             int64_t n_long, int64_t n_lchunk, int64_t b,
+                                             const int32_t* __restrict__ perm_a,
+                                             const int32_t* __restrict__ perm_b, const float* __restrict__ src,
+                                             int D, float* W, float lr, float* lpart, uint32_t* lcnt, float* Y,
+                                             uint32_t* err) {
+    constexpr int G = 256 / LPB;
+    constexpr int GW = 32 / LPB;
+    constexpr int CH = kPiece / NV > 4 ? kPiece / NV : 4;
+    __shared__ float4 s_part[2 * G][NV * LPB];
+    const int lane = threadIdx.x % LPB;
+    const int grp = threadIdx.x / LPB;
+    const int64_t short_blocks = (n_short + G - 1) / G;
+    const int64_t med_blocks = (n_med + 7) / 8;
+    if (b >= n_lchunk) {
+        b -= n_lchunk;
+        if (b < med_blocks) {
+            const int64_t m = b * 8 + (threadIdx.x >> 5);
+            if (m >= n_med) return;
+            const SegRec* rp = rec + n_short + m;
+            const int4 r = __ldg(reinterpret_cast<const int4*>(rp));
+            const int2 nx = __ldg(reinterpret_cast<const int2*>(rp) + 2);
+            const int gi = (threadIdx.x & 31) / LPB;
+            PieceSum<NV> ps;
+            ps.init();
+            for (int32_t c0 = 0; c0 < r.y; c0 += GW * kPiece) {
+                const int32_t p0 = c0 + gi * kPiece;
+                const int32_t n = p0 < r.y ? min(kPiece, r.y - p0) : 0;
+                float4 g[NV];
+                sum_rows16<LPB, NV>(perm_a, r.x + p0, n, src, D, lane, g);
+                const int ng = min(GW, (r.y - c0 + kPiece - 1) / kPiece);
+                for (int j = 0; j < ng; j++) {
+                    float4 p[NV];
+#pragma unroll
+                    for (int k = 0; k < NV; k++) {
+                        p[k].x = __shfl_sync(0xffffffffu, g[k].x, j * LPB + lane);
+                        p[k].y = __shfl_sync(0xffffffffu, g[k].y, j * LPB + lane);
+                        p[k].z = __shfl_sync(0xffffffffu, g[k].z, j * LPB + lane);
+                        p[k].w = __shfl_sync(0xffffffffu, g[k].w, j * LPB + lane);
+                    }
+                    ps.template add<CH>(p);
+                }
+            }
+            ps.flush();
+            pdl_wait();
+            float4 v[NV];
+            if (gi == 0) sgd_row<LPB, NV>(ps.tot, lane, r.z, W, D, lr, err, v);
+            if (nx.x >= 0) {
+#pragma unroll
+                for (int k = 0; k < NV; k++) {   // broadcast group 0's new row to the warp
+                    v[k].x = __shfl_sync(0xffffffffu, v[k].x, lane);
+                    v[k].y = __shfl_sync(0xffffffffu, v[k].y, lane);
+                    v[k].z = __shfl_sync(0xffffffffu, v[k].z, lane);
+                    v[k].w = __shfl_sync(0xffffffffu, v[k].w, lane);
+                }
+                write_y<LPB, NV>(v, perm_b, nx.x, nx.y, Y, D, lane, gi, GW);
+            }
+            return;
+        }
+        b -= med_blocks;
+        if (b >= short_blocks) return;
+        const int64_t q = b * G + grp;
+        if (q >= n_short) return;
+        const SegRec* rp = rec + q;
+        const int4 r = __ldg(reinterpret_cast<const int4*>(rp));
+        const int2 nx = __ldg(reinterpret_cast<const int2*>(rp) + 2);
+        float4 g[NV];
+        sum_rows16<LPB, NV>(perm_a, r.x, r.y, src, D, lane, g);
+        pdl_wait();
+        float4 v[NV];
+        sgd_row<LPB, NV>(g, lane, r.z, W, D, lr, err, v);
+        if (nx.x >= 0) write_y<LPB, NV>(v, perm_b, nx.x, nx.y, Y, D, lane, 0, 1);
+        return;
+    }
+    long_chunk<LPB, NV, true, true>(rec + n_short + n_med, n_long, b, perm_a, perm_b, src, D, W, lr, lpart, lcnt,
+                                    0, nullptr, Y, err);
+}
+
+template <int LPB, int NV, int MB>
+__global__ void __launch_bounds__(256, MB)
+k_grp_fused_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ run, int64_t* base, int s,
+                int last_step, uint32_t* done_ctr, const SegRec* __restrict__ rec,
+                const FreeRec* __restrict__ freer, const int32_t* __restrict__ perm,
+                const float* __restrict__ dY, int64_t n_dy, int64_t dy_stride, int D, float* W, float lr,
+                float* lpart, uint32_t* lcnt, float* __restrict__ Y, uint32_t* err,
+                unsigned long long* stamps, int trig) {
+    constexpr int G = 256 / LPB;
+    if (!(trig & 1)) pdl_trigger();
+    const int64_t b0 = *base;
+    const int64_t rel = b0 + s;          // kernel index in the run: 0 .. n
+    const int64_t n = run[1];
+    if (rel <= n) {
+        if (stamps && threadIdx.x == 0) {
+            atomicMin(&stamps[rel * 8 + 4], (unsigned long long)gtimer());
+            pdl_wait();
+            atomicMin(&stamps[rel * 8 + 2], (unsigned long long)gtimer());
+        }
+        const int64_t first = run[0];
+        const bool has_a = rel >= 1, has_b = rel < n;
+        int64_t bid = blockIdx.x;
+        int64_t red_blocks = 0;
+        const int32_t* perm_b = nullptr;
+        BatchDesc db{};
+        if (has_b) {
+            db = desc[first + rel];
+            perm_b = perm + db.lk0;
+        }
+        if (has_a) {
+            const BatchDesc da = desc[first + rel - 1];
+            const int64_t n_long = (da.sb1 - da.sb0) - da.n_short - da.n_med;
+            red_blocks = da.n_lchunk + (da.n_med + 7) / 8 + (da.n_short + G - 1) / G;
+            if (bid < red_blocks) {
+                fused_reduce<LPB, NV>(rec + da.sb0, da.n_short, da.n_med, n_long, da.n_lchunk, bid, perm + da.lk0,
+                                      perm_b, dY + ((rel - 1) % n_dy) * dy_stride, D, W, lr, lpart, lcnt, Y, err);
+            }
+        }
+        if (has_b && bid >= red_blocks) {
+            // forward of batch b for rows not produced by part R: the free list
+            // of b when batch a is in this kernel, else every segment of b
+            bid -= red_blocks;
+            const int lane = threadIdx.x % LPB;
+            const int64_t q = bid * G + threadIdx.x / LPB;
+            int32_t pos = -1, len = 0, row = 0;
+            if (has_a) {
+                if (q < db.n_free) {
+                    const int4 f = __ldg(reinterpret_cast<const int4*>(freer + db.sb0 + q));
+                    pos = f.x;
+                    len = f.y;
+                    row = f.z;
+                }
+            } else if (q < db.sb1 - db.sb0) {
+                const int4 r = __ldg(reinterpret_cast<const int4*>(rec + db.sb0 + q));
+                pos = r.x;
+                len = r.y;
+                row = r.z;
+            }
+            if (pos >= 0) {
+                pdl_wait();
+                float4 v[NV];
+                load_row<LPB, NV>(W, row, D, lane, v);
+                write_y<LPB, NV>(v, perm_b, pos, len, Y, D, lane, 0, 1);
+            }
+        }
+        if (stamps) {
+            __syncthreads();
+            if (threadIdx.x == 0) atomicMax(&stamps[rel * 8 + 3], (unsigned long long)gtimer());
+        }
+        if (trig & 1) {
+            pdl_wait();
+            pdl_trigger();
+        }
+    } else if (trig & 1) {
+        pdl_trigger();
+    }
+    if (last_step) {   // the last CTA of the replay's last kernel advances the base
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            pdl_wait();
+            __threadfence();
+            const uint32_t old = atomicAdd(done_ctr, 1u);
+            if (old == gridDim.x - 1) {
+                *done_ctr = 0u;
+                *base = b0 + last_step;
+                __threadfence();
+            }
+        }
     }
 }
 
@@ -259,13 +586,14 @@ __global__ void __launch_bounds__(256)
 k_grp_reduce(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ run,
              int64_t* cursor, uint32_t* done_ctr, const SegRec* __restrict__ rec,
              const int32_t* __restrict__ perm, const float* __restrict__ dY, int64_t n_dy,
-             int64_t dy_stride, int D, float* W, float lr, int emit, float* grad_out, uint32_t* err) {
+             int64_t dy_stride, int D, float* W, float lr, float* lpart, uint32_t* lcnt, int emit,
+             float* grad_out, uint32_t* err) {
     const int64_t i = *cursor;
     if (i < run[1]) {
         const BatchDesc d = desc[run[0] + i];
         reduce_segments<LPB, NV, false>(rec + d.sb0, d.n_short, d.n_med, (d.sb1 - d.sb0) - d.n_short - d.n_med,
-                                        perm + d.lk0,
-                                        dY + (i % n_dy) * dy_stride, D, W, lr, emit, grad_out, err);
+                                        d.n_lchunk, perm + d.lk0, dY + (i % n_dy) * dy_stride, D, W, lr, lpart,
+                                        lcnt, emit, grad_out, err);
     }
     __syncthreads();
     if (threadIdx.x == 0) {   // the last CTA to finish advances the cursor
@@ -323,7 +651,7 @@ k_grp_reduce_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__
                  int64_t* base, int s, int last_step, uint32_t* done_ctr,
                  const SegRec* __restrict__ rec, const int32_t* __restrict__ perm,
                  const float* __restrict__ dY, int64_t n_dy, int64_t dy_stride, int D, float* W,
-                 float lr, uint32_t* err, unsigned long long* stamps, int trig) {
+                 float lr, float* lpart, uint32_t* lcnt, uint32_t* err, unsigned long long* stamps, int trig) {
     if (!(trig & 1)) pdl_trigger();
     const int64_t b0 = *base;
     const int64_t rel = b0 + s;
@@ -335,12 +663,12 @@ k_grp_reduce_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__
             atomicMin(&stamps[rel * 8 + 2], (unsigned long long)gtimer());
         }
         const int64_t n_long = (d.sb1 - d.sb0) - d.n_short - d.n_med;
-        reduce_segments<LPB, NV, true>(rec + d.sb0, d.n_short, d.n_med, n_long, perm + d.lk0,
-                                       dY + (rel % n_dy) * dy_stride, D, W, lr, 0, nullptr, err);
+        reduce_segments<LPB, NV, true>(rec + d.sb0, d.n_short, d.n_med, n_long, d.n_lchunk, perm + d.lk0,
+                                       dY + (rel % n_dy) * dy_stride, D, W, lr, lpart, lcnt, 0, nullptr, err);
         if (stamps) {   // per-tier completion: [6] long CTAs, [7] short/medium CTAs
             __syncthreads();
             if (threadIdx.x == 0)
-                atomicMax(&stamps[rel * 8 + (blockIdx.x < n_long ? 6 : 7)], (unsigned long long)gtimer());
+                atomicMax(&stamps[rel * 8 + (blockIdx.x < d.n_lchunk ? 6 : 7)], (unsigned long long)gtimer());
         }
         if (trig & 1) {
             pdl_wait();
@@ -394,10 +722,10 @@ static void launch_grp_step(Ctx* c, cudaStream_t s, float* W, int64_t H, int D, 
                                                        W, H, D, Y, c->d_err);
     if (mid) cudaEventRecordWithFlags(mid, s, cudaEventRecordExternal);
     (void)maxb;
-    const int64_t rb = std::max<int64_t>(1, cdiv(g.max_short, gpb) + cdiv(g.max_med, 8) + g.max_long);
+    const int64_t rb = std::max<int64_t>(1, cdiv(g.max_short, gpb) + cdiv(g.max_med, 8) + g.max_lchunk);
     k_grp_reduce<LPB, NV><<<(unsigned)rb, threads, 0, s>>>(g.desc, g.run, g.cursor, g.done_ctr, g.rec, g.perm,
-                                                          dY, n_dy, g.max_bags * (int64_t)D, D, W, lr, emit,
-                                                          c->ws.grad, c->d_err);
+                                                          dY, n_dy, g.max_bags * (int64_t)D, D, W, lr, g.lpart,
+                                                          g.lcnt, emit, c->ws.grad, c->d_err);
 }
 
 template <int LPB, int NV>
@@ -422,14 +750,62 @@ static fae_status launch_pdl_step(Ctx* c, cudaStream_t st, int s, float* W, int6
     FAE_CUDA(c, cudaLaunchKernelEx(&cfg, k_grp_fwd_pdl<LPB, NV>, (const BatchDesc*)g.desc, (const int64_t*)g.run,
                                    (const int64_t*)g.cursor, s, g.hot_idx, g.hot_off, (int)g.P, (const float*)W, H, D,
                                    Y, c->d_err, stamps, c->pdl_trig));
-    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, cdiv(g.max_short, gpb) + cdiv(g.max_med, 8) + g.max_long));
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, cdiv(g.max_short, gpb) + cdiv(g.max_med, 8) + g.max_lchunk));
     const int last = (s == kUnroll - 1) ? kUnroll : 0;
     auto kern = c->red_mb >= 8 ? k_grp_reduce_pdl<LPB, NV, 8>
               : (c->red_mb >= 6 ? k_grp_reduce_pdl<LPB, NV, 6> : k_grp_reduce_pdl<LPB, NV, 4>);
     FAE_CUDA(c, cudaLaunchKernelEx(&cfg, kern, (const BatchDesc*)g.desc, (const int64_t*)g.run,
                                    g.cursor, s, last, g.done_ctr, (const SegRec*)g.rec, (const int32_t*)g.perm,
-                                   dY, n_dy, g.max_bags * (int64_t)D, D, W, lr, c->d_err, stamps, c->pdl_trig));
+                                   dY, n_dy, g.max_bags * (int64_t)D, D, W, lr,
+                                   g.lpart + (int64_t)s * std::max<int64_t>(g.max_lchunk, 1) * 8 * D,
+                                   g.lcnt + (int64_t)s * std::max<int64_t>(g.max_long, 1), c->d_err, stamps,
+                                   c->pdl_trig));
     return FAE_OK;
+}
+
+template <int LPB, int NV>
+static fae_status launch_fused_step(Ctx* c, cudaStream_t st, int s, float* W, int64_t H, int D,
+                                    const float* dY, int64_t n_dy, float* Y, float lr,
+                                    unsigned long long* stamps) {
+    Group& g = c->grp;
+    constexpr int G = 256 / LPB;
+    int64_t red = 0;
+    for (const BatchDesc& d : g.hdesc) {
+        const int64_t nl = (d.sb1 - d.sb0) - d.n_short - d.n_med;
+        (void)nl;
+        red = std::max<int64_t>(red, d.n_lchunk + cdiv(d.n_med, 8) + cdiv(d.n_short, G));
+    }
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = c->no_pdl ? 0 : 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, red + cdiv(g.max_segs, G)));
+    const int last = (s == kUnroll - 1) ? kUnroll : 0;
+    auto kern = c->red_mb >= 8 ? k_grp_fused_pdl<LPB, NV, 8>
+              : (c->red_mb >= 6 ? k_grp_fused_pdl<LPB, NV, 6> : k_grp_fused_pdl<LPB, NV, 4>);
+    (void)H;
+    FAE_CUDA(c, cudaLaunchKernelEx(&cfg, kern, (const BatchDesc*)g.desc, (const int64_t*)g.run, g.cursor, s, last,
+                                   g.done_ctr, (const SegRec*)g.rec, (const FreeRec*)g.freer, (const int32_t*)g.perm,
+                                   dY, n_dy, g.max_bags * (int64_t)D, D, W, lr,
+                                   g.lpart + (int64_t)s * std::max<int64_t>(g.max_lchunk, 1) * 8 * D,
+                                   g.lcnt + (int64_t)s * std::max<int64_t>(g.max_long, 1), Y, c->d_err, stamps,
+                                   c->pdl_trig));
+    return FAE_OK;
+}
+
+static fae_status launch_fused(Ctx* c, cudaStream_t st, int s, float* W, int64_t H, int D, const float* dY,
+                               int64_t n_dy, float* Y, float lr, unsigned long long* stamps) {
+    FAE_DISPATCH_D(D, return launch_fused_step, c, st, s, W, H, D, dY, n_dy, Y, lr, stamps);
+    return FAE_OK;
+}
+
+static bool use_fused(Ctx* c) {
+    const Group& g = c->grp;
+    return g.P == 1 && !g.hot_off && c->world == 1 && !c->no_fused;
 }
 
 static fae_status launch_step(Ctx* c, cudaStream_t s, float* W, int64_t H, int D, const float* dY,
@@ -460,6 +836,8 @@ static fae_status capture(Ctx* c, cudaGraphExec_t* out, float* W, int64_t H, int
             cudaEventRecordWithFlags(ev[3 * s], cs, cudaEventRecordExternal);
             st = launch_step(c, cs, W, H, D, dY, n_dy, Y, lr, 0, ev[3 * s + 1]);
             cudaEventRecordWithFlags(ev[3 * s + 2], cs, cudaEventRecordExternal);
+        } else if (use_fused(c)) {
+            st = launch_fused(c, cs, s, W, H, D, dY, n_dy, Y, lr, stamps);
         } else {
             st = launch_pdl(c, cs, s, W, H, D, dY, n_dy, Y, lr, stamps);
         }
@@ -487,7 +865,7 @@ void group_free(Ctx* c) {
     for (int v = 0; v < 2; v++)
         for (int e = 0; e < 3 * kUnroll; e++)
             if (g.tev[v][e]) cudaEventDestroy(g.tev[v][e]);
-    void* ptrs[] = {g.desc, g.perm, g.rec, g.keys[0], g.keys[1], g.vals, g.seg_start, g.seg_row,
+    void* ptrs[] = {g.desc, g.perm, g.rec, g.freer, g.nxt, g.lpart, g.lcnt, g.keys[0], g.keys[1], g.vals, g.seg_start, g.seg_row,
                     g.tile_start, g.tile_batch, g.sstatus, g.pstatus, g.ghist, g.cursor, g.done_ctr, g.stamps};
     for (void* p : ptrs) cudaFree(p);
     g = Group{};
@@ -504,6 +882,7 @@ extern "C" fae_status fae_set_kernel_timing(fae_ctx* h, int32_t enable) {
     h->c.t_n[0] = h->c.t_n[1] = 0;
     h->c.t_overlap_n = 0;
     h->c.t_tier_ms[0] = h->c.t_tier_ms[1] = 0.0;
+    h->c.t_fused = false;
     h->c.t_red_entry_lead_ms = 0.0;
     return FAE_OK;
 }
@@ -513,9 +892,11 @@ extern "C" fae_status fae_get_kernel_timing(const fae_ctx* h, double* ms, int64_
     ms[0] = h->c.t_ms[0];
     ms[1] = h->c.t_ms[1];
     ms[2] = h->c.t_red_entry_lead_ms;
+    ms[3] = 0.0;
     n[0] = h->c.t_n[0];
     n[1] = h->c.t_n[1];
     n[2] = h->c.t_overlap_n;
+    n[3] = h->c.t_fused ? 1 : 0;
     return FAE_OK;
 }
 
@@ -574,9 +955,13 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
     mix((uint64_t)g.max_short);
     mix((uint64_t)g.max_long);
     mix((uint64_t)g.max_med);
+    mix((uint64_t)g.max_lchunk);
+    mix((uint64_t)(uintptr_t)g.lpart);
     mix((uint64_t)g.max_bags);
     mix((uint64_t)(uintptr_t)c->d_err);
-    const int64_t reps = cdiv(n, kUnroll);
+    const bool fused = use_fused(c) && c->timing != 2;
+    const int64_t reps = cdiv(fused ? n + 1 : n, kUnroll);
+    mix((uint64_t)fused);
     if (c->timing == 2) {
         // event mode (cross-check): event nodes between the kernels (this
         // serialises the PDL edges); two graph instances so replay r+1 runs
@@ -623,15 +1008,15 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
     }
     unsigned long long* stamps = nullptr;
     if (c->timing == 1) {
-        if (g.stamp_cap < n) {
+        if (g.stamp_cap < n + 1) {
             cudaFree(g.stamps);
             g.stamps = nullptr;
             g.stamp_cap = n + n / 4 + 64;
             FAE_CUDA(c, cudaMalloc(&g.stamps, sizeof(unsigned long long) * 8 * g.stamp_cap));
         }
         stamps = g.stamps;
-        std::vector<unsigned long long> init(8 * n);
-        for (int64_t i = 0; i < n; i++) {
+        std::vector<unsigned long long> init(8 * (n + 1));
+        for (int64_t i = 0; i <= n; i++) {
             init[8 * i + 0] = ~0ull;
             init[8 * i + 1] = 0;
             init[8 * i + 2] = ~0ull;
@@ -641,7 +1026,7 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
             init[8 * i + 6] = 0;
             init[8 * i + 7] = 0;   // tier ends
         }
-        FAE_CUDA(c, cudaMemcpyAsync(stamps, init.data(), sizeof(unsigned long long) * 8 * n,
+        FAE_CUDA(c, cudaMemcpyAsync(stamps, init.data(), sizeof(unsigned long long) * 8 * (n + 1),
                                     cudaMemcpyHostToDevice, c->stream));
         FAE_CUDA(c, cudaStreamSynchronize(c->stream));
     }
@@ -656,7 +1041,24 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
     }
     for (int64_t r = 0; r < reps; r++) FAE_CUDA(c, cudaGraphLaunch(g.graph, c->stream));
     c->launches += 2 * reps * g.graph_steps;
-    if (stamps) {
+    if (stamps && fused) {
+        // one kernel per step: K(i)'s exclusive share runs from the end of
+        // K(i-1) (same replay) to its own end; attributed to slot 1
+        std::vector<unsigned long long> st(8 * (n + 1));
+        FAE_CUDA(c, cudaMemcpyAsync(st.data(), stamps, sizeof(unsigned long long) * 8 * (n + 1),
+                                    cudaMemcpyDeviceToHost, c->stream));
+        FAE_CUDA(c, cudaStreamSynchronize(c->stream));
+        for (int64_t i = 0; i <= n; i++) {
+            const unsigned long long rs = st[8 * i + 2], re = st[8 * i + 3];
+            if (re == 0) continue;
+            unsigned long long r0 = rs;
+            if (i > 0 && (i % kUnroll) != 0 && st[8 * (i - 1) + 3] > r0) r0 = st[8 * (i - 1) + 3];
+            if (i > 0 && st[8 * i + 4] < st[8 * (i - 1) + 3]) c->t_overlap_n++;
+            c->t_ms[1] += re > r0 ? (double)(re - r0) * 1e-6 : 0.0;
+            c->t_n[1]++;
+        }
+        c->t_fused = true;
+    } else if (stamps) {
         // exclusive critical-path share of each kernel: fwd(s) from the end of
         // reduce(s-1) (same replay), reduce(s) from the end of fwd(s)
         std::vector<unsigned long long> st(8 * n);

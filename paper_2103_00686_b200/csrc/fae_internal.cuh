@@ -23,6 +23,7 @@ constexpr int kMaxSortPasses = 4;      // 32-bit keys
 constexpr int kPiece = 16;             // max lookups per reduction piece
 constexpr int kUnroll = 128;           // steps per captured epoch graph
 constexpr int kMedium = 128;           // segments of (kPiece, kMedium] lookups: one warp
+constexpr int kChunk = 512;            // long segments: one CTA per kChunk lookups
 constexpr int kGSThreads = 256;        // grouping sort: threads per tile
 constexpr int kGSItems = 16;           // grouping sort: items per thread
 constexpr int kGSTile = kGSThreads * kGSItems;   // 4096 lookups per tile
@@ -86,7 +87,10 @@ struct BatchDesc {
     int64_t sb0, sb1;      // segments [sb0, sb1) (records: short first)
     int32_t n_short;       // segments of <= kPiece lookups (records first)
     int32_t n_med;         // then segments of <= kMedium lookups; then the long ones
-    int32_t n_bags, pad;
+    int32_t n_bags;
+    int32_t n_free;        // segments whose row is not in batch b-1 (FreeRecs at sb0)
+    int32_t n_lchunk;      // chunks of the long segments (one CTA each)
+    int32_t pad;
 };
 
 // One segment (a run of equal hot ids in a grouped batch), batch-local
@@ -98,6 +102,16 @@ struct alignas(16) SegRec {
     int32_t len;    // lookups of the segment
     int32_t row;    // hot id
     int32_t seg;    // segment index in the batch (ascending hot id)
+    int32_t npos;   // same row in the NEXT batch: its first position, or -1
+    int32_t nlen;   //   and its number of lookups (0 if absent)
+    int32_t c0;     // long segments: index of its first kChunk-chunk in the batch
+    int32_t nc;     //   and its number of chunks (1 otherwise)
+};
+
+// A segment of batch b whose row is not in batch b-1 (the fused step gathers
+// it for the forward of batch b); 16 bytes.
+struct alignas(16) FreeRec {
+    int32_t pos, len, row, pad;
 };
 
 struct Group {
@@ -114,6 +128,12 @@ struct Group {
     // grouping result
     int32_t* perm = nullptr;          // [L_total] local bag index, grouped by hot id
     SegRec* rec = nullptr;            // [S_total]
+    FreeRec* freer = nullptr;         // [S_total] (per batch at sb0, n_free entries)
+    int32_t* nxt = nullptr;           // [S_total] link to the next batch's segment (local) or -1
+    int64_t max_free = 0;
+    int64_t max_lchunk = 0;
+    float* lpart = nullptr;           // [kUnroll][max_lchunk][8][max_dim] chunk block sums
+    uint32_t* lcnt = nullptr;         // [kUnroll][max_long] arrival counters (kept zero)
     int64_t cap_L = 0, cap_R = 0;
     // grouping scratch (kept for reuse)
     uint32_t* keys[2] = {nullptr, nullptr};
@@ -173,6 +193,8 @@ struct Ctx {
     double t_red_entry_lead_ms = 0.0; // sum of (fwd end - reduce entry)
     double t_tier_ms[2] = {0.0, 0.0}; // reduce tiers' completion after fwd end
     bool no_pdl = false;              // FAE_NO_PDL=1: plain serialized launches
+    bool no_fused = true;             // FAE_FUSED=1: one fused kernel per step for P = 1
+    bool t_fused = false;             // timing came from the fused kernel
     int red_mb = 4;                   // FAE_RED_MB: min resident reduce CTAs per SM (4/6/8)
     int pdl_trig = 0;                 // FAE_PDL_TRIG bit0: reduce triggers after its wait, bit1: fwd too
 };

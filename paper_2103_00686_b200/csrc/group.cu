@@ -252,12 +252,73 @@ k_gs_segments(const uint32_t* __restrict__ keys, const int64_t* __restrict__ til
     }
 }
 
+// one block per batch b (grid-stride): link each segment t of batch b to
+// the segment of batch b-1 with the same row (binary search in b-1's
+// ascending rows): nxt[σ] = t; segments without one go to batch b's free
+// list (stable order) and desc[b].n_free.
+__global__ void __launch_bounds__(256)
+k_gs_links(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __restrict__ seg_start,
+           const int32_t* __restrict__ seg_row, int32_t* __restrict__ nxt, FreeRec* __restrict__ freer) {
+    __shared__ uint32_t s_w[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int64_t b = blockIdx.x; b < n_batches; b += gridDim.x) {
+        const BatchDesc d = desc[b];
+        const int64_t S = d.sb1 - d.sb0;
+        int64_t ps0 = 0, ps1 = 0;
+        if (b > 0) {
+            ps0 = desc[b - 1].sb0;
+            ps1 = desc[b - 1].sb1;
+        }
+        uint32_t run = 0;
+        for (int64_t q0 = 0; q0 < S; q0 += 256) {
+            const int64_t q = q0 + tid;
+            bool fr = false;
+            int32_t row = 0;
+            if (q < S) {
+                row = seg_row[d.sb0 + q];
+                int64_t lo = ps0, hi = ps1;   // first position with seg_row >= row
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi) >> 1;
+                    if (seg_row[mid] < row) lo = mid + 1;
+                    else hi = mid;
+                }
+                if (lo < ps1 && seg_row[lo] == row) nxt[lo] = (int32_t)q;
+                else fr = true;
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, fr);
+            __syncthreads();
+            if (lane == 0) s_w[warp] = __popc(bal);
+            __syncthreads();
+            uint32_t pre = 0, tot = 0;
+            for (int w = 0; w < 8; w++) {
+                if (w < warp) pre += s_w[w];
+                tot += s_w[w];
+            }
+            if (fr) {
+                const int64_t s = d.sb0 + q;
+                const int64_t st = seg_start[s];
+                const int64_t e = q + 1 < S ? seg_start[s + 1] : d.lk1;
+                FreeRec f;
+                f.pos = (int32_t)(st - d.lk0);
+                f.len = (int32_t)(e - st);
+                f.row = row;
+                f.pad = 0;
+                freer[d.sb0 + run + pre + __popc(bal & lanemask_lt())] = f;
+            }
+            run += tot;
+        }
+        if (tid == 0) desc[b].n_free = (int32_t)run;
+        __syncthreads();
+    }
+}
+
 // one block per batch (grid-stride over batches): batch-local SegRecs,
 // stably partitioned by length class (<= kPiece, <= kMedium, longer), each
 // class in ascending hot id; desc[b].n_short, n_med
 __global__ void __launch_bounds__(256)
 k_gs_records(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __restrict__ seg_start,
-             const int32_t* __restrict__ seg_row, SegRec* __restrict__ rec) {
+             const int32_t* __restrict__ seg_row, const int32_t* __restrict__ nxt,
+             SegRec* __restrict__ rec) {
     __shared__ uint32_t s_w[3][8];
     __shared__ uint32_t s_n[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -272,6 +333,18 @@ k_gs_records(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __r
             r.len = (int32_t)(e - st);
             r.row = seg_row[s];
             r.seg = (int32_t)q;
+            r.npos = -1;
+            r.nlen = 0;
+            r.c0 = 0;
+            r.nc = 1;
+            const int32_t t = nxt[s];
+            if (t >= 0 && b + 1 < n_batches) {
+                const BatchDesc& dn = desc[b + 1];
+                const int64_t sn = dn.sb0 + t;
+                const int64_t en = sn + 1 < dn.sb1 ? seg_start[sn + 1] : dn.lk1;
+                r.npos = (int32_t)(seg_start[sn] - dn.lk0);
+                r.nlen = (int32_t)(en - seg_start[sn]);
+            }
             return r.len <= kPiece ? 0 : (r.len <= kMedium ? 1 : 2);
         };
         // pass 1: class sizes
@@ -331,6 +404,17 @@ k_gs_records(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __r
             for (int c = 0; c < 3; c++) run[c] += tot[c];
         }
         __syncthreads();
+        if (tid == 0) {   // chunks of the long segments, in record order
+            int32_t cc = 0;
+            for (int64_t q = (int64_t)base[2]; q < S; q++) {
+                SegRec& lr = rec[d.sb0 + q];
+                lr.c0 = cc;
+                lr.nc = (lr.len + kChunk - 1) / kChunk;
+                cc += lr.nc;
+            }
+            desc[b].n_lchunk = cc;
+        }
+        __syncthreads();
     }
 }
 
@@ -361,6 +445,10 @@ extern "C" fae_status fae_group_info(const fae_ctx* h, int64_t* info) {
     info[3] = g.S_total;
     info[4] = g.max_long;
     info[5] = g.max_bags;
+    int64_t nf = 0;
+    for (const BatchDesc& d : g.hdesc) nf += d.n_free;
+    info[6] = nf;
+    info[7] = g.P == 1 && !g.hot_off && h->c.world == 1 && !h->c.no_fused;
     return FAE_OK;
 }
 
@@ -455,7 +543,10 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
     if ((st = ensure(c, &g.seg_start, &c3, L + 2)) != FAE_OK) return st;
     if ((st = ensure(c, &g.seg_row, &c4, L + 2)) != FAE_OK) return st;
     if ((st = ensure(c, &g.rec, &c5, L + 2)) != FAE_OK) return st;
-    g.cap_S = std::min(std::min(c3, c4), c5);
+    int64_t c6 = g.cap_S, c7 = g.cap_S;
+    if ((st = ensure(c, &g.freer, &c6, L + 2)) != FAE_OK) return st;
+    if ((st = ensure(c, &g.nxt, &c7, L + 2)) != FAE_OK) return st;
+    g.cap_S = std::min(std::min(std::min(c3, c4), c5), std::min(c6, c7));
     if ((st = ensure(c, &g.desc, &g.cap_B, std::max<int64_t>(nb, 1))) != FAE_OK) return st;
     int64_t t1 = g.cap_T, t2 = g.cap_T, t3 = g.cap_T * kSortBins, t4 = g.cap_T;
     if ((st = ensure(c, &g.tile_start, &t1, nt + 2)) != FAE_OK) return st;
@@ -474,6 +565,8 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
     stage("alloc");
     g.S_total = 0;
     g.max_short = g.max_med = g.max_long = 0;
+    g.max_free = 0;
+    g.max_lchunk = 0;
     g.max_segs = 1;
     g.n_long_total = 0;
     if (nb > 0) {
@@ -530,7 +623,10 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
         }
         FAE_CUDA(c, cudaMemcpyAsync(g.desc, g.hdesc.data(), sizeof(BatchDesc) * nb, cudaMemcpyHostToDevice, c->stream));
         const int64_t gr = std::max<int64_t>(1, std::min<int64_t>(nb, (int64_t)sm_count(c) * 8));
-        k_gs_records<<<(unsigned)gr, 256, 0, c->stream>>>(g.desc, nb, g.seg_start, g.seg_row, g.rec);
+        FAE_CUDA(c, cudaMemsetAsync(g.nxt, 0xFF, sizeof(int32_t) * std::max<int64_t>(g.S_total, 1), c->stream));
+        k_gs_links<<<(unsigned)gr, 256, 0, c->stream>>>(g.desc, nb, g.seg_start, g.seg_row, g.nxt, g.freer);
+        FAE_LAUNCHED(c);
+        k_gs_records<<<(unsigned)gr, 256, 0, c->stream>>>(g.desc, nb, g.seg_start, g.seg_row, g.nxt, g.rec);
         FAE_LAUNCHED(c);
         FAE_CUDA(c, cudaMemcpyAsync(g.hdesc.data(), g.desc, sizeof(BatchDesc) * nb, cudaMemcpyDeviceToHost, c->stream));
         st = read_latched(c);
@@ -543,10 +639,22 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
             g.max_med = std::max<int64_t>(g.max_med, d.n_med);
             g.max_long = std::max<int64_t>(g.max_long, nl);
             g.max_segs = std::max<int64_t>(g.max_segs, S);
+            g.max_free = std::max<int64_t>(g.max_free, d.n_free);
+            g.max_lchunk = std::max<int64_t>(g.max_lchunk, d.n_lchunk);
             g.n_long_total += S - d.n_short;
         }
     }
     if (g.max_segs > c->ws.cap_L) return set_err(c, FAE_ERR_CAPACITY, "fae_group_batches: batch segments exceed ctx capacity");
+    cudaFree(g.lpart);
+    cudaFree(g.lcnt);
+    g.lpart = nullptr;
+    g.lcnt = nullptr;
+    {
+        const int64_t lc = std::max<int64_t>(g.max_lchunk, 1), ll = std::max<int64_t>(g.max_long, 1);
+        FAE_CUDA(c, cudaMalloc(&g.lpart, sizeof(float) * kUnroll * lc * 8 * c->cfg.max_dim));
+        FAE_CUDA(c, cudaMalloc(&g.lcnt, sizeof(uint32_t) * kUnroll * ll));
+        FAE_CUDA(c, cudaMemsetAsync(g.lcnt, 0, sizeof(uint32_t) * kUnroll * ll, c->stream));
+    }
     st = read_latched(c);
     if (st != FAE_OK) return st;
     g.valid = true;

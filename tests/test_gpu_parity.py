@@ -152,17 +152,17 @@ def test_step_edge_cases(dev):
 # ----------------------------------------------------------------------------
 # a1-a7 preprocessing
 # ----------------------------------------------------------------------------
-def _prep_ref(ds, x, seed, mode, t=None, budget=None, small=0):
+def _prep_ref(ds, x, seed, mode, t=None, budget=None, small=0, dim=16):
     samp = oracle.sample(ds.n_records, x, seed)
     counts, T, st = oracle.histogram(ds.rows, ds.idx, ds.off, ds.fixed_pool, ds.n_records, samp)
     assert st == 0
     if mode == "t":
-        kmin = oracle.kmin_fixed_t(ds.rows, 16, small, T, t, x)
+        kmin = oracle.kmin_fixed_t(ds.rows, dim, small, T, t, x)
         extra = {}
     else:
-        r = oracle.budget_exact(ds.rows, 16, small, counts, T, x, budget)
+        r = oracle.budget_exact(ds.rows, dim, small, counts, T, x, budget)
         kmin, extra = r["kmin"], r
-    hot = oracle.tag_rows(ds.rows, 16, small, counts, kmin)
+    hot = oracle.tag_rows(ds.rows, dim, small, counts, kmin)
     rm, base, H = oracle.remap(ds.rows, hot)
     flag = oracle.classify(ds.rows, ds.idx, ds.off, ds.fixed_pool, ds.n_records, rm)
     pk = oracle.pack(ds.rows, ds.idx, ds.off, ds.fixed_pool, ds.n_records, rm, flag)
@@ -341,15 +341,23 @@ def test_pipeline_end_to_end_kaggle(dev):
     assert ok, worst
 
 
+# Terabyte-shaped (26 tables with the same skew of sizes, D = 64), scaled down
+TB_SMALL = gen.Config("tb-small", [max(3, r // 200) for r in gen.TERABYTE_ROWS], 64, 512, 1,
+                      records=30_000, t=1e-6)
+
+
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("cfg,R,t,small", [("kaggle", 100_000, 1e-6, 1 << 20),
                                            ("alibaba", 20_000, 1e-5, 1 << 20),
-                                           ("tiny", 10_000, 1e-2, 0)])
-def test_grouped_training(dev, cfg, R, t, small):
+                                           ("tiny", 10_000, 1e-2, 0),
+                                           ("tb-small", 30_000, 1e-6, 1 << 20)])
+def test_grouped_training(dev, cfg, R, t, small, fused, monkeypatch):
     """fae_group_batches + fae_train_hot_batches (graph replay, device cursor)
     == the standalone per-step calls bit for bit, and == the oracle's
     sequential SGD within tolerance; includes the ragged last batch."""
     from paper_2103_00686_b200.pipeline import FaePipeline
-    c = gen.CONFIGS[cfg]
+    monkeypatch.setenv("FAE_FUSED", "1" if fused else "0")   # read at fae_create
+    c = TB_SMALL if cfg == "tb-small" else gen.CONFIGS[cfg]
     ds = gen.make_dataset(c, n_records=R, seed=5)
     dd = ds.to(dev)
     pipe = FaePipeline(ds.rows, c.dim, c.batch, c.pool, max_pool=max(c.pool_hi, 1))
@@ -364,6 +372,8 @@ def test_grouped_training(dev, cfg, R, t, small):
     dY = gen.make_dy(nb * S, c.dim, seed=9).view(nb, S, c.dim).to(dev)
     lr = 0.05
     pipe.group(prep)
+    from paper_2103_00686_b200 import fae_group_info
+    assert fae_group_info(pipe.ctx)["fused"] == int(fused and c.pool == 1)
     Y = torch.zeros(S, c.dim, device=dev)
     pipe.train(W_hot, first, nb, dY, Y, lr)
     pipe.ctx.check()
@@ -375,7 +385,7 @@ def test_grouped_training(dev, cfg, R, t, small):
     assert torch.equal(W_hot, W_std)
     assert torch.equal(Y, Y2)
     # oracle: sequential SGD over the same batches
-    ref = _prep_ref(ds, 5.0, 2, "t", t=t, small=small)
+    ref = _prep_ref(ds, 5.0, 2, "t", t=t, small=small, dim=c.dim)
     Wr = oracle.extract(W, ref["remap"], ref["H"])
     pk = ref["pack"]
     Tn = c.n_tables
