@@ -165,9 +165,10 @@ def run_fae(args):
         t = time.perf_counter()
         prep = pipe.preprocess(ds.idx, ds.off, R, x_pct=5.0, seed=args.seed, mode=mode,
                                t=cfg.t, budget_bytes=cfg.budget_bytes,
-                               small_table_bytes=cfg.small_bytes, bufs=state.get("prep"))
+                               small_table_bytes=cfg.small_bytes, bufs=state.get("prep"),
+                               times=phases)
         state["prep"] = prep
-        t = mark("profile_threshold_classify", t)
+        t = mark("preprocess_total", t)
         pipe.group(prep)
         t = mark("group", t)
         W_hot = pipe.extract(W, prep)

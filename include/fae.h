@@ -309,7 +309,9 @@ fae_status fae_sync_hot_grads(fae_ctx* ctx, int32_t* rows, float* vals,
  * whole run (the paper pre-processes once and stores the FAE format,
  * P:L262, L496), so grouping each batch's lookups by hot id is hoisted out of
  * the training step.  Per batch: a stable sort of (hot id, bag) and the
- * run-length segments of equal hot id (split into pieces of <= 16 lookups).
+ * run-length segments of equal hot id (split into pieces of <= 16 lookups;
+ * long segments into chunks reduced by separate CTAs, 512 lookups at
+ * D <= 16 and 256 above, so the chunking depends on tabs->dim).
  * The grouping is kept in the ctx and refers to pk->hot_idx / pk->hot_off,
  * which must stay valid and unchanged until the next fae_group_batches.
  *  pk          the fae_packed filled by fae_classify (device hot_idx, hot_off;
@@ -334,7 +336,8 @@ fae_status fae_group_batches(fae_ctx* ctx, const fae_tables* tabs,
  * batch i+1 sees the rows batch i updated.  World 1: replays a captured
  * CUDA graph of 2 kernels per step (no host work per step).  World > 1: the
  * sparse gradient is exchanged every step (fae_sync_hot_grads semantics).
- * H must equal the H given to fae_group_batches.
+ * H must equal the H given to fae_group_batches and D the tabs->dim given
+ * to it (the long-segment chunking is sized for that row width).
  * ------------------------------------------------------------------------ */
 fae_status fae_train_hot_batches(fae_ctx* ctx, float* W_hot, int64_t H,
                                  int32_t D, int64_t first, int64_t n,

@@ -18,7 +18,8 @@ from typing import Optional, Sequence
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libfae.so")
+# FAE_LIB: load another build of the same ABI (A/B timing of two builds)
+LIB_PATH = os.environ.get("FAE_LIB") or os.path.join(_HERE, "_lib", "libfae.so")
 _lib = None
 
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "CAPACITY", 3: "BUDGET_INFEASIBLE",

@@ -56,22 +56,41 @@ k_classify_fixed(const int32_t* __restrict__ idx, int64_t n_rec, int Tn, int P, 
     const int TnP = Tn * P;
     const int nitems = nrec * TnP;
     const int32_t* src = idx + r0 * (int64_t)TnP;
-    for (int q = tid; q < nitems; q += kClsThreads) {
-        const int rl = q / TnP;
-        const int qq = q - rl * TnP;
-        const int z = qq / P;
-        const int32_t j = __ldg(src + q);
-        int32_t hid = -1;
-        if (j < 0 || (int64_t)j >= s_rows[z]) {
-            atomicOr(err, kErrIndex);
-            s_cold[rl] = 1;
-        } else {
-            const int64_t g = s_rb[z] + j;
-            uint32_t rk;
-            if (hs_test(__ldg(dir + (g >> 6)), g, &rk)) hid = (int32_t)rk;
-            else s_cold[rl] = 1;
+    // 8 lookups per thread in flight: all index loads, then all rank-directory
+    // loads (L2-resident), then the tests
+    for (int q0 = 0; q0 < nitems; q0 += kClsThreads * 8) {
+        int32_t jv[8];
+        int zv[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const int q = q0 + u * kClsThreads + tid;
+            jv[u] = q < nitems ? __ldg(src + q) : 0;
+            zv[u] = q < nitems ? (q % TnP) / P : -1;
         }
-        s_hid[q] = hid;
+        uint4 e[8];
+        int64_t gv[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            gv[u] = -1;
+            if (zv[u] >= 0) {
+                if (jv[u] < 0 || (int64_t)jv[u] >= s_rows[zv[u]]) {
+                    atomicOr(err, kErrIndex);
+                } else {
+                    gv[u] = s_rb[zv[u]] + jv[u];
+                    e[u] = __ldg(dir + (gv[u] >> 6));
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const int q = q0 + u * kClsThreads + tid;
+            if (zv[u] < 0) continue;
+            int32_t hid = -1;
+            uint32_t rk;
+            if (gv[u] >= 0 && hs_test(e[u], gv[u], &rk)) hid = (int32_t)rk;
+            else s_cold[q / TnP] = 1;
+            s_hid[q] = hid;
+        }
     }
     __syncthreads();
     const bool hot = tid < nrec && !s_cold[tid];

@@ -139,9 +139,9 @@ __device__ __forceinline__ void write_y(const float4 (&v)[NV], const int32_t* __
     }
 }
 
-// Long segments (> kMedium lookups): one CTA per kChunk-lookup chunk.  A
+// Long segments (> kMedium lookups): one CTA per CHUNK-lookup chunk.  A
 // chunk's pieces (16 lookups from the segment start) are summed by the
-// CTA's groups (2G pieces per pass), then its CH-piece block sums are formed
+// CTA's groups in one pass, then its CH-piece block sums are formed
 // in shared memory.  Single-chunk segments finish in place; otherwise each
 // chunk publishes its block sums (one fence per CTA) and the last-arriving
 // chunk adds all block sums of the segment in order — the standalone path's
@@ -150,6 +150,7 @@ __device__ __forceinline__ void write_y(const float4 (&v)[NV], const int32_t* __
 // into Y_b for the linked segment of the next batch.
 template <int LPB, int NV, bool kPDL, bool kFused>
 __device__ __forceinline__ void long_chunk(const SegRec* __restrict__ lrec, int64_t n_long, int64_t lb,
+                                           bool direct,
                                            const int32_t* __restrict__ perm_a,
                                            const int32_t* __restrict__ perm_b,
                                            const float* __restrict__ src, int D, float* W, float lr,
@@ -161,36 +162,48 @@ __device__ __forceinline__ void long_chunk(const SegRec* __restrict__ lrec, int6
     __shared__ int s_last;
     const int lane = threadIdx.x % LPB;
     const int grp = threadIdx.x / LPB;
-    // the segment of this chunk: last k with c0 <= lb
-    int64_t lo = 0, hi = n_long - 1;
-    while (lo < hi) {
-        const int64_t mid = (lo + hi + 1) >> 1;
-        if (__ldg(&lrec[mid].c0) <= lb) lo = mid;
-        else hi = mid - 1;
-    }
-    const int64_t k = lo;
-    const int4 r = __ldg(reinterpret_cast<const int4*>(lrec + k));          // pos, len, row, seg
-    const int4 r2 = __ldg(reinterpret_cast<const int4*>(lrec + k) + 1);     // npos, nlen, c0, nc
-    const int32_t cidx = (int32_t)(lb - r2.z);
-    const int32_t cbeg = cidx * kChunk, cend = min(r.y, cbeg + kChunk);
-    // block sums of this chunk, in shared memory rows [0, nblk_total)
-    int nblk_total = 0;
-    for (int32_t c0 = cbeg; c0 < cend; c0 += 2 * G * kPiece) {
-        const int np = min(2 * G, (cend - c0 + kPiece - 1) / kPiece);
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const int pc = grp + h * G;
-            const int32_t p0 = c0 + pc * kPiece;
-            const int32_t n = pc < np ? min(kPiece, cend - p0) : 0;
-            float4 g[NV];
-            sum_rows16<LPB, NV>(perm_a, r.x + p0, n, src, D, lane, g);
-#pragma unroll
-            for (int kk = 0; kk < NV; kk++) s_part[pc][kk * LPB + lane] = g[kk];
+    // the segment of this chunk: last k with c0 <= lb (direct: record lb,
+    // a single chunk)
+    int64_t k = lb;
+    if (!direct) {
+        int64_t lo = 0, hi = n_long - 1;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (__ldg(&lrec[mid].c0) <= lb) lo = mid;
+            else hi = mid - 1;
         }
-        __syncthreads();
-        const int nblk = (np + CH - 1) / CH;
+        k = lo;
+    }
+    const int4 r = __ldg(reinterpret_cast<const int4*>(lrec + k));          // pos, len, row, seg
+    int4 r2 = __ldg(reinterpret_cast<const int4*>(lrec + k) + 1);           // npos, nlen, c0, nc
+    if (direct) {
+        r2.z = (int32_t)lb;
+        r2.w = 1;
+    }
+    constexpr int CHUNK = chunk_of_lpb(LPB);
+    static_assert(CHUNK <= 2 * G * kPiece, "a chunk is one CTA pass");
+    static_assert(CHUNK / kPiece / CH <= 8, "lpart holds <= 8 block sums per chunk");
+    const int32_t cidx = (int32_t)(lb - r2.z);
+    const int32_t cbeg = cidx * CHUNK, cend = min(r.y, cbeg + CHUNK);
+    // the chunk's pieces, one pass: piece pc by group pc % G
+    const int np = (cend - cbeg + kPiece - 1) / kPiece;
+#pragma unroll
+    for (int h = 0; h < (CHUNK / kPiece + G - 1) / G; h++) {
+        const int pc = grp + h * G;
+        if (pc >= CHUNK / kPiece) break;
+        const int32_t p0 = cbeg + pc * kPiece;
+        const int32_t n = pc < np ? min(kPiece, cend - p0) : 0;
+        float4 g[NV];
+        sum_rows16<LPB, NV>(perm_a, r.x + p0, n, src, D, lane, g);
+#pragma unroll
+        for (int kk = 0; kk < NV; kk++) s_part[pc][kk * LPB + lane] = g[kk];
+    }
+    __syncthreads();
+    // block sums of CH pieces, in shared memory rows [0, nblk_total)
+    const int nblk_total = (np + CH - 1) / CH;
+    {
         float4 sub[NV];
-        if (grp < nblk) {
+        if (grp < nblk_total) {
             const int q0 = grp * CH, q1 = min(np, q0 + CH);
 #pragma unroll
             for (int kk = 0; kk < NV; kk++) sub[kk] = s_part[q0][kk * LPB + lane];
@@ -199,10 +212,9 @@ __device__ __forceinline__ void long_chunk(const SegRec* __restrict__ lrec, int6
                 for (int kk = 0; kk < NV; kk++) add4(sub[kk], s_part[q][kk * LPB + lane]);
         }
         __syncthreads();
-        if (grp < nblk)
+        if (grp < nblk_total)
 #pragma unroll
-            for (int kk = 0; kk < NV; kk++) s_part[nblk_total + grp][kk * LPB + lane] = sub[kk];
-        nblk_total += nblk;
+            for (int kk = 0; kk < NV; kk++) s_part[grp][kk * LPB + lane] = sub[kk];
         __syncthreads();
     }
     float4 tot[NV];
@@ -231,7 +243,7 @@ __device__ __forceinline__ void long_chunk(const SegRec* __restrict__ lrec, int6
         if (!s_last) return;
         if (grp == 0) {
             for (int32_t cc = 0; cc < r2.w; cc++) {
-                const int32_t len_c = min(kChunk, r.y - cc * kChunk);
+                const int32_t len_c = min(CHUNK, r.y - cc * CHUNK);
                 const int nb = ((len_c + kPiece - 1) / kPiece + CH - 1) / CH;
                 const int64_t base = (int64_t)(r2.z + cc) * 8;
                 for (int j = 0; j < nb; j++) {
@@ -285,7 +297,7 @@ __device__ __forceinline__ void long_chunk(const SegRec* __restrict__ lrec, int6
 // kPDL: all loads of static data happen before griddepcontrol.wait; only
 // the W read-modify-write waits for the forward of this batch.
 template <int LPB, int NV, bool kPDL>
-__device__ __forceinline__ void reduce_segments(const SegRec* __restrict__ rec, int64_t n_short,
+__device__ __forceinline__ void reduce_segments(const SegRec* __restrict__ rec, int64_t n_tiny, int64_t n_short,
                                                 int64_t n_med, int64_t n_long, int64_t n_lchunk,
                                                 const int32_t* __restrict__ perm,
                                                 const float* __restrict__ src, int D, float* W,
@@ -301,9 +313,15 @@ __device__ __forceinline__ void reduce_segments(const SegRec* __restrict__ rec, 
     // must not form the tail), then medium, then short
     int64_t b = blockIdx.x;
     const int64_t short_blocks = (n_short + G - 1) / G;
-    const int64_t med_blocks = (n_med + 7) / 8;
+    constexpr bool kMedWarp = LPB <= 4;   // medium segments: one warp, else one CTA
+    const int64_t med_blocks = med_blocks_for(n_med, LPB);
     if (b >= n_lchunk) {
         b -= n_lchunk;
+        if (!kMedWarp && b < med_blocks) {
+            long_chunk<LPB, NV, kPDL, false>(rec + n_short, n_med, b, true, perm, nullptr, src, D, W, lr,
+                                             lpart, lcnt, emit, grad_out, nullptr, err);
+            return;
+        }
         if (b < med_blocks) {
             const int64_t m = b * 8 + (threadIdx.x >> 5);
             if (m >= n_med) return;
@@ -337,9 +355,49 @@ __device__ __forceinline__ void reduce_segments(const SegRec* __restrict__ rec, 
             return;
         }
         b -= med_blocks;
-        if (b >= short_blocks) return;
-        const int64_t q = b * G + grp;
-        if (q >= n_short) return;
+        // tiny segments (<= kTinySeg lookups): kTinySeg per lane group
+        const int64_t n_small = n_short - n_tiny;
+        const int64_t tiny_blocks = (n_tiny + G * kTinySeg - 1) / (G * kTinySeg);
+        if (b < tiny_blocks) {
+            const int64_t q0 = (b * G + grp) * kTinySeg;
+            if (q0 >= n_tiny) return;
+            int4 r[kTinySeg];
+            int32_t bag[kTinySeg][kTinySeg];
+#pragma unroll
+            for (int t = 0; t < kTinySeg; t++)
+                r[t] = q0 + t < n_tiny ? __ldg(reinterpret_cast<const int4*>(rec + q0 + t)) : make_int4(0, 0, 0, 0);
+#pragma unroll
+            for (int t = 0; t < kTinySeg; t++)
+#pragma unroll
+                for (int u = 0; u < kTinySeg; u++) bag[t][u] = u < r[t].y ? __ldg(perm + r[t].x + u) : -1;
+            float4 g[kTinySeg][NV];
+#pragma unroll
+            for (int t = 0; t < kTinySeg; t++) {
+                float4 v[kTinySeg][NV];
+#pragma unroll
+                for (int u = 0; u < kTinySeg; u++) {
+                    const float4* rp = reinterpret_cast<const float4*>(src + (int64_t)(bag[t][u] < 0 ? 0 : bag[t][u]) * D) + lane;
+#pragma unroll
+                    for (int k = 0; k < NV; k++)
+                        v[u][k] = bag[t][u] < 0 ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldg(rp + k * LPB);
+                }
+#pragma unroll
+                for (int k = 0; k < NV; k++) {
+                    g[t][k] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                    for (int u = 0; u < kTinySeg; u++)
+                        if (bag[t][u] >= 0) add4(g[t][k], v[u][k]);
+                }
+            }
+            if (kPDL) pdl_wait();
+#pragma unroll
+            for (int t = 0; t < kTinySeg; t++)
+                if (q0 + t < n_tiny) seg_finish<LPB, NV>(g[t], lane, r[t].z, r[t].w, W, D, lr, emit, grad_out, err);
+            return;
+        }
+        b -= tiny_blocks;
+        const int64_t q = n_tiny + b * G + grp;
+        if (b * G + grp >= n_small) return;
         const int4 r = __ldg(reinterpret_cast<const int4*>(rec + q));
         float4 g[NV];
         sum_rows16<LPB, NV>(perm, r.x, r.y, src, D, lane, g);
@@ -347,8 +405,8 @@ __device__ __forceinline__ void reduce_segments(const SegRec* __restrict__ rec, 
         seg_finish<LPB, NV>(g, lane, r.z, r.w, W, D, lr, emit, grad_out, err);
         return;
     }
-    long_chunk<LPB, NV, kPDL, false>(rec + n_short + n_med, n_long, b, perm, nullptr, src, D, W, lr, lpart,
-                                     lcnt, emit, grad_out, nullptr, err);
+    long_chunk<LPB, NV, kPDL, false>(rec + n_short + n_med, n_long, b, false, perm, nullptr, src, D, W, lr,
+                                     lpart, lcnt, emit, grad_out, nullptr, err);
 }
 
 // ---------------------------------------------------------------------------
@@ -364,6 +422,29 @@ __device__ __forceinline__ void reduce_segments(const SegRec* __restrict__ rec, 
 // results are bit-identical to the two-kernel path.  One kernel boundary per
 // step instead of two.
 // ---------------------------------------------------------------------------
+// prefetch up to 16 bag ids of a Y-write run (static data: before the wait)
+__device__ __forceinline__ void prefetch_bags(const int32_t* __restrict__ perm_b, int32_t pos, int32_t len,
+                                              int32_t (&bg)[16]) {
+#pragma unroll
+    for (int u = 0; u < 16; u++) bg[u] = u < len ? __ldg(perm_b + pos + u) : -1;
+}
+
+// write_y for one worker whose first 16 bag ids are prefetched
+template <int LPB, int NV>
+__device__ __forceinline__ void write_y_pf(const float4 (&v)[NV], const int32_t (&bg)[16],
+                                           const int32_t* __restrict__ perm_b, int32_t pos, int32_t len,
+                                           float* __restrict__ Y, int D, int lane) {
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+        if (bg[u] >= 0) {
+            float4* y = reinterpret_cast<float4*>(Y + (int64_t)bg[u] * D) + lane;
+#pragma unroll
+            for (int k = 0; k < NV; k++) __stcs(y + k * LPB, v[k]);
+        }
+    }
+    if (len > 16) write_y<LPB, NV>(v, perm_b, pos + 16, len - 16, Y, D, lane, 0, 1);
+}
+
 // W[row] -= lr * g; returns the new row part of this lane in v
 template <int LPB, int NV>
 __device__ __forceinline__ void sgd_row(const float4 (&g)[NV], int lane, int32_t row, float* W, int D,
@@ -407,9 +488,15 @@ __device__ __forceinline__ void fused_reduce(const SegRec* __restrict__ rec, int
     const int lane = threadIdx.x % LPB;
     const int grp = threadIdx.x / LPB;
     const int64_t short_blocks = (n_short + G - 1) / G;
-    const int64_t med_blocks = (n_med + 7) / 8;
+    constexpr bool kMedWarp = LPB <= 4;   // medium segments: one warp, else one CTA
+    const int64_t med_blocks = med_blocks_for(n_med, LPB);
     if (b >= n_lchunk) {
         b -= n_lchunk;
+        if (!kMedWarp && b < med_blocks) {
+            long_chunk<LPB, NV, true, true>(rec + n_short, n_med, b, true, perm_a, perm_b, src, D, W, lr,
+                                            lpart, lcnt, 0, nullptr, Y, err);
+            return;
+        }
         if (b < med_blocks) {
             const int64_t m = b * 8 + (threadIdx.x >> 5);
             if (m >= n_med) return;
@@ -462,14 +549,16 @@ __device__ __forceinline__ void fused_reduce(const SegRec* __restrict__ rec, int
         const int2 nx = __ldg(reinterpret_cast<const int2*>(rp) + 2);
         float4 g[NV];
         sum_rows16<LPB, NV>(perm_a, r.x, r.y, src, D, lane, g);
+        int32_t bg[16];
+        prefetch_bags(perm_b, nx.x, nx.x >= 0 ? nx.y : 0, bg);
         pdl_wait();
         float4 v[NV];
         sgd_row<LPB, NV>(g, lane, r.z, W, D, lr, err, v);
-        if (nx.x >= 0) write_y<LPB, NV>(v, perm_b, nx.x, nx.y, Y, D, lane, 0, 1);
+        if (nx.x >= 0) write_y_pf<LPB, NV>(v, bg, perm_b, nx.x, nx.y, Y, D, lane);
         return;
     }
-    long_chunk<LPB, NV, true, true>(rec + n_short + n_med, n_long, b, perm_a, perm_b, src, D, W, lr, lpart, lcnt,
-                                    0, nullptr, Y, err);
+    long_chunk<LPB, NV, true, true>(rec + n_short + n_med, n_long, b, false, perm_a, perm_b, src, D, W, lr,
+                                    lpart, lcnt, 0, nullptr, Y, err);
 }
 
 template <int LPB, int NV, int MB>
@@ -504,7 +593,7 @@ k_grp_fused_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ 
         if (has_a) {
             const BatchDesc da = desc[first + rel - 1];
             const int64_t n_long = (da.sb1 - da.sb0) - da.n_short - da.n_med;
-            red_blocks = da.n_lchunk + (da.n_med + 7) / 8 + (da.n_short + G - 1) / G;
+            red_blocks = da.n_lchunk + med_blocks_for(da.n_med, LPB) + (da.n_short + G - 1) / G;
             if (bid < red_blocks) {
                 fused_reduce<LPB, NV>(rec + da.sb0, da.n_short, da.n_med, n_long, da.n_lchunk, bid, perm + da.lk0,
                                       perm_b, dY + ((rel - 1) % n_dy) * dy_stride, D, W, lr, lpart, lcnt, Y, err);
@@ -531,10 +620,12 @@ k_grp_fused_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ 
                 row = r.z;
             }
             if (pos >= 0) {
+                int32_t bg[16];
+                prefetch_bags(perm_b, pos, len, bg);
                 pdl_wait();
                 float4 v[NV];
                 load_row<LPB, NV>(W, row, D, lane, v);
-                write_y<LPB, NV>(v, perm_b, pos, len, Y, D, lane, 0, 1);
+                write_y_pf<LPB, NV>(v, bg, perm_b, pos, len, Y, D, lane);
             }
         }
         if (stamps) {
@@ -591,7 +682,7 @@ k_grp_reduce(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ run
     const int64_t i = *cursor;
     if (i < run[1]) {
         const BatchDesc d = desc[run[0] + i];
-        reduce_segments<LPB, NV, false>(rec + d.sb0, d.n_short, d.n_med, (d.sb1 - d.sb0) - d.n_short - d.n_med,
+        reduce_segments<LPB, NV, false>(rec + d.sb0, d.n_tiny, d.n_short, d.n_med, (d.sb1 - d.sb0) - d.n_short - d.n_med,
                                         d.n_lchunk, perm + d.lk0, dY + (i % n_dy) * dy_stride, D, W, lr, lpart,
                                         lcnt, emit, grad_out, err);
     }
@@ -663,7 +754,7 @@ k_grp_reduce_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__
             atomicMin(&stamps[rel * 8 + 2], (unsigned long long)gtimer());
         }
         const int64_t n_long = (d.sb1 - d.sb0) - d.n_short - d.n_med;
-        reduce_segments<LPB, NV, true>(rec + d.sb0, d.n_short, d.n_med, n_long, d.n_lchunk, perm + d.lk0,
+        reduce_segments<LPB, NV, true>(rec + d.sb0, d.n_tiny, d.n_short, d.n_med, n_long, d.n_lchunk, perm + d.lk0,
                                        dY + (rel % n_dy) * dy_stride, D, W, lr, lpart, lcnt, 0, nullptr, err);
         if (stamps) {   // per-tier completion: [6] long CTAs, [7] short/medium CTAs
             __syncthreads();
@@ -709,6 +800,15 @@ void drop_graphs(Group& g) {
     g.tgraph_key = 0;
 }
 
+// blocks of the reduce kernel for the largest batch
+static int64_t red_grid(const Group& g, int64_t G) {
+    int64_t m = 1;
+    for (const BatchDesc& d : g.hdesc)
+        m = std::max<int64_t>(m, d.n_lchunk + med_blocks_for(d.n_med, (int)(256 / G)) + cdiv(d.n_tiny, G * kTinySeg) +
+                                     cdiv(d.n_short - d.n_tiny, G));
+    return m;
+}
+
 template <int LPB, int NV>
 static void launch_grp_step(Ctx* c, cudaStream_t s, float* W, int64_t H, int D, const float* dY,
                             int64_t n_dy, float* Y, float lr, int emit, cudaEvent_t mid) {
@@ -722,7 +822,7 @@ static void launch_grp_step(Ctx* c, cudaStream_t s, float* W, int64_t H, int D, 
                                                        W, H, D, Y, c->d_err);
     if (mid) cudaEventRecordWithFlags(mid, s, cudaEventRecordExternal);
     (void)maxb;
-    const int64_t rb = std::max<int64_t>(1, cdiv(g.max_short, gpb) + cdiv(g.max_med, 8) + g.max_lchunk);
+    const int64_t rb = std::max<int64_t>(1, red_grid(g, gpb));
     k_grp_reduce<LPB, NV><<<(unsigned)rb, threads, 0, s>>>(g.desc, g.run, g.cursor, g.done_ctr, g.rec, g.perm,
                                                           dY, n_dy, g.max_bags * (int64_t)D, D, W, lr, g.lpart,
                                                           g.lcnt, emit, c->ws.grad, c->d_err);
@@ -750,7 +850,7 @@ static fae_status launch_pdl_step(Ctx* c, cudaStream_t st, int s, float* W, int6
     FAE_CUDA(c, cudaLaunchKernelEx(&cfg, k_grp_fwd_pdl<LPB, NV>, (const BatchDesc*)g.desc, (const int64_t*)g.run,
                                    (const int64_t*)g.cursor, s, g.hot_idx, g.hot_off, (int)g.P, (const float*)W, H, D,
                                    Y, c->d_err, stamps, c->pdl_trig));
-    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, cdiv(g.max_short, gpb) + cdiv(g.max_med, 8) + g.max_lchunk));
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, red_grid(g, gpb)));
     const int last = (s == kUnroll - 1) ? kUnroll : 0;
     auto kern = c->red_mb >= 8 ? k_grp_reduce_pdl<LPB, NV, 8>
               : (c->red_mb >= 6 ? k_grp_reduce_pdl<LPB, NV, 6> : k_grp_reduce_pdl<LPB, NV, 4>);
@@ -773,7 +873,7 @@ static fae_status launch_fused_step(Ctx* c, cudaStream_t st, int s, float* W, in
     for (const BatchDesc& d : g.hdesc) {
         const int64_t nl = (d.sb1 - d.sb0) - d.n_short - d.n_med;
         (void)nl;
-        red = std::max<int64_t>(red, d.n_lchunk + cdiv(d.n_med, 8) + cdiv(d.n_short, G));
+        red = std::max<int64_t>(red, d.n_lchunk + med_blocks_for(d.n_med, (int)(256 / G)) + cdiv(d.n_short, G));
     }
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -908,6 +1008,8 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
     if (!g.valid) return set_err(c, FAE_ERR_NOT_INIT, "fae_train_hot_batches: no grouped batches (fae_group_batches)");
     if (!dim_ok(D) || D > c->cfg.max_dim) return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_hot_batches: unsupported dim");
     if (H != g.H) return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_hot_batches: H differs from the grouped H");
+    if (chunk_for_dim(D) != g.chunk)
+        return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_hot_batches: D differs from the grouped tables' dim");
     if (first < 0 || n < 0 || n_dy < 1 || (c->world == 1 && first + n > g.n_batches))
         return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_hot_batches: batch range outside the grouped batches");
     if (!(lr == lr)) return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_hot_batches: lr is NaN");

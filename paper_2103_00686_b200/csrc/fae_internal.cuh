@@ -23,7 +23,17 @@ constexpr int kMaxSortPasses = 4;      // 32-bit keys
 constexpr int kPiece = 16;             // max lookups per reduction piece
 constexpr int kUnroll = 128;           // steps per captured epoch graph
 constexpr int kMedium = 128;           // segments of (kPiece, kMedium] lookups: one warp
-constexpr int kChunk = 512;            // long segments: one CTA per kChunk lookups
+// Lookups per long-segment CTA (one CTA pass).  Measured on B200: at D = 16
+// (LPB = 4) four 512-chunks combined across CTAs beat larger chunks; at
+// D = 64 (LPB = 16) 256-chunks beat 512 (reduce 17.0 vs 20.0 us per batch).
+__host__ __device__ constexpr int chunk_of_lpb(int lpb) { return lpb <= 4 ? 512 : 256; }
+inline int chunk_for_dim(int D) { return chunk_of_lpb(D / 4 < 32 ? D / 4 : 32); }
+// reduce blocks of a batch's medium segments: one warp each when a warp holds
+// >= 8 lane groups (LPB <= 4), else one CTA each (single-chunk long path)
+__host__ __device__ inline int64_t med_blocks_for(int64_t n_med, int lpb) {
+    return lpb <= 4 ? (n_med + 7) / 8 : n_med;
+}
+constexpr int kTinySeg = 4;            // segments of <= kTinySeg lookups: 4 per lane group
 constexpr int kGSThreads = 256;        // grouping sort: threads per tile
 constexpr int kGSItems = 16;           // grouping sort: items per thread
 constexpr int kGSTile = kGSThreads * kGSItems;   // 4096 lookups per tile
@@ -90,13 +100,13 @@ struct BatchDesc {
     int32_t n_bags;
     int32_t n_free;        // segments whose row is not in batch b-1 (FreeRecs at sb0)
     int32_t n_lchunk;      // chunks of the long segments (one CTA each)
-    int32_t pad;
+    int32_t n_tiny;        // leading segments of <= kTinySeg lookups (4 per lane group)
 };
 
 // One segment (a run of equal hot ids in a grouped batch), batch-local
-// indices, 16 bytes.  Per batch the records are stably partitioned by length:
-// <= kPiece lookups (one lane group each), then <= kMedium (one warp each),
-// then longer (one CTA each).
+// indices, 32 bytes.  Per batch the records are stably partitioned by length:
+// <= kTinySeg lookups (4 per lane group), <= kPiece (one lane group each),
+// <= kMedium (one warp each), longer (one CTA per chunk_for_dim lookups).
 struct alignas(16) SegRec {
     int32_t pos;    // first position of the segment in the batch
     int32_t len;    // lookups of the segment
@@ -104,7 +114,7 @@ struct alignas(16) SegRec {
     int32_t seg;    // segment index in the batch (ascending hot id)
     int32_t npos;   // same row in the NEXT batch: its first position, or -1
     int32_t nlen;   //   and its number of lookups (0 if absent)
-    int32_t c0;     // long segments: index of its first kChunk-chunk in the batch
+    int32_t c0;     // long segments: index of its first chunk in the batch
     int32_t nc;     //   and its number of chunks (1 otherwise)
 };
 
@@ -132,8 +142,10 @@ struct Group {
     int32_t* nxt = nullptr;           // [S_total] link to the next batch's segment (local) or -1
     int64_t max_free = 0;
     int64_t max_lchunk = 0;
+    int32_t chunk = 512;              // lookups per long-segment chunk (chunk_for_dim)
     float* lpart = nullptr;           // [kUnroll][max_lchunk][8][max_dim] chunk block sums
     uint32_t* lcnt = nullptr;         // [kUnroll][max_long] arrival counters (kept zero)
+    int64_t cap_lpart = 0, cap_lcnt = 0;
     int64_t cap_L = 0, cap_R = 0;
     // grouping scratch (kept for reuse)
     uint32_t* keys[2] = {nullptr, nullptr};

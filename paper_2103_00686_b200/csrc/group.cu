@@ -41,59 +41,69 @@ __device__ __forceinline__ int32_t find_bag_g(const int64_t* __restrict__ off, i
     return (int32_t)lo;
 }
 
+// per-batch digit histograms of every pass (+ the bag ids, offsets input
+// only): one block per batch (grid-stride over batches), 16 hot ids per
+// thread per 4096-lookup chunk, match_any aggregation into shared memory, one
+// plain store per bin at the end (the block owns the batch: no atomics)
 __global__ void __launch_bounds__(kGSThreads)
-k_gs_init(const int32_t* __restrict__ hot_idx, const int64_t* __restrict__ hot_off, int P,
-          const int64_t* __restrict__ tile_start, const int32_t* __restrict__ tile_batch,
-          const BatchDesc* __restrict__ desc, int64_t n_tiles, int64_t H, int passes,
-          uint32_t* __restrict__ keys, int32_t* __restrict__ vals, uint32_t* __restrict__ ghist,
-          uint32_t* err) {
+k_gs_init(const int32_t* __restrict__ hot_idx, const int64_t* __restrict__ hot_off,
+          const BatchDesc* __restrict__ desc, int64_t n_batches, int64_t H, int passes,
+          int32_t* __restrict__ vals, uint32_t* __restrict__ ghist) {
     __shared__ uint32_t sh[kMaxSortPasses][kSortBins];
-    const int tid = threadIdx.x, lane = tid & 31;
-    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int64_t b = blockIdx.x; b < n_batches; b += gridDim.x) {
         for (int i = tid; i < kMaxSortPasses * kSortBins; i += kGSThreads) (&sh[0][0])[i] = 0;
         __syncthreads();
-        const int64_t s0 = tile_start[t], s1 = tile_start[t + 1];
-        const int b = tile_batch[t] & 0x7FFFFFFF;
         const BatchDesc d = desc[b];
-        for (int64_t j0 = s0; j0 < s1; j0 += kGSThreads) {
-            const int64_t j = j0 + tid;
-            uint32_t key = 0;
-            if (j < s1) {
-                const int32_t r = hot_idx[j];
-                if ((uint32_t)r >= (uint64_t)H) {
-                    atomicOr(err, kErrIndex);
-                    key = (uint32_t)H;
+        for (int64_t s0 = d.lk0; s0 < d.lk1; s0 += kGSTile) {
+            const int64_t s1 = s0 + kGSTile < d.lk1 ? s0 + kGSTile : d.lk1;
+            uint32_t key[kGSItems];
+            const int64_t wb = s0 + (int64_t)warp * 32 * kGSItems;
+#pragma unroll
+            for (int r = 0; r < kGSItems; r++) {
+                const int64_t j = wb + r * 32 + lane;
+                if (j < s1) {
+                    const int32_t hv = hot_idx[j];
+                    key[r] = (uint32_t)hv >= (uint64_t)H ? (uint32_t)H : (uint32_t)hv;
+                    if (hot_off) vals[j] = find_bag_g(hot_off + d.bag0, d.n_bags, j);
                 } else {
-                    key = (uint32_t)r;
+                    key[r] = 0xFFFFFFFFu;
                 }
-                keys[j] = key;
-                vals[j] = hot_off ? find_bag_g(hot_off + d.bag0, d.n_bags, j) : (int32_t)((j - d.lk0) / P);
             }
             for (int ps = 0; ps < passes; ps++) {
-                const uint32_t dg = j < s1 ? ((key >> (ps * kSortBits)) & (kSortBins - 1)) : (uint32_t)kSortBins + lane;
-                const uint32_t peers = __match_any_sync(0xffffffffu, dg);
-                if (dg < (uint32_t)kSortBins && (__ffs(peers) - 1) == lane) atomicAdd(&sh[ps][dg], (uint32_t)__popc(peers));
+#pragma unroll
+                for (int r = 0; r < kGSItems; r++) {
+                    const bool ok = wb + r * 32 + lane < s1;
+                    const uint32_t dg = ok ? ((key[r] >> (ps * kSortBits)) & (kSortBins - 1)) : (uint32_t)kSortBins + lane;
+                    const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+                    if (ok && (__ffs(peers) - 1) == lane) atomicAdd(&sh[ps][dg], (uint32_t)__popc(peers));
+                }
             }
         }
         __syncthreads();
-        for (int i = tid; i < passes * kSortBins; i += kGSThreads) {
-            const uint32_t v = (&sh[0][0])[i];
-            if (v) atomicAdd(&ghist[(int64_t)b * kMaxSortPasses * kSortBins + i], v);
-        }
+        for (int i = tid; i < kMaxSortPasses * kSortBins; i += kGSThreads)
+            ghist[b * kMaxSortPasses * kSortBins + i] = (&sh[0][0])[i];
         __syncthreads();
     }
 }
 
-// status word: bits 31..30 flag (1 aggregate, 2 inclusive), 29..0 count
+// status word: bits 31..30 flag (1 aggregate, 2 inclusive), 29..0 count.
+// kin == nullptr: pass 0 reads the keys from the hot CSR (ids >= H map to
+// H); vin == nullptr: the bag ids are (j - lk0) / P (fixed pooling).  The
+// tile is ranked (warp match_any), staged in shared memory in local sorted
+// order, and written with one contiguous run per digit (coalesced).
 __global__ void __launch_bounds__(kGSThreads)
-k_gs_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
-          uint32_t* __restrict__ kout, int32_t* __restrict__ vout,
+k_gs_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ hot_idx, int64_t H,
+          const int32_t* __restrict__ vin, int P, uint32_t* __restrict__ kout, int32_t* __restrict__ vout,
           const int64_t* __restrict__ tile_start, const int32_t* __restrict__ tile_batch,
           const BatchDesc* __restrict__ desc, const uint32_t* __restrict__ ghist, int pass,
-          uint32_t* __restrict__ status, uint32_t* __restrict__ tile_ctr) {
+          uint32_t* __restrict__ status, uint32_t* __restrict__ tile_ctr, uint32_t* err) {
     __shared__ uint32_t s_w[kGSW][kSortBins];
     __shared__ uint32_t s_goff[kSortBins];
+    __shared__ uint32_t s_tds[kSortBins];
     __shared__ uint32_t s_ws[kGSW];
+    __shared__ uint32_t s_k[kGSTile];
+    __shared__ int32_t s_v[kGSTile];
     __shared__ int64_t s_tile;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int shift = pass * kSortBits;
@@ -102,6 +112,7 @@ k_gs_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
     __syncthreads();
     const int64_t t = s_tile;
     const int64_t s0 = tile_start[t], s1 = tile_start[t + 1];
+    const int n_tile = (int)(s1 - s0);
     const int32_t tb = tile_batch[t];
     const int b = tb & 0x7FFFFFFF;
     const bool first = tb < 0;
@@ -119,19 +130,35 @@ k_gs_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
         for (int w = 0; w < warp; w++) wp += s_ws[w];
         s_goff[tid] = wp + x - v;
     }
-    const int64_t wb = s0 + (int64_t)warp * 32 * kGSItems;
+    const int wl = warp * 32 * kGSItems;   // warp's first local position
     uint32_t k[kGSItems];
     int32_t v[kGSItems];
     uint16_t rk[kGSItems];
 #pragma unroll
     for (int r = 0; r < kGSItems; r++) {
-        const int64_t i = wb + r * 32 + lane;
-        k[r] = i < s1 ? kin[i] : 0u;
-        v[r] = i < s1 ? vin[i] : 0;
+        const int li = wl + r * 32 + lane;
+        const int64_t i = s0 + li;
+        if (li < n_tile) {
+            if (kin) {
+                k[r] = kin[i];
+            } else {
+                const int32_t hv = hot_idx[i];
+                if ((uint32_t)hv >= (uint64_t)H) {
+                    atomicOr(err, kErrIndex);
+                    k[r] = (uint32_t)H;
+                } else {
+                    k[r] = (uint32_t)hv;
+                }
+            }
+            v[r] = vin ? vin[i] : (int32_t)((i - lk0) / P);
+        } else {
+            k[r] = 0u;
+            v[r] = 0;
+        }
     }
 #pragma unroll
     for (int r = 0; r < kGSItems; r++) {
-        const bool ok = wb + r * 32 + lane < s1;
+        const bool ok = wl + r * 32 + lane < n_tile;
         const uint32_t dg = ok ? ((k[r] >> shift) & (kSortBins - 1)) : (uint32_t)kSortBins;
         const uint32_t peers = __match_any_sync(0xffffffffu, dg);
         const uint32_t lt = __popc(peers & lanemask_lt());
@@ -143,45 +170,66 @@ k_gs_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
         rk[r] = (uint16_t)(cnt + lt);
     }
     __syncthreads();
-    {
-        const int d = tid;   // kGSThreads == kSortBins
-        uint32_t tot = 0;
+    const int d = tid;   // kGSThreads == kSortBins
+    uint32_t tot = 0;
 #pragma unroll
-        for (int w = 0; w < kGSW; w++) {
-            const uint32_t c = s_w[w][d];
-            s_w[w][d] = tot;
-            tot += c;
+    for (int w = 0; w < kGSW; w++) {
+        const uint32_t c = s_w[w][d];
+        s_w[w][d] = tot;
+        tot += c;
+    }
+    // publish this tile's digit count early; finish the look-back later
+    uint32_t* st = status + t * kSortBins + d;
+    st_relaxed_u32(st, ((first ? 2u : 1u) << 30) | tot);
+    {   // tile-local digit starts (exclusive scan of tot over digits)
+        uint32_t x = tot;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
         }
-        uint32_t excl = 0;
-        uint32_t* st = status + t * kSortBins + d;
-        if (first) {
-            st_relaxed_u32(st, (2u << 30) | tot);
-        } else {
-            st_relaxed_u32(st, (1u << 30) | tot);
-            int64_t q = t - 1;
-            while (true) {
-                uint32_t sv;
-                do {
-                    sv = ld_relaxed_u32(status + q * kSortBins + d);
-                } while ((sv >> 30) == 0);
-                excl += sv & 0x3FFFFFFFu;
-                if ((sv >> 30) == 2) break;
-                --q;
-            }
-            st_relaxed_u32(st, (2u << 30) | (excl + tot));
-        }
-        s_goff[d] += excl;
+        __syncthreads();
+        if (lane == 31) s_ws[warp] = x;
+        __syncthreads();
+        uint32_t wp = 0;
+        for (int w = 0; w < warp; w++) wp += s_ws[w];
+        s_tds[d] = wp + x - tot;
     }
     __syncthreads();
+    // stage the tile in local sorted order
 #pragma unroll
     for (int r = 0; r < kGSItems; r++) {
-        const int64_t i = wb + r * 32 + lane;
-        if (i < s1) {
+        if (wl + r * 32 + lane < n_tile) {
             const uint32_t dg = (k[r] >> shift) & (kSortBins - 1);
-            const int64_t pos = lk0 + s_goff[dg] + s_w[warp][dg] + rk[r];
-            kout[pos] = k[r];
-            vout[pos] = v[r];
+            const uint32_t lp = s_tds[dg] + s_w[warp][dg] + rk[r];
+            s_k[lp] = k[r];
+            s_v[lp] = v[r];
         }
+    }
+    // look-back for digit d within the batch's tiles
+    uint32_t excl = 0;
+    if (!first) {
+        int64_t q = t - 1;
+        while (true) {
+            uint32_t sv;
+            do {
+                sv = ld_relaxed_u32(status + q * kSortBins + d);
+            } while ((sv >> 30) == 0);
+            excl += sv & 0x3FFFFFFFu;
+            if ((sv >> 30) == 2) break;
+            --q;
+        }
+        st_relaxed_u32(st, (2u << 30) | (excl + tot));
+    }
+    s_goff[d] += excl;
+    __syncthreads();
+    // coalesced write-out: consecutive local positions of one digit are
+    // consecutive output positions
+    for (int i = tid; i < n_tile; i += kGSThreads) {
+        const uint32_t kk = s_k[i];
+        const uint32_t dg = (kk >> shift) & (kSortBins - 1);
+        const int64_t pos = lk0 + s_goff[dg] + (i - s_tds[dg]);
+        kout[pos] = kk;
+        vout[pos] = s_v[i];
     }
 }
 
@@ -313,14 +361,16 @@ k_gs_links(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __res
 }
 
 // one block per batch (grid-stride over batches): batch-local SegRecs,
-// stably partitioned by length class (<= kPiece, <= kMedium, longer), each
-// class in ascending hot id; desc[b].n_short, n_med
+// stably partitioned by length class (<= kTinySeg, <= kPiece, <= kMedium,
+// longer), each class in ascending hot id; desc[b].n_tiny, n_short (tiny +
+// small), n_med; long segments get their chunk range (c0, nc)
 __global__ void __launch_bounds__(256)
 k_gs_records(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __restrict__ seg_start,
              const int32_t* __restrict__ seg_row, const int32_t* __restrict__ nxt,
-             SegRec* __restrict__ rec) {
-    __shared__ uint32_t s_w[3][8];
-    __shared__ uint32_t s_n[2];
+             SegRec* __restrict__ rec, int chunk) {
+    constexpr int NC = 4;
+    __shared__ uint32_t s_w[NC][8];
+    __shared__ uint32_t s_n[NC];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int64_t b = blockIdx.x; b < n_batches; b += gridDim.x) {
         const BatchDesc d = desc[b];
@@ -345,71 +395,66 @@ k_gs_records(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __r
                 r.npos = (int32_t)(seg_start[sn] - dn.lk0);
                 r.nlen = (int32_t)(en - seg_start[sn]);
             }
-            return r.len <= kPiece ? 0 : (r.len <= kMedium ? 1 : 2);
+            return r.len <= kTinySeg ? 0 : (r.len <= kPiece ? 1 : (r.len <= kMedium ? 2 : 3));
         };
         // pass 1: class sizes
-        uint32_t n0 = 0, n1 = 0;
+        uint32_t nn[NC] = {0u, 0u, 0u, 0u};
         for (int64_t q = tid; q < S; q += 256) {
             SegRec r;
-            const int k = cls(q, r);
-            n0 += k == 0;
-            n1 += k == 1;
+            nn[cls(q, r)]++;
         }
-        for (int o = 16; o; o >>= 1) {
-            n0 += __shfl_xor_sync(0xffffffffu, n0, o);
-            n1 += __shfl_xor_sync(0xffffffffu, n1, o);
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+            for (int o = 16; o; o >>= 1) nn[c] += __shfl_xor_sync(0xffffffffu, nn[c], o);
+            if (lane == 0) s_w[c][warp] = nn[c];
         }
-        if (lane == 0) {
-            s_w[0][warp] = n0;
-            s_w[1][warp] = n1;
+        __syncthreads();
+        if (tid < NC) {
+            uint32_t t = 0;
+            for (int w = 0; w < 8; w++) t += s_w[tid][w];
+            s_n[tid] = t;
         }
         __syncthreads();
         if (tid == 0) {
-            uint32_t t0 = 0, t1 = 0;
-            for (int w = 0; w < 8; w++) {
-                t0 += s_w[0][w];
-                t1 += s_w[1][w];
-            }
-            s_n[0] = t0;
-            s_n[1] = t1;
-            desc[b].n_short = (int32_t)t0;
-            desc[b].n_med = (int32_t)t1;
+            desc[b].n_tiny = (int32_t)s_n[0];
+            desc[b].n_short = (int32_t)(s_n[0] + s_n[1]);
+            desc[b].n_med = (int32_t)s_n[2];
         }
+        const uint32_t base[NC] = {0u, s_n[0], s_n[0] + s_n[1], s_n[0] + s_n[1] + s_n[2]};
+        uint32_t run[NC] = {0u, 0u, 0u, 0u};
         __syncthreads();
-        const uint32_t base[3] = {0u, s_n[0], s_n[0] + s_n[1]};
-        uint32_t run[3] = {0u, 0u, 0u};
         // pass 2: stable partition, chunks of 256 segments
         for (int64_t q0 = 0; q0 < S; q0 += 256) {
             const int64_t q = q0 + tid;
             const bool valid = q < S;
             SegRec r{};
             const int k = valid ? cls(q, r) : -1;
-            uint32_t bal[3];
+            uint32_t bal[NC];
 #pragma unroll
-            for (int c = 0; c < 3; c++) bal[c] = __ballot_sync(0xffffffffu, k == c);
+            for (int c = 0; c < NC; c++) bal[c] = __ballot_sync(0xffffffffu, k == c);
             __syncthreads();
             if (lane == 0)
 #pragma unroll
-                for (int c = 0; c < 3; c++) s_w[c][warp] = __popc(bal[c]);
+                for (int c = 0; c < NC; c++) s_w[c][warp] = __popc(bal[c]);
             __syncthreads();
-            uint32_t pre[3] = {0u, 0u, 0u}, tot[3] = {0u, 0u, 0u};
+            uint32_t pre[NC] = {0u, 0u, 0u, 0u}, tot[NC] = {0u, 0u, 0u, 0u};
             for (int w = 0; w < 8; w++)
 #pragma unroll
-                for (int c = 0; c < 3; c++) {
+                for (int c = 0; c < NC; c++) {
                     if (w < warp) pre[c] += s_w[c][w];
                     tot[c] += s_w[c][w];
                 }
             if (valid) rec[d.sb0 + base[k] + run[k] + pre[k] + __popc(bal[k] & lanemask_lt())] = r;
 #pragma unroll
-            for (int c = 0; c < 3; c++) run[c] += tot[c];
+            for (int c = 0; c < NC; c++) run[c] += tot[c];
         }
         __syncthreads();
         if (tid == 0) {   // chunks of the long segments, in record order
             int32_t cc = 0;
-            for (int64_t q = (int64_t)base[2]; q < S; q++) {
+            for (int64_t q = (int64_t)base[3]; q < S; q++) {
                 SegRec& lr = rec[d.sb0 + q];
                 lr.c0 = cc;
-                lr.nc = (lr.len + kChunk - 1) / kChunk;
+                lr.nc = (lr.len + chunk - 1) / chunk;
                 cc += lr.nc;
             }
             desc[b].n_lchunk = cc;
@@ -576,34 +621,45 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
         FAE_CUDA(c, cudaMemcpyAsync(g.desc, g.hdesc.data(), sizeof(BatchDesc) * nb, cudaMemcpyHostToDevice, c->stream));
         FAE_CUDA(c, cudaMemcpyAsync(g.tile_start, tstart.data(), sizeof(int64_t) * (nt + 1), cudaMemcpyHostToDevice, c->stream));
         FAE_CUDA(c, cudaMemcpyAsync(g.tile_batch, tbatch.data(), sizeof(int32_t) * nt, cudaMemcpyHostToDevice, c->stream));
-        FAE_CUDA(c, cudaMemsetAsync(g.ghist, 0, sizeof(uint32_t) * nb * kMaxSortPasses * kSortBins, c->stream));
+
         FAE_CUDA(c, cudaMemsetAsync(totals, 0, 64, c->stream));
         const int64_t gi = std::max<int64_t>(1, std::min<int64_t>(nt, (int64_t)sm_count(c) * 8));
-        k_gs_init<<<(unsigned)gi, kGSThreads, 0, c->stream>>>(g.hot_idx, g.hot_off, fixed_pool, g.tile_start, g.tile_batch,
-                                                             g.desc, nt, H, passes, g.keys[0], g.vals, g.ghist, c->d_err);
+        const int64_t gb = std::max<int64_t>(1, std::min<int64_t>(nb, (int64_t)sm_count(c) * 8));
+        (void)gi;
+        k_gs_init<<<(unsigned)gb, kGSThreads, 0, c->stream>>>(g.hot_idx, g.hot_off, g.desc, nb, H, passes, g.vals,
+                                                             g.ghist);
         FAE_LAUNCHED(c);
         stage("init");
-        // passes: keys k0 -> k1 -> k0 ...; values vals <-> perm, the last pass lands in perm
-        uint32_t* kin = g.keys[0];
-        uint32_t* kout = g.keys[1];
+        // passes: pass 0 reads the hot CSR (and, for fixed pooling, derives the
+        // bag ids); the values ping-pong so that the last pass lands in perm
+        uint32_t* kbuf[2] = {g.keys[0], g.keys[1]};
         int32_t* vbuf[2] = {g.vals, g.perm};
-        int vin_i = (passes % 2 == 1) ? 0 : 1;
-        if (vin_i == 1)
+        int vo = (passes % 2 == 1) ? 1 : 0;          // value buffer written by pass 0
+        const uint32_t* kin = nullptr;
+        const int32_t* vin = offs ? g.vals : nullptr;
+        if (offs && vo == 0) {                       // keep vals as pass 0's input
             FAE_CUDA(c, cudaMemcpyAsync(g.perm, g.vals, sizeof(int32_t) * L, cudaMemcpyDeviceToDevice, c->stream));
+            vin = g.perm;
+        }
+        int ko = 0;
         for (int ps = 0; ps < passes; ps++) {
             FAE_CUDA(c, cudaMemsetAsync(g.sstatus, 0, sizeof(uint32_t) * nt * kSortBins, c->stream));
             FAE_CUDA(c, cudaMemsetAsync(ctr, 0, sizeof(uint32_t), c->stream));
-            k_gs_pass<<<(unsigned)nt, kGSThreads, 0, c->stream>>>(kin, vbuf[vin_i], kout, vbuf[vin_i ^ 1], g.tile_start,
-                                                                  g.tile_batch, g.desc, g.ghist, ps, g.sstatus, ctr);
+            k_gs_pass<<<(unsigned)nt, kGSThreads, 0, c->stream>>>(kin, g.hot_idx, H, vin, fixed_pool, kbuf[ko],
+                                                                  vbuf[vo], g.tile_start, g.tile_batch, g.desc,
+                                                                  g.ghist, ps, g.sstatus, ctr, c->d_err);
             FAE_LAUNCHED(c);
-            std::swap(kin, kout);
-            vin_i ^= 1;
+            kin = kbuf[ko];
+            vin = vbuf[vo];
+            ko ^= 1;
+            vo ^= 1;
         }
+        // sorted keys in kin, bag ids in perm
         stage("passes");
         // sorted keys in kin, bag ids in perm
         FAE_CUDA(c, cudaMemsetAsync(g.pstatus, 0, sizeof(uint64_t) * nt, c->stream));
         FAE_CUDA(c, cudaMemsetAsync(ctr + 1, 0, sizeof(uint32_t), c->stream));
-        k_gs_segments<<<(unsigned)nt, kGSThreads, 0, c->stream>>>(kin, g.tile_start, g.tile_batch, g.desc, nt, H, L,
+        k_gs_segments<<<(unsigned)nt, kGSThreads, 0, c->stream>>>(kin ? kin : (const uint32_t*)g.hot_idx, g.tile_start, g.tile_batch, g.desc, nt, H, L,
                                                                  g.pstatus, ctr + 1, g.seg_start, g.seg_row, totals);
         FAE_LAUNCHED(c);
         stage("segments");
@@ -626,7 +682,8 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
         FAE_CUDA(c, cudaMemsetAsync(g.nxt, 0xFF, sizeof(int32_t) * std::max<int64_t>(g.S_total, 1), c->stream));
         k_gs_links<<<(unsigned)gr, 256, 0, c->stream>>>(g.desc, nb, g.seg_start, g.seg_row, g.nxt, g.freer);
         FAE_LAUNCHED(c);
-        k_gs_records<<<(unsigned)gr, 256, 0, c->stream>>>(g.desc, nb, g.seg_start, g.seg_row, g.nxt, g.rec);
+        g.chunk = chunk_for_dim(tabs->dim);
+        k_gs_records<<<(unsigned)gr, 256, 0, c->stream>>>(g.desc, nb, g.seg_start, g.seg_row, g.nxt, g.rec, g.chunk);
         FAE_LAUNCHED(c);
         FAE_CUDA(c, cudaMemcpyAsync(g.hdesc.data(), g.desc, sizeof(BatchDesc) * nb, cudaMemcpyDeviceToHost, c->stream));
         st = read_latched(c);
@@ -645,15 +702,22 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
         }
     }
     if (g.max_segs > c->ws.cap_L) return set_err(c, FAE_ERR_CAPACITY, "fae_group_batches: batch segments exceed ctx capacity");
-    cudaFree(g.lpart);
-    cudaFree(g.lcnt);
-    g.lpart = nullptr;
-    g.lcnt = nullptr;
-    {
+    {   // grow-only (cudaFree would synchronise the device on every call)
         const int64_t lc = std::max<int64_t>(g.max_lchunk, 1), ll = std::max<int64_t>(g.max_long, 1);
-        FAE_CUDA(c, cudaMalloc(&g.lpart, sizeof(float) * kUnroll * lc * 8 * c->cfg.max_dim));
-        FAE_CUDA(c, cudaMalloc(&g.lcnt, sizeof(uint32_t) * kUnroll * ll));
-        FAE_CUDA(c, cudaMemsetAsync(g.lcnt, 0, sizeof(uint32_t) * kUnroll * ll, c->stream));
+        const int64_t need_p = kUnroll * lc * 8 * c->cfg.max_dim, need_c = kUnroll * ll;
+        if (g.cap_lpart < need_p) {
+            cudaFree(g.lpart);
+            g.lpart = nullptr;
+            g.cap_lpart = need_p + need_p / 4;
+            FAE_CUDA(c, cudaMalloc(&g.lpart, sizeof(float) * g.cap_lpart));
+        }
+        if (g.cap_lcnt < need_c) {
+            cudaFree(g.lcnt);
+            g.lcnt = nullptr;
+            g.cap_lcnt = need_c + need_c / 4;
+            FAE_CUDA(c, cudaMalloc(&g.lcnt, sizeof(uint32_t) * g.cap_lcnt));
+            FAE_CUDA(c, cudaMemsetAsync(g.lcnt, 0, sizeof(uint32_t) * g.cap_lcnt, c->stream));
+        }
     }
     st = read_latched(c);
     if (st != FAE_OK) return st;

@@ -186,6 +186,60 @@ k_histogram(const int64_t* __restrict__ sampled, int64_t n_s, const int32_t* __r
     }
 }
 
+// fixed pooling: thread per sampled lookup, 8 in flight; rows of tiny tables
+// (tiny_off[z] >= 0) count in shared memory (one flush per block), the others
+// in global memory with warp match_any aggregation.
+constexpr int kTinySlots = 8192;
+__global__ void __launch_bounds__(256)
+k_histogram_fixed(const int64_t* __restrict__ sampled, int64_t n_s, const int32_t* __restrict__ idx,
+                  int P, int Tn, const int64_t* __restrict__ rowbase, const int64_t* __restrict__ rows,
+                  const int32_t* __restrict__ tiny_off, const int64_t* __restrict__ slot_row, int n_slots,
+                  uint32_t* __restrict__ counts, uint32_t* err) {
+    __shared__ uint32_t tiny[kTinySlots];
+    const int lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < n_slots; i += blockDim.x) tiny[i] = 0;
+    __syncthreads();
+    const int TnP = Tn * P;
+    const int64_t n = n_s * TnP;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 8;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x * 8; i0 < n; i0 += stride) {
+        int32_t jv[8];
+        int zv[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const int64_t i = i0 + (int64_t)u * blockDim.x + threadIdx.x;
+            zv[u] = -1;
+            jv[u] = 0;
+            if (i < n) {
+                const int64_t rs = i / TnP;
+                const int qq = (int)(i - rs * TnP);
+                zv[u] = qq / P;
+                jv[u] = __ldg(idx + __ldg(sampled + rs) * TnP + qq);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            uint64_t key = ~(uint64_t)lane;   // unique sentinel: not counted globally
+            const int z = zv[u];
+            if (z >= 0) {
+                const int32_t j = jv[u];
+                if (j < 0 || (int64_t)j >= __ldg(rows + z)) {
+                    atomicOr(err, kErrIndex);
+                } else {
+                    const int32_t to = __ldg(tiny_off + z);
+                    if (to >= 0) atomicAdd(&tiny[to + j], 1u);
+                    else key = (uint64_t)(__ldg(rowbase + z) + j);
+                }
+            }
+            const uint32_t peers = __match_any_sync(0xffffffffu, key);
+            if ((key >> 63) == 0 && (__ffs(peers) - 1) == lane) atomicAdd(&counts[key], (uint32_t)__popc(peers));
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_slots; i += blockDim.x)
+        if (tiny[i]) atomicAdd(&counts[slot_row[i]], tiny[i]);
+}
+
 // T_z for offsets datasets: per-table lookup totals
 __global__ void __launch_bounds__(256)
 k_table_totals(const int64_t* __restrict__ off, int64_t n_bags, int Tn,
@@ -280,6 +334,8 @@ extern "C" fae_status fae_profile(fae_ctx* h, const fae_tables* tabs, const fae_
     const size_t o_st = take(sizeof(uint64_t) * tiles);
     const size_t o_tot = take(sizeof(int64_t) * 2);
     const size_t o_T = take(sizeof(unsigned long long) * Tn);
+    const size_t o_toff = take(sizeof(int32_t) * Tn);
+    const size_t o_srow = take(sizeof(int64_t) * kTinySlots);
     char* sc = (char*)scratch(c, o);
     if (!sc) return set_err(c, FAE_ERR_CUDA, "fae_profile: scratch allocation failed");
     int64_t* ids = (int64_t*)(sc + o_ids);
@@ -366,7 +422,27 @@ extern "C" fae_status fae_profile(fae_ctx* h, const fae_tables* tabs, const fae_
     // a2 histogram
     FAE_CUDA(c, cudaMemsetAsync(counts, 0, sizeof(uint32_t) * total_rows, c->stream));
     FAE_CUDA(c, cudaStreamSynchronize(c->stream));
-    if (ns > 0) {
+    if (ns > 0 && !data->off && data->fixed_pool > 0) {
+        // tiny tables (<= 2048 rows) privatised in shared memory, up to kTinySlots
+        std::vector<int32_t> toff(Tn, -1);
+        std::vector<int64_t> srow;
+        for (int z = 0; z < Tn; z++)
+            if (tabs->rows[z] <= 2048 && (int64_t)srow.size() + tabs->rows[z] <= kTinySlots) {
+                toff[z] = (int32_t)srow.size();
+                for (int64_t j = 0; j < tabs->rows[z]; j++) srow.push_back(rowbase[z] + j);
+            }
+        int32_t* d_toff = (int32_t*)(sc + o_toff);
+        int64_t* d_srow = (int64_t*)(sc + o_srow);
+        FAE_CUDA(c, cudaMemcpyAsync(d_toff, toff.data(), sizeof(int32_t) * Tn, cudaMemcpyHostToDevice, c->stream));
+        if (!srow.empty())
+            FAE_CUDA(c, cudaMemcpyAsync(d_srow, srow.data(), sizeof(int64_t) * srow.size(), cudaMemcpyHostToDevice, c->stream));
+        const int64_t items = ns * (int64_t)Tn * data->fixed_pool;
+        const int64_t g = std::max<int64_t>(1, std::min<int64_t>(cdiv(items, 256 * 8), (int64_t)sms(c) * 4));
+        k_histogram_fixed<<<(unsigned)g, 256, 0, c->stream>>>(ids, ns, data->idx, data->fixed_pool, Tn,
+                                                              c->d_rowbase_tmp, c->d_rows_tmp, d_toff, d_srow,
+                                                              (int)srow.size(), counts, c->d_err);
+        FAE_LAUNCHED(c);
+    } else if (ns > 0) {
         const int64_t g = std::max<int64_t>(1, std::min<int64_t>(cdiv(ns, 8), (int64_t)sms(c) * 16));
         k_histogram<<<(unsigned)g, 256, 0, c->stream>>>(ids, ns, data->idx, data->off, data->fixed_pool, Tn,
                                                         c->d_rowbase_tmp, c->d_rows_tmp, counts, c->d_err);

@@ -60,15 +60,29 @@ class FaePipeline:
                    mode: int = FIXED_T, t: float = 1e-7,
                    budget_bytes: int = 0, small_table_bytes: int = 1 << 20,
                    want_estimate: bool = False,
-                   bufs: Optional[Prepared] = None) -> Prepared:
+                   bufs: Optional[Prepared] = None,
+                   times: Optional[dict] = None) -> Prepared:
+        """times: optional dict accumulating ms per call (the calls return
+        host values, so each has synchronised the stream)."""
+        import time as _t
         dev = self.dev
+        t0 = _t.perf_counter()
+
+        def lap(name):
+            nonlocal t0
+            if times is not None:
+                t1 = _t.perf_counter()
+                times[name] = times.get(name, 0.0) + (t1 - t0) * 1e3
+                t0 = t1
         counts = bufs.counts if bufs else torch.empty(sum(self.rows), dtype=torch.int32, device=dev)
         T, ns = fae_profile(self.ctx, self.rows, self.dim, idx, off, self.pool,
                             n_records, x_pct, seed, counts)
+        lap("profile")
         th = fae_threshold(self.ctx, self.rows, self.dim, counts, T, x_pct,
                            mode=mode, t=t, budget_bytes=budget_bytes,
                            small_table_bytes=small_table_bytes,
                            want_estimate=want_estimate)
+        lap("threshold")
         if bufs is None:
             hot_ids = torch.empty(max(n_records, 1), dtype=torch.int64, device=dev)
             cold_ids = torch.empty(max(n_records, 1), dtype=torch.int64, device=dev)
@@ -79,6 +93,7 @@ class FaePipeline:
             hot_ids, cold_ids, hot_idx, hot_off = bufs.hot_ids, bufs.cold_ids, bufs.hot_idx, bufs.hot_off
         pk = fae_classify(self.ctx, self.rows, self.dim, idx, off, self.pool,
                           n_records, self.batch, hot_ids, cold_ids, hot_idx, hot_off)
+        lap("classify")
         return Prepared(counts, T, ns, th, hot_ids, cold_ids, hot_idx, hot_off, pk)
 
     def extract(self, W: torch.Tensor, prep: Prepared) -> torch.Tensor:
