@@ -333,8 +333,12 @@ fae_status fae_group_batches(fae_ctx* ctx, const fae_tables* tabs,
  * with dY_i = dY + (i % n_dy) * (B*Tn) * D (device [n_dy][B*Tn][D]; the
  * upstream gradient of each step, e.g. written by the MLP backward) and Y
  * device [B*Tn][D] (overwritten every step).  Sequential SGD semantics:
- * batch i+1 sees the rows batch i updated.  World 1: replays a captured
- * CUDA graph of 2 kernels per step (no host work per step).  World > 1: the
+ * batch i+1 sees the rows batch i updated.  World 1, single-lookup bags:
+ * ONE cooperative persistent kernel for the whole range (a grid-wide barrier
+ * between steps; step i does the backward + SGD of batch i-1 and the
+ * forward of batch i; FAE_PERSIST=0 selects the graph path instead).  Other
+ * world-1 inputs: replays a captured CUDA graph of 2 kernels per step (no
+ * host work per step).  World > 1: the
  * sparse gradient is exchanged every step (fae_sync_hot_grads semantics).
  * H must equal the H given to fae_group_batches and D the tabs->dim given
  * to it (the long-segment chunking is sized for that row width).
@@ -356,8 +360,10 @@ fae_status fae_train_hot_batches(fae_ctx* ctx, float* W_hot, int64_t H,
  * SGD kernel (k_grp_reduce_pdl); mode 1 also reports ms[2] = summed lead of
  * each reduce's entry over its forward's end and n[2] = steps where the
  * reduce entered before the forward ended (PDL overlap evidence); n[3] = 1
- * when the fused single-kernel step ran (its time is in ms[1]/n[1]); ms, n
- * have 4 entries.  Enabling resets the totals.
+ * when the fused single-kernel step ran (its time is in ms[1]/n[1]); n[3] = 2
+ * when the persistent epoch kernel ran (ms[1]/n[1] = its CUDA-event time and
+ * launches, ms[3] = the batches those launches trained); ms, n have 4
+ * entries.  Enabling resets the totals.
  * ------------------------------------------------------------------------ */
 fae_status fae_set_kernel_timing(fae_ctx* ctx, int32_t enable);
 /* Grouping summary: info[8] = {n_batches, hot lookups, segments of more

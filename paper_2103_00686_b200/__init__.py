@@ -346,12 +346,15 @@ def fae_set_kernel_timing(ctx: Ctx, mode: int):
 
 
 def fae_get_kernel_timing(ctx: Ctx) -> dict:
-    """{'fwd': (total_ms, launches), 'reduce': (total_ms, launches)}."""
+    """{'fwd': (total_ms, launches), 'reduce': (total_ms, launches), ...};
+    mode 'persist': 'reduce' holds the persistent epoch kernel's (total_ms,
+    launches) and 'persist_batches' the batches those launches trained."""
     ms = (c_dbl * 4)()
     n = (c_i64 * 4)()
     ctx._ok(lib().fae_get_kernel_timing(ctx.h, ctypes.cast(ms, c_ptr), ctypes.cast(n, c_ptr)))
     return {"fwd": (ms[0], n[0]), "reduce": (ms[1], n[1]),
-            "overlap": (ms[2], n[2]), "fused": bool(n[3])}
+            "overlap": (ms[2], n[2]), "fused": n[3] == 1, "persist": n[3] == 2,
+            "persist_batches": int(ms[3])}
 
 
 def fae_group_info(ctx: Ctx) -> dict:

@@ -42,25 +42,47 @@ def stale() -> bool:
     return any(os.path.getmtime(f) > t for f in sources() + headers())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = OUT) -> str:
+    """Compile every csrc/*.cu to an object in parallel (one nvcc per file),
+    then link libfae.so (`defines`/`out`: an A/B variant build)."""
+    if not force and out == OUT and not stale():
         return OUT
-    os.makedirs(os.path.dirname(OUT), exist_ok=True)
+    os.makedirs(os.path.dirname(out), exist_ok=True)
     inc, lib = nccl_paths()
-    cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
-           "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
-           "-I", inc, "-I", os.path.join(ROOT, "include"),
-           "-o", OUT + ".tmp", *sources(),
+    objdir = os.path.join(HERE, "_lib", "obj" + ("_" + os.path.basename(out)[:-3] if out != OUT else ""))
+    os.makedirs(objdir, exist_ok=True)
+    common = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
+              "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
+              "-I", inc, "-I", os.path.join(ROOT, "include"), *["-D" + d for d in defines]]
+    procs, objs = [], []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        objs.append(obj)
+        procs.append((src, subprocess.Popen(common + ["-c", src, "-o", obj],
+                                            stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                            text=True)))
+    failed = False
+    for src, pr in procs:
+        so, err = pr.communicate()
+        if pr.returncode != 0:
+            failed = True
+            sys.stderr.write(so + err)
+        elif verbose:
+            sys.stderr.write(err)
+    if failed:
+        raise RuntimeError("nvcc failed building libfae.so")
+    cmd = ["nvcc", *ARCH, "-shared", "-o", out + ".tmp", *objs,
            "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath," + lib]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libfae.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
-    os.replace(OUT + ".tmp", OUT)
-    return OUT
+        raise RuntimeError("nvcc failed linking libfae.so")
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs,
+                out=os.path.abspath(outs[0]) if outs else OUT))

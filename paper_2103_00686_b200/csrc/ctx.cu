@@ -44,6 +44,7 @@ fae_status read_latched(Ctx* c) {
         if (bits & kErrIndex) return set_err(c, FAE_ERR_INDEX_RANGE, "index outside its table (latched on device)");
         if (bits & kErrNonfinite) return set_err(c, FAE_ERR_NONFINITE, "non-finite value in update (latched on device)");
         if (bits & kErrOverflow) return set_err(c, FAE_ERR_CAPACITY, "counter overflow (latched on device)");
+        if (bits & kErrBarrier) return set_err(c, FAE_ERR_CUDA, "persistent kernel: grid barrier timed out (latched on device)");
     }
     return FAE_OK;
 }
@@ -136,6 +137,12 @@ fae_status fae_create(const fae_config* cfg, fae_ctx** out) {
         c->no_fused = !(f && f[0] == '1');
         const char* m = getenv("FAE_RED_MB");
         c->red_mb = m ? atoi(m) : 4;
+        // the persistent grid-barrier kernel is opt-in (FAE_PERSIST=1): on
+        // B200 a grid barrier costs more than a graph kernel boundary
+        const char* pe = getenv("FAE_PERSIST");
+        c->persist = pe && pe[0] == '1';
+        const char* pm = getenv("FAE_PERSIST_MB");
+        c->persist_mb = pm ? atoi(pm) : 0;
     }
     cudaError_t e = cudaSetDevice(cfg->device);
     if (e != cudaSuccess) {

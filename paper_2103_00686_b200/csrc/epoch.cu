@@ -154,7 +154,8 @@ __device__ __forceinline__ void long_chunk(const SegRec* __restrict__ lrec, int6
                                            const int32_t* __restrict__ perm_a,
                                            const int32_t* __restrict__ perm_b,
                                            const float* __restrict__ src, int D, float* W, float lr,
-                                           float* lpart, uint32_t* lcnt, int emit, float* grad_out,
+                                           float* lpart, uint32_t* lcnt, const int32_t* __restrict__ lmap,
+                                           int emit, float* grad_out,
                                            float* Y, uint32_t* err) {
     constexpr int G = 256 / LPB;
     constexpr int CH = kPiece / NV > 4 ? kPiece / NV : 4;
@@ -162,10 +163,12 @@ __device__ __forceinline__ void long_chunk(const SegRec* __restrict__ lrec, int6
     __shared__ int s_last;
     const int lane = threadIdx.x % LPB;
     const int grp = threadIdx.x / LPB;
-    // the segment of this chunk: last k with c0 <= lb (direct: record lb,
-    // a single chunk)
+    // the segment of this chunk: lmap[lb] (the grouping's chunk map), else
+    // the last k with c0 <= lb (direct: record lb, a single chunk)
     int64_t k = lb;
-    if (!direct) {
+    if (!direct && lmap) {
+        k = __ldg(lmap + lb);
+    } else if (!direct) {
         int64_t lo = 0, hi = n_long - 1;
         while (lo < hi) {
             const int64_t mid = (lo + hi + 1) >> 1;
@@ -301,7 +304,8 @@ __device__ __forceinline__ void reduce_segments(const SegRec* __restrict__ rec, 
                                                 int64_t n_med, int64_t n_long, int64_t n_lchunk,
                                                 const int32_t* __restrict__ perm,
                                                 const float* __restrict__ src, int D, float* W,
-                                                float lr, float* lpart, uint32_t* lcnt, int emit,
+                                                float lr, float* lpart, uint32_t* lcnt,
+                                                const int32_t* __restrict__ lmap, int emit,
                                                 float* grad_out, uint32_t* err) {
     constexpr int G = 256 / LPB;     // groups per block
     constexpr int GW = 32 / LPB;     // groups per warp
@@ -319,7 +323,7 @@ __device__ __forceinline__ void reduce_segments(const SegRec* __restrict__ rec, 
         b -= n_lchunk;
         if (!kMedWarp && b < med_blocks) {
             long_chunk<LPB, NV, kPDL, false>(rec + n_short, n_med, b, true, perm, nullptr, src, D, W, lr,
-                                             lpart, lcnt, emit, grad_out, nullptr, err);
+                                             lpart, lcnt, lmap, emit, grad_out, nullptr, err);
             return;
         }
         if (b < med_blocks) {
@@ -406,7 +410,7 @@ __device__ __forceinline__ void reduce_segments(const SegRec* __restrict__ rec, 
         return;
     }
     long_chunk<LPB, NV, kPDL, false>(rec + n_short + n_med, n_long, b, false, perm, nullptr, src, D, W, lr,
-                                     lpart, lcnt, emit, grad_out, nullptr, err);
+                                     lpart, lcnt, lmap, emit, grad_out, nullptr, err);
 }
 
 // ---------------------------------------------------------------------------
@@ -479,7 +483,8 @@ __device__ __forceinline__ void fused_reduce(const SegRec* __restrict__ rec, int
                                              int64_t n_long, int64_t n_lchunk, int64_t b,
                                              const int32_t* __restrict__ perm_a,
                                              const int32_t* __restrict__ perm_b, const float* __restrict__ src,
-                                             int D, float* W, float lr, float* lpart, uint32_t* lcnt, float* Y,
+                                             int D, float* W, float lr, float* lpart, uint32_t* lcnt,
+                                             const int32_t* __restrict__ lmap, float* Y,
                                              uint32_t* err) {
     constexpr int G = 256 / LPB;
     constexpr int GW = 32 / LPB;
@@ -494,7 +499,7 @@ __device__ __forceinline__ void fused_reduce(const SegRec* __restrict__ rec, int
         b -= n_lchunk;
         if (!kMedWarp && b < med_blocks) {
             long_chunk<LPB, NV, true, true>(rec + n_short, n_med, b, true, perm_a, perm_b, src, D, W, lr,
-                                            lpart, lcnt, 0, nullptr, Y, err);
+                                            lpart, lcnt, lmap, 0, nullptr, Y, err);
             return;
         }
         if (b < med_blocks) {
@@ -558,7 +563,7 @@ __device__ __forceinline__ void fused_reduce(const SegRec* __restrict__ rec, int
         return;
     }
     long_chunk<LPB, NV, true, true>(rec + n_short + n_med, n_long, b, false, perm_a, perm_b, src, D, W, lr,
-                                    lpart, lcnt, 0, nullptr, Y, err);
+                                    lpart, lcnt, lmap, 0, nullptr, Y, err);
 }
 
 template <int LPB, int NV, int MB>
@@ -567,7 +572,8 @@ k_grp_fused_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ 
                 int last_step, uint32_t* done_ctr, const SegRec* __restrict__ rec,
                 const FreeRec* __restrict__ freer, const int32_t* __restrict__ perm,
                 const float* __restrict__ dY, int64_t n_dy, int64_t dy_stride, int D, float* W, float lr,
-                float* lpart, uint32_t* lcnt, float* __restrict__ Y, uint32_t* err,
+                float* lpart, uint32_t* lcnt, const int32_t* __restrict__ lmap, float* __restrict__ Y,
+                uint32_t* err,
                 unsigned long long* stamps, int trig) {
     constexpr int G = 256 / LPB;
     if (!(trig & 1)) pdl_trigger();
@@ -596,7 +602,8 @@ k_grp_fused_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ 
             red_blocks = da.n_lchunk + med_blocks_for(da.n_med, LPB) + (da.n_short + G - 1) / G;
             if (bid < red_blocks) {
                 fused_reduce<LPB, NV>(rec + da.sb0, da.n_short, da.n_med, n_long, da.n_lchunk, bid, perm + da.lk0,
-                                      perm_b, dY + ((rel - 1) % n_dy) * dy_stride, D, W, lr, lpart, lcnt, Y, err);
+                                      perm_b, dY + ((rel - 1) % n_dy) * dy_stride, D, W, lr, lpart, lcnt,
+                                      lmap + lmap_base(da, run[0] + rel - 1), Y, err);
             }
         }
         if (has_b && bid >= red_blocks) {
@@ -677,14 +684,15 @@ __global__ void __launch_bounds__(256)
 k_grp_reduce(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ run,
              int64_t* cursor, uint32_t* done_ctr, const SegRec* __restrict__ rec,
              const int32_t* __restrict__ perm, const float* __restrict__ dY, int64_t n_dy,
-             int64_t dy_stride, int D, float* W, float lr, float* lpart, uint32_t* lcnt, int emit,
+             int64_t dy_stride, int D, float* W, float lr, float* lpart, uint32_t* lcnt,
+             const int32_t* __restrict__ lmap, int emit,
              float* grad_out, uint32_t* err) {
     const int64_t i = *cursor;
     if (i < run[1]) {
         const BatchDesc d = desc[run[0] + i];
         reduce_segments<LPB, NV, false>(rec + d.sb0, d.n_tiny, d.n_short, d.n_med, (d.sb1 - d.sb0) - d.n_short - d.n_med,
                                         d.n_lchunk, perm + d.lk0, dY + (i % n_dy) * dy_stride, D, W, lr, lpart,
-                                        lcnt, emit, grad_out, err);
+                                        lcnt, lmap + lmap_base(d, run[0] + i), emit, grad_out, err);
     }
     __syncthreads();
     if (threadIdx.x == 0) {   // the last CTA to finish advances the cursor
@@ -742,7 +750,8 @@ k_grp_reduce_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__
                  int64_t* base, int s, int last_step, uint32_t* done_ctr,
                  const SegRec* __restrict__ rec, const int32_t* __restrict__ perm,
                  const float* __restrict__ dY, int64_t n_dy, int64_t dy_stride, int D, float* W,
-                 float lr, float* lpart, uint32_t* lcnt, uint32_t* err, unsigned long long* stamps, int trig) {
+                 float lr, float* lpart, uint32_t* lcnt, const int32_t* __restrict__ lmap, uint32_t* err,
+                 unsigned long long* stamps, int trig) {
     if (!(trig & 1)) pdl_trigger();
     const int64_t b0 = *base;
     const int64_t rel = b0 + s;
@@ -755,7 +764,8 @@ k_grp_reduce_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__
         }
         const int64_t n_long = (d.sb1 - d.sb0) - d.n_short - d.n_med;
         reduce_segments<LPB, NV, true>(rec + d.sb0, d.n_tiny, d.n_short, d.n_med, n_long, d.n_lchunk, perm + d.lk0,
-                                       dY + (rel % n_dy) * dy_stride, D, W, lr, lpart, lcnt, 0, nullptr, err);
+                                       dY + (rel % n_dy) * dy_stride, D, W, lr, lpart, lcnt,
+                                       lmap ? lmap + lmap_base(d, run[0] + rel) : nullptr, 0, nullptr, err);
         if (stamps) {   // per-tier completion: [6] long CTAs, [7] short/medium CTAs
             __syncthreads();
             if (threadIdx.x == 0)
@@ -825,7 +835,7 @@ static void launch_grp_step(Ctx* c, cudaStream_t s, float* W, int64_t H, int D, 
     const int64_t rb = std::max<int64_t>(1, red_grid(g, gpb));
     k_grp_reduce<LPB, NV><<<(unsigned)rb, threads, 0, s>>>(g.desc, g.run, g.cursor, g.done_ctr, g.rec, g.perm,
                                                           dY, n_dy, g.max_bags * (int64_t)D, D, W, lr, g.lpart,
-                                                          g.lcnt, emit, c->ws.grad, c->d_err);
+                                                          g.lcnt, g.lmap, emit, c->ws.grad, c->d_err);
 }
 
 template <int LPB, int NV>
@@ -858,7 +868,8 @@ static fae_status launch_pdl_step(Ctx* c, cudaStream_t st, int s, float* W, int6
                                    g.cursor, s, last, g.done_ctr, (const SegRec*)g.rec, (const int32_t*)g.perm,
                                    dY, n_dy, g.max_bags * (int64_t)D, D, W, lr,
                                    g.lpart + (int64_t)s * std::max<int64_t>(g.max_lchunk, 1) * 8 * D,
-                                   g.lcnt + (int64_t)s * std::max<int64_t>(g.max_long, 1), c->d_err, stamps,
+                                   g.lcnt + (int64_t)s * std::max<int64_t>(g.max_long, 1),
+                                   getenv("FAE_NOLMAP") ? nullptr : (const int32_t*)g.lmap, c->d_err, stamps,
                                    c->pdl_trig));
     return FAE_OK;
 }
@@ -892,7 +903,8 @@ static fae_status launch_fused_step(Ctx* c, cudaStream_t st, int s, float* W, in
                                    g.done_ctr, (const SegRec*)g.rec, (const FreeRec*)g.freer, (const int32_t*)g.perm,
                                    dY, n_dy, g.max_bags * (int64_t)D, D, W, lr,
                                    g.lpart + (int64_t)s * std::max<int64_t>(g.max_lchunk, 1) * 8 * D,
-                                   g.lcnt + (int64_t)s * std::max<int64_t>(g.max_long, 1), Y, c->d_err, stamps,
+                                   g.lcnt + (int64_t)s * std::max<int64_t>(g.max_long, 1), (const int32_t*)g.lmap, Y,
+                                   c->d_err, stamps,
                                    c->pdl_trig));
     return FAE_OK;
 }
@@ -901,6 +913,11 @@ static fae_status launch_fused(Ctx* c, cudaStream_t st, int s, float* W, int64_t
                                int64_t n_dy, float* Y, float lr, unsigned long long* stamps) {
     FAE_DISPATCH_D(D, return launch_fused_step, c, st, s, W, H, D, dY, n_dy, Y, lr, stamps);
     return FAE_OK;
+}
+
+static bool use_persist(Ctx* c) {
+    const Group& g = c->grp;
+    return g.P == 1 && !g.hot_off && c->world == 1 && c->persist;
 }
 
 static bool use_fused(Ctx* c) {
@@ -965,8 +982,9 @@ void group_free(Ctx* c) {
     for (int v = 0; v < 2; v++)
         for (int e = 0; e < 3 * kUnroll; e++)
             if (g.tev[v][e]) cudaEventDestroy(g.tev[v][e]);
-    void* ptrs[] = {g.desc, g.perm, g.rec, g.freer, g.nxt, g.lpart, g.lcnt, g.keys[0], g.keys[1], g.vals, g.seg_start, g.seg_row,
-                    g.tile_start, g.tile_batch, g.sstatus, g.pstatus, g.ghist, g.cursor, g.done_ctr, g.stamps};
+    void* ptrs[] = {g.desc, g.perm, g.rec, g.freer, g.nxt, g.lpart, g.lcnt, g.lmap, g.keys[0], g.keys[1], g.vals, g.seg_start,
+                    g.seg_row, g.tile_start, g.tile_batch, g.sstatus, g.pstatus, g.ghist, g.cursor, g.done_ctr, g.pbar,
+                    g.stamps};
     for (void* p : ptrs) cudaFree(p);
     g = Group{};
 }
@@ -983,6 +1001,8 @@ extern "C" fae_status fae_set_kernel_timing(fae_ctx* h, int32_t enable) {
     h->c.t_overlap_n = 0;
     h->c.t_tier_ms[0] = h->c.t_tier_ms[1] = 0.0;
     h->c.t_fused = false;
+    h->c.t_persist = false;
+    h->c.t_persist_batches = 0;
     h->c.t_red_entry_lead_ms = 0.0;
     return FAE_OK;
 }
@@ -992,11 +1012,11 @@ extern "C" fae_status fae_get_kernel_timing(const fae_ctx* h, double* ms, int64_
     ms[0] = h->c.t_ms[0];
     ms[1] = h->c.t_ms[1];
     ms[2] = h->c.t_red_entry_lead_ms;
-    ms[3] = 0.0;
+    ms[3] = (double)h->c.t_persist_batches;
     n[0] = h->c.t_n[0];
     n[1] = h->c.t_n[1];
     n[2] = h->c.t_overlap_n;
-    n[3] = h->c.t_fused ? 1 : 0;
+    n[3] = h->c.t_persist ? 2 : (h->c.t_fused ? 1 : 0);
     return FAE_OK;
 }
 
@@ -1037,6 +1057,26 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
             }
             fae_status st = sync_merge_apply(c, rows, c->ws.grad, U, D, W_hot, H, lr, nullptr, nullptr, nullptr, 0);
             if (st != FAE_OK) return st;
+        }
+        return FAE_OK;
+    }
+    if (use_persist(c) && c->timing != 2) {
+        cudaEvent_t* ev = nullptr;
+        if (c->timing == 1) {
+            for (int e = 0; e < 2; e++)
+                if (!g.tev[0][e]) FAE_CUDA(c, cudaEventCreate(&g.tev[0][e]));
+            ev = g.tev[0];
+        }
+        fae_status st = launch_train_persist(c, W_hot, D, dY, n_dy, Y, lr, first, n, ev);
+        if (st != FAE_OK) return st;
+        if (ev) {
+            float ms = 0.f;
+            FAE_CUDA(c, cudaEventSynchronize(ev[1]));
+            FAE_CUDA(c, cudaEventElapsedTime(&ms, ev[0], ev[1]));
+            c->t_ms[1] += ms;
+            c->t_n[1] += 1;
+            c->t_persist = true;
+            c->t_persist_batches += n;
         }
         return FAE_OK;
     }

@@ -26,13 +26,17 @@ constexpr int kMedium = 128;           // segments of (kPiece, kMedium] lookups:
 // Lookups per long-segment CTA (one CTA pass).  Measured on B200: at D = 16
 // (LPB = 4) four 512-chunks combined across CTAs beat larger chunks; at
 // D = 64 (LPB = 16) 256-chunks beat 512 (reduce 17.0 vs 20.0 us per batch).
-__host__ __device__ constexpr int chunk_of_lpb(int lpb) { return lpb <= 4 ? 512 : 256; }
+#ifndef FAE_CHUNK_SMALL
+#define FAE_CHUNK_SMALL 512
+#endif
+__host__ __device__ constexpr int chunk_of_lpb(int lpb) { return lpb <= 4 ? FAE_CHUNK_SMALL : 256; }
 inline int chunk_for_dim(int D) { return chunk_of_lpb(D / 4 < 32 ? D / 4 : 32); }
 // reduce blocks of a batch's medium segments: one warp each when a warp holds
 // >= 8 lane groups (LPB <= 4), else one CTA each (single-chunk long path)
 __host__ __device__ inline int64_t med_blocks_for(int64_t n_med, int lpb) {
     return lpb <= 4 ? (n_med + 7) / 8 : n_med;
 }
+constexpr int kMaxPersistCtas = 2048;  // persistent kernel: barrier flag slots
 constexpr int kTinySeg = 4;            // segments of <= kTinySeg lookups: 4 per lane group
 constexpr int kGSThreads = 256;        // grouping sort: threads per tile
 constexpr int kGSItems = 16;           // grouping sort: items per thread
@@ -42,6 +46,7 @@ constexpr int kGSTile = kGSThreads * kGSItems;   // 4096 lookups per tile
 constexpr uint32_t kErrIndex = 1u;
 constexpr uint32_t kErrNonfinite = 2u;
 constexpr uint32_t kErrOverflow = 4u;
+constexpr uint32_t kErrBarrier = 8u;    // persistent kernel: grid barrier timed out
 
 // Look-back status words: 2 flag bits on top of the value.
 constexpr uint64_t kFlagAgg = 1ull << 62;
@@ -124,6 +129,12 @@ struct alignas(16) FreeRec {
     int32_t pos, len, row, pad;
 };
 
+// Long-chunk -> long-segment map (Group::lmap) of batch `bi`: its slice
+// starts at lk0 / 64 + bi.  A batch has at most L_b / 128 chunks (every long
+// segment has > kMedium = 128 lookups and a chunk >= 128), so the slices of
+// consecutive batches never overlap; capacity L_total / 64 + n_batches + 1.
+__host__ __device__ inline int64_t lmap_base(const BatchDesc& d, int64_t bi) { return d.lk0 / 64 + bi; }
+
 struct Group {
     bool valid = false;
     int64_t n_batches = 0, L_total = 0, S_total = 0, n_long_total = 0;
@@ -163,6 +174,9 @@ struct Group {
     int64_t* cursor = nullptr;        // device: [0] base / cursor, [2] first, [3] n
     int64_t* run = nullptr;
     uint32_t* done_ctr = nullptr;
+    int32_t* lmap = nullptr;          // long chunk -> long record index (lmap_base per batch)
+    int64_t cap_lmap = 0;
+    uint32_t* pbar = nullptr;         // persistent kernel: [0] arrivals, [1] abort, [2 + 32 c] CTA c's flag
 
     cudaGraphExec_t graph = nullptr;
     int graph_steps = 0;
@@ -207,6 +221,10 @@ struct Ctx {
     bool no_pdl = false;              // FAE_NO_PDL=1: plain serialized launches
     bool no_fused = true;             // FAE_FUSED=1: one fused kernel per step for P = 1
     bool t_fused = false;             // timing came from the fused kernel
+    bool t_persist = false;           // timing came from the persistent kernel
+    int64_t t_persist_batches = 0;    // batches trained by the timed persistent launches
+    bool persist = false;             // FAE_PERSIST=1: the persistent grid-barrier kernel
+    int persist_mb = 0;               // FAE_PERSIST_MB: CTAs per SM (0 = occupancy limit)
     int red_mb = 4;                   // FAE_RED_MB: min resident reduce CTAs per SM (4/6/8)
     int pdl_trig = 0;                 // FAE_PDL_TRIG bit0: reduce triggers after its wait, bit1: fwd too
 };
@@ -245,6 +263,10 @@ fae_status sync_merge_apply(Ctx* c, const int32_t* rows, const float* vals, int6
                             float* W, int64_t H, float lr, int32_t* out_rows, float* out_vals,
                             int64_t* out_count, int64_t out_cap);
 fae_status step_ws_alloc(Ctx* c);
+// persistent epoch kernel (persist.cu): batches [first, first + n) of the
+// grouping, world 1, single-lookup bags; ev (optional) brackets the launch
+fae_status launch_train_persist(Ctx* c, float* W, int D, const float* dY, int64_t n_dy, float* Y, float lr,
+                                int64_t first, int64_t n, cudaEvent_t* ev);
 void group_free(Ctx* c);
 fae_status validate_schema(Ctx* c, const fae_tables* t, const char* who);
 void step_ws_free(Ctx* c);

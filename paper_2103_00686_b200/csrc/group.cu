@@ -367,7 +367,7 @@ k_gs_links(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __res
 __global__ void __launch_bounds__(256)
 k_gs_records(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __restrict__ seg_start,
              const int32_t* __restrict__ seg_row, const int32_t* __restrict__ nxt,
-             SegRec* __restrict__ rec, int chunk) {
+             SegRec* __restrict__ rec, int chunk, int32_t* __restrict__ lmap) {
     constexpr int NC = 4;
     __shared__ uint32_t s_w[NC][8];
     __shared__ uint32_t s_n[NC];
@@ -451,10 +451,12 @@ k_gs_records(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __r
         __syncthreads();
         if (tid == 0) {   // chunks of the long segments, in record order
             int32_t cc = 0;
+            int32_t* lm = lmap + lmap_base(d, b);
             for (int64_t q = (int64_t)base[3]; q < S; q++) {
                 SegRec& lr = rec[d.sb0 + q];
                 lr.c0 = cc;
                 lr.nc = (lr.len + chunk - 1) / chunk;
+                for (int32_t j = 0; j < lr.nc; j++) lm[cc + j] = (int32_t)(q - (int64_t)base[3]);
                 cc += lr.nc;
             }
             desc[b].n_lchunk = cc;
@@ -493,7 +495,7 @@ extern "C" fae_status fae_group_info(const fae_ctx* h, int64_t* info) {
     int64_t nf = 0;
     for (const BatchDesc& d : g.hdesc) nf += d.n_free;
     info[6] = nf;
-    info[7] = g.P == 1 && !g.hot_off && h->c.world == 1 && !h->c.no_fused;
+    info[7] = (g.P == 1 && !g.hot_off && h->c.world == 1) ? (h->c.persist ? 2 : (h->c.no_fused ? 0 : 1)) : 0;
     return FAE_OK;
 }
 
@@ -590,6 +592,7 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
     if ((st = ensure(c, &g.rec, &c5, L + 2)) != FAE_OK) return st;
     int64_t c6 = g.cap_S, c7 = g.cap_S;
     if ((st = ensure(c, &g.freer, &c6, L + 2)) != FAE_OK) return st;
+    if ((st = ensure(c, &g.lmap, &g.cap_lmap, L / 64 + nb + 2)) != FAE_OK) return st;
     if ((st = ensure(c, &g.nxt, &c7, L + 2)) != FAE_OK) return st;
     g.cap_S = std::min(std::min(std::min(c3, c4), c5), std::min(c6, c7));
     if ((st = ensure(c, &g.desc, &g.cap_B, std::max<int64_t>(nb, 1))) != FAE_OK) return st;
@@ -606,6 +609,7 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
         g.run = g.cursor + 2;
         FAE_CUDA(c, cudaMalloc(&g.done_ctr, sizeof(uint32_t) * 16));
         FAE_CUDA(c, cudaMemset(g.done_ctr, 0, sizeof(uint32_t) * 16));
+        FAE_CUDA(c, cudaMalloc(&g.pbar, sizeof(uint32_t) * (2 + 32 * kMaxPersistCtas)));
     }
     stage("alloc");
     g.S_total = 0;
@@ -683,7 +687,8 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
         k_gs_links<<<(unsigned)gr, 256, 0, c->stream>>>(g.desc, nb, g.seg_start, g.seg_row, g.nxt, g.freer);
         FAE_LAUNCHED(c);
         g.chunk = chunk_for_dim(tabs->dim);
-        k_gs_records<<<(unsigned)gr, 256, 0, c->stream>>>(g.desc, nb, g.seg_start, g.seg_row, g.nxt, g.rec, g.chunk);
+        k_gs_records<<<(unsigned)gr, 256, 0, c->stream>>>(g.desc, nb, g.seg_start, g.seg_row, g.nxt, g.rec, g.chunk,
+                                                          g.lmap);
         FAE_LAUNCHED(c);
         FAE_CUDA(c, cudaMemcpyAsync(g.hdesc.data(), g.desc, sizeof(BatchDesc) * nb, cudaMemcpyDeviceToHost, c->stream));
         st = read_latched(c);

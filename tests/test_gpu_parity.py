@@ -346,17 +346,20 @@ TB_SMALL = gen.Config("tb-small", [max(3, r // 200) for r in gen.TERABYTE_ROWS],
                       records=30_000, t=1e-6)
 
 
-@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("mode", ["graph", "fused", "persist"])
 @pytest.mark.parametrize("cfg,R,t,small", [("kaggle", 100_000, 1e-6, 1 << 20),
                                            ("alibaba", 20_000, 1e-5, 1 << 20),
                                            ("tiny", 10_000, 1e-2, 0),
                                            ("tb-small", 30_000, 1e-6, 1 << 20)])
-def test_grouped_training(dev, cfg, R, t, small, fused, monkeypatch):
-    """fae_group_batches + fae_train_hot_batches (graph replay, device cursor)
-    == the standalone per-step calls bit for bit, and == the oracle's
+def test_grouped_training(dev, cfg, R, t, small, mode, monkeypatch):
+    """fae_group_batches + fae_train_hot_batches (graph replay with a device
+    cursor, the fused graph step, or the persistent grid-barrier kernel) ==
+    the standalone per-step calls bit for bit, and == the oracle's
     sequential SGD within tolerance; includes the ragged last batch."""
     from paper_2103_00686_b200.pipeline import FaePipeline
-    monkeypatch.setenv("FAE_FUSED", "1" if fused else "0")   # read at fae_create
+    # read at fae_create
+    monkeypatch.setenv("FAE_FUSED", "1" if mode == "fused" else "0")
+    monkeypatch.setenv("FAE_PERSIST", "1" if mode == "persist" else "0")
     c = TB_SMALL if cfg == "tb-small" else gen.CONFIGS[cfg]
     ds = gen.make_dataset(c, n_records=R, seed=5)
     dd = ds.to(dev)
@@ -366,14 +369,15 @@ def test_grouped_training(dev, cfg, R, t, small, fused, monkeypatch):
     W_hot = pipe.extract(W.to(dev), prep).clone()
     W_std = W_hot.clone()
     nbt = prep.packed["n_hot_batches"]
-    nb = min(5, nbt)
+    nb = min(24 if mode == "persist" else 5, nbt)
     first = nbt - nb
     S = c.batch * c.n_tables
     dY = gen.make_dy(nb * S, c.dim, seed=9).view(nb, S, c.dim).to(dev)
     lr = 0.05
     pipe.group(prep)
     from paper_2103_00686_b200 import fae_group_info
-    assert fae_group_info(pipe.ctx)["fused"] == int(fused and c.pool == 1)
+    want = {"graph": 0, "fused": 1, "persist": 2}[mode] if c.pool == 1 else 0
+    assert fae_group_info(pipe.ctx)["fused"] == want
     Y = torch.zeros(S, c.dim, device=dev)
     pipe.train(W_hot, first, nb, dY, Y, lr)
     pipe.ctx.check()
