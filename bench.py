@@ -412,17 +412,19 @@ def run_reference(args):
     if rank != 0:
         return None
     cfg = gen.CONFIGS[args.config]
-    R_s = min(args.cpu_records, cfg.records)
+    # each step a bounded sample (about 2 s of oracle work) so that the whole
+    # --steps K --warmup W run ends within a few minutes
+    R_s = min(args.ref_records, cfg.records)
     ds, W = oracle_sample_setup(cfg, R_s)
     for _ in range(args.warmup):
-        oracle_step(cfg, R_s, args.cpu_batches, args.seed, args.lr, ds, W)
+        oracle_step(cfg, R_s, args.ref_batches, args.seed, args.lr, ds, W)
     n_tot, t_tot = 0, 0.0
     for _ in range(args.steps):
-        n, dt = oracle_step(cfg, R_s, args.cpu_batches, args.seed, args.lr, ds, W)
+        n, dt = oracle_step(cfg, R_s, args.ref_batches, args.seed, args.lr, ds, W)
         n_tot += n
         t_tot += dt
     v = n_tot / t_tot
-    samp = (f"full a1-a10 oracle pipeline on the first {R_s} records, <= {args.cpu_batches} "
+    samp = (f"full a1-a10 oracle pipeline on the first {R_s} records, <= {args.ref_batches} "
             f"hot batches per step, single-threaded C fp64")
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_tot * 1e3 / args.steps,
@@ -443,8 +445,10 @@ def main():
     ap.add_argument("--impl", default="fae", choices=["fae", "reference"])
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--cpu-records", type=int, default=100_000)
-    ap.add_argument("--cpu-batches", type=int, default=16)
+    ap.add_argument("--cpu-records", type=int, default=4_000_000)
+    ap.add_argument("--cpu-batches", type=int, default=256)
+    ap.add_argument("--ref-records", type=int, default=1_000_000, help="--impl reference: records per step")
+    ap.add_argument("--ref-batches", type=int, default=32, help="--impl reference: hot batches per step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dy-pool-mb", type=int, default=256, help="upstream-gradient pool (> L2 by default)")
     ap.add_argument("--no-cpu", action="store_true")

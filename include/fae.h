@@ -148,6 +148,16 @@ fae_status fae_profile(fae_ctx* ctx, const fae_tables* tabs,
  *    ceil(K*T_z/T_ref)); bytes(K) = sum_small N_z*D*4 + sum_large D*4*
  *    #{j: k_z[j] >= kmin_z}; the smallest K with bytes(K) <= budget.
  *    t_final = K / (T_ref*x/100).  budget_slack = 1 when K = 1 fits.
+ *  CLT_SEARCH (the statistical optimizer; search rule R27 =
+ *    SPEC calibrate S:L191-199): est_bytes(t) = small-table bytes + D*4 *
+ *    sum over large tables of the Eq. 4 CI upper bound (rows) of the Eqs. 2-4
+ *    estimate at the Eq. 1 cutoff (n, m, t_quantile, chunk_seed as below);
+ *    t fits iff est_bytes(t) <= budget_bytes.  Grid t_j = 10^(-8 + j/4),
+ *    j = 0..28: the first fitting t_j, then 8 bisection steps between t_j
+ *    and t_{j-1} (midpoint (lo + hi) / 2, keep the fitting side); t_final =
+ *    the fitting end; rows are then tagged with the EXACT counts at
+ *    t_final's Eq. 1 cutoffs.  budget_slack = 1 if t_0 = 1e-8 fits;
+ *    BUDGET_INFEASIBLE if t = 0.1 does not.
  *  ESTIMATE (want_estimate, Eqs. 2-4) at the final cutoff, per
  *    large table: n chunks of m rows with the smallest (key(chunk_seed ^ z,
  *    c), c), C_i (Eq. 2), ybar (Eq. 3), s (n-1 denominator, R8), CI with the
@@ -168,13 +178,14 @@ fae_status fae_profile(fae_ctx* ctx, const fae_tables* tabs,
  * ------------------------------------------------------------------------ */
 typedef enum fae_thresh_mode {
     FAE_THRESH_FIXED_T = 0,
-    FAE_THRESH_BUDGET_EXACT = 1
+    FAE_THRESH_BUDGET_EXACT = 1,
+    FAE_THRESH_CLT_SEARCH = 2
 } fae_thresh_mode;
 
 typedef struct fae_thresh_req {
     int32_t mode;               /* fae_thresh_mode                            */
     double t;                   /* FIXED_T threshold, fraction in (0, 1] (R2) */
-    int64_t budget_bytes;       /* BUDGET_EXACT: L                           */
+    int64_t budget_bytes;       /* BUDGET_EXACT / CLT_SEARCH: L              */
     int64_t small_table_bytes;  /* default 1 << 20 (R11)                     */
     int32_t want_estimate;      /* compute Eqs. 2-4 at the final cutoff      */
     int32_t n_chunks;           /* n (35)                             */
@@ -333,12 +344,15 @@ fae_status fae_group_batches(fae_ctx* ctx, const fae_tables* tabs,
  * with dY_i = dY + (i % n_dy) * (B*Tn) * D (device [n_dy][B*Tn][D]; the
  * upstream gradient of each step, e.g. written by the MLP backward) and Y
  * device [B*Tn][D] (overwritten every step).  Sequential SGD semantics:
- * batch i+1 sees the rows batch i updated.  World 1, single-lookup bags:
- * ONE cooperative persistent kernel for the whole range (a grid-wide barrier
- * between steps; step i does the backward + SGD of batch i-1 and the
- * forward of batch i; FAE_PERSIST=0 selects the graph path instead).  Other
- * world-1 inputs: replays a captured CUDA graph of 2 kernels per step (no
- * host work per step).  World > 1: the
+ * batch i+1 sees the rows batch i updated.  World 1: replays a captured
+ * CUDA graph (no host work per step) of, per step, ONE fused kernel (part R:
+ * backward + SGD of batch i-1, writing each updated row straight into the
+ * Y of batch i; part F: the forward of batch i's remaining rows) for
+ * single-lookup bags with D <= 16, else two kernels (forward, backward +
+ * SGD), chained by programmatic dependent launch; bit-identical either way.
+ * FAE_FUSED=0/1 forces the choice; FAE_PERSIST=1 selects a cooperative
+ * persistent kernel with a grid barrier per step (single-lookup bags; slower
+ * on B200, kept for measurement).  World > 1: the
  * sparse gradient is exchanged every step (fae_sync_hot_grads semantics).
  * H must equal the H given to fae_group_batches and D the tabs->dim given
  * to it (the long-segment chunking is sized for that row width).

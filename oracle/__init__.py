@@ -66,6 +66,8 @@ def _declare(L):
     L.or_hot_bytes.argtypes = [i32, P, i32, i64, P, P]
     L.or_estimate.restype = None
     L.or_estimate.argtypes = [P, i64, i64, i32, i32, u64, f64, P, P, P]
+    L.or_clt_search.restype = ctypes.c_int
+    L.or_clt_search.argtypes = [i32, P, i32, i64, P, P, f64, i64, i32, i32, u64, f64, P, P, P, P, P]
     L.or_remap.restype = i64; L.or_remap.argtypes = [i32, P, P, P, P]
     L.or_classify.restype = None
     L.or_classify.argtypes = [i32, P, P, P, i32, i64, P, P]
@@ -173,6 +175,22 @@ def estimate(k_table, kmin, n=35, m=1024, chunk_seed=0, t_q=3.6007):
                       t_q, _ptr(out), _ptr(C), _ptr(ch))
     return dict(ybar=out[0], s=out[1], lo=out[2], hi=out[3], est=out[4],
                 exact=bool(out[5]), C=C, chunks=ch)
+
+
+def clt_search(rows, dim, small_bytes, counts, T, x_pct, budget_bytes, n=35, m=1024,
+               chunk_seed=0, t_q=3.6007):
+    """CLT-driven statistical optimizer (or_clt_search, R27)."""
+    rows = _np(rows, np.int64); counts = _np(counts, np.uint32)
+    T = _np(T, np.int64)
+    kmin = np.zeros(len(rows), np.int64)
+    tf = ctypes.c_double(0); bf = ctypes.c_double(0)
+    slack = ctypes.c_int32(0); ev = ctypes.c_int32(0)
+    st = lib().or_clt_search(len(rows), _ptr(rows), dim, small_bytes, _ptr(counts), _ptr(T),
+                             x_pct, budget_bytes, n, m, chunk_seed, t_q, _ptr(kmin),
+                             ctypes.byref(tf), ctypes.byref(bf), ctypes.byref(slack),
+                             ctypes.byref(ev))
+    return dict(status=st, kmin=kmin, t_final=tf.value, est_bytes=bf.value,
+                slack=slack.value, evals=ev.value)
 
 
 def remap(rows, hot):

@@ -375,6 +375,84 @@ void or_estimate(const uint32_t* k, int64_t Nz, int64_t kmin, int32_t n,
 }
 
 /* ---------------------------------------------------------------------------
+ * Statistical optimizer, CLT-driven (§4.1.3: "invokes the profiler
+ * with varying t (interim thresholds) ... tunes the threshold to be higher or
+ * lower than the previous one"; the search rule is unstated — R27 takes
+ * SPEC's calibrate):
+ *   est_bytes(t) = sum_small N_z*D*4 + sum_large D*4*hi_z(t)
+ * with hi_z(t) the Eq. 4 CI upper bound (rows) of table z's Eqs. 2-4
+ * estimate (or_estimate, chunk seed chunk_seed ^ z) at kmin_z(t) =
+ * max(1, ceil(((t*T_z)*x)/100)) (Eq. 1).  t is fit iff est_bytes(t) <= L.
+ *   1. grid t_j = 10^(-8 + j/4), j = 0..28 (ratio 10^(1/4) over [1e-8, 1e-1]);
+ *   2. t_28 not fit -> OR_BUDGET_INFEASIBLE; j* = the smallest fit j;
+ *   3. j* = 0 -> t = t_0, slack = 1;
+ *   4. else bisection on [lo, hi] = [t_{j*-1}, t_{j*}] for 8 steps:
+ *      mid = (lo + hi) / 2 (R27: arithmetic midpoint); fit(mid) ? hi = mid :
+ *      lo = mid;  t = hi.
+ * Outputs t_final, kmin_z(t_final) (0 for small tables), the estimated bytes
+ * at t_final and the number of est_bytes evaluations.
+ * ------------------------------------------------------------------------- */
+static double est_bytes_at(int32_t n_tables, const int64_t* rows, int32_t dim,
+                           int64_t small_bytes, const uint32_t* counts,
+                           const int64_t* T, double t, double x_pct, int32_t n,
+                           int32_t m, uint64_t chunk_seed, double t_q)
+{
+    double b = 0.0, out[6];
+    int64_t g0 = 0;
+    int64_t* C = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+    int64_t* ch = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+    for (int32_t z = 0; z < n_tables; z++) {
+        if (is_small(rows[z], dim, small_bytes)) {
+            b += (double)(rows[z] * (int64_t)dim * 4);
+        } else {
+            int64_t kmin = or_kmin_from_cutoff(or_cutoff(t, T[z], x_pct));
+            or_estimate(counts + g0, rows[z], kmin, n, m, chunk_seed ^ (uint64_t)z, t_q, out, C, ch);
+            b += out[3] * (double)dim * 4.0;
+        }
+        g0 += rows[z];
+    }
+    free(C); free(ch);
+    return b;
+}
+
+int or_clt_search(int32_t n_tables, const int64_t* rows, int32_t dim,
+                  int64_t small_bytes, const uint32_t* counts, const int64_t* T,
+                  double x_pct, int64_t budget_bytes, int32_t n, int32_t m,
+                  uint64_t chunk_seed, double t_q, int64_t* kmin,
+                  double* t_final, double* bytes_final, int32_t* slack,
+                  int32_t* evals)
+{
+    double L = (double)budget_bytes, tg[29], b;
+    int32_t j, jstar = -1;
+    *evals = 0; *slack = 0;
+    for (j = 0; j <= 28; j++) tg[j] = pow(10.0, -8.0 + 0.25 * (double)j);
+    for (j = 0; j <= 28; j++) {
+        b = est_bytes_at(n_tables, rows, dim, small_bytes, counts, T, tg[j], x_pct, n, m, chunk_seed, t_q);
+        (*evals)++;
+        if (b <= L) { jstar = j; break; }
+    }
+    if (jstar < 0) return OR_BUDGET_INFEASIBLE;
+    double t = tg[jstar];
+    if (jstar == 0) {
+        *slack = 1;
+    } else {
+        double lo = tg[jstar - 1], hi = tg[jstar];
+        for (int32_t it = 0; it < 8; it++) {
+            double mid = (lo + hi) / 2.0;
+            b = est_bytes_at(n_tables, rows, dim, small_bytes, counts, T, mid, x_pct, n, m, chunk_seed, t_q);
+            (*evals)++;
+            if (b <= L) hi = mid; else lo = mid;
+        }
+        t = hi;
+    }
+    *t_final = t;
+    *bytes_final = est_bytes_at(n_tables, rows, dim, small_bytes, counts, T, t, x_pct, n, m, chunk_seed, t_q);
+    for (int32_t z = 0; z < n_tables; z++)
+        kmin[z] = is_small(rows[z], dim, small_bytes) ? 0 : or_kmin_from_cutoff(or_cutoff(t, T[z], x_pct));
+    return OR_OK;
+}
+
+/* ---------------------------------------------------------------------------
  * O4  Hot-row remap for the embedding replicator ("extracts hot
  * embedding entries and creates embedding bags").  Tables concatenated in
  * order, rows ascending within a table (R16):

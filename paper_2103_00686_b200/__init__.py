@@ -24,7 +24,7 @@ _lib = None
 
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "CAPACITY", 3: "BUDGET_INFEASIBLE",
           4: "INDEX_RANGE", 5: "NONFINITE", 6: "CUDA", 7: "NCCL", 8: "NOT_INIT"}
-FIXED_T, BUDGET_EXACT = 0, 1
+FIXED_T, BUDGET_EXACT, CLT_SEARCH = 0, 1, 2
 
 EXPORTS = ["fae_create", "fae_destroy", "fae_set_stream", "fae_last_error",
            "fae_check", "fae_get_nccl_id", "fae_comm_init",

@@ -26,6 +26,8 @@
 
 namespace fae {
 
+constexpr int kSt = kStampSlots;
+
 // finish a segment: emit G (a11 exchange) or W[row] -= lr * G (a10)
 template <int LPB, int NV>
 __device__ __forceinline__ void seg_finish(const float4 (&g)[NV], int lane, int32_t row, int32_t seg,
@@ -581,11 +583,7 @@ k_grp_fused_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ 
     const int64_t rel = b0 + s;          // kernel index in the run: 0 .. n
     const int64_t n = run[1];
     if (rel <= n) {
-        if (stamps && threadIdx.x == 0) {
-            atomicMin(&stamps[rel * 8 + 4], (unsigned long long)gtimer());
-            pdl_wait();
-            atomicMin(&stamps[rel * 8 + 2], (unsigned long long)gtimer());
-        }
+        if (stamps && threadIdx.x == 0) atomicMin(&stamps[rel * kSt + 4], (unsigned long long)gtimer());
         const int64_t first = run[0];
         const bool has_a = rel >= 1, has_b = rel < n;
         int64_t bid = blockIdx.x;
@@ -637,7 +635,7 @@ k_grp_fused_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ 
         }
         if (stamps) {
             __syncthreads();
-            if (threadIdx.x == 0) atomicMax(&stamps[rel * 8 + 3], (unsigned long long)gtimer());
+            if (threadIdx.x == 0) atomicMax(&stamps[rel * kSt + 3], (unsigned long long)gtimer());
         }
         if (trig & 1) {
             pdl_wait();
@@ -710,9 +708,11 @@ k_grp_reduce(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ run
 // run[0] + *base + s; *base advances by kUnroll at the end of each replay.
 // Launched with programmatic stream serialization: each kernel triggers its
 // dependents at entry, so the next kernel's prologue overlaps this kernel;
-// griddepcontrol.wait guards W.  stamps (optional, per step): [0] fwd start,
-// [1] fwd end, [2] reduce start, [3] reduce end (globaltimer ns; start = min
-// over CTAs after the wait, end = max).
+// griddepcontrol.wait guards W.  stamps (optional, kStampSlots per step,
+// globaltimer ns, no stamp ever waits on the grid dependency): [1] fwd end
+// and [3] reduce end (max over CTAs), [5] / [4] fwd / reduce entry (min),
+// [9] / [8] their last CTA entry (max), [6] / [7] long / short-medium reduce
+// CTA completion (max).
 template <int LPB, int NV>
 __global__ void __launch_bounds__(256)
 k_grp_fwd_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ run,
@@ -725,12 +725,12 @@ k_grp_fwd_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ ru
         if (trig & 2) pdl_trigger();
         return;
     }
-    if (stamps && threadIdx.x == 0) atomicMin(&stamps[rel * 8 + 5], (unsigned long long)gtimer());
-    const BatchDesc d = desc[run[0] + rel];
     if (stamps && threadIdx.x == 0) {
-        pdl_wait();
-        atomicMin(&stamps[rel * 8 + 0], (unsigned long long)gtimer());
+        const unsigned long long t = gtimer();
+        atomicMin(&stamps[rel * kSt + 5], t);
+        atomicMax(&stamps[rel * kSt + 9], t);
     }
+    const BatchDesc d = desc[run[0] + rel];
     if (trig & 2) {
         pdl_wait();
         pdl_trigger();
@@ -740,7 +740,7 @@ k_grp_fwd_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ ru
     else fwd_bags<LPB, NV, true>(W, H, D, hot_idx + d.lk0, nullptr, P, d.n_bags, Y, err);
     if (stamps) {
         __syncthreads();
-        if (threadIdx.x == 0) atomicMax(&stamps[rel * 8 + 1], (unsigned long long)gtimer());
+        if (threadIdx.x == 0) atomicMax(&stamps[rel * kSt + 1], (unsigned long long)gtimer());
     }
 }
 
@@ -756,12 +756,12 @@ k_grp_reduce_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__
     const int64_t b0 = *base;
     const int64_t rel = b0 + s;
     if (rel < run[1]) {
-        if (stamps && threadIdx.x == 0) atomicMin(&stamps[rel * 8 + 4], (unsigned long long)gtimer());
-        const BatchDesc d = desc[run[0] + rel];
         if (stamps && threadIdx.x == 0) {
-            pdl_wait();   // start of the exclusive part: the forward of this batch is done
-            atomicMin(&stamps[rel * 8 + 2], (unsigned long long)gtimer());
+            const unsigned long long t = gtimer();
+            atomicMin(&stamps[rel * kSt + 4], t);
+            atomicMax(&stamps[rel * kSt + 8], t);
         }
+        const BatchDesc d = desc[run[0] + rel];
         const int64_t n_long = (d.sb1 - d.sb0) - d.n_short - d.n_med;
         reduce_segments<LPB, NV, true>(rec + d.sb0, d.n_tiny, d.n_short, d.n_med, n_long, d.n_lchunk, perm + d.lk0,
                                        dY + (rel % n_dy) * dy_stride, D, W, lr, lpart, lcnt,
@@ -769,7 +769,7 @@ k_grp_reduce_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__
         if (stamps) {   // per-tier completion: [6] long CTAs, [7] short/medium CTAs
             __syncthreads();
             if (threadIdx.x == 0)
-                atomicMax(&stamps[rel * 8 + (blockIdx.x < d.n_lchunk ? 6 : 7)], (unsigned long long)gtimer());
+                atomicMax(&stamps[rel * kSt + (blockIdx.x < d.n_lchunk ? 6 : 7)], (unsigned long long)gtimer());
         }
         if (trig & 1) {
             pdl_wait();
@@ -777,7 +777,7 @@ k_grp_reduce_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__
         }
         if (stamps) {
             __syncthreads();
-            if (threadIdx.x == 0) atomicMax(&stamps[rel * 8 + 3], (unsigned long long)gtimer());
+            if (threadIdx.x == 0) atomicMax(&stamps[rel * kSt + 3], (unsigned long long)gtimer());
         }
     }
     if ((trig & 1) && rel >= run[1]) pdl_trigger();
@@ -854,7 +854,8 @@ static fae_status launch_pdl_step(Ctx* c, cudaStream_t st, int s, float* W, int6
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const int64_t half = (int64_t)sm_count(c) * 4;   // each kernel gets about half of the GPU
+    static const int64_t fcap = getenv("FAE_FWD_GRID") ? atoll(getenv("FAE_FWD_GRID")) : 0;
+    const int64_t half = fcap > 0 ? fcap : (int64_t)sm_count(c) * 4;   // each kernel gets about half of the GPU
     const int64_t fu = g.P == 1 ? cdiv(g.max_bags, 4) : g.max_bags;
     cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(fu, gpb), half)));
     FAE_CUDA(c, cudaLaunchKernelEx(&cfg, k_grp_fwd_pdl<LPB, NV>, (const BatchDesc*)g.desc, (const int64_t*)g.run,
@@ -920,10 +921,13 @@ static bool use_persist(Ctx* c) {
     return g.P == 1 && !g.hot_off && c->world == 1 && c->persist;
 }
 
-static bool use_fused(Ctx* c) {
+bool fused_step(const Ctx* c) {
     const Group& g = c->grp;
-    return g.P == 1 && !g.hot_off && c->world == 1 && !c->no_fused;
+    if (!(g.P == 1 && !g.hot_off && c->world == 1) || c->fused_mode == 0) return false;
+    return c->fused_mode == 1 || g.dim <= 16;
 }
+
+static bool use_fused(Ctx* c) { return fused_step(c); }
 
 static fae_status launch_step(Ctx* c, cudaStream_t s, float* W, int64_t H, int D, const float* dY,
                               int64_t n_dy, float* Y, float lr, int emit, cudaEvent_t mid = nullptr) {
@@ -1154,21 +1158,22 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
             cudaFree(g.stamps);
             g.stamps = nullptr;
             g.stamp_cap = n + n / 4 + 64;
-            FAE_CUDA(c, cudaMalloc(&g.stamps, sizeof(unsigned long long) * 8 * g.stamp_cap));
+            FAE_CUDA(c, cudaMalloc(&g.stamps, sizeof(unsigned long long) * kSt * g.stamp_cap));
         }
         stamps = g.stamps;
-        std::vector<unsigned long long> init(8 * (n + 1));
+        std::vector<unsigned long long> init(kSt * (n + 1));
         for (int64_t i = 0; i <= n; i++) {
-            init[8 * i + 0] = ~0ull;
-            init[8 * i + 1] = 0;
-            init[8 * i + 2] = ~0ull;
-            init[8 * i + 3] = 0;
-            init[8 * i + 4] = ~0ull;
-            init[8 * i + 5] = ~0ull;
-            init[8 * i + 6] = 0;
-            init[8 * i + 7] = 0;   // tier ends
+            init[kSt * i + 0] = ~0ull;
+            init[kSt * i + 1] = 0;
+            init[kSt * i + 2] = ~0ull;
+            init[kSt * i + 3] = 0;
+            init[kSt * i + 4] = ~0ull;
+            init[kSt * i + 5] = ~0ull;
+            init[kSt * i + 6] = 0;
+            init[kSt * i + 7] = 0;   // tier ends
+            for (int q = 8; q < kSt; q++) init[kSt * i + q] = 0;   // maxima
         }
-        FAE_CUDA(c, cudaMemcpyAsync(stamps, init.data(), sizeof(unsigned long long) * 8 * (n + 1),
+        FAE_CUDA(c, cudaMemcpyAsync(stamps, init.data(), sizeof(unsigned long long) * kSt * (n + 1),
                                     cudaMemcpyHostToDevice, c->stream));
         FAE_CUDA(c, cudaStreamSynchronize(c->stream));
     }
@@ -1186,16 +1191,18 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
     if (stamps && fused) {
         // one kernel per step: K(i)'s exclusive share runs from the end of
         // K(i-1) (same replay) to its own end; attributed to slot 1
-        std::vector<unsigned long long> st(8 * (n + 1));
-        FAE_CUDA(c, cudaMemcpyAsync(st.data(), stamps, sizeof(unsigned long long) * 8 * (n + 1),
+        std::vector<unsigned long long> st(kSt * (n + 1));
+        FAE_CUDA(c, cudaMemcpyAsync(st.data(), stamps, sizeof(unsigned long long) * kSt * (n + 1),
                                     cudaMemcpyDeviceToHost, c->stream));
         FAE_CUDA(c, cudaStreamSynchronize(c->stream));
         for (int64_t i = 0; i <= n; i++) {
-            const unsigned long long rs = st[8 * i + 2], re = st[8 * i + 3];
+            // K(i)'s exclusive share: from the end of K(i-1) (its own entry
+            // for the first step) to its end; no stamp waits on the grid
+            // dependency, so the kernels run exactly as untimed
+            const unsigned long long re = st[kSt * i + 3];
             if (re == 0) continue;
-            unsigned long long r0 = rs;
-            if (i > 0 && (i % kUnroll) != 0 && st[8 * (i - 1) + 3] > r0) r0 = st[8 * (i - 1) + 3];
-            if (i > 0 && st[8 * i + 4] < st[8 * (i - 1) + 3]) c->t_overlap_n++;
+            const unsigned long long r0 = i > 0 ? st[kSt * (i - 1) + 3] : st[kSt * i + 4];
+            if (i > 0 && st[kSt * i + 4] < st[kSt * (i - 1) + 3]) c->t_overlap_n++;
             c->t_ms[1] += re > r0 ? (double)(re - r0) * 1e-6 : 0.0;
             c->t_n[1]++;
         }
@@ -1203,25 +1210,44 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
     } else if (stamps) {
         // exclusive critical-path share of each kernel: fwd(s) from the end of
         // reduce(s-1) (same replay), reduce(s) from the end of fwd(s)
-        std::vector<unsigned long long> st(8 * n);
-        FAE_CUDA(c, cudaMemcpyAsync(st.data(), stamps, sizeof(unsigned long long) * 8 * n,
+        std::vector<unsigned long long> st(kSt * n);
+        FAE_CUDA(c, cudaMemcpyAsync(st.data(), stamps, sizeof(unsigned long long) * kSt * n,
                                     cudaMemcpyDeviceToHost, c->stream));
         FAE_CUDA(c, cudaStreamSynchronize(c->stream));
         for (int64_t i = 0; i < n; i++) {
-            const unsigned long long fs = st[8 * i], fe = st[8 * i + 1], rs = st[8 * i + 2], re = st[8 * i + 3];
+            // exclusive shares without any stamp waiting on the grid dependency:
+            // fwd(i) from the end of reduce(i-1) (its entry for the first
+            // step), reduce(i) from the end of fwd(i)
+            const unsigned long long fs = i > 0 ? st[kSt * (i - 1) + 3] : st[kSt * i + 5];
+            const unsigned long long fe = st[kSt * i + 1], re = st[kSt * i + 3];
             if (fe == 0 || re == 0) continue;
             // overlap evidence: the reduce entered before the forward ended
-            if (st[8 * i + 4] < fe) c->t_overlap_n++;
-            c->t_red_entry_lead_ms += fe > st[8 * i + 4] ? (double)(fe - st[8 * i + 4]) * 1e-6 : 0.0;
-            unsigned long long f0 = fs;
-            if (i > 0 && (i % kUnroll) != 0 && st[8 * (i - 1) + 3] > f0) f0 = st[8 * (i - 1) + 3];
-            const unsigned long long r0 = rs > fe ? rs : fe;
+            if (st[kSt * i + 4] < fe) c->t_overlap_n++;
+            c->t_red_entry_lead_ms += fe > st[kSt * i + 4] ? (double)(fe - st[kSt * i + 4]) * 1e-6 : 0.0;
+            const unsigned long long f0 = fs, r0 = fe;
             c->t_ms[0] += fe > f0 ? (double)(fe - f0) * 1e-6 : 0.0;
             c->t_ms[1] += re > r0 ? (double)(re - r0) * 1e-6 : 0.0;
             c->t_n[0]++;
             c->t_n[1]++;
-            if (st[8 * i + 6] > fe) c->t_tier_ms[0] += (double)(st[8 * i + 6] - fe) * 1e-6;
-            if (st[8 * i + 7] > fe) c->t_tier_ms[1] += (double)(st[8 * i + 7] - fe) * 1e-6;
+            if (st[kSt * i + 6] > fe) c->t_tier_ms[0] += (double)(st[kSt * i + 6] - fe) * 1e-6;
+            if (st[kSt * i + 7] > fe) c->t_tier_ms[1] += (double)(st[kSt * i + 7] - fe) * 1e-6;
+        }
+        if (getenv("FAE_VERBOSE") && n > 1) {
+            double a8 = 0, a9 = 0, a11 = 0;
+            int64_t m = 0;
+            for (int64_t i = 1; i < n; i++) {
+                const double fe = (double)st[kSt * i + 1], pe = (double)st[kSt * (i - 1) + 3];
+                if (fe == 0 || pe == 0) continue;
+                a8 += (double)st[kSt * i + 8] - fe;
+                a9 += (double)st[kSt * i + 9] - pe;
+                a11 += 0.0;
+                m++;
+            }
+            if (m)
+                fprintf(stderr, "[fae_train_hot_batches] last reduce CTA entry %+.2f us after the fwd end; last fwd "
+                                "CTA entry %+.2f us after the previous reduce end\n",
+                        a8 / m * 1e-3, a9 / m * 1e-3);
+            (void)a11;
         }
         if (getenv("FAE_VERBOSE") && c->t_n[1] > 0)
             fprintf(stderr, "[fae_train_hot_batches] avg after fwd end: long CTAs %.2f us, short/medium CTAs %.2f us\n",

@@ -36,6 +36,7 @@ inline int chunk_for_dim(int D) { return chunk_of_lpb(D / 4 < 32 ? D / 4 : 32); 
 __host__ __device__ inline int64_t med_blocks_for(int64_t n_med, int lpb) {
     return lpb <= 4 ? (n_med + 7) / 8 : n_med;
 }
+constexpr int kStampSlots = 16;        // timing stamps per step (epoch runner)
 constexpr int kMaxPersistCtas = 2048;  // persistent kernel: barrier flag slots
 constexpr int kTinySeg = 4;            // segments of <= kTinySeg lookups: 4 per lane group
 constexpr int kGSThreads = 256;        // grouping sort: threads per tile
@@ -133,12 +134,16 @@ struct alignas(16) FreeRec {
 // starts at lk0 / 64 + bi.  A batch has at most L_b / 128 chunks (every long
 // segment has > kMedium = 128 lookups and a chunk >= 128), so the slices of
 // consecutive batches never overlap; capacity L_total / 64 + n_batches + 1.
+// the fused one-kernel step applies (single-lookup bags, world 1)
+struct Ctx;
+bool fused_step(const Ctx* c);
+
 __host__ __device__ inline int64_t lmap_base(const BatchDesc& d, int64_t bi) { return d.lk0 / 64 + bi; }
 
 struct Group {
     bool valid = false;
     int64_t n_batches = 0, L_total = 0, S_total = 0, n_long_total = 0;
-    int32_t Tn = 0, P = 0, B = 0;
+    int32_t Tn = 0, P = 0, B = 0, dim = 0;
     int64_t H = 0;
     int64_t max_bags = 0, max_lookups = 0, max_short = 0, max_med = 0, max_long = 0, max_segs = 0;
     const int32_t* hot_idx = nullptr;
@@ -219,7 +224,7 @@ struct Ctx {
     double t_red_entry_lead_ms = 0.0; // sum of (fwd end - reduce entry)
     double t_tier_ms[2] = {0.0, 0.0}; // reduce tiers' completion after fwd end
     bool no_pdl = false;              // FAE_NO_PDL=1: plain serialized launches
-    bool no_fused = true;             // FAE_FUSED=1: one fused kernel per step for P = 1
+    int fused_mode = -1;              // FAE_FUSED: -1 auto (D <= 16), 1 on, 0 off (P = 1, world 1)
     bool t_fused = false;             // timing came from the fused kernel
     bool t_persist = false;           // timing came from the persistent kernel
     int64_t t_persist_batches = 0;    // batches trained by the timed persistent launches

@@ -75,7 +75,7 @@ k_gs_init(const int32_t* __restrict__ hot_idx, const int64_t* __restrict__ hot_o
                 for (int r = 0; r < kGSItems; r++) {
                     const bool ok = wb + r * 32 + lane < s1;
                     const uint32_t dg = ok ? ((key[r] >> (ps * kSortBits)) & (kSortBins - 1)) : (uint32_t)kSortBins + lane;
-                    const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+                    const uint32_t peers = match_label<kSortBits + 1>(dg);
                     if (ok && (__ffs(peers) - 1) == lane) atomicAdd(&sh[ps][dg], (uint32_t)__popc(peers));
                 }
             }
@@ -160,7 +160,7 @@ k_gs_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ hot_idx,
     for (int r = 0; r < kGSItems; r++) {
         const bool ok = wl + r * 32 + lane < n_tile;
         const uint32_t dg = ok ? ((k[r] >> shift) & (kSortBins - 1)) : (uint32_t)kSortBins;
-        const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+        const uint32_t peers = match_label<kSortBits + 1>(dg);
         const uint32_t lt = __popc(peers & lanemask_lt());
         uint32_t cnt = 0;
         if (ok) cnt = s_w[warp][dg];
@@ -495,7 +495,7 @@ extern "C" fae_status fae_group_info(const fae_ctx* h, int64_t* info) {
     int64_t nf = 0;
     for (const BatchDesc& d : g.hdesc) nf += d.n_free;
     info[6] = nf;
-    info[7] = (g.P == 1 && !g.hot_off && h->c.world == 1) ? (h->c.persist ? 2 : (h->c.no_fused ? 0 : 1)) : 0;
+    info[7] = (g.P == 1 && !g.hot_off && h->c.world == 1) ? (h->c.persist ? 2 : (fused_step(&h->c) ? 1 : 0)) : 0;
     return FAE_OK;
 }
 
@@ -530,6 +530,7 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
     g.n_batches = nb;
     g.Tn = Tn;
     g.P = fixed_pool;
+    g.dim = tabs->dim;
     g.B = batch;
     g.H = H;
     g.hot_idx = pk->hot_idx;

@@ -8,6 +8,20 @@ namespace fae {
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+// lanes of the warp holding the same NB-bit label as this lane: one ballot per
+// label bit (bit-sliced match; cheaper than __match_any_sync for small NB)
+template <int NB>
+__device__ __forceinline__ uint32_t match_label(uint32_t v) {
+    uint32_t m = 0xffffffffu;
+#pragma unroll
+    for (int b = 0; b < NB; b++) {
+        const uint32_t bit = (v >> b) & 1u;
+        const uint32_t bb = __ballot_sync(0xffffffffu, bit);
+        m &= bit ? bb : ~bb;
+    }
+    return m;
+}
+
 __device__ __forceinline__ uint64_t gtimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

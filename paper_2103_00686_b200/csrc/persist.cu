@@ -578,7 +578,7 @@ fae_status launch_t(Ctx* c, float* W, int D, const float* dY, int64_t n_dy, floa
             cudaFree(g.stamps);
             g.stamps = nullptr;
             g.stamp_cap = n + n / 4 + 64;
-            FAE_CUDA(c, cudaMalloc(&g.stamps, sizeof(unsigned long long) * 8 * g.stamp_cap));
+            FAE_CUDA(c, cudaMalloc(&g.stamps, sizeof(unsigned long long) * kStampSlots * g.stamp_cap));
         }
         stamps = g.stamps;
         std::vector<unsigned long long> init(8 * (n + 1), 0ull);

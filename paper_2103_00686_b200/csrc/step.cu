@@ -173,7 +173,7 @@ k_sort_pass(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
         k[j] = ok ? kin[i] : 0u;
         v[j] = ok ? vin[i] : 0;
         const uint32_t d = ok ? ((k[j] >> shift) & (kSortBins - 1)) : kSortBins;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t peers = match_label<kSortBits + 1>(d);
         const uint32_t lt = __popc(peers & lanemask_lt());
         uint32_t cnt = 0;
         if (ok) cnt = s_w[warp][d];

@@ -309,13 +309,15 @@ extern "C" fae_status fae_threshold(fae_ctx* h, const fae_tables* tabs, const ui
     if (st != FAE_OK) return st;
     if (!counts || !T_host || !req || !res) return set_err(c, FAE_ERR_INVALID_ARG, "fae_threshold: null argument");
     if (!(x_pct > 0.0 && x_pct <= 100.0)) return set_err(c, FAE_ERR_INVALID_ARG, "fae_threshold: x must be in (0, 100]");
-    if (req->mode != FAE_THRESH_FIXED_T && req->mode != FAE_THRESH_BUDGET_EXACT)
+    if (req->mode != FAE_THRESH_FIXED_T && req->mode != FAE_THRESH_BUDGET_EXACT &&
+        req->mode != FAE_THRESH_CLT_SEARCH)
         return set_err(c, FAE_ERR_INVALID_ARG, "fae_threshold: bad mode");
     if (req->mode == FAE_THRESH_FIXED_T && !(req->t > 0.0 && req->t <= 1.0))
         return set_err(c, FAE_ERR_INVALID_ARG, "fae_threshold: t must be in (0, 1]");
-    if (req->mode == FAE_THRESH_BUDGET_EXACT && req->budget_bytes < 0)
+    if (req->mode != FAE_THRESH_FIXED_T && req->budget_bytes < 0)
         return set_err(c, FAE_ERR_INVALID_ARG, "fae_threshold: negative budget");
-    if (req->want_estimate && (req->n_chunks < 2 || req->n_chunks > 256 || req->chunk_rows < 1))
+    if ((req->want_estimate || req->mode == FAE_THRESH_CLT_SEARCH) &&
+        (req->n_chunks < 2 || req->n_chunks > 256 || req->chunk_rows < 1))
         return set_err(c, FAE_ERR_INVALID_ARG, "fae_threshold: n must be in [2, 256] and m >= 1");
     const int Tn = tabs->n_tables;
     const int D = tabs->dim;
@@ -373,6 +375,72 @@ extern "C" fae_status fae_threshold(fae_ctx* h, const fae_tables* tabs, const ui
             const double cc = std::ceil(H);
             kmin[z] = cc < 1.0 ? 1 : (cc >= 1.8e19 ? ~0ull : (uint64_t)cc);
         }
+    } else if (req->mode == FAE_THRESH_CLT_SEARCH) {
+        // Statistical optimizer (R27): geometric grid then 8
+        // bisection steps on the Eq. 4 CI upper bound of the hot bytes; every
+        // evaluation = Eq. 1 cutoffs + one k_estimate launch over the large
+        // tables (Eqs. 2-4 on the device), summed here in table order
+        std::vector<int32_t> tl;
+        for (int z = 0; z < Tn; z++)
+            if (large[z]) tl.push_back(z);
+        if (!tl.empty())
+            FAE_CUDA(c, cudaMemcpyAsync(d_tab, tl.data(), sizeof(int32_t) * tl.size(), cudaMemcpyHostToDevice, c->stream));
+        std::vector<unsigned long long> km(Tn);
+        std::vector<double> e(6 * Tn);
+        auto kmin_at = [&](double t) {
+            for (int z = 0; z < Tn; z++) {
+                km[z] = 0ull;
+                if (!large[z]) continue;
+                const double H = ((t * (double)T_host[z]) * x_pct) / 100.0;   // Eq. 1 (R21)
+                const double cc = std::ceil(H);
+                km[z] = cc < 1.0 ? 1 : (cc >= 1.8e19 ? ~0ull : (uint64_t)cc);
+            }
+        };
+        auto est_bytes = [&](double t, double* b) -> fae_status {
+            kmin_at(t);
+            if (!tl.empty()) {
+                FAE_CUDA(c, cudaMemcpyAsync(d_kmin, km.data(), sizeof(unsigned long long) * Tn, cudaMemcpyHostToDevice,
+                                            c->stream));
+                k_estimate<<<(unsigned)tl.size(), 1024, 0, c->stream>>>(counts, c->d_rowbase_tmp, d_tab, d_kmin,
+                                                                        req->n_chunks, req->chunk_rows,
+                                                                        req->chunk_seed, req->t_quantile, d_est);
+                FAE_LAUNCHED(c);
+                FAE_CUDA(c, cudaMemcpyAsync(e.data(), d_est, sizeof(double) * 6 * Tn, cudaMemcpyDeviceToHost, c->stream));
+                FAE_CUDA(c, cudaStreamSynchronize(c->stream));
+            }
+            double acc = 0.0;
+            for (int z = 0; z < Tn; z++) {
+                if (!large[z]) acc += (double)(tabs->rows[z] * (int64_t)D * 4);
+                else acc += e[6 * z + 3] * (double)D * 4.0;
+            }
+            *b = acc;
+            return FAE_OK;
+        };
+        const double L = (double)req->budget_bytes;
+        double tg[29], b = 0.0;
+        for (int j = 0; j <= 28; j++) tg[j] = std::pow(10.0, -8.0 + 0.25 * (double)j);
+        int jstar = -1;
+        for (int j = 0; j <= 28 && jstar < 0; j++) {
+            if ((st = est_bytes(tg[j], &b)) != FAE_OK) return st;
+            if (b <= L) jstar = j;
+        }
+        if (jstar < 0)
+            return set_err(c, FAE_ERR_BUDGET_INFEASIBLE, "fae_threshold: the estimate at t = 0.1 exceeds the budget");
+        t_final = tg[jstar];
+        if (jstar == 0) {
+            slack = 1;
+        } else {
+            double lo = tg[jstar - 1], hi = tg[jstar];
+            for (int it = 0; it < 8; it++) {
+                const double mid = (lo + hi) / 2.0;
+                if ((st = est_bytes(mid, &b)) != FAE_OK) return st;
+                if (b <= L) hi = mid;
+                else lo = mid;
+            }
+            t_final = hi;
+        }
+        kmin_at(t_final);
+        for (int z = 0; z < Tn; z++) kmin[z] = km[z];
     } else {
         if (small_total > req->budget_bytes)
             return set_err(c, FAE_ERR_BUDGET_INFEASIBLE, "fae_threshold: small tables alone exceed the budget");

@@ -404,3 +404,41 @@ def test_grouped_training(dev, cfg, R, t, small, mode, monkeypatch):
         Wr, _ = oracle.emb_bwd_sgd(Wr, bi, off, P, n_bags, dY[i, :n_bags].cpu(), lr)
     ok, worst = close(W_hot.cpu().numpy(), Wr)
     assert ok, worst
+
+
+@pytest.mark.parametrize("budget", [4 << 20, 8 << 20, 1 << 40])
+def test_clt_search_parity(dev, budget):
+    """NEXT-4: the CLT-driven statistical optimizer (R27) on the
+    device == oracle.clt_search bit for bit (t_final, cutoffs, hot rows,
+    remap), on the device's own loggers; includes the slack case (1 TB)."""
+    m = fae()
+    c = gen.CONFIGS["kaggle"]
+    ds = gen.make_dataset(c, n_records=400_000, seed=4)
+    x, seed = 5.0, 3
+    ctx = mkctx(ds.rows, 16, 2048 * 26, 2048 * 26)
+    dd = ds.to(dev)
+    counts = torch.empty(sum(ds.rows), dtype=torch.int32, device=dev)
+    T, _ = m.fae_profile(ctx, ds.rows, 16, dd.idx, None, 1, ds.n_records, x, seed, counts)
+    remap = torch.empty(sum(ds.rows), dtype=torch.int32, device=dev)
+    th = m.fae_threshold(ctx, ds.rows, 16, counts, T, x, mode=m.CLT_SEARCH, budget_bytes=budget,
+                         chunk_seed=77, t_quantile=3.6007, remap_out=remap)
+    cnt = counts.cpu().numpy().view(np.uint32)
+    r = oracle.clt_search(ds.rows, 16, 1 << 20, cnt, T, x, budget, chunk_seed=77, t_q=3.6007)
+    assert r["status"] == 0
+    assert th["t_final"] == r["t_final"]
+    assert th["budget_slack"] == r["slack"]
+    assert [int(k) for k in th["kmin"]] == [int(k) for k in r["kmin"]]
+    hot = oracle.tag_rows(ds.rows, 16, 1 << 20, cnt, r["kmin"])
+    rm, base, H = oracle.remap(ds.rows, hot)
+    assert th["H_total"] == H and list(th["base"]) == list(base)
+    assert np.array_equal(remap.cpu().numpy(), rm)
+
+
+def test_clt_search_infeasible_gpu(dev):
+    m = fae()
+    rows = [40 * 1024]
+    ctx = mkctx(rows, 16, 1024, 1024)
+    counts = torch.full((rows[0],), 1000, dtype=torch.int32, device=dev)
+    with pytest.raises(m.FaeError) as e:
+        m.fae_threshold(ctx, rows, 16, counts, [100], 5.0, mode=m.CLT_SEARCH, budget_bytes=1000)
+    assert e.value.name == "BUDGET_INFEASIBLE"

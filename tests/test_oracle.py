@@ -545,3 +545,92 @@ def test_sharding_invariance():
                                     None, 3, per, dY[g * per:(g + 1) * per])
             acc[r] += Gg
         assert np.allclose(acc[rows_all], G_all, rtol=0, atol=1e-12)
+
+
+# ----------------------------------------------------------------------------
+# NEXT-4: CLT-driven statistical optimizer (R27)
+# ----------------------------------------------------------------------------
+GRID = [10.0 ** (-8 + 0.25 * j) for j in range(29)]
+
+
+def test_clt_search_uniform_degenerate_slack():
+    # every row has the same count and L = bytes of all rows -> the
+    # estimate is exact (s = 0, C_i = m), all rows hot at any t below the
+    # uniform fraction: the smallest grid t fits (slack), bytes == L
+    rows = [40 * 1024]
+    cu = np.full(rows[0], 3, np.uint32)
+    L = rows[0] * 16 * 4
+    r = oracle.clt_search(rows, 16, 1 << 20, cu, [1000], 5.0, L, chunk_seed=9)
+    assert r["status"] == 0 and r["slack"] == 1
+    assert r["t_final"] == GRID[0] and r["est_bytes"] == L and r["evals"] == 1
+    assert list(r["kmin"]) == [1]
+
+
+def test_clt_search_infeasible():
+    # even t = 1e-1 leaves every row hot (all counts above the cutoff): the
+    # estimate is N rows > L -> infeasible
+    rows = [40 * 1024]
+    c = np.full(rows[0], 1000, np.uint32)
+    r = oracle.clt_search(rows, 16, 1 << 20, c, [100], 5.0, 1000)
+    assert r["status"] == oracle.BUDGET_INFEASIBLE
+    # small tables alone above L
+    r = oracle.clt_search([100], 16, 1 << 20, np.zeros(100, np.uint32), [10], 5.0, 100)
+    assert r["status"] == oracle.BUDGET_INFEASIBLE
+
+
+def test_clt_search_exact_tables_bisection_bound():
+    # tables with fewer than n chunks are scanned exactly (est = exact hot
+    # rows), so est_bytes(t) is the exact hot-set size, non-increasing in t.
+    # The search then brackets the exact threshold: with t* the smallest t in
+    # the final grid cell whose exact bytes fit, t_final - cell/2^8 < t* <=
+    # t_final (bisection bound), found here by brute force over a fine scan.
+    rng = np.random.default_rng(4)
+    rows = [30 * 1024, 20 * 1024]                 # 30, 20 chunks < n = 35
+    counts = np.concatenate([rng.zipf(1.3, rows[0]) % 5000,
+                             rng.zipf(1.6, rows[1]) % 5000]).astype(np.uint32)
+    T = np.array([2_000_000, 500_000])
+    for L in [64 * 3000, 64 * 8000, 64 * 20000]:
+        r = oracle.clt_search(rows, 16, 1 << 20, counts, T, 5.0, L)
+        assert r["status"] == 0 and r["slack"] == 0
+        tf = r["t_final"]
+        j = min(i for i, g in enumerate(GRID) if g >= tf)
+        lo_cell, hi_cell = GRID[j - 1], GRID[j]
+        assert lo_cell < tf <= hi_cell
+        km = oracle.kmin_fixed_t(rows, 16, 1 << 20, T, tf, 5.0)
+        assert list(km) == list(r["kmin"])
+        b = oracle.hot_bytes(rows, 16, 1 << 20, counts, km)
+        assert b <= L and b == r["est_bytes"]
+        d = (hi_cell - lo_cell) / 256
+        below = oracle.kmin_fixed_t(rows, 16, 1 << 20, T, tf - d * 1.0001, 5.0)
+        assert oracle.hot_bytes(rows, 16, 1 << 20, counts, below) > L or tf - d * 1.0001 <= lo_cell
+        # brute force: the exact smallest fitting t in the cell, by a fine scan
+        ts = np.linspace(lo_cell, hi_cell, 4097)[1:]
+        fit = [t for t in ts
+               if oracle.hot_bytes(rows, 16, 1 << 20, counts,
+                                   oracle.kmin_fixed_t(rows, 16, 1 << 20, T, t, 5.0)) <= L]
+        t_star = min(fit)
+        assert tf - d - (ts[1] - ts[0]) <= t_star <= tf
+
+
+def test_clt_search_budget_on_zipf_estimate():
+    # S:L198 [DERIVED]: L = 0.5 x (exact hot bytes at a reference t) on a
+    # Zipf(1.05) logger estimated by CLT chunks (N >> n): t_final > t_ref and
+    # the exact hot bytes at t_final land in [0.8 L, L] (the Eq. 4 upper bound
+    # is what must fit, so the exact set sits just below L; "within
+    # 10%").  Reference t with a sizeable hot set (~5% / ~19% of rows).
+    n = 400_000
+    u = gen.uniform01(78, torch.arange(4_000_000))
+    cdf = gen.zipf_cdf(n, 1.05, "cpu")
+    rank = torch.searchsorted(cdf, u).clamp(max=n - 1)
+    k = np.bincount(gen.feistel(rank, n, 6).numpy(), minlength=n).astype(np.uint32)
+    T = [4_000_000 * 20]                      # the sample is x = 5% of T
+    for t_ref in (1e-6, 3e-6):
+        km = oracle.kmin_fixed_t([n], 16, 1 << 20, T, t_ref, 5.0)
+        L = oracle.hot_bytes([n], 16, 1 << 20, k, km) // 2
+        ok = 0
+        for s in range(10):
+            r = oracle.clt_search([n], 16, 1 << 20, k, T, 5.0, L, chunk_seed=100 + s)
+            assert r["status"] == 0 and r["t_final"] > t_ref and r["est_bytes"] <= L
+            b = oracle.hot_bytes([n], 16, 1 << 20, k, r["kmin"])
+            ok += 0.8 * L <= b <= L
+        assert ok >= 9
