@@ -102,6 +102,20 @@ class Clocks:
 # ----------------------------------------------------------------------------
 # algorithmic bytes
 # ----------------------------------------------------------------------------
+def ncu_traffic(kernel, workload):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)
+    of `kernel` from the committed `ncu --set full` summary
+    (profiles/ncu_traffic.json, written by tools/ncu_summary.py traffic);
+    None when no capture of this kernel on this workload is committed."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        e = t.get(workload, {}).get(kernel)
+        return float(e["dram_bytes_per_launch"]) if e else None
+    except Exception:
+        return None
+
+
 def fwd_bytes(L, S, D, explicit_off):
     """a8 per batch: idx (4L) [+ offsets 8(S+1)] + row gathers 4DL + Y 4DS."""
     return 4 * L + (8 * (S + 1) if explicit_off else 0) + 4 * D * L + 4 * D * S
@@ -247,6 +261,8 @@ def run_fae(args):
         else:
             kb = red_bytes(L_b, S_b, U_b, D)
         achieved = kb / avg_s / 1e9 if avg_s > 0 else 0.0
+        kname_full = ("k_train_persist" if persist else "k_grp_fused_pdl" if fused else
+                      {"fwd": "k_grp_fwd_pdl", "reduce": "k_grp_reduce_pdl"}[kname])
         res = {
             "metric": METRIC, "value": lookups_all / (ms_max / 1e3), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -266,14 +282,14 @@ def run_fae(args):
                            ds.idx.numel() * 4 / 1e9, n_dy * dy_bytes >> 20),
                        "parallelism": f"dp{world}"},
             "gpu_launches": launches,
-            "roofline": {"kernel": ("k_train_persist" if persist else "k_grp_fused_pdl" if fused else
-                                    {"fwd": "k_grp_fwd_pdl", "reduce": "k_grp_reduce_pdl"}[kname]),
+            "roofline": {"kernel": kname_full,
                          "timing": ("CUDA events around each cooperative launch on the ctx stream, every launch "
                                     "of the timed region" if persist else
                                     "in-kernel globaltimer, exclusive share of the step, every launch of the timed region"),
                          "bound": "hbm", "achieved": achieved,
                          "peak": peak, "peak_kind": kind, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak,
+                         "traffic": ncu_traffic(kname_full, f"{cfg.name}-shaped"),
                          "bytes_per_launch": kb, "avg_launch_us": avg_s * 1e6,
                          "kernels_us": {k: (kt[k][0] / max(kt[k][1], 1)) * 1e3 for k in ("fwd", "reduce")},
                          "launches_timed": kn,
@@ -445,8 +461,8 @@ def main():
     ap.add_argument("--impl", default="fae", choices=["fae", "reference"])
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--cpu-records", type=int, default=4_000_000)
-    ap.add_argument("--cpu-batches", type=int, default=256)
+    ap.add_argument("--cpu-records", type=int, default=12_000_000)
+    ap.add_argument("--cpu-batches", type=int, default=1024)
     ap.add_argument("--ref-records", type=int, default=1_000_000, help="--impl reference: records per step")
     ap.add_argument("--ref-batches", type=int, default=32, help="--impl reference: hot batches per step")
     ap.add_argument("--no-e2e", action="store_true")

@@ -24,10 +24,11 @@ constexpr int kPiece = 16;             // max lookups per reduction piece
 constexpr int kUnroll = 128;           // steps per captured epoch graph
 constexpr int kMedium = 128;           // segments of (kPiece, kMedium] lookups: one warp
 // Lookups per long-segment CTA (one CTA pass).  Measured on B200: at D = 16
-// (LPB = 4) four 512-chunks combined across CTAs beat larger chunks; at
-// D = 64 (LPB = 16) 256-chunks beat 512 (reduce 17.0 vs 20.0 us per batch).
+// (LPB = 4) with the fused step, 1024-chunks 6.59, 512 6.65, 2048 7.62 us
+// per step (Kaggle-shaped); at D = 64 (LPB = 16) 256-chunks beat 512
+// (reduce 17.0 vs 20.0 us per batch).
 #ifndef FAE_CHUNK_SMALL
-#define FAE_CHUNK_SMALL 512
+#define FAE_CHUNK_SMALL 1024
 #endif
 __host__ __device__ constexpr int chunk_of_lpb(int lpb) { return lpb <= 4 ? FAE_CHUNK_SMALL : 256; }
 inline int chunk_for_dim(int D) { return chunk_of_lpb(D / 4 < 32 ? D / 4 : 32); }
@@ -230,6 +231,7 @@ struct Ctx {
     int64_t t_persist_batches = 0;    // batches trained by the timed persistent launches
     bool persist = false;             // FAE_PERSIST=1: the persistent grid-barrier kernel
     int persist_mb = 0;               // FAE_PERSIST_MB: CTAs per SM (0 = occupancy limit)
+    bool gs_generic = false;          // FAE_GS_GENERIC=1: radix-pass grouping even where the unit path applies
     int red_mb = 4;                   // FAE_RED_MB: min resident reduce CTAs per SM (4/6/8)
     int pdl_trig = 0;                 // FAE_PDL_TRIG bit0: reduce triggers after its wait, bit1: fwd too
 };

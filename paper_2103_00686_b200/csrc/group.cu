@@ -300,6 +300,292 @@ k_gs_segments(const uint32_t* __restrict__ keys, const int64_t* __restrict__ til
     }
 }
 
+// ---------------------------------------------------------------------------
+// Fixed-pooling fast path (replaces k_gs_init + the k_gs_pass passes +
+// k_gs_segments when every (batch, table) unit holds <= kUnitMax lookups).
+// Hot ids are table-ordered (tables in order, R16), so a batch's stable sort
+// by hot id is the concatenation over z of each unit's stable sort: unit
+// (b, z) = the B_b*P lookups of table z in batch b, positions lk0 +
+// (r*Tn + z)*P + p, bag id r*Tn + z.  One CTA per unit, in unit order:
+//   1. keys into shared memory; the key range (min, max) of the unit;
+//   2. stable LSD radix sort of (key - min, bag) in shared memory, 8-bit
+//      digits, only ceil(bits(range)/8) passes (ballot ranking per warp,
+//      items warp-strided in position order);
+//   3. perm[lk0 + z*n + i] = bag of the i-th smallest (coalesced);
+//   4. segments (runs of equal hot id; ids >= H make none): counted, the
+//      global segment number by a decoupled look-back over units, seg_start
+//      (= lk0 + z*n + i) / seg_row written; unit z = 0 sets desc[b].sb0.
+// Same outputs as the generic path (perm, seg_start, seg_row, sb0, totals).
+// ---------------------------------------------------------------------------
+constexpr int kUnitThreads = 256;
+constexpr int kUnitIPT = 16;
+constexpr int kUnitMax = kUnitThreads * kUnitIPT;   // 4096 lookups per unit
+constexpr int kMaxUnitTables = 1024;                 // unit path: tables per batch
+
+template <int IPT>
+__global__ void __launch_bounds__(kUnitThreads, IPT <= 8 ? 3 : 2)
+k_gs_units(const int32_t* __restrict__ hot_idx, int64_t H, int Tn, int P, const BatchDesc* __restrict__ desc,
+           int32_t* __restrict__ perm, int32_t* __restrict__ useg_pos, int32_t* __restrict__ useg_row,
+           uint32_t* __restrict__ ucnt, uint32_t* err) {
+    constexpr int NW = kUnitThreads / 32;
+    __shared__ uint32_t s_k[kUnitThreads * IPT];
+    __shared__ int32_t s_v[kUnitThreads * IPT];
+    __shared__ uint32_t s_w[NW][kSortBins];
+    __shared__ uint32_t s_tds[kSortBins];
+    __shared__ uint32_t s_ws[NW];
+    __shared__ uint32_t s_mm[2][NW];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t u = blockIdx.x;
+    const int64_t b = u / Tn;
+    const int z = (int)(u - b * Tn);
+    const BatchDesc d = desc[b];
+    const int nrec = d.n_bags / Tn;
+    const int n = nrec * P;
+    const int64_t out0 = d.lk0 + (int64_t)z * n;
+    // 1. keys (invalid ids -> 0xFFFFFFFF, sorted last, no segment)
+    const int wl = warp * 32 * IPT;
+    uint32_t k[IPT];
+    uint32_t mn = 0xFFFFFFFFu, mx = 0u;
+    bool bad = false;
+#pragma unroll
+    for (int r = 0; r < IPT; r++) {
+        const int i = wl + r * 32 + lane;
+        k[r] = 0xFFFFFFFFu;
+        if (i < n) {
+            const int rr = i / P, p = i - rr * P;
+            const int32_t hv = hot_idx[d.lk0 + ((int64_t)rr * Tn + z) * P + p];
+            if ((uint32_t)hv >= (uint64_t)H) {
+                bad = true;
+            } else {
+                k[r] = (uint32_t)hv;
+                mn = min(mn, k[r]);
+                mx = max(mx, k[r]);
+            }
+        }
+    }
+    if (bad) atomicOr(err, kErrIndex);
+    for (int o = 16; o; o >>= 1) {
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    if (lane == 0) {
+        s_mm[0][warp] = mn;
+        s_mm[1][warp] = mx;
+    }
+    __syncthreads();
+    mn = 0xFFFFFFFFu;
+    mx = 0u;
+#pragma unroll
+    for (int w = 0; w < NW; w++) {
+        mn = min(mn, s_mm[0][w]);
+        mx = max(mx, s_mm[1][w]);
+    }
+    // local keys: valid ids -> id - mn in [0, range]; invalid -> range + 1
+    const uint32_t range = mx >= mn ? mx - mn : 0u;
+    const uint32_t top = range + 1u;
+    int bits = 0;
+    while (bits < 32 && (top >> bits) != 0u) bits++;
+    const int passes = (bits + kSortBits - 1) / kSortBits;
+    int32_t v[IPT];
+#pragma unroll
+    for (int r = 0; r < IPT; r++) {
+        const int i = wl + r * 32 + lane;
+        k[r] = k[r] == 0xFFFFFFFFu ? top : k[r] - mn;
+        v[r] = i < n ? (int32_t)((i / P) * Tn + z) : 0;
+    }
+    // 2. stable LSD passes; items stay warp-strided in position order
+    for (int ps = 0; ps < passes; ps++) {
+        const int shift = ps * kSortBits;
+        for (int i = tid; i < NW * kSortBins; i += kUnitThreads) (&s_w[0][0])[i] = 0;
+        __syncthreads();
+        uint16_t rk[IPT];
+#pragma unroll
+        for (int r = 0; r < IPT; r++) {
+            const bool ok = wl + r * 32 + lane < n;
+            const uint32_t dg = ok ? ((k[r] >> shift) & (kSortBins - 1)) : (uint32_t)kSortBins;
+            const uint32_t peers = match_label<kSortBits + 1>(dg);
+            const uint32_t lt = __popc(peers & lanemask_lt());
+            uint32_t cnt = 0;
+            if (ok) cnt = s_w[warp][dg];
+            __syncwarp();
+            if (ok && lt == 0) s_w[warp][dg] = cnt + __popc(peers);
+            __syncwarp();
+            rk[r] = (uint16_t)(cnt + lt);
+        }
+        __syncthreads();
+        {   // per digit: warp prefix (in place) and digit total; then the
+            // exclusive scan of the totals over digits (kUnitThreads == bins)
+            const int dg = tid;
+            uint32_t tot = 0;
+#pragma unroll
+            for (int w = 0; w < NW; w++) {
+                const uint32_t c = s_w[w][dg];
+                s_w[w][dg] = tot;
+                tot += c;
+            }
+            uint32_t x = tot;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) s_ws[warp] = x;
+            __syncthreads();
+            uint32_t wp = 0;
+            for (int w = 0; w < warp; w++) wp += s_ws[w];
+            s_tds[dg] = wp + x - tot;
+        }
+        __syncthreads();
+        // scatter (every thread finished reading the buffer before the syncs above)
+#pragma unroll
+        for (int r = 0; r < IPT; r++) {
+            if (wl + r * 32 + lane < n) {
+                const uint32_t dg = (k[r] >> shift) & (kSortBins - 1);
+                const uint32_t pos = s_tds[dg] + s_w[warp][dg] + rk[r];
+                s_k[pos] = k[r];
+                s_v[pos] = v[r];
+            }
+        }
+        __syncthreads();
+        if (ps + 1 < passes) {   // reload in position order for the next pass
+#pragma unroll
+            for (int r = 0; r < IPT; r++) {
+                const int i = wl + r * 32 + lane;
+                if (i < n) {
+                    k[r] = s_k[i];
+                    v[r] = s_v[i];
+                }
+            }
+        }
+    }
+    if (passes == 0) {   // all keys equal: already in order
+#pragma unroll
+        for (int r = 0; r < IPT; r++) {
+            const int i = wl + r * 32 + lane;
+            if (i < n) {
+                s_k[i] = k[r];
+                s_v[i] = v[r];
+            }
+        }
+        __syncthreads();
+    }
+    // 3. perm (coalesced)
+    for (int i = tid; i < n; i += kUnitThreads) perm[out0 + i] = s_v[i];
+    // 4. segments: thread-contiguous chunks of IPT positions
+    const int j0 = tid * IPT;
+    uint32_t fl = 0, cs = 0;
+#pragma unroll
+    for (int r = 0; r < IPT; r++) {
+        const int i = j0 + r;
+        if (i < n) {
+            const uint32_t kk = s_k[i];
+            if (kk != top && (i == 0 || s_k[i - 1] != kk)) {
+                fl |= 1u << r;
+                cs++;
+            }
+        }
+    }
+    uint32_t x = cs;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    __syncthreads();
+    if (lane == 31) s_ws[warp] = x;
+    __syncthreads();
+    uint32_t wp = 0, tot = 0;
+    for (int w = 0; w < NW; w++) {
+        if (w < warp) wp += s_ws[w];
+        tot += s_ws[w];
+    }
+    // the unit's segments at its own lookup range (compacted by k_gs_ucompact)
+    if (tid == 0) ucnt[u] = tot;
+    (void)tot;
+    int64_t si = out0 + wp + x - cs;
+#pragma unroll
+    for (int r = 0; r < IPT; r++) {
+        if ((fl >> r) & 1u) {
+            useg_pos[si] = (int32_t)(z * n + j0 + r);          // position in the batch
+            useg_row[si] = (int32_t)(s_k[j0 + r] + mn);
+            si++;
+        }
+    }
+}
+
+// Batch segment bases (one CTA): sb0/sb1 of every batch = prefix over
+// batches of the sum of its Tn unit counts; totals[0] = S_total and the
+// seg_start sentinel.  Units of batch b are b*Tn .. b*Tn + Tn - 1.
+__global__ void __launch_bounds__(1024)
+k_gs_ubase(BatchDesc* __restrict__ desc, int64_t nb, int Tn, const uint32_t* __restrict__ ucnt,
+           int64_t* __restrict__ totals, int64_t* __restrict__ seg_start, int64_t L_total) {
+    __shared__ int64_t s_w[32];
+    __shared__ int64_t s_carry;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_carry = 0;
+    __syncthreads();
+    for (int64_t b0 = 0; b0 < nb; b0 += 1024) {
+        const int64_t b = b0 + tid;
+        int64_t c = 0;
+        if (b < nb)
+            for (int z = 0; z < Tn; z++) c += ucnt[b * Tn + z];
+        int64_t x = c;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_w[warp] = x;
+        __syncthreads();
+        int64_t wp = 0, tot = 0;
+        for (int w = 0; w < 32; w++) {
+            if (w < warp) wp += s_w[w];
+            tot += s_w[w];
+        }
+        const int64_t ex = s_carry + wp + x - c;
+        if (b < nb) {
+            desc[b].sb0 = ex;
+            desc[b].sb1 = ex + c;
+        }
+        __syncthreads();
+        if (tid == 0) s_carry += tot;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        totals[0] = s_carry;
+        seg_start[s_carry] = L_total;
+    }
+}
+
+// Compaction: one CTA per batch (grid-stride); unit offsets by a scan of its
+// Tn counts, then seg_start (global lookup position) / seg_row in unit order.
+__global__ void __launch_bounds__(256)
+k_gs_ucompact(const BatchDesc* __restrict__ desc, int64_t nb, int Tn, int P, const uint32_t* __restrict__ ucnt,
+              const int32_t* __restrict__ useg_pos, const int32_t* __restrict__ useg_row,
+              int64_t* __restrict__ seg_start, int32_t* __restrict__ seg_row) {
+    __shared__ uint32_t s_off[kMaxUnitTables + 1];
+    for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+        const BatchDesc d = desc[b];
+        const int n = (d.n_bags / Tn) * P;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t acc = 0;
+            for (int z = 0; z < Tn; z++) {
+                s_off[z] = acc;
+                acc += ucnt[b * Tn + z];
+            }
+            s_off[Tn] = acc;
+        }
+        __syncthreads();
+        for (int z = 0; z < Tn; z++) {
+            const uint32_t cnt = s_off[z + 1] - s_off[z];
+            const int64_t src = d.lk0 + (int64_t)z * n;
+            const int64_t dst = d.sb0 + s_off[z];
+            for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+                seg_start[dst + i] = d.lk0 + useg_pos[src + i];
+                seg_row[dst + i] = useg_row[src + i];
+            }
+        }
+    }
+}
+
 // one block per batch b (grid-stride): link each segment t of batch b to
 // the segment of batch b-1 with the same row (binary search in b-1's
 // ascending rows): nxt[σ] = t; segments without one go to batch b's free
@@ -573,6 +859,9 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
     }
     if (max_lk >= (1ll << 30)) return set_err(c, FAE_ERR_CAPACITY, "fae_group_batches: batch too large");
     const int64_t nt = (int64_t)tbatch.size();
+    const int64_t n_units = nb * (int64_t)Tn;
+    const bool unit_path = !c->gs_generic && !offs && fixed_pool > 0 && (int64_t)batch * fixed_pool <= kUnitMax &&
+                           Tn <= kMaxUnitTables && n_units < (1ll << 31);
     stage("host");
     tstart.push_back(L);
     g.max_bags = max_bags;
@@ -631,42 +920,59 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
         const int64_t gi = std::max<int64_t>(1, std::min<int64_t>(nt, (int64_t)sm_count(c) * 8));
         const int64_t gb = std::max<int64_t>(1, std::min<int64_t>(nb, (int64_t)sm_count(c) * 8));
         (void)gi;
-        k_gs_init<<<(unsigned)gb, kGSThreads, 0, c->stream>>>(g.hot_idx, g.hot_off, g.desc, nb, H, passes, g.vals,
-                                                             g.ghist);
-        FAE_LAUNCHED(c);
-        stage("init");
-        // passes: pass 0 reads the hot CSR (and, for fixed pooling, derives the
-        // bag ids); the values ping-pong so that the last pass lands in perm
-        uint32_t* kbuf[2] = {g.keys[0], g.keys[1]};
-        int32_t* vbuf[2] = {g.vals, g.perm};
-        int vo = (passes % 2 == 1) ? 1 : 0;          // value buffer written by pass 0
-        const uint32_t* kin = nullptr;
-        const int32_t* vin = offs ? g.vals : nullptr;
-        if (offs && vo == 0) {                       // keep vals as pass 0's input
-            FAE_CUDA(c, cudaMemcpyAsync(g.perm, g.vals, sizeof(int32_t) * L, cudaMemcpyDeviceToDevice, c->stream));
-            vin = g.perm;
-        }
-        int ko = 0;
-        for (int ps = 0; ps < passes; ps++) {
-            FAE_CUDA(c, cudaMemsetAsync(g.sstatus, 0, sizeof(uint32_t) * nt * kSortBins, c->stream));
-            FAE_CUDA(c, cudaMemsetAsync(ctr, 0, sizeof(uint32_t), c->stream));
-            k_gs_pass<<<(unsigned)nt, kGSThreads, 0, c->stream>>>(kin, g.hot_idx, H, vin, fixed_pool, kbuf[ko],
-                                                                  vbuf[vo], g.tile_start, g.tile_batch, g.desc,
-                                                                  g.ghist, ps, g.sstatus, ctr, c->d_err);
+        if (unit_path) {
+            // fixed pooling, every (batch, table) unit <= kUnitMax lookups:
+            // one in-shared-memory sort per unit (k_gs_units)
+            auto ku = (int64_t)batch * fixed_pool <= kUnitThreads * 8 ? k_gs_units<8> : k_gs_units<kUnitIPT>;
+            ku<<<(unsigned)n_units, kUnitThreads, 0, c->stream>>>(g.hot_idx, H, Tn, fixed_pool, g.desc, g.perm,
+                                                                  (int32_t*)g.keys[0], (int32_t*)g.keys[1],
+                                                                  (uint32_t*)g.vals, c->d_err);
             FAE_LAUNCHED(c);
-            kin = kbuf[ko];
-            vin = vbuf[vo];
-            ko ^= 1;
-            vo ^= 1;
+            k_gs_ubase<<<1, 1024, 0, c->stream>>>(g.desc, nb, Tn, (const uint32_t*)g.vals, totals, g.seg_start, L);
+            FAE_LAUNCHED(c);
+            const int64_t gc = std::max<int64_t>(1, std::min<int64_t>(nb, (int64_t)sm_count(c) * 8));
+            k_gs_ucompact<<<(unsigned)gc, 256, 0, c->stream>>>(g.desc, nb, Tn, fixed_pool, (const uint32_t*)g.vals,
+                                                               (const int32_t*)g.keys[0], (const int32_t*)g.keys[1],
+                                                               g.seg_start, g.seg_row);
+            FAE_LAUNCHED(c);
+        } else {
+            k_gs_init<<<(unsigned)gb, kGSThreads, 0, c->stream>>>(g.hot_idx, g.hot_off, g.desc, nb, H, passes, g.vals,
+                                                                 g.ghist);
+            FAE_LAUNCHED(c);
+            stage("init");
+            // passes: pass 0 reads the hot CSR (and, for fixed pooling, derives the
+            // bag ids); the values ping-pong so that the last pass lands in perm
+            uint32_t* kbuf[2] = {g.keys[0], g.keys[1]};
+            int32_t* vbuf[2] = {g.vals, g.perm};
+            int vo = (passes % 2 == 1) ? 1 : 0;          // value buffer written by pass 0
+            const uint32_t* kin = nullptr;
+            const int32_t* vin = offs ? g.vals : nullptr;
+            if (offs && vo == 0) {                       // keep vals as pass 0's input
+                FAE_CUDA(c, cudaMemcpyAsync(g.perm, g.vals, sizeof(int32_t) * L, cudaMemcpyDeviceToDevice, c->stream));
+                vin = g.perm;
+            }
+            int ko = 0;
+            for (int ps = 0; ps < passes; ps++) {
+                FAE_CUDA(c, cudaMemsetAsync(g.sstatus, 0, sizeof(uint32_t) * nt * kSortBins, c->stream));
+                FAE_CUDA(c, cudaMemsetAsync(ctr, 0, sizeof(uint32_t), c->stream));
+                k_gs_pass<<<(unsigned)nt, kGSThreads, 0, c->stream>>>(kin, g.hot_idx, H, vin, fixed_pool, kbuf[ko],
+                                                                      vbuf[vo], g.tile_start, g.tile_batch, g.desc,
+                                                                      g.ghist, ps, g.sstatus, ctr, c->d_err);
+                FAE_LAUNCHED(c);
+                kin = kbuf[ko];
+                vin = vbuf[vo];
+                ko ^= 1;
+                vo ^= 1;
+            }
+            // sorted keys in kin, bag ids in perm
+            stage("passes");
+            // sorted keys in kin, bag ids in perm
+            FAE_CUDA(c, cudaMemsetAsync(g.pstatus, 0, sizeof(uint64_t) * nt, c->stream));
+            FAE_CUDA(c, cudaMemsetAsync(ctr + 1, 0, sizeof(uint32_t), c->stream));
+            k_gs_segments<<<(unsigned)nt, kGSThreads, 0, c->stream>>>(kin ? kin : (const uint32_t*)g.hot_idx, g.tile_start, g.tile_batch, g.desc, nt, H, L,
+                                                                     g.pstatus, ctr + 1, g.seg_start, g.seg_row, totals);
+            FAE_LAUNCHED(c);
         }
-        // sorted keys in kin, bag ids in perm
-        stage("passes");
-        // sorted keys in kin, bag ids in perm
-        FAE_CUDA(c, cudaMemsetAsync(g.pstatus, 0, sizeof(uint64_t) * nt, c->stream));
-        FAE_CUDA(c, cudaMemsetAsync(ctr + 1, 0, sizeof(uint32_t), c->stream));
-        k_gs_segments<<<(unsigned)nt, kGSThreads, 0, c->stream>>>(kin ? kin : (const uint32_t*)g.hot_idx, g.tile_start, g.tile_batch, g.desc, nt, H, L,
-                                                                 g.pstatus, ctr + 1, g.seg_start, g.seg_row, totals);
-        FAE_LAUNCHED(c);
         stage("segments");
         int64_t tot = 0;
         FAE_CUDA(c, cudaMemcpyAsync(&tot, totals, sizeof(tot), cudaMemcpyDeviceToHost, c->stream));

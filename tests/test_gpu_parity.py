@@ -442,3 +442,35 @@ def test_clt_search_infeasible_gpu(dev):
     with pytest.raises(m.FaeError) as e:
         m.fae_threshold(ctx, rows, 16, counts, [100], 5.0, mode=m.CLT_SEARCH, budget_bytes=1000)
     assert e.value.name == "BUDGET_INFEASIBLE"
+
+
+@pytest.mark.parametrize("cfg,R,pool", [("kaggle", 60_000, 1), ("tb-small", 30_000, 1), ("tiny", 10_000, 3)])
+def test_grouping_unit_path_equals_generic(dev, cfg, R, pool, monkeypatch):
+    """The fixed-pooling per-(batch, table) shared-memory grouping and the
+    generic segmented radix passes give the same grouping: identical
+    segment statistics and bit-identical training results."""
+    from paper_2103_00686_b200 import fae_group_info
+    from paper_2103_00686_b200.pipeline import FaePipeline
+    c = TB_SMALL if cfg == "tb-small" else gen.CONFIGS[cfg]
+    if pool != c.pool:
+        c = gen.Config(c.name + "-p", c.rows, c.dim, c.batch, pool, records=R, t=c.t)
+    ds = gen.make_dataset(c, n_records=R, seed=6)
+    dd = ds.to(dev)
+    W = gen.make_weights(sum(ds.rows), c.dim)
+    outs = []
+    for generic in ("1", "0"):
+        monkeypatch.setenv("FAE_GS_GENERIC", generic)   # read at fae_create
+        pipe = FaePipeline(ds.rows, c.dim, c.batch, c.pool, max_pool=max(c.pool, 1))
+        prep = pipe.preprocess(dd.idx, dd.off, R, x_pct=5.0, seed=2, t=1e-6, small_table_bytes=1 << 20)
+        W_hot = pipe.extract(W.to(dev), prep).clone()
+        pipe.group(prep)
+        info = fae_group_info(pipe.ctx)
+        nb = prep.packed["n_hot_batches"]
+        S = c.batch * c.n_tables
+        dY = gen.make_dy(nb * S, c.dim, seed=9).view(nb, S, c.dim).to(dev)
+        Y = torch.zeros(S, c.dim, device=dev)
+        pipe.train(W_hot, 0, nb, dY, Y, 0.05)
+        pipe.ctx.check()
+        outs.append((info, W_hot.cpu(), Y.cpu()))
+    assert outs[0][0] == outs[1][0]
+    assert torch.equal(outs[0][1], outs[1][1]) and torch.equal(outs[0][2], outs[1][2])

@@ -70,5 +70,62 @@ def full(path, out):
     print(json.dumps(res, indent=1)[:3000])
 
 
+_SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
+def traffic(path, workload, out="profiles/ncu_traffic.json"):
+    """Merge per-kernel DRAM bytes per launch (read + write, averaged over the
+    captured launches of each kernel) of one `--set full` report into
+    profiles/ncu_traffic.json under `workload` (bench.py reads it for the
+    roofline `traffic` field)."""
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    h, u = rows[0], rows[1]
+    per = collections.defaultdict(list)
+    for r in rows[2:]:
+        k = r[h.index("Kernel Name")].split("(")[0].split("<")[0].replace("void ", "").replace("fae::", "").strip()
+        b = 0.0
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            b += float(r[h.index(m)].replace(",", "")) * _SCALE[u[h.index(m)]]
+        per[k].append(b)
+    try:
+        cur = json.load(open(out))
+    except Exception:
+        cur = {}
+    w = cur.setdefault(workload, {})
+    for k, v in per.items():
+        w[k] = {"dram_bytes_per_launch": sum(v) / len(v), "launches": len(v), "report": path.split("/")[-1]}
+    json.dump(cur, open(out, "w"), indent=1)
+    print(json.dumps(cur, indent=1))
+
+
+def traffic_launches(path, workload, out="profiles/ncu_traffic.json"):
+    """Same as `traffic`, from a launch list (`--metrics gpu__time_duration.sum,
+    dram__bytes_read.sum,dram__bytes_write.sum`: one pass per launch, no
+    kernel replay, so the caches hold what the real run left in them;
+    averaged over every captured launch of each kernel)."""
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h = rows[hi]
+    ki, vi, mi, ii, ui = (h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Name"),
+                          h.index("ID"), h.index("Metric Unit"))
+    per = collections.defaultdict(lambda: collections.defaultdict(float))
+    for r in rows[hi + 1:]:
+        if len(r) > vi and r[mi].startswith("dram__bytes"):
+            k = r[ki].split("(")[0].split("<")[0].replace("void ", "").replace("fae::", "").strip()
+            per[k][r[ii]] += float(r[vi].replace(",", "")) * _SCALE.get(r[ui], 1.0)
+    try:
+        cur = json.load(open(out))
+    except Exception:
+        cur = {}
+    w = cur.setdefault(workload, {})
+    for k, v in per.items():
+        w[k] = {"dram_bytes_per_launch": sum(v.values()) / len(v), "launches": len(v),
+                "source": path.split("/")[-1] + " (launch list, no replay)"}
+    json.dump(cur, open(out, "w"), indent=1)
+    print(json.dumps(cur, indent=1)[:1500])
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"launches": launches, "full": full, "traffic": traffic, "traffic_launches": traffic_launches}[sys.argv[1]](sys.argv[2], sys.argv[3])
