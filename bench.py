@@ -197,7 +197,7 @@ def run_fae(args):
 
     # kernel timing on from the warm-up: the captured training graph (keyed on
     # its buffers, including the timing stamps) is built outside the timed region
-    fae.fae_set_kernel_timing(pipe.ctx, 1)
+    fae.fae_set_kernel_timing(pipe.ctx, 0 if args.no_ktiming else 1)
     for _ in range(args.warmup):
         one_step()
     torch.cuda.synchronize()
@@ -209,7 +209,7 @@ def run_fae(args):
     clocks.start()
     l0 = pipe.ctx.launches
     phases.clear()
-    fae.fae_set_kernel_timing(pipe.ctx, 1)
+    fae.fae_set_kernel_timing(pipe.ctx, 0 if args.no_ktiming else 1)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     wall0 = time.perf_counter()
@@ -466,6 +466,7 @@ def main():
     ap.add_argument("--ref-records", type=int, default=1_000_000, help="--impl reference: records per step")
     ap.add_argument("--ref-batches", type=int, default=32, help="--impl reference: hot batches per step")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-ktiming", action="store_true", help="no in-kernel stamps (overhead check; no roofline)")
     ap.add_argument("--dy-pool-mb", type=int, default=256, help="upstream-gradient pool (> L2 by default)")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -607,30 +607,25 @@ k_grp_fused_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ 
         if (has_b && bid >= red_blocks) {
             // forward of batch b for rows not produced by part R: the free list
             // of b when batch a is in this kernel, else every segment of b
+            // (grid-stride over the F blocks: the grid is sized for the
+            // largest free list; the first step of a run covers all of b)
             bid -= red_blocks;
             const int lane = threadIdx.x % LPB;
-            const int64_t q = bid * G + threadIdx.x / LPB;
-            int32_t pos = -1, len = 0, row = 0;
-            if (has_a) {
-                if (q < db.n_free) {
-                    const int4 f = __ldg(reinterpret_cast<const int4*>(freer + db.sb0 + q));
-                    pos = f.x;
-                    len = f.y;
-                    row = f.z;
-                }
-            } else if (q < db.sb1 - db.sb0) {
-                const int4 r = __ldg(reinterpret_cast<const int4*>(rec + db.sb0 + q));
-                pos = r.x;
-                len = r.y;
-                row = r.z;
-            }
-            if (pos >= 0) {
+            const int64_t nF = has_a ? (int64_t)db.n_free : db.sb1 - db.sb0;
+            const int64_t fstride = ((int64_t)gridDim.x - red_blocks) * G;
+            bool waited = false;
+            for (int64_t q = bid * G + threadIdx.x / LPB; q < nF; q += fstride) {
+                const int4 f = has_a ? __ldg(reinterpret_cast<const int4*>(freer + db.sb0 + q))
+                                     : __ldg(reinterpret_cast<const int4*>(rec + db.sb0 + q));
                 int32_t bg[16];
-                prefetch_bags(perm_b, pos, len, bg);
-                pdl_wait();
+                prefetch_bags(perm_b, f.x, f.y, bg);
+                if (!waited) {
+                    pdl_wait();
+                    waited = true;
+                }
                 float4 v[NV];
-                load_row<LPB, NV>(W, row, D, lane, v);
-                write_y_pf<LPB, NV>(v, bg, perm_b, pos, len, Y, D, lane);
+                load_row<LPB, NV>(W, f.z, D, lane, v);
+                write_y_pf<LPB, NV>(v, bg, perm_b, f.x, f.y, Y, D, lane);
             }
         }
         if (stamps) {
@@ -895,7 +890,7 @@ static fae_status launch_fused_step(Ctx* c, cudaStream_t st, int s, float* W, in
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, red + cdiv(g.max_segs, G)));
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, red + std::max<int64_t>(1, cdiv(g.max_free, G))));
     const int last = (s == kUnroll - 1) ? kUnroll : 0;
     auto kern = c->red_mb >= 8 ? k_grp_fused_pdl<LPB, NV, 8>
               : (c->red_mb >= 6 ? k_grp_fused_pdl<LPB, NV, 6> : k_grp_fused_pdl<LPB, NV, 4>);

@@ -592,7 +592,9 @@ k_gs_ucompact(const BatchDesc* __restrict__ desc, int64_t nb, int Tn, int P, con
 // list (stable order) and desc[b].n_free.
 __global__ void __launch_bounds__(256)
 k_gs_links(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __restrict__ seg_start,
-           const int32_t* __restrict__ seg_row, int32_t* __restrict__ nxt, FreeRec* __restrict__ freer) {
+           const int32_t* __restrict__ seg_row, int32_t* __restrict__ nxt, FreeRec* __restrict__ freer,
+           int smem_rows) {
+    extern __shared__ int32_t s_prev[];   // batch b-1's rows when they fit (smem_rows)
     __shared__ uint32_t s_w[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int64_t b = blockIdx.x; b < n_batches; b += gridDim.x) {
@@ -604,19 +606,26 @@ k_gs_links(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __res
             ps1 = desc[b - 1].sb1;
         }
         uint32_t run = 0;
+        // the previous batch's ascending rows in shared memory: the searches
+        // then cost shared-memory latency instead of dependent L2 loads
+        const bool staged = ps1 - ps0 <= (int64_t)smem_rows;
+        __syncthreads();
+        if (staged)
+            for (int64_t i = tid; i < ps1 - ps0; i += 256) s_prev[i] = seg_row[ps0 + i];
+        __syncthreads();
         for (int64_t q0 = 0; q0 < S; q0 += 256) {
             const int64_t q = q0 + tid;
             bool fr = false;
             int32_t row = 0;
             if (q < S) {
                 row = seg_row[d.sb0 + q];
-                int64_t lo = ps0, hi = ps1;   // first position with seg_row >= row
+                int64_t lo = 0, hi = ps1 - ps0;   // first position with row >= row
                 while (lo < hi) {
                     const int64_t mid = (lo + hi) >> 1;
-                    if (seg_row[mid] < row) lo = mid + 1;
+                    if ((staged ? s_prev[mid] : seg_row[ps0 + mid]) < row) lo = mid + 1;
                     else hi = mid;
                 }
-                if (lo < ps1 && seg_row[lo] == row) nxt[lo] = (int32_t)q;
+                if (lo < ps1 - ps0 && (staged ? s_prev[lo] : seg_row[ps0 + lo]) == row) nxt[ps0 + lo] = (int32_t)q;
                 else fr = true;
             }
             const uint32_t bal = __ballot_sync(0xffffffffu, fr);
@@ -735,17 +744,36 @@ k_gs_records(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __r
             for (int c = 0; c < NC; c++) run[c] += tot[c];
         }
         __syncthreads();
-        if (tid == 0) {   // chunks of the long segments, in record order
-            int32_t cc = 0;
+        {   // chunks of the long segments, in record order: block scan of nc
             int32_t* lm = lmap + lmap_base(d, b);
-            for (int64_t q = (int64_t)base[3]; q < S; q++) {
-                SegRec& lr = rec[d.sb0 + q];
-                lr.c0 = cc;
-                lr.nc = (lr.len + chunk - 1) / chunk;
-                for (int32_t j = 0; j < lr.nc; j++) lm[cc + j] = (int32_t)(q - (int64_t)base[3]);
-                cc += lr.nc;
+            uint32_t carry = 0;
+            for (int64_t q0 = (int64_t)base[3]; q0 < S; q0 += 256) {
+                const int64_t q = q0 + tid;
+                uint32_t nc = 0;
+                if (q < S) nc = (uint32_t)((rec[d.sb0 + q].len + chunk - 1) / chunk);
+                uint32_t x = nc;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                __syncthreads();
+                if (lane == 31) s_w[0][warp] = x;
+                __syncthreads();
+                uint32_t wp = 0, tot = 0;
+                for (int w = 0; w < 8; w++) {
+                    if (w < warp) wp += s_w[0][w];
+                    tot += s_w[0][w];
+                }
+                if (q < S) {
+                    const uint32_t c0 = carry + wp + x - nc;
+                    SegRec& lr = rec[d.sb0 + q];
+                    lr.c0 = (int32_t)c0;
+                    lr.nc = (int32_t)nc;
+                    for (uint32_t j = 0; j < nc; j++) lm[c0 + j] = (int32_t)(q - (int64_t)base[3]);
+                }
+                carry += tot;
             }
-            desc[b].n_lchunk = cc;
+            if (tid == 0) desc[b].n_lchunk = (int32_t)carry;
         }
         __syncthreads();
     }
@@ -991,7 +1019,16 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
         FAE_CUDA(c, cudaMemcpyAsync(g.desc, g.hdesc.data(), sizeof(BatchDesc) * nb, cudaMemcpyHostToDevice, c->stream));
         const int64_t gr = std::max<int64_t>(1, std::min<int64_t>(nb, (int64_t)sm_count(c) * 8));
         FAE_CUDA(c, cudaMemsetAsync(g.nxt, 0xFF, sizeof(int32_t) * std::max<int64_t>(g.S_total, 1), c->stream));
-        k_gs_links<<<(unsigned)gr, 256, 0, c->stream>>>(g.desc, nb, g.seg_start, g.seg_row, g.nxt, g.freer);
+        {
+            int64_t ms = 0;
+            for (const BatchDesc& d : g.hdesc) ms = std::max<int64_t>(ms, d.sb1 - d.sb0);
+            const int smem_rows = (int)std::min<int64_t>(ms, 40 * 1024);   // <= 160 KB
+            const size_t lsm = sizeof(int32_t) * std::max(smem_rows, 1);
+            if (lsm > 48 * 1024)
+                FAE_CUDA(c, cudaFuncSetAttribute(k_gs_links, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+            k_gs_links<<<(unsigned)gr, 256, lsm, c->stream>>>(g.desc, nb, g.seg_start, g.seg_row, g.nxt, g.freer,
+                                                               smem_rows);
+        }
         FAE_LAUNCHED(c);
         g.chunk = chunk_for_dim(tabs->dim);
         k_gs_records<<<(unsigned)gr, 256, 0, c->stream>>>(g.desc, nb, g.seg_start, g.seg_row, g.nxt, g.rec, g.chunk,
