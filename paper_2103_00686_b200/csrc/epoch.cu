@@ -821,7 +821,8 @@ static void launch_grp_step(Ctx* c, cudaStream_t s, float* W, int64_t H, int D, 
     const int threads = 256;
     const int64_t gpb = threads / LPB;
     const int64_t maxb = (int64_t)sm_count(c) * 16;
-    const int64_t fu = g.P == 1 ? cdiv(g.max_bags, 4) : g.max_bags;
+    const int64_t fu = g.P == 1 ? cdiv(g.max_bags, 4)
+                     : (g.hot_off || g.P >= kWarpBagMinP) ? g.max_bags * (32 / LPB) : g.max_bags;
     const int64_t fb = std::max<int64_t>(1, std::min<int64_t>(cdiv(fu, gpb), maxb));
     k_grp_fwd<LPB, NV><<<(unsigned)fb, threads, 0, s>>>(g.desc, g.run, g.cursor, g.hot_idx, g.hot_off, g.P,
                                                        W, H, D, Y, c->d_err);
@@ -851,7 +852,8 @@ static fae_status launch_pdl_step(Ctx* c, cudaStream_t st, int s, float* W, int6
     cfg.numAttrs = 1;
     static const int64_t fcap = getenv("FAE_FWD_GRID") ? atoll(getenv("FAE_FWD_GRID")) : 0;
     const int64_t half = fcap > 0 ? fcap : (int64_t)sm_count(c) * 4;   // each kernel gets about half of the GPU
-    const int64_t fu = g.P == 1 ? cdiv(g.max_bags, 4) : g.max_bags;
+    const int64_t fu = g.P == 1 ? cdiv(g.max_bags, 4)
+                     : (g.hot_off || g.P >= kWarpBagMinP) ? g.max_bags * (32 / LPB) : g.max_bags;
     cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(fu, gpb), half)));
     FAE_CUDA(c, cudaLaunchKernelEx(&cfg, k_grp_fwd_pdl<LPB, NV>, (const BatchDesc*)g.desc, (const int64_t*)g.run,
                                    (const int64_t*)g.cursor, s, g.hot_idx, g.hot_off, (int)g.P, (const float*)W, H, D,

@@ -35,7 +35,7 @@ __device__ __forceinline__ uint64_t gtimer() {
 // kPDL: the indices of the first chunk are loaded before griddepcontrol.wait
 // (they are static), the rows of W after it (written by the previous kernel).
 template <int LPB, int NV, bool kPDL = false>
-__device__ __forceinline__ void fwd_bags(const float* __restrict__ W, int64_t H, int D,
+__device__ __forceinline__ void fwd_bags_group(const float* __restrict__ W, int64_t H, int D,
                                          const int32_t* __restrict__ idx,
                                          const int64_t* __restrict__ off, int P, int64_t n_bags,
                                          float* __restrict__ Y, uint32_t* err) {
@@ -92,6 +92,101 @@ __device__ __forceinline__ void fwd_bags(const float* __restrict__ W, int64_t H,
 #pragma unroll
         for (int k = 0; k < NV; k++) __stcs(y + k * LPB, acc[k]);
     }
+}
+
+// a8 for multi-hot bags (explicit offsets, or fixed P >= 8): one warp per
+// bag; lane group j of the warp's GW = 32/LPB groups sums the bag's chunks of
+// 8 lookups j, j+GW, ... (8 indices, then 8 rows in flight; chunk sum
+// ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)) as above), then the group partials
+// are combined by a fixed xor tree (offsets 16 .. LPB): deterministic, the
+// same bits in every caller.
+template <int LPB, int NV, bool kPDL = false>
+__device__ __forceinline__ void fwd_bags_warp(const float* __restrict__ W, int64_t H, int D,
+                                              const int32_t* __restrict__ idx,
+                                              const int64_t* __restrict__ off, int P, int64_t n_bags,
+                                              float* __restrict__ Y, uint32_t* err) {
+    constexpr int GW = 32 / LPB;
+    const int lane = threadIdx.x % LPB;
+    const int gi = (threadIdx.x & 31) / LPB;
+    const int64_t wpb = blockDim.x / 32;
+    const int64_t stride = (int64_t)gridDim.x * wpb;
+    bool waited = !kPDL;
+    for (int64_t b = blockIdx.x * wpb + threadIdx.x / 32; b < n_bags; b += stride) {
+        int64_t lo, hi;
+        if (off) {
+            lo = off[b];
+            hi = off[b + 1];
+        } else {
+            lo = b * P;
+            hi = lo + P;
+        }
+        float4 acc[NV];
+#pragma unroll
+        for (int k = 0; k < NV; k++) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int64_t p = lo + 8 * gi; p < hi; p += 8 * GW) {
+            int32_t r[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                r[u] = p + u < hi ? __ldg(idx + p + u) : -1;
+                if (p + u < hi && (uint32_t)r[u] >= (uint64_t)H) {
+                    atomicOr(err, kErrIndex);
+                    r[u] = -1;
+                }
+            }
+            if (!waited) {
+                pdl_wait();
+                waited = true;
+            }
+            float4 v[8][NV];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const float4* row = reinterpret_cast<const float4*>(W + (int64_t)(r[u] < 0 ? 0 : r[u]) * D) + lane;
+#pragma unroll
+                for (int k = 0; k < NV; k++)
+                    v[u][k] = r[u] < 0 ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldg(row + k * LPB);
+            }
+#pragma unroll
+            for (int k = 0; k < NV; k++) {
+#pragma unroll
+                for (int h = 0; h < 8; h += 4) {
+                    acc[k].x += (v[h][k].x + v[h + 1][k].x) + (v[h + 2][k].x + v[h + 3][k].x);
+                    acc[k].y += (v[h][k].y + v[h + 1][k].y) + (v[h + 2][k].y + v[h + 3][k].y);
+                    acc[k].z += (v[h][k].z + v[h + 1][k].z) + (v[h + 2][k].z + v[h + 3][k].z);
+                    acc[k].w += (v[h][k].w + v[h + 1][k].w) + (v[h + 2][k].w + v[h + 3][k].w);
+                }
+            }
+        }
+        if (!waited) {   // a warp whose bags are all empty still orders after W
+            pdl_wait();
+            waited = true;
+        }
+#pragma unroll
+        for (int o = 16; o >= LPB; o >>= 1)
+#pragma unroll
+            for (int k = 0; k < NV; k++) {
+                acc[k].x += __shfl_xor_sync(0xffffffffu, acc[k].x, o);
+                acc[k].y += __shfl_xor_sync(0xffffffffu, acc[k].y, o);
+                acc[k].z += __shfl_xor_sync(0xffffffffu, acc[k].z, o);
+                acc[k].w += __shfl_xor_sync(0xffffffffu, acc[k].w, o);
+            }
+        if (gi == 0) {
+            float4* y = reinterpret_cast<float4*>(Y + b * D) + lane;
+#pragma unroll
+            for (int k = 0; k < NV; k++) __stcs(y + k * LPB, acc[k]);
+        }
+    }
+}
+
+// pooled forward: warp per bag for multi-hot bags (offsets or P >= 8), lane
+// group per bag otherwise
+constexpr int kWarpBagMinP = 8;
+template <int LPB, int NV, bool kPDL = false>
+__device__ __forceinline__ void fwd_bags(const float* __restrict__ W, int64_t H, int D,
+                                         const int32_t* __restrict__ idx,
+                                         const int64_t* __restrict__ off, int P, int64_t n_bags,
+                                         float* __restrict__ Y, uint32_t* err) {
+    if (off || P >= kWarpBagMinP) fwd_bags_warp<LPB, NV, kPDL>(W, H, D, idx, off, P, n_bags, Y, err);
+    else fwd_bags_group<LPB, NV, kPDL>(W, H, D, idx, off, P, n_bags, Y, err);
 }
 
 // a8 for single-lookup bags (fixed pooling P = 1): Y[b] = W[idx[b]] — a row

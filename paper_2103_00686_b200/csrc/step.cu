@@ -376,7 +376,8 @@ template <int LPB, int NV>
 static void launch_fwd(Ctx* c, const float* W, int64_t H, int D, const int32_t* idx,
                        const int64_t* off, int P, int64_t n_bags, float* Y) {
     const int threads = 256;
-    const int64_t gpb = threads / LPB;
+    // bags per block: one per lane group, or one per warp for multi-hot bags
+    const int64_t gpb = (off || P >= kWarpBagMinP) ? threads / 32 : threads / LPB;
     int64_t blocks = cdiv(n_bags, gpb);
     const int64_t maxb = (int64_t)sm_count(c) * 16;
     if (blocks > maxb) blocks = maxb;
