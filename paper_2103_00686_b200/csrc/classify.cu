@@ -59,16 +59,30 @@ k_classify_fixed(const int32_t* __restrict__ idx, int64_t n_rec, int Tn, int P, 
     const int TnP = Tn * P;
     const int nitems = nrec * TnP;
     const int32_t* src = idx + r0 * (int64_t)TnP;
-    // 8 lookups per thread in flight: all index loads, then all rank-directory
-    // loads (L2-resident), then the tests
+    // 8 lookups per thread in flight: index loads, then the rank-directory
+    // loads (L2-resident), then the tests; the next round's index loads are
+    // issued before this round's directory loads (one dependent trip per round)
+    int32_t jn[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) {
+        const int q = u * kClsFix + tid;
+        jn[u] = q < nitems ? __ldg(src + q) : 0;
+    }
     for (int q0 = 0; q0 < nitems; q0 += kClsFix * 8) {
         int32_t jv[8];
         int zv[8];
 #pragma unroll
         for (int u = 0; u < 8; u++) {
             const int q = q0 + u * kClsFix + tid;
-            jv[u] = q < nitems ? __ldg(src + q) : 0;
+            jv[u] = jn[u];
             zv[u] = q < nitems ? (q % TnP) / P : -1;
+        }
+        if (q0 + kClsFix * 8 < nitems) {
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const int q = q0 + kClsFix * 8 + u * kClsFix + tid;
+                jn[u] = q < nitems ? __ldg(src + q) : 0;
+            }
         }
         uint4 e[8];
         int64_t gv[8];
