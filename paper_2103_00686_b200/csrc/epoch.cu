@@ -791,6 +791,15 @@ k_grp_reduce_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__
     }
 }
 
+__global__ void k_set_run(int64_t* cursor, int64_t first, int64_t n) {
+    if (threadIdx.x == 0) {
+        cursor[0] = 0;
+        cursor[1] = 0;
+        cursor[2] = first;
+        cursor[3] = n;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // host
 // ---------------------------------------------------------------------------
@@ -1038,8 +1047,10 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
     if (((uintptr_t)W_hot | (uintptr_t)dY | (uintptr_t)Y) & 15)
         return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_hot_batches: buffers must be 16-byte aligned");
     if (n == 0) return FAE_OK;
-    const int64_t hrun[4] = {0, 0, first, n};   // cursor, pad, run[0], run[1]
-    FAE_CUDA(c, cudaMemcpyAsync(g.cursor, hrun, sizeof(hrun), cudaMemcpyHostToDevice, c->stream));
+    // cursor, pad, run[0], run[1] — set by a kernel, not a host copy, so the
+    // loop never queues behind a bulk host->device transfer on the copy engine
+    k_set_run<<<1, 32, 0, c->stream>>>(g.cursor, first, n);
+    FAE_LAUNCHED(c);
     if (c->world > 1) {
         // a11 each step: emit the local sparse gradient, exchange, merge, apply
         // ranks may hold different numbers of hot batches: a rank past its
