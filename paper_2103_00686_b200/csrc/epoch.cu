@@ -992,7 +992,7 @@ void group_free(Ctx* c) {
     for (int v = 0; v < 2; v++)
         for (int e = 0; e < 3 * kUnroll; e++)
             if (g.tev[v][e]) cudaEventDestroy(g.tev[v][e]);
-    void* ptrs[] = {g.desc, g.perm, g.rec, g.freer, g.nxt, g.lpart, g.lcnt, g.lmap, g.keys[0], g.keys[1], g.vals, g.seg_start,
+    void* ptrs[] = {g.desc, g.perm, g.rec, g.freer, g.nxt, g.lpart, g.lcnt, g.lmap, g.xcnt, g.keys[0], g.keys[1], g.vals, g.seg_start,
                     g.seg_row, g.tile_start, g.tile_batch, g.sstatus, g.pstatus, g.ghist, g.cursor, g.done_ctr, g.pbar,
                     g.stamps};
     for (void* p : ptrs) cudaFree(p);
@@ -1051,10 +1051,43 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
     // loop never queues behind a bulk host->device transfer on the copy engine
     k_set_run<<<1, 32, 0, c->stream>>>(g.cursor, first, n);
     FAE_LAUNCHED(c);
-    if (c->world > 1) {
-        // a11 each step: emit the local sparse gradient, exchange, merge, apply
-        // ranks may hold different numbers of hot batches: a rank past its
-        // last batch contributes an empty gradient to every remaining exchange
+    if (c->world > 1 || c->force_merge) {
+        // a11 each step: emit the local sparse gradient, exchange, merge, apply.
+        // Ranks may hold different numbers of hot batches: a rank past its
+        // last batch contributes an empty gradient to every remaining
+        // exchange.  Every step's per-rank gradient size is known after the
+        // grouping, so all of them are exchanged once here (one all-gather,
+        // one host read) and the loop itself never synchronises the host.
+        if (!c->comm) return set_err(c, FAE_ERR_NOT_INIT, "fae_train_hot_batches: world > 1 without a communicator");
+        const int world = c->world;
+        if (g.cap_xcnt < 2 * n * world) {
+            cudaFree(g.xcnt);
+            g.xcnt = nullptr;
+            g.cap_xcnt = 2 * n * world + 1024;
+            FAE_CUDA(c, cudaMalloc(&g.xcnt, sizeof(int32_t) * g.cap_xcnt));
+        }
+        std::vector<int32_t> mine(n, 0);
+        for (int64_t i = 0; i < n; i++)
+            if (first + i < g.n_batches) mine[i] = (int32_t)(g.hdesc[first + i].sb1 - g.hdesc[first + i].sb0);
+        int32_t* all = g.xcnt;                 // [world][n]
+        int32_t* per_step = g.xcnt + n * world;  // [n][world]
+        FAE_CUDA(c, cudaMemcpyAsync(all + (int64_t)c->rank * n, mine.data(), sizeof(int32_t) * n,
+                                    cudaMemcpyHostToDevice, c->stream));
+        ncclResult_t r = ncclAllGather(all + (int64_t)c->rank * n, all, n, ncclInt32, c->comm, c->stream);
+        if (r != ncclSuccess) return set_err(c, FAE_ERR_NCCL, std::string("ncclAllGather counts: ") + ncclGetErrorString(r));
+        std::vector<int32_t> hall((size_t)n * world), ht((size_t)n * world);
+        FAE_CUDA(c, cudaMemcpyAsync(hall.data(), all, sizeof(int32_t) * n * world, cudaMemcpyDeviceToHost, c->stream));
+        FAE_CUDA(c, cudaStreamSynchronize(c->stream));
+        std::vector<int64_t> cap(n, 0);
+        for (int64_t i = 0; i < n; i++)
+            for (int rk = 0; rk < world; rk++) {
+                const int32_t v = hall[(size_t)rk * n + i];
+                ht[(size_t)i * world + rk] = v;
+                cap[i] = std::max<int64_t>(cap[i], v);
+            }
+        FAE_CUDA(c, cudaMemcpyAsync(per_step, ht.data(), sizeof(int32_t) * n * world, cudaMemcpyHostToDevice,
+                                    c->stream));
+        FAE_CUDA(c, cudaStreamSynchronize(c->stream));   // ht is pageable and goes out of scope
         for (int64_t i = 0; i < n; i++) {
             int64_t U = 0;
             const int32_t* rows = g.seg_row;
@@ -1067,7 +1100,8 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
                 rows = g.seg_row + d.sb0;
                 U = d.sb1 - d.sb0;
             }
-            fae_status st = sync_merge_apply(c, rows, c->ws.grad, U, D, W_hot, H, lr, nullptr, nullptr, nullptr, 0);
+            fae_status st = sync_merge_apply(c, rows, c->ws.grad, U, D, W_hot, H, lr, nullptr, nullptr, nullptr, 0,
+                                             per_step + i * world, cap[i]);
             if (st != FAE_OK) return st;
         }
         return FAE_OK;

@@ -181,6 +181,8 @@ struct Group {
     int64_t* run = nullptr;
     uint32_t* done_ctr = nullptr;
     int32_t* lmap = nullptr;          // long chunk -> long record index (lmap_base per batch)
+    int32_t* xcnt = nullptr;          // world > 1: every step's per-rank gradient sizes
+    int64_t cap_xcnt = 0;
     int64_t cap_lmap = 0;
     uint32_t* pbar = nullptr;         // persistent kernel: [0] arrivals, [1] abort, [2 + 32 c] CTA c's flag
 
@@ -231,6 +233,7 @@ struct Ctx {
     int64_t t_persist_batches = 0;    // batches trained by the timed persistent launches
     bool persist = false;             // FAE_PERSIST=1: the persistent grid-barrier kernel
     int persist_mb = 0;               // FAE_PERSIST_MB: CTAs per SM (0 = occupancy limit)
+    bool force_merge = false;         // FAE_FORCE_MERGE=1: the multi-rank exchange loop even at world 1 (tests)
     bool gs_generic = false;          // FAE_GS_GENERIC=1: radix-pass grouping even where the unit path applies
     int red_mb = 4;                   // FAE_RED_MB: min resident reduce CTAs per SM (4/6/8)
     int pdl_trig = 0;                 // FAE_PDL_TRIG bit0: reduce triggers after its wait, bit1: fwd too
@@ -268,7 +271,8 @@ fae_status bwd_group_and_reduce(Ctx* c, float* W_hot, int64_t H, int32_t D,
                                 bool emit);
 fae_status sync_merge_apply(Ctx* c, const int32_t* rows, const float* vals, int64_t U, int32_t D,
                             float* W, int64_t H, float lr, int32_t* out_rows, float* out_vals,
-                            int64_t* out_count, int64_t out_cap);
+                            int64_t* out_count, int64_t out_cap, const int32_t* known_counts = nullptr,
+                            int64_t known_cap = 0);
 fae_status step_ws_alloc(Ctx* c);
 // persistent epoch kernel (persist.cu): batches [first, first + n) of the
 // grouping, world 1, single-lookup bags; ev (optional) brackets the launch

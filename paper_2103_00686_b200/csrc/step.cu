@@ -525,22 +525,34 @@ namespace fae {
 
 // Gather every rank's sorted (row, G) list, merge in rank order and either
 // apply SGD to W (W != nullptr) or write the merged list to out_rows/out_vals.
+// known_counts (optional, device [world]) + known_cap: the per-rank counts of
+// this exchange are already on the device and their maximum on the host (the
+// training loop exchanges every step's counts once up front), so there is no
+// count all-gather and no host synchronisation here when W != nullptr.
 fae_status sync_merge_apply(Ctx* c, const int32_t* rows, const float* vals, int64_t U, int32_t D,
                             float* W, int64_t H, float lr, int32_t* out_rows, float* out_vals,
-                            int64_t* out_count, int64_t out_cap) {
+                            int64_t* out_count, int64_t out_cap, const int32_t* known_counts,
+                            int64_t known_cap) {
     if (!c->comm) return set_err(c, FAE_ERR_NOT_INIT, "sync: no communicator");
     const int world = c->world;
     if (U > c->g_cap) return set_err(c, FAE_ERR_CAPACITY, "sync: local U exceeds capacity");
-    // 1. counts
-    int32_t Ui = (int32_t)U;
-    FAE_CUDA(c, cudaMemcpyAsync(c->g_counts + c->rank, &Ui, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
-    ncclResult_t r = ncclAllGather(c->g_counts + c->rank, c->g_counts, 1, ncclInt32, c->comm, c->stream);
-    if (r != ncclSuccess) return set_err(c, FAE_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
-    std::vector<int32_t> counts(world);
-    FAE_CUDA(c, cudaMemcpyAsync(counts.data(), c->g_counts, sizeof(int32_t) * world, cudaMemcpyDeviceToHost, c->stream));
-    FAE_CUDA(c, cudaStreamSynchronize(c->stream));
+    ncclResult_t r;
     int64_t cap = 0;
-    for (int i = 0; i < world; i++) cap = std::max<int64_t>(cap, counts[i]);
+    const int32_t* dcounts = known_counts;
+    if (!known_counts) {
+        // 1. counts
+        int32_t Ui = (int32_t)U;
+        FAE_CUDA(c, cudaMemcpyAsync(c->g_counts + c->rank, &Ui, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+        r = ncclAllGather(c->g_counts + c->rank, c->g_counts, 1, ncclInt32, c->comm, c->stream);
+        if (r != ncclSuccess) return set_err(c, FAE_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+        std::vector<int32_t> counts(world);
+        FAE_CUDA(c, cudaMemcpyAsync(counts.data(), c->g_counts, sizeof(int32_t) * world, cudaMemcpyDeviceToHost, c->stream));
+        FAE_CUDA(c, cudaStreamSynchronize(c->stream));
+        for (int i = 0; i < world; i++) cap = std::max<int64_t>(cap, counts[i]);
+        dcounts = c->g_counts;
+    } else {
+        cap = known_cap;
+    }
     if (cap == 0) {
         if (out_count) *out_count = 0;
         return FAE_OK;
@@ -570,7 +582,7 @@ fae_status sync_merge_apply(Ctx* c, const int32_t* rows, const float* vals, int6
     }
     const int passes = (key_bits(Hk) + kSortBits - 1) / kSortBits;
     int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), (int64_t)sm_count(c) * 8));
-    k_merge_prep<<<(unsigned)blocks, 256, 0, c->stream>>>(c->g_rows, c->g_counts, world, cap, Hk, passes,
+    k_merge_prep<<<(unsigned)blocks, 256, 0, c->stream>>>(c->g_rows, dcounts, world, cap, Hk, passes,
                                                           c->ws.keys[0], c->ws.vals[0], c->ws.ghist,
                                                           c->ws.scalars);
     FAE_LAUNCHED(c);

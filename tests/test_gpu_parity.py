@@ -474,3 +474,35 @@ def test_grouping_unit_path_equals_generic(dev, cfg, R, pool, monkeypatch):
         outs.append((info, W_hot.cpu(), Y.cpu()))
     assert outs[0][0] == outs[1][0]
     assert torch.equal(outs[0][1], outs[1][1]) and torch.equal(outs[0][2], outs[1][2])
+
+
+@pytest.mark.parametrize("cfg", ["kaggle", "tb-small"])
+def test_train_exchange_loop_world1(dev, cfg, monkeypatch):
+    """The multi-rank training loop (per-step sparse-gradient exchange over
+    NCCL, every step's sizes exchanged once up front, rank-ordered merge)
+    run on a 1-rank communicator == the single-GPU loop, bit for bit."""
+    m = fae()
+    from paper_2103_00686_b200.pipeline import FaePipeline
+    c = TB_SMALL if cfg == "tb-small" else gen.CONFIGS[cfg]
+    R = 30_000 if cfg == "tb-small" else 100_000
+    ds = gen.make_dataset(c, n_records=R, seed=8)
+    dd = ds.to(dev)
+    W = gen.make_weights(sum(ds.rows), c.dim)
+    outs = []
+    for force in ("0", "1"):
+        monkeypatch.setenv("FAE_FORCE_MERGE", force)   # read at fae_create
+        pipe = FaePipeline(ds.rows, c.dim, c.batch, c.pool, max_pool=max(c.pool, 1))
+        if force == "1":
+            m.fae_comm_init(pipe.ctx, m.fae_get_nccl_id(), 0, 1)
+        prep = pipe.preprocess(dd.idx, dd.off, R, x_pct=5.0, seed=2, t=1e-6, small_table_bytes=1 << 20)
+        W_hot = pipe.extract(W.to(dev), prep).clone()
+        pipe.group(prep)
+        nb = min(prep.packed["n_hot_batches"], 12)
+        S = c.batch * c.n_tables
+        dY = gen.make_dy(nb * S, c.dim, seed=10).view(nb, S, c.dim).to(dev)
+        Y = torch.zeros(S, c.dim, device=dev)
+        pipe.train(W_hot, 0, nb, dY, Y, 0.05)
+        pipe.ctx.check()
+        outs.append((W_hot.cpu(), Y.cpu()))
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1])
