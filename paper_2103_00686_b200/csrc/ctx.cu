@@ -148,6 +148,8 @@ fae_status fae_create(const fae_config* cfg, fae_ctx** out) {
         // B200 a grid barrier costs more than a graph kernel boundary
         const char* pe = getenv("FAE_PERSIST");
         c->persist = pe && pe[0] == '1';
+        const char* ms = getenv("FAE_MERGE_SORT");
+        c->merge_sort = ms && ms[0] == '1';
         const char* fm = getenv("FAE_FORCE_MERGE");
         c->force_merge = fm && fm[0] == '1';
         const char* gg = getenv("FAE_GS_GENERIC");

@@ -233,6 +233,7 @@ struct Ctx {
     int64_t t_persist_batches = 0;    // batches trained by the timed persistent launches
     bool persist = false;             // FAE_PERSIST=1: the persistent grid-barrier kernel
     int persist_mb = 0;               // FAE_PERSIST_MB: CTAs per SM (0 = occupancy limit)
+    bool merge_sort = false;          // FAE_MERGE_SORT=1: sort-based merge of the exchanged gradients
     bool force_merge = false;         // FAE_FORCE_MERGE=1: the multi-rank exchange loop even at world 1 (tests)
     bool gs_generic = false;          // FAE_GS_GENERIC=1: radix-pass grouping even where the unit path applies
     int red_mb = 4;                   // FAE_RED_MB: min resident reduce CTAs per SM (4/6/8)

@@ -523,6 +523,83 @@ fae_status fae_emb_bwd_update(fae_ctx* h, float* W_hot, int64_t H, int32_t D, co
 
 namespace fae {
 
+// Rank-ordered merge of the gathered sorted lists (no re-sort): block r of
+// g_rows / g_vals holds rank r's counts[r] (row, G) entries, rows ascending
+// and unique within a rank.  The lane group of entry (r, j) owns row x iff no
+// lower rank holds x (binary search in each lower list); the owner sums
+// 0 + G_r + G_{r'} + ... over the ranks r' > r holding x, in rank order — the
+// order the sort-based merge uses (one piece of <= world terms), so the
+// result is identical on every rank and to the single-rank step — and
+// applies W[x] = fmaf(-lr, G, W[x]).
+__device__ __forceinline__ int64_t find_row(const int32_t* __restrict__ rows, int64_t n, int32_t x) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(rows + mid) < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo < n && __ldg(rows + lo) == x ? lo : -1;
+}
+
+template <int LPB, int NV>
+__global__ void __launch_bounds__(256)
+k_merge_apply(const int32_t* __restrict__ g_rows, const float* __restrict__ g_vals,
+              const int32_t* __restrict__ counts, int world, int64_t cap, int D, float* W, float lr,
+              uint32_t* err) {
+    const int lane = threadIdx.x % LPB;
+    const int64_t gpb = blockDim.x / LPB;
+    const int64_t n = cap * world;
+    for (int64_t e = blockIdx.x * gpb + threadIdx.x / LPB; e < n; e += (int64_t)gridDim.x * gpb) {
+        const int r = (int)(e / cap);
+        const int64_t j = e - (int64_t)r * cap;
+        if (j >= counts[r]) continue;
+        const int32_t x = __ldg(g_rows + e);
+        bool owner = true;
+        for (int q = 0; q < r && owner; q++)
+            if (find_row(g_rows + (int64_t)q * cap, counts[q], x) >= 0) owner = false;
+        if (!owner) continue;
+        float4 acc[NV];
+#pragma unroll
+        for (int k = 0; k < NV; k++) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = r; q < world; q++) {
+            const int64_t t = q == r ? j : find_row(g_rows + (int64_t)q * cap, counts[q], x);
+            if (t < 0) continue;
+            const float4* v = reinterpret_cast<const float4*>(g_vals + ((int64_t)q * cap + t) * D) + lane;
+#pragma unroll
+            for (int k = 0; k < NV; k++) add4(acc[k], __ldg(v + k * LPB));
+        }
+        float4* w = reinterpret_cast<float4*>(W + (int64_t)x * D) + lane;
+        bool bad = false;
+#pragma unroll
+        for (int k = 0; k < NV; k++) {
+            float4 y = w[k * LPB];
+            y.x = __fmaf_rn(-lr, acc[k].x, y.x);
+            y.y = __fmaf_rn(-lr, acc[k].y, y.y);
+            y.z = __fmaf_rn(-lr, acc[k].z, y.z);
+            y.w = __fmaf_rn(-lr, acc[k].w, y.w);
+            bad |= !(isfinite(y.x) && isfinite(y.y) && isfinite(y.z) && isfinite(y.w));
+            w[k * LPB] = y;
+        }
+        if (bad) atomicOr(err, kErrNonfinite);
+    }
+}
+
+template <int LPB, int NV>
+static fae_status launch_merge_apply(Ctx* c, const int32_t* counts, int64_t cap, int D, float* W, float lr) {
+    const int64_t gpb = 256 / LPB;
+    const int64_t n = cap * c->world;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(cdiv(n, gpb), (int64_t)sm_count(c) * 16));
+    k_merge_apply<LPB, NV><<<(unsigned)blocks, 256, 0, c->stream>>>(c->g_rows, c->g_vals, counts, c->world, cap, D,
+                                                                    W, lr, c->d_err);
+    FAE_LAUNCHED(c);
+    return FAE_OK;
+}
+
+static fae_status merge_apply(Ctx* c, const int32_t* counts, int64_t cap, int D, float* W, float lr) {
+    FAE_DISPATCH_D(D, return launch_merge_apply, c, counts, cap, D, W, lr);
+    return FAE_OK;
+}
+
 // Gather every rank's sorted (row, G) list, merge in rank order and either
 // apply SGD to W (W != nullptr) or write the merged list to out_rows/out_vals.
 // known_counts (optional, device [world]) + known_cap: the per-rank counts of
@@ -570,10 +647,20 @@ fae_status sync_merge_apply(Ctx* c, const int32_t* rows, const float* vals, int6
     ncclAllGather(my_vals, c->g_vals, cap * D, ncclFloat32, c->comm, c->stream);
     r = ncclGroupEnd();
     if (r != ncclSuccess) return set_err(c, FAE_ERR_NCCL, std::string("ncclAllGather payload: ") + ncclGetErrorString(r));
-    // 3. deterministic merge: stable sort by row over the rank-ordered
-    //    concatenation, segment sums in fixed order, then SGD or emit.
+    // 3. deterministic merge.  Applying to W: the rank-ordered merge of the
+    //    sorted lists (one kernel).  Emitting the merged list: a stable sort by
+    //    row over the rank-ordered concatenation, segment sums in fixed order.
+    fae_status st = FAE_OK;
+    if (W && !c->merge_sort) {
+        st = merge_apply(c, dcounts, cap, D, W, lr);
+        if (st != FAE_OK) return st;
+        ncclResult_t ae;
+        if (ncclCommGetAsyncError(c->comm, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress)
+            return set_err(c, FAE_ERR_NCCL, std::string("nccl async: ") + ncclGetErrorString(ae));
+        return FAE_OK;
+    }
     const int64_t n = cap * world;
-    fae_status st = zero_ws(c, n);
+    st = zero_ws(c, n);
     if (st != FAE_OK) return st;
     int64_t Hk = H;
     if (!W) {

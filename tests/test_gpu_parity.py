@@ -506,3 +506,32 @@ def test_train_exchange_loop_world1(dev, cfg, monkeypatch):
         outs.append((W_hot.cpu(), Y.cpu()))
     assert torch.equal(outs[0][0], outs[1][0])
     assert torch.equal(outs[0][1], outs[1][1])
+
+
+def test_merge_apply_equals_sort_merge(dev, monkeypatch):
+    """The rank-ordered merge kernel and the sort-based merge of the exchanged
+    gradients apply the same update to W (fae_train_hot_batches through the
+    exchange loop on a 1-rank communicator)."""
+    m = fae()
+    from paper_2103_00686_b200.pipeline import FaePipeline
+    c = gen.CONFIGS["kaggle"]
+    ds = gen.make_dataset(c, n_records=100_000, seed=12)
+    dd = ds.to(dev)
+    W = gen.make_weights(sum(ds.rows), c.dim)
+    outs = []
+    monkeypatch.setenv("FAE_FORCE_MERGE", "1")
+    for sort in ("1", "0"):
+        monkeypatch.setenv("FAE_MERGE_SORT", sort)
+        pipe = FaePipeline(ds.rows, c.dim, c.batch, c.pool)
+        m.fae_comm_init(pipe.ctx, m.fae_get_nccl_id(), 0, 1)
+        prep = pipe.preprocess(dd.idx, None, 100_000, x_pct=5.0, seed=2, t=1e-6)
+        W_hot = pipe.extract(W.to(dev), prep).clone()
+        pipe.group(prep)
+        nb = min(prep.packed["n_hot_batches"], 8)
+        S = c.batch * c.n_tables
+        dY = gen.make_dy(nb * S, c.dim, seed=11).view(nb, S, c.dim).to(dev)
+        Y = torch.zeros(S, c.dim, device=dev)
+        pipe.train(W_hot, 0, nb, dY, Y, 0.05)
+        pipe.ctx.check()
+        outs.append(W_hot.cpu())
+    assert torch.equal(outs[0], outs[1])
