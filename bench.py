@@ -136,6 +136,14 @@ def pipe_stats(pipe):
 # ----------------------------------------------------------------------------
 # CUDA arm
 # ----------------------------------------------------------------------------
+def config_of(args):
+    import dataclasses
+    cfg = gen.CONFIGS[args.config]
+    if args.batch:
+        cfg = dataclasses.replace(cfg, batch=args.batch)
+    return cfg
+
+
 def run_fae(args):
     import paper_2103_00686_b200 as fae
     from paper_2103_00686_b200.pipeline import FaePipeline
@@ -149,7 +157,7 @@ def run_fae(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    cfg = gen.CONFIGS[args.config]
+    cfg = config_of(args)
     R = args.records or cfg.records
     Tn, D, B = cfg.n_tables, cfg.dim, cfg.batch
     ds = gen.make_dataset(cfg, n_records=R, device=dev, record_base=rank * R)
@@ -505,6 +513,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="kaggle", choices=sorted(gen.CONFIGS))
     ap.add_argument("--records", type=int, default=0, help="records per GPU (default: config)")
+    ap.add_argument("--batch", type=int, default=0, help="hot mini-batch size B (default: config; batch sweeps)")
     ap.add_argument("--impl", default="fae", choices=["fae", "reference"])
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--seed", type=int, default=1)
