@@ -867,9 +867,12 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
         for (int64_t i = 0; i <= nb; i++)
             starts[i] = std::min<int64_t>(i * batch, pk->n_hot) * Tn * (int64_t)fixed_pool;
     }
-    std::vector<int64_t> tstart;
+    const int64_t n_units = nb * (int64_t)Tn;
+    const bool unit_path = !c->gs_generic && !offs && fixed_pool > 0 && (int64_t)batch * fixed_pool <= kUnitMax &&
+                           Tn <= kMaxUnitTables && n_units < (1ll << 31);
+    std::vector<int64_t> tstart;   // radix-pass tiles (generic path only)
     std::vector<int32_t> tbatch;
-    tstart.reserve(L / kGSTile + nb + 1);
+    if (!unit_path) tstart.reserve(L / kGSTile + nb + 1);
     int64_t max_bags = 0, max_lk = 0;
     for (int64_t i = 0; i < nb; i++) {
         BatchDesc& d = g.hdesc[i];
@@ -880,16 +883,14 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
         d.n_bags = (int32_t)((r1 - r0) * Tn);
         max_bags = std::max<int64_t>(max_bags, d.n_bags);
         max_lk = std::max<int64_t>(max_lk, d.lk1 - d.lk0);
-        for (int64_t s = d.lk0; s < d.lk1; s += kGSTile) {
-            tstart.push_back(s);
-            tbatch.push_back((int32_t)i | (s == d.lk0 ? (int32_t)0x80000000 : 0));
-        }
+        if (!unit_path)
+            for (int64_t s = d.lk0; s < d.lk1; s += kGSTile) {
+                tstart.push_back(s);
+                tbatch.push_back((int32_t)i | (s == d.lk0 ? (int32_t)0x80000000 : 0));
+            }
     }
     if (max_lk >= (1ll << 30)) return set_err(c, FAE_ERR_CAPACITY, "fae_group_batches: batch too large");
     const int64_t nt = (int64_t)tbatch.size();
-    const int64_t n_units = nb * (int64_t)Tn;
-    const bool unit_path = !c->gs_generic && !offs && fixed_pool > 0 && (int64_t)batch * fixed_pool <= kUnitMax &&
-                           Tn <= kMaxUnitTables && n_units < (1ll << 31);
     stage("host");
     tstart.push_back(L);
     g.max_bags = max_bags;
@@ -941,8 +942,10 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
         int64_t* totals = (int64_t*)scratch(c, 64);
         if (!totals) return set_err(c, FAE_ERR_CUDA, "fae_group_batches: scratch allocation failed");
         FAE_CUDA(c, cudaMemcpyAsync(g.desc, g.hdesc.data(), sizeof(BatchDesc) * nb, cudaMemcpyHostToDevice, c->stream));
-        FAE_CUDA(c, cudaMemcpyAsync(g.tile_start, tstart.data(), sizeof(int64_t) * (nt + 1), cudaMemcpyHostToDevice, c->stream));
-        FAE_CUDA(c, cudaMemcpyAsync(g.tile_batch, tbatch.data(), sizeof(int32_t) * nt, cudaMemcpyHostToDevice, c->stream));
+        if (!unit_path) {
+            FAE_CUDA(c, cudaMemcpyAsync(g.tile_start, tstart.data(), sizeof(int64_t) * (nt + 1), cudaMemcpyHostToDevice, c->stream));
+            FAE_CUDA(c, cudaMemcpyAsync(g.tile_batch, tbatch.data(), sizeof(int32_t) * nt, cudaMemcpyHostToDevice, c->stream));
+        }
 
         FAE_CUDA(c, cudaMemsetAsync(totals, 0, 64, c->stream));
         const int64_t gi = std::max<int64_t>(1, std::min<int64_t>(nt, (int64_t)sm_count(c) * 8));
