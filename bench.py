@@ -307,6 +307,10 @@ def run_fae(args):
             "clocks": ck,
             "wall_s": wall,
             "phases_ms_per_step": {k: v / args.steps for k, v in phases.items()},
+            # the a8-a10 training loop alone (the value above times the whole
+            # hot path a1-a10 per step)
+            "train_only_lookups_per_s": (lookups_all / (phases["train"] / 1e3)
+                                         if phases.get("train") else None),
         }
     return res, (pipe, ds, W, cfg, R, dist, rank, world, dev, dY, Y)
 
