@@ -670,6 +670,9 @@ k_gs_records(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __r
     for (int64_t b = blockIdx.x; b < n_batches; b += gridDim.x) {
         const BatchDesc d = desc[b];
         const int64_t S = d.sb1 - d.sb0;
+        const bool has_next = b + 1 < n_batches;
+        BatchDesc dn{};
+        if (has_next) dn = desc[b + 1];
         auto cls = [&](int64_t q, SegRec& r) -> int {
             const int64_t s = d.sb0 + q;
             const int64_t st = seg_start[s];
@@ -683,8 +686,7 @@ k_gs_records(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __r
             r.c0 = 0;
             r.nc = 1;
             const int32_t t = nxt[s];
-            if (t >= 0 && b + 1 < n_batches) {
-                const BatchDesc& dn = desc[b + 1];
+            if (t >= 0 && has_next) {
                 const int64_t sn = dn.sb0 + t;
                 const int64_t en = sn + 1 < dn.sb1 ? seg_start[sn + 1] : dn.lk1;
                 r.npos = (int32_t)(seg_start[sn] - dn.lk0);
@@ -692,11 +694,15 @@ k_gs_records(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __r
             }
             return r.len <= kTinySeg ? 0 : (r.len <= kPiece ? 1 : (r.len <= kMedium ? 2 : 3));
         };
-        // pass 1: class sizes
+        // pass 1: class sizes (the class depends on the length only)
         uint32_t nn[NC] = {0u, 0u, 0u, 0u};
         for (int64_t q = tid; q < S; q += 256) {
-            SegRec r;
-            nn[cls(q, r)]++;
+            const int64_t s = d.sb0 + q;
+            const int64_t len = (q + 1 < S ? seg_start[s + 1] : d.lk1) - seg_start[s];
+            nn[0] += len <= kTinySeg;
+            nn[1] += len > kTinySeg && len <= kPiece;
+            nn[2] += len > kPiece && len <= kMedium;
+            nn[3] += len > kMedium;
         }
 #pragma unroll
         for (int c = 0; c < NC; c++) {
