@@ -323,7 +323,7 @@ constexpr int kUnitMax = kUnitThreads * kUnitIPT;   // 4096 lookups per unit
 constexpr int kMaxUnitTables = 1024;                 // unit path: tables per batch
 
 template <int IPT>
-__global__ void __launch_bounds__(kUnitThreads, IPT <= 8 ? 4 : 2)
+__global__ void __launch_bounds__(kUnitThreads, IPT <= 8 ? 5 : 2)
 k_gs_units(const int32_t* __restrict__ hot_idx, int64_t H, int Tn, int P, const BatchDesc* __restrict__ desc,
            int32_t* __restrict__ perm, int32_t* __restrict__ useg_pos, int32_t* __restrict__ useg_row,
            uint32_t* __restrict__ ucnt, uint32_t* err) {
