@@ -269,6 +269,22 @@ fae_status fae_extract(fae_ctx* ctx, const float* W, int32_t dim,
                        float* W_hot);
 
 /* --------------------------------------------------------------------------
+ * fae_scatter_hot — the hot/cold swap synchronisation back to the master
+ * tables (at a swap from
+ * hot to cold mini-batches the hot rows trained on the GPU are written back
+ * to the CPU master copy, the "embedding sync"):
+ *   W[g, :] = W_hot[hot_id(g), :] for every hot global row g (bit copy);
+ *   cold rows of W are not touched.  The inverse of fae_extract.
+ *  W_hot  device [H_total][dim].
+ *  W      [sum N_z][dim] fp32: device memory, or pinned host memory mapped
+ *         into the device address space (only hot rows cross the link).
+ * Uses the hot set of the last fae_threshold.  Asynchronous on the ctx
+ * stream.  Errors: NOT_INIT without a hot set, INVALID_ARG.
+ * ------------------------------------------------------------------------ */
+fae_status fae_scatter_hot(fae_ctx* ctx, const float* W_hot, int32_t dim,
+                           float* W);
+
+/* --------------------------------------------------------------------------
  * fae_emb_fwd — hot embedding-bag forward (a8; sum
  * pooling, R12):
  *   Y[b, :] = sum_{p in bag b} W_hot[idx[p], :]           (fp32)

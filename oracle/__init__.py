@@ -74,6 +74,7 @@ def _declare(L):
     L.or_pack.restype = None
     L.or_pack.argtypes = [i32, P, P, P, i32, i64, P, P, P, P, P, P, P]
     L.or_extract.restype = None; L.or_extract.argtypes = [i64, i32, P, P, P]
+    L.or_scatter_hot.restype = None; L.or_scatter_hot.argtypes = [i64, i32, P, P, P]
     L.or_emb_fwd.restype = ctypes.c_int
     L.or_emb_fwd.argtypes = [P, i64, i32, P, P, i32, i64, P]
     L.or_emb_bwd_sgd.restype = ctypes.c_int
@@ -236,6 +237,14 @@ def extract(W, remap_, H):
     out = np.zeros((max(H, 1), dim), np.float32)
     lib().or_extract(W.shape[0], dim, _ptr(W), _ptr(remap_), _ptr(out))
     return out[:H]
+
+
+def scatter_hot(W, W_hot, remap_):
+    """NEXT-1 swap sync: a copy of W with W[g] = W_hot[remap[g]] for hot g."""
+    W = _np(W, np.float32).copy(); W_hot = _np(W_hot, np.float32)
+    remap_ = _np(remap_, np.int32)
+    lib().or_scatter_hot(W.shape[0], W.shape[1], _ptr(W_hot), _ptr(remap_), _ptr(W))
+    return W
 
 
 def emb_fwd(W_hot, idx, off, fixed_pool, n_bags):

@@ -544,6 +544,20 @@ void or_extract(int64_t total_rows, int32_t dim, const float* W,
 }
 
 /* ---------------------------------------------------------------------------
+ * Swap sync back to the master tables (P:L299-302,
+ * L540: at a hot -> cold swap the hot rows trained on the GPU are written to
+ * the CPU master copy): W[g] = W_hot[remap[g]] for every hot row g; cold rows
+ * are not touched.  The inverse of or_extract.
+ * ------------------------------------------------------------------------- */
+void or_scatter_hot(int64_t total_rows, int32_t dim, const float* W_hot,
+                    const int32_t* remap, float* W)
+{
+    for (int64_t g = 0; g < total_rows; g++)
+        if (remap[g] >= 0)
+            memcpy(W + g * dim, W_hot + (int64_t)remap[g] * dim, sizeof(float) * (size_t)dim);
+}
+
+/* ---------------------------------------------------------------------------
  * O8  Hot embedding-bag forward ("embedding bags"; sum
  * pooling, R12):  Y[b,:] = sum_{p in bag b} W_hot[idx[p], :], accumulated in
  * fp64 in bag order and rounded once.  Bag b = lookups [off[b], off[b+1])

@@ -29,7 +29,7 @@ FIXED_T, BUDGET_EXACT, CLT_SEARCH = 0, 1, 2
 EXPORTS = ["fae_create", "fae_destroy", "fae_set_stream", "fae_last_error",
            "fae_check", "fae_get_nccl_id", "fae_comm_init",
            "fae_kernel_launches", "fae_profile", "fae_threshold",
-           "fae_classify", "fae_extract", "fae_emb_fwd", "fae_emb_bwd_update",
+           "fae_classify", "fae_extract", "fae_scatter_hot", "fae_emb_fwd", "fae_emb_bwd_update",
            "fae_sync_hot_grads", "fae_group_batches", "fae_train_hot_batches",
            "fae_set_kernel_timing", "fae_get_kernel_timing", "fae_group_info"]
 
@@ -110,6 +110,7 @@ def lib():
             "fae_classify": ([P, ctypes.POINTER(FaeTables), ctypes.POINTER(FaeCsr),
                               c_i32, c_u64, ctypes.POINTER(FaePacked)], c_i32),
             "fae_extract": ([P, P, c_i32, P], c_i32),
+            "fae_scatter_hot": ([P, P, c_i32, P], c_i32),
             "fae_emb_fwd": ([P, P, c_i64, c_i32, P, P, c_i32, c_i64, P], c_i32),
             "fae_emb_bwd_update": ([P, P, c_i64, c_i32, P, P, c_i32, c_i64, P,
                                     ctypes.c_float], c_i32),
@@ -285,6 +286,13 @@ def fae_extract(ctx: Ctx, W: torch.Tensor, W_hot: torch.Tensor):
     """a7: W may be a CUDA tensor or a pinned CPU tensor (mapped)."""
     assert W.dtype == torch.float32 and W.is_contiguous()
     ctx._ok(lib().fae_extract(ctx.h, _p(W), int(W.shape[1]), _p(W_hot)))
+
+
+def fae_scatter_hot(ctx: Ctx, W_hot: torch.Tensor, W: torch.Tensor):
+    """NEXT-1 swap sync: W[g] = W_hot[hot_id(g)] for hot rows (inverse of
+    fae_extract); W may be a CUDA tensor or a pinned CPU tensor (mapped)."""
+    assert W.dtype == torch.float32 and W.is_contiguous()
+    ctx._ok(lib().fae_scatter_hot(ctx.h, _p(W_hot), int(W.shape[1]), _p(W)))
 
 
 def fae_emb_fwd(ctx: Ctx, W_hot: torch.Tensor, idx: torch.Tensor,

@@ -263,10 +263,11 @@ k_classify_general(const int32_t* __restrict__ idx, const int64_t* __restrict__ 
 }
 
 // extract: warp per 64-row word; lane l owns bits l (lo) and l (hi)
-template <int NV4>
+// kBack = false: W_hot[hot_id(g)] = W[g] (a7, extract); kBack = true:
+// W[g] = W_hot[hot_id(g)] (the swap sync back to the master tables).
+template <int NV4, bool kBack = false>
 __global__ void __launch_bounds__(256)
-k_extract(const uint4* __restrict__ dir, int64_t total, const float* __restrict__ W, int D,
-          float* __restrict__ W_hot) {
+k_extract(const uint4* __restrict__ dir, int64_t total, const float* W, int D, float* W_hot) {
     const int lane = threadIdx.x & 31;
     const int64_t wpb = blockDim.x >> 5;
     const int64_t words = (total + 63) >> 6;
@@ -278,28 +279,33 @@ k_extract(const uint4* __restrict__ dir, int64_t total, const float* __restrict_
         if ((lo >> lane) & 1u) {
             const int64_t g = w * 64 + lane;
             const int64_t hid = (int64_t)e.z + __popc(lo & lt);
-            const float4* s = reinterpret_cast<const float4*>(W + g * D);
+            float4* s = reinterpret_cast<float4*>(const_cast<float*>(W) + g * D);
             float4* d = reinterpret_cast<float4*>(W_hot + hid * D);
-            for (int k = 0; k < nd4; k++) d[k] = s[k];
+            if (kBack) for (int k = 0; k < nd4; k++) s[k] = d[k];
+            else for (int k = 0; k < nd4; k++) d[k] = s[k];
         }
         if ((hi >> lane) & 1u) {
             const int64_t g = w * 64 + 32 + lane;
             const int64_t hid = (int64_t)e.z + __popc(lo) + __popc(hi & lt);
-            const float4* s = reinterpret_cast<const float4*>(W + g * D);
+            float4* s = reinterpret_cast<float4*>(const_cast<float*>(W) + g * D);
             float4* d = reinterpret_cast<float4*>(W_hot + hid * D);
-            for (int k = 0; k < nd4; k++) d[k] = s[k];
+            if (kBack) for (int k = 0; k < nd4; k++) s[k] = d[k];
+            else for (int k = 0; k < nd4; k++) d[k] = s[k];
         }
     }
 }
 
+template <bool kBack = false>
 __global__ void __launch_bounds__(256)
-k_extract_scalar(const uint4* __restrict__ dir, int64_t total, const float* __restrict__ W, int D,
-                 float* __restrict__ W_hot) {
+k_extract_scalar(const uint4* __restrict__ dir, int64_t total, const float* W, int D, float* W_hot) {
     for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
          g += (int64_t)gridDim.x * blockDim.x) {
         uint32_t rk;
         if (hs_test(dir[g >> 6], g, &rk))
-            for (int d = 0; d < D; d++) W_hot[(int64_t)rk * D + d] = W[g * D + d];
+            for (int d = 0; d < D; d++) {
+                if (kBack) const_cast<float*>(W)[g * D + d] = W_hot[(int64_t)rk * D + d];
+                else W_hot[(int64_t)rk * D + d] = W[g * D + d];
+            }
     }
 }
 
@@ -399,7 +405,28 @@ extern "C" fae_status fae_extract(fae_ctx* h, const float* W, int32_t dim, float
         k_extract<1><<<(unsigned)g, 256, 0, c->stream>>>(hs.dir, total, W, dim, W_hot);
     } else {
         const int64_t g = std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), (int64_t)sms(c) * 8));
-        k_extract_scalar<<<(unsigned)g, 256, 0, c->stream>>>(hs.dir, total, W, dim, W_hot);
+        k_extract_scalar<false><<<(unsigned)g, 256, 0, c->stream>>>(hs.dir, total, W, dim, W_hot);
+    }
+    FAE_LAUNCHED(c);
+    return FAE_OK;
+}
+
+extern "C" fae_status fae_scatter_hot(fae_ctx* h, const float* W_hot, int32_t dim, float* W) {
+    if (!h) return FAE_ERR_NOT_INIT;
+    Ctx* c = &h->c;
+    HotSet& hs = c->hs;
+    if (!hs.valid) return set_err(c, FAE_ERR_NOT_INIT, "fae_scatter_hot: no hot set");
+    if (!W || (!W_hot && hs.H_total > 0) || dim < 1) return set_err(c, FAE_ERR_INVALID_ARG, "fae_scatter_hot: bad arguments");
+    if (hs.H_total == 0) return FAE_OK;
+    const int64_t total = hs.total_rows;
+    const bool vec = dim % 4 == 0 && (((uintptr_t)W | (uintptr_t)W_hot) & 15) == 0;
+    if (vec) {
+        const int64_t words = cdiv(total, 64);
+        const int64_t g = std::max<int64_t>(1, std::min<int64_t>(cdiv(words, 8), (int64_t)sms(c) * 16));
+        k_extract<1, true><<<(unsigned)g, 256, 0, c->stream>>>(hs.dir, total, W, dim, const_cast<float*>(W_hot));
+    } else {
+        const int64_t g = std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), (int64_t)sms(c) * 8));
+        k_extract_scalar<true><<<(unsigned)g, 256, 0, c->stream>>>(hs.dir, total, W, dim, const_cast<float*>(W_hot));
     }
     FAE_LAUNCHED(c);
     return FAE_OK;

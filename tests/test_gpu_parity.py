@@ -535,3 +535,36 @@ def test_merge_apply_equals_sort_merge(dev, monkeypatch):
         pipe.ctx.check()
         outs.append(W_hot.cpu())
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("host", [False, True])
+def test_scatter_hot_swap_sync(dev, host):
+    """NEXT-1 swap sync: after training the hot table on
+    the GPU, fae_scatter_hot writes its rows back into the master tables
+    (device or pinned host memory) == oracle.scatter_hot, bit for bit; cold
+    rows untouched."""
+    m = fae()
+    from paper_2103_00686_b200.pipeline import FaePipeline
+    c = gen.CONFIGS["kaggle"]
+    ds = gen.make_dataset(c, n_records=100_000, seed=14)
+    dd = ds.to(dev)
+    pipe = FaePipeline(ds.rows, c.dim, c.batch, c.pool)
+    remap = torch.empty(sum(ds.rows), dtype=torch.int32, device=dev)
+    prep = pipe.preprocess(dd.idx, None, 100_000, x_pct=5.0, seed=2, t=1e-6)
+    W = gen.make_weights(sum(ds.rows), c.dim)
+    W_hot = pipe.extract(W.to(dev), prep).clone()
+    pipe.group(prep)
+    nb = min(prep.packed["n_hot_batches"], 4)
+    S = c.batch * c.n_tables
+    dY = gen.make_dy(nb * S, c.dim, seed=15).view(nb, S, c.dim).to(dev)
+    Y = torch.zeros(S, c.dim, device=dev)
+    pipe.train(W_hot, 0, nb, dY, Y, 0.05)
+    # the remap of the ctx's hot set (same threshold call again, remap out)
+    m.fae_threshold(pipe.ctx, ds.rows, c.dim, prep.counts, prep.T, 5.0, mode=m.FIXED_T, t=1e-6,
+                    remap_out=remap)
+    Wm = W.clone().pin_memory() if host else W.to(dev)
+    m.fae_scatter_hot(pipe.ctx, W_hot, Wm)
+    torch.cuda.synchronize()
+    pipe.ctx.check()
+    ref = oracle.scatter_hot(W, W_hot.cpu(), remap.cpu())
+    assert np.array_equal(Wm.cpu().numpy(), ref)

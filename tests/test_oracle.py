@@ -634,3 +634,23 @@ def test_clt_search_budget_on_zipf_estimate():
             b = oracle.hot_bytes([n], 16, 1 << 20, k, r["kmin"])
             ok += 0.8 * L <= b <= L
         assert ok >= 9
+
+
+# ----------------------------------------------------------------------------
+# NEXT-1: swap sync back to the master tables
+# ----------------------------------------------------------------------------
+def test_scatter_hot_inverse_of_extract():
+    rng = np.random.default_rng(21)
+    rows = [300, 500, 200]
+    hot = (rng.random(sum(rows)) < 0.3).astype(np.uint8)
+    rm, base, H = oracle.remap(rows, hot)
+    W = rng.standard_normal((sum(rows), 8)).astype(np.float32)
+    # round trip: scattering the extracted table back is the identity
+    assert np.array_equal(oracle.scatter_hot(W, oracle.extract(W, rm, H), rm), W)
+    # a trained hot table: hot rows take its rows, cold rows stay bit-identical
+    W_hot = rng.standard_normal((H, 8)).astype(np.float32)
+    W2 = oracle.scatter_hot(W, W_hot, rm)
+    g_hot = np.nonzero(rm >= 0)[0]
+    assert np.array_equal(W2[g_hot], W_hot[rm[g_hot]])           # brute force
+    cold = rm < 0
+    assert np.array_equal(W2[cold], W[cold])
