@@ -285,6 +285,26 @@ fae_status fae_scatter_hot(fae_ctx* ctx, const float* W_hot, int32_t dim,
                            float* W);
 
 /* --------------------------------------------------------------------------
+ * fae_pack_cold — the cold mini-batches' CSR in GLOBAL row ids (SURVEY §8(f)
+ * NEXT-1, the cold-batch side; a cold input touches cold
+ * rows, so its embeddings train against the full tables — here the
+ * HBM-resident master tables, with the same step calls, H = sum N_z):
+ *   cold_idx[k*Tn*P + z*P + p] = base_z + idx[cold_ids[k]*Tn*P + z*P + p],
+ *   base_z = sum_{z' < z} N_z'.
+ *  data      fixed pooling only (off == NULL), device idx.
+ *  cold_ids  device int64 [n_cold] (fae_classify's cold_ids).
+ *  cold_idx  device int32 [n_cold*Tn*P], caller-owned.
+ * Cold batch i = records [i*B, min((i+1)*B, n_cold)) of cold_idx; train it
+ * with fae_emb_fwd / fae_emb_bwd_update on W (H = sum N_z) after the hot
+ * rows were written back (fae_scatter_hot), and re-extract before the next
+ * hot batch.  Errors: INVALID_ARG (offsets, null buffers), CAPACITY
+ * (sum N_z >= 2^31), INDEX_RANGE (latched).  Synchronises the stream.
+ * ------------------------------------------------------------------------ */
+fae_status fae_pack_cold(fae_ctx* ctx, const fae_tables* tabs,
+                         const fae_csr* data, const int64_t* cold_ids,
+                         int64_t n_cold, int32_t* cold_idx);
+
+/* --------------------------------------------------------------------------
  * fae_emb_fwd — hot embedding-bag forward (a8; sum
  * pooling, R12):
  *   Y[b, :] = sum_{p in bag b} W_hot[idx[p], :]           (fp32)

@@ -29,7 +29,7 @@ FIXED_T, BUDGET_EXACT, CLT_SEARCH = 0, 1, 2
 EXPORTS = ["fae_create", "fae_destroy", "fae_set_stream", "fae_last_error",
            "fae_check", "fae_get_nccl_id", "fae_comm_init",
            "fae_kernel_launches", "fae_profile", "fae_threshold",
-           "fae_classify", "fae_extract", "fae_scatter_hot", "fae_emb_fwd", "fae_emb_bwd_update",
+           "fae_classify", "fae_extract", "fae_scatter_hot", "fae_pack_cold", "fae_emb_fwd", "fae_emb_bwd_update",
            "fae_sync_hot_grads", "fae_group_batches", "fae_train_hot_batches",
            "fae_set_kernel_timing", "fae_get_kernel_timing", "fae_group_info"]
 
@@ -111,6 +111,7 @@ def lib():
                               c_i32, c_u64, ctypes.POINTER(FaePacked)], c_i32),
             "fae_extract": ([P, P, c_i32, P], c_i32),
             "fae_scatter_hot": ([P, P, c_i32, P], c_i32),
+            "fae_pack_cold": ([P, P, P, P, c_i64, P], c_i32),
             "fae_emb_fwd": ([P, P, c_i64, c_i32, P, P, c_i32, c_i64, P], c_i32),
             "fae_emb_bwd_update": ([P, P, c_i64, c_i32, P, P, c_i32, c_i64, P,
                                     ctypes.c_float], c_i32),
@@ -293,6 +294,16 @@ def fae_scatter_hot(ctx: Ctx, W_hot: torch.Tensor, W: torch.Tensor):
     fae_extract); W may be a CUDA tensor or a pinned CPU tensor (mapped)."""
     assert W.dtype == torch.float32 and W.is_contiguous()
     ctx._ok(lib().fae_scatter_hot(ctx.h, _p(W_hot), int(W.shape[1]), _p(W)))
+
+
+def fae_pack_cold(ctx: Ctx, rows, dim: int, idx: torch.Tensor, fixed_pool: int, n_records: int,
+                  cold_ids: torch.Tensor, n_cold: int, cold_idx: torch.Tensor):
+    """NEXT-1 cold side: the cold records' lookups in global row ids."""
+    tabs, keep = _tables(rows, dim)
+    csr = _csr(idx, None, fixed_pool, n_records, len(rows))
+    ctx._ok(lib().fae_pack_cold(ctx.h, ctypes.byref(tabs), ctypes.byref(csr), _p(cold_ids),
+                                int(n_cold), _p(cold_idx)))
+    del keep
 
 
 def fae_emb_fwd(ctx: Ctx, W_hot: torch.Tensor, idx: torch.Tensor,

@@ -20,6 +20,7 @@ namespace fae {
 
 fae_status validate_schema(Ctx* c, const fae_tables* t, const char* who);
 fae_status validate_csr(Ctx* c, const fae_tables* t, const fae_csr* d, const char* who);
+fae_status upload_schema(Ctx* c, const fae_tables* t, std::vector<int64_t>& rowbase);
 
 constexpr int kClsThreads = 256;
 // fixed pooling: threads per tile (measured on B200, 45M Kaggle-shaped
@@ -409,6 +410,49 @@ extern "C" fae_status fae_extract(fae_ctx* h, const float* W, int32_t dim, float
     }
     FAE_LAUNCHED(c);
     return FAE_OK;
+}
+
+// cold CSR in global row ids: out[k*TnP + q] = rowbase[z] + idx[cold[k]*TnP + q]
+__global__ void __launch_bounds__(256)
+k_pack_cold(const int32_t* __restrict__ idx, const int64_t* __restrict__ cold_ids, int64_t n_cold, int Tn, int P,
+            const int64_t* __restrict__ rowbase, const int64_t* __restrict__ rows, int32_t* __restrict__ out,
+            uint32_t* err) {
+    const int64_t TnP = (int64_t)Tn * P;
+    const int64_t n = n_cold * TnP;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = e / TnP, q = e - k * TnP;
+        const int z = (int)(q / P);
+        const int32_t j = idx[cold_ids[k] * TnP + q];
+        if (j < 0 || (int64_t)j >= rows[z]) {
+            atomicOr(err, kErrIndex);
+            out[e] = 0;
+        } else {
+            out[e] = (int32_t)(rowbase[z] + j);
+        }
+    }
+}
+
+extern "C" fae_status fae_pack_cold(fae_ctx* h, const fae_tables* tabs, const fae_csr* data,
+                                    const int64_t* cold_ids, int64_t n_cold, int32_t* cold_idx) {
+    if (!h) return FAE_ERR_NOT_INIT;
+    Ctx* c = &h->c;
+    fae_status st = validate_schema(c, tabs, "fae_pack_cold");
+    if (st != FAE_OK) return st;
+    if (!data || data->off || data->fixed_pool < 1 || n_cold < 0 || (n_cold > 0 && (!cold_ids || !cold_idx || !data->idx)))
+        return set_err(c, FAE_ERR_INVALID_ARG, "fae_pack_cold: fixed pooling and non-null buffers required");
+    int64_t total = 0;
+    for (int z = 0; z < tabs->n_tables; z++) total += tabs->rows[z];
+    if (total >= (1ll << 31)) return set_err(c, FAE_ERR_CAPACITY, "fae_pack_cold: global row ids >= 2^31");
+    if (n_cold == 0) return FAE_OK;
+    std::vector<int64_t> rowbase;
+    st = upload_schema(c, tabs, rowbase);
+    if (st != FAE_OK) return st;
+    const int64_t n = n_cold * tabs->n_tables * (int64_t)data->fixed_pool;
+    const int64_t g = std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), (int64_t)sms(c) * 16));
+    k_pack_cold<<<(unsigned)g, 256, 0, c->stream>>>(data->idx, cold_ids, n_cold, tabs->n_tables, data->fixed_pool,
+                                                    c->d_rowbase_tmp, c->d_rows_tmp, cold_idx, c->d_err);
+    FAE_LAUNCHED(c);
+    return read_latched(c);
 }
 
 extern "C" fae_status fae_scatter_hot(fae_ctx* h, const float* W_hot, int32_t dim, float* W) {

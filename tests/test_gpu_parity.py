@@ -568,3 +568,69 @@ def test_scatter_hot_swap_sync(dev, host):
     pipe.ctx.check()
     ref = oracle.scatter_hot(W, W_hot.cpu(), remap.cpu())
     assert np.array_equal(Wm.cpu().numpy(), ref)
+
+
+def test_mixed_hot_cold_schedule(dev):
+    """NEXT-1 end to end: hot batches on the replicated hot table, swap sync
+    (fae_scatter_hot), cold batches on the full tables through the cold CSR in
+    global row ids (fae_pack_cold + the standalone step calls), re-extract,
+    more hot batches == the oracle's sequential SGD over the same schedule
+    (the swaps; 1e-5 / 1e-6)."""
+    m = fae()
+    from paper_2103_00686_b200.pipeline import FaePipeline
+    c = gen.CONFIGS["tiny"]
+    R, x, seed, t = 10_000, 5.0, 7, 1e-2
+    ds = gen.make_dataset(c, n_records=R, seed=3)
+    dd = ds.to(dev)
+    Tn, D, B = c.n_tables, c.dim, c.batch
+    pipe = FaePipeline(ds.rows, D, B, 1)
+    prep = pipe.preprocess(dd.idx, None, R, x_pct=x, seed=seed, t=t, small_table_bytes=0)
+    W0 = gen.make_weights(sum(ds.rows), D)
+    Wd = W0.to(dev).clone()
+    W_hot = pipe.extract(Wd, prep).clone()
+    n_cold = prep.packed["n_cold"]
+    cold_idx = torch.empty(max(n_cold, 1) * Tn, dtype=torch.int32, device=dev)
+    m.fae_pack_cold(pipe.ctx, ds.rows, D, dd.idx, 1, R, prep.cold_ids, n_cold, cold_idx)
+    # oracle side
+    ref = _prep_ref(ds, x, seed, "t", t=t, small=0, dim=D)
+    pk, rm, H = ref["pack"], ref["remap"], ref["H"]
+    assert prep.packed["n_cold"] == pk["n_cold"]
+    base = np.concatenate([[0], np.cumsum(ds.rows)])
+    cold_ref = (ds.idx.numpy().reshape(R, Tn)[pk["cold_ids"]] + base[:Tn]).reshape(-1).astype(np.int32)
+    assert np.array_equal(cold_idx[:n_cold * Tn].cpu().numpy(), cold_ref)
+    Wr_full = W0.numpy().copy()
+    Wr_hot = oracle.extract(Wr_full, rm, H)
+    lr = 0.05
+    sched = [("hot", 0), ("hot", 1), ("cold", 0), ("cold", 1), ("hot", 2)]
+    Y = torch.empty(B * Tn, D, device=dev)
+    k = 0
+    prev = "hot"
+    for kind, i in sched:
+        dY = gen.make_dy(B * Tn, D, seed=200 + k)
+        k += 1
+        if kind != prev:   # swap
+            if kind == "cold":
+                m.fae_scatter_hot(pipe.ctx, W_hot, Wd)
+                Wr_full = oracle.scatter_hot(Wr_full, Wr_hot, rm)
+            else:
+                pipe.extract(Wd, prep)   # refresh the replica from the master
+                W_hot.copy_(pipe.extract(Wd, prep))
+                Wr_hot = oracle.extract(Wr_full, rm, H)
+            prev = kind
+        if kind == "hot":
+            idx, _, nb_ = pipe.batch_args(prep, i)
+            pipe.step(W_hot, prep, i, Y[:nb_], dY[:nb_].to(dev), lr)
+            bi = pk["hot_idx"][i * B * Tn: i * B * Tn + nb_]
+            Wr_hot, _ = oracle.emb_bwd_sgd(Wr_hot, bi, None, 1, nb_, dY[:nb_], lr)
+        else:
+            r0, r1 = i * B, min((i + 1) * B, n_cold)
+            nb_ = (r1 - r0) * Tn
+            ci = cold_idx[r0 * Tn: r1 * Tn]
+            m.fae_emb_fwd(pipe.ctx, Wd, ci, None, 1, nb_, Y[:nb_])
+            m.fae_emb_bwd_update(pipe.ctx, Wd, ci, None, 1, nb_, dY[:nb_].to(dev), lr)
+            Wr_full, _ = oracle.emb_bwd_sgd(Wr_full, cold_ref[r0 * Tn: r1 * Tn], None, 1, nb_, dY[:nb_], lr)
+    m.fae_scatter_hot(pipe.ctx, W_hot, Wd)
+    Wr_full = oracle.scatter_hot(Wr_full, Wr_hot, rm)
+    pipe.ctx.check()
+    ok, worst = close(Wd.cpu().numpy(), Wr_full)
+    assert ok, worst
