@@ -188,7 +188,7 @@ def run_fae(args):
         prep = pipe.preprocess(ds.idx, ds.off, R, x_pct=5.0, seed=args.seed, mode=mode,
                                t=cfg.t, budget_bytes=cfg.budget_bytes,
                                small_table_bytes=cfg.small_bytes, bufs=state.get("prep"),
-                               times=phases)
+                               times=phases, record_base=rank * R, n_records_global=world * R)
         state["prep"] = prep
         t = mark("preprocess_total", t)
         pipe.group(prep)
@@ -368,7 +368,8 @@ def run_e2e(args, ctxs):
         tt = mark("wait-in", tt)
         prep = pipe.preprocess(idx_d[b], off_d[b] if off_d is not None else None, R, x_pct=5.0,
                                seed=args.seed, mode=mode, t=cfg.t, budget_bytes=cfg.budget_bytes,
-                               small_table_bytes=cfg.small_bytes, bufs=st.get("prep"))
+                               small_table_bytes=cfg.small_bytes, bufs=st.get("prep"),
+                               record_base=rank * R, n_records_global=world * R)
         tt = mark("preprocess", tt)
         free[b].record()          # the hot CSR is built: this input buffer is free
         st["prep"] = prep

@@ -113,16 +113,24 @@ _CDF_CACHE: dict = {}
 
 
 def zipf_cdf(n: int, s: float, device) -> torch.Tensor:
-    """Normalised CDF of Zipf(s) on ranks 1..n (fp64): cdf[i] = P(rank <= i+1)."""
+    """Normalised CDF of Zipf(s) on ranks 1..n (fp64): cdf[i] = P(rank <= i+1).
+    Always computed on the CPU (a CUDA cumsum rounds differently, which moved
+    a few inverse-CDF draws at bucket edges of 10M-row tables) and copied to
+    `device`, so the same counters draw the same rows on every device."""
     key = (n, s, str(device))
     c = _CDF_CACHE.get(key)
     if c is None:
-        r = torch.arange(1, n + 1, dtype=torch.float64, device=device)
-        w = r.pow(-s)
-        c = torch.cumsum(w, 0)
-        c = c / c[-1]
+        ckey = (n, s, "cpu")
+        c = _CDF_CACHE.get(ckey)
+        if c is None:
+            r = torch.arange(1, n + 1, dtype=torch.float64)
+            w = r.pow(-s)
+            c = torch.cumsum(w, 0)
+            c = c / c[-1]
         if len(_CDF_CACHE) > 8:
             _CDF_CACHE.clear()
+        _CDF_CACHE[ckey] = c
+        c = c.to(device)
         _CDF_CACHE[key] = c
     return c
 

@@ -107,6 +107,20 @@ fae_status fae_check(fae_ctx* ctx);
 fae_status fae_get_nccl_id(void* id128);
 fae_status fae_comm_init(fae_ctx* ctx, const void* id128, int32_t rank,
                          int32_t world);
+/* TEST-ONLY transport ("virtual ranks"): `world` ctxs of ONE process on ONE
+ * GPU, each driven by its own host thread, join the loopback group
+ * `group_key` as ranks 0..world-1.  Every collective of the library (the
+ * sharded profile's select histograms / candidates / loggers / T, the a11
+ * count and payload all-gathers) then runs as a host rendezvous plus device
+ * copies and a rank-ordered integer sum, instead of NCCL; all other code is
+ * the same as with fae_comm_init.  Collectives block the calling thread
+ * (each synchronises the ctx stream), so the world > 1 step calls are not
+ * graph-capturable on this transport.  A peer that does not arrive within
+ * 120 s breaks the group (FAE_ERR_NCCL on every member).
+ * Errors: INVALID_ARG unless the environment has FAE_LOOPBACK=1, or bad
+ * rank/world (world <= cfg.max_world). */
+fae_status fae_comm_init_loopback(fae_ctx* ctx, uint64_t group_key,
+                                  int32_t rank, int32_t world);
 /* Number of kernels this ctx has launched so far (bench evidence). */
 int64_t fae_kernel_launches(const fae_ctx* ctx);
 
@@ -289,20 +303,29 @@ fae_status fae_scatter_hot(fae_ctx* ctx, const float* W_hot, int32_t dim,
  * NEXT-1, the cold-batch side; a cold input touches cold
  * rows, so its embeddings train against the full tables — here the
  * HBM-resident master tables, with the same step calls, H = sum N_z):
- *   cold_idx[k*Tn*P + z*P + p] = base_z + idx[cold_ids[k]*Tn*P + z*P + p],
+ *   for each cold record k in order, z = 0..Tn-1, each lookup p of bag
+ *   (cold_ids[k], z) in bag order: cold_idx[...] = base_z + idx[p],
  *   base_z = sum_{z' < z} N_z'.
- *  data      fixed pooling only (off == NULL), device idx.
- *  cold_ids  device int64 [n_cold] (fae_classify's cold_ids).
- *  cold_idx  device int32 [n_cold*Tn*P], caller-owned.
- * Cold batch i = records [i*B, min((i+1)*B, n_cold)) of cold_idx; train it
- * with fae_emb_fwd / fae_emb_bwd_update on W (H = sum N_z) after the hot
- * rows were written back (fae_scatter_hot), and re-extract before the next
- * hot batch.  Errors: INVALID_ARG (offsets, null buffers), CAPACITY
- * (sum N_z >= 2^31), INDEX_RANGE (latched).  Synchronises the stream.
+ *  data      fixed pooling (off == NULL) or explicit offsets; device idx/off.
+ *  cold_ids  device int64 [n_cold] (fae_classify's cold_ids), each in
+ *            [0, data->n_records) (else INDEX_RANGE).
+ *  cold_idx  device int32 [>= cold lookups], caller-owned (fixed pooling:
+ *            n_cold*Tn*P; offsets: n_lookups - n_hot_lookups suffices).
+ *  cold_off  device int64 [n_cold*Tn + 1], caller-owned, offsets input only
+ *            (NULL with fixed pooling): cold bag b's lookups are
+ *            cold_idx[cold_off[b] .. cold_off[b+1]).
+ * Cold batch i = records [i*B, min((i+1)*B, n_cold)); train it with
+ * fae_emb_fwd / fae_emb_bwd_update on W (H = sum N_z) after the hot rows
+ * were written back (fae_scatter_hot), and re-extract before the next hot
+ * batch.  Errors: INVALID_ARG (null buffers, n_cold > n_records, offsets
+ * without cold_off), CAPACITY (sum N_z >= 2^31 - 1, the step calls' bound),
+ * INDEX_RANGE (latched: a cold id or an index outside its table).
+ * Synchronises the stream.
  * ------------------------------------------------------------------------ */
 fae_status fae_pack_cold(fae_ctx* ctx, const fae_tables* tabs,
                          const fae_csr* data, const int64_t* cold_ids,
-                         int64_t n_cold, int32_t* cold_idx);
+                         int64_t n_cold, int32_t* cold_idx,
+                         int64_t* cold_off);
 
 /* --------------------------------------------------------------------------
  * fae_emb_fwd — hot embedding-bag forward (a8; sum

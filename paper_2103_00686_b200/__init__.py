@@ -27,7 +27,7 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "CAPACITY", 3: "BUDGET_INFEASIBLE",
 FIXED_T, BUDGET_EXACT, CLT_SEARCH = 0, 1, 2
 
 EXPORTS = ["fae_create", "fae_destroy", "fae_set_stream", "fae_last_error",
-           "fae_check", "fae_get_nccl_id", "fae_comm_init",
+           "fae_check", "fae_get_nccl_id", "fae_comm_init", "fae_comm_init_loopback",
            "fae_kernel_launches", "fae_profile", "fae_threshold",
            "fae_classify", "fae_extract", "fae_scatter_hot", "fae_pack_cold", "fae_emb_fwd", "fae_emb_bwd_update",
            "fae_sync_hot_grads", "fae_group_batches", "fae_train_hot_batches",
@@ -101,6 +101,7 @@ def lib():
             "fae_check": ([P], c_i32),
             "fae_get_nccl_id": ([P], c_i32),
             "fae_comm_init": ([P, P, c_i32, c_i32], c_i32),
+            "fae_comm_init_loopback": ([P, c_u64, c_i32, c_i32], c_i32),
             "fae_kernel_launches": ([P], c_i64),
             "fae_profile": ([P, ctypes.POINTER(FaeTables), ctypes.POINTER(FaeCsr),
                              c_dbl, c_u64, P, P, P, P], c_i32),
@@ -111,7 +112,7 @@ def lib():
                               c_i32, c_u64, ctypes.POINTER(FaePacked)], c_i32),
             "fae_extract": ([P, P, c_i32, P], c_i32),
             "fae_scatter_hot": ([P, P, c_i32, P], c_i32),
-            "fae_pack_cold": ([P, P, P, P, c_i64, P], c_i32),
+            "fae_pack_cold": ([P, ctypes.POINTER(FaeTables), ctypes.POINTER(FaeCsr), P, c_i64, P, P], c_i32),
             "fae_emb_fwd": ([P, P, c_i64, c_i32, P, P, c_i32, c_i64, P], c_i32),
             "fae_emb_bwd_update": ([P, P, c_i64, c_i32, P, P, c_i32, c_i64, P,
                                     ctypes.c_float], c_i32),
@@ -198,6 +199,11 @@ def fae_get_nccl_id() -> bytes:
 def fae_comm_init(ctx: Ctx, nccl_id: bytes, rank: int, world: int):
     buf = ctypes.create_string_buffer(nccl_id, 128)
     ctx._ok(lib().fae_comm_init(ctx.h, buf, rank, world))
+
+
+def fae_comm_init_loopback(ctx: Ctx, group_key: int, rank: int, world: int):
+    """TEST-ONLY virtual ranks on one GPU (needs FAE_LOOPBACK=1); see fae.h."""
+    ctx._ok(lib().fae_comm_init_loopback(ctx.h, ctypes.c_uint64(group_key), rank, world))
 
 
 def _tables(rows: Sequence[int], dim: int):
@@ -297,12 +303,14 @@ def fae_scatter_hot(ctx: Ctx, W_hot: torch.Tensor, W: torch.Tensor):
 
 
 def fae_pack_cold(ctx: Ctx, rows, dim: int, idx: torch.Tensor, fixed_pool: int, n_records: int,
-                  cold_ids: torch.Tensor, n_cold: int, cold_idx: torch.Tensor):
-    """NEXT-1 cold side: the cold records' lookups in global row ids."""
+                  cold_ids: torch.Tensor, n_cold: int, cold_idx: torch.Tensor,
+                  off: Optional[torch.Tensor] = None, cold_off: Optional[torch.Tensor] = None):
+    """NEXT-1 cold side: the cold records' lookups in global row ids
+    (cold_off: their bag offsets, explicit-offset inputs only)."""
     tabs, keep = _tables(rows, dim)
-    csr = _csr(idx, None, fixed_pool, n_records, len(rows))
+    csr = _csr(idx, off, fixed_pool, n_records, len(rows))
     ctx._ok(lib().fae_pack_cold(ctx.h, ctypes.byref(tabs), ctypes.byref(csr), _p(cold_ids),
-                                int(n_cold), _p(cold_idx)))
+                                int(n_cold), _p(cold_idx), _p(cold_off)))
     del keep
 
 

@@ -412,17 +412,20 @@ extern "C" fae_status fae_extract(fae_ctx* h, const float* W, int32_t dim, float
     return FAE_OK;
 }
 
-// cold CSR in global row ids: out[k*TnP + q] = rowbase[z] + idx[cold[k]*TnP + q]
+// cold CSR in global row ids (fixed pooling): out[k*TnP + q] = rowbase[z] +
+// idx[cold[k]*TnP + q].  A cold id outside [0, n_rec) latches INDEX_RANGE and
+// its lookups are written as row 0 (the call then fails).
 __global__ void __launch_bounds__(256)
-k_pack_cold(const int32_t* __restrict__ idx, const int64_t* __restrict__ cold_ids, int64_t n_cold, int Tn, int P,
-            const int64_t* __restrict__ rowbase, const int64_t* __restrict__ rows, int32_t* __restrict__ out,
-            uint32_t* err) {
+k_pack_cold(const int32_t* __restrict__ idx, const int64_t* __restrict__ cold_ids, int64_t n_cold, int64_t n_rec,
+            int Tn, int P, const int64_t* __restrict__ rowbase, const int64_t* __restrict__ rows,
+            int32_t* __restrict__ out, uint32_t* err) {
     const int64_t TnP = (int64_t)Tn * P;
     const int64_t n = n_cold * TnP;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t k = e / TnP, q = e - k * TnP;
         const int z = (int)(q / P);
-        const int32_t j = idx[cold_ids[k] * TnP + q];
+        const int64_t r = cold_ids[k];
+        const int32_t j = (r >= 0 && r < n_rec) ? idx[r * TnP + q] : -1;
         if (j < 0 || (int64_t)j >= rows[z]) {
             atomicOr(err, kErrIndex);
             out[e] = 0;
@@ -432,25 +435,155 @@ k_pack_cold(const int32_t* __restrict__ idx, const int64_t* __restrict__ cold_id
     }
 }
 
+// explicit offsets, pass 1: bag sizes of the cold records, sz[k*Tn + z]
+__global__ void __launch_bounds__(256)
+k_cold_sizes(const int64_t* __restrict__ off, const int64_t* __restrict__ cold_ids, int64_t n_cold, int64_t n_rec,
+             int Tn, int64_t* __restrict__ sz, uint32_t* err) {
+    const int64_t n = n_cold * Tn;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = e / Tn, z = e - k * Tn;
+        const int64_t r = cold_ids[k];
+        if (r < 0 || r >= n_rec) {
+            atomicOr(err, kErrIndex);
+            sz[e] = 0;
+        } else {
+            sz[e] = off[r * Tn + z + 1] - off[r * Tn + z];
+        }
+    }
+}
+
+// exclusive scan of n int64 values (< 2^62 in total) into out[0..n], out[n] =
+// total: tiles of 256 x 16, block scan + decoupled look-back
+constexpr int kScanItems = 16;
+__global__ void __launch_bounds__(256)
+k_scan_i64(const int64_t* __restrict__ in, int64_t n, int64_t* __restrict__ out, uint64_t* __restrict__ status,
+           uint32_t* __restrict__ ctr) {
+    __shared__ int s_tile;
+    __shared__ uint64_t s_w[8];
+    __shared__ uint64_t s_ex;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_tile = (int)atomicAdd(ctr, 1u);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    const int64_t i0 = tile * (256 * kScanItems) + (int64_t)tid * kScanItems;
+    uint64_t v[kScanItems], sum = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; j++) {
+        v[j] = i0 + j < n ? (uint64_t)in[i0 + j] : 0ull;
+        sum += v[j];
+    }
+    uint64_t x = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    uint64_t wp = 0, tot = 0;
+    for (int w = 0; w < 8; w++) {
+        if (w < warp) wp += s_w[w];
+        tot += s_w[w];
+    }
+    if (tid == 0) {
+        s_ex = lookback_u64(status, tile, tot);
+        const int64_t last = n > 0 ? (n - 1) / (256 * kScanItems) : 0;
+        if (tile == last) out[n] = (int64_t)(s_ex + tot);
+    }
+    __syncthreads();
+    uint64_t run = s_ex + wp + x - sum;
+#pragma unroll
+    for (int j = 0; j < kScanItems; j++) {
+        if (i0 + j < n) out[i0 + j] = (int64_t)run;
+        run += v[j];
+    }
+}
+
+// explicit offsets, pass 2: warp per cold record, lookups in global row ids
+__global__ void __launch_bounds__(256)
+k_pack_cold_off(const int32_t* __restrict__ idx, const int64_t* __restrict__ off,
+                const int64_t* __restrict__ cold_ids, int64_t n_cold, int64_t n_rec, int Tn,
+                const int64_t* __restrict__ rowbase, const int64_t* __restrict__ rows,
+                const int64_t* __restrict__ cold_off, int32_t* __restrict__ out, uint32_t* err) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wpb = blockDim.x >> 5;
+    for (int64_t k = blockIdx.x * wpb + (threadIdx.x >> 5); k < n_cold; k += (int64_t)gridDim.x * wpb) {
+        const int64_t r = cold_ids[k];
+        if (r < 0 || r >= n_rec) continue;   // latched by k_cold_sizes
+        for (int z = 0; z < Tn; z++) {
+            const int64_t lo = off[r * Tn + z], hi = off[r * Tn + z + 1];
+            const int64_t o = cold_off[k * Tn + z];
+            for (int64_t p = lo + lane; p < hi; p += 32) {
+                const int32_t j = idx[p];
+                if (j < 0 || (int64_t)j >= rows[z]) {
+                    atomicOr(err, kErrIndex);
+                    out[o + (p - lo)] = 0;
+                } else {
+                    out[o + (p - lo)] = (int32_t)(rowbase[z] + j);
+                }
+            }
+        }
+    }
+}
+
 extern "C" fae_status fae_pack_cold(fae_ctx* h, const fae_tables* tabs, const fae_csr* data,
-                                    const int64_t* cold_ids, int64_t n_cold, int32_t* cold_idx) {
+                                    const int64_t* cold_ids, int64_t n_cold, int32_t* cold_idx,
+                                    int64_t* cold_off) {
     if (!h) return FAE_ERR_NOT_INIT;
     Ctx* c = &h->c;
     fae_status st = validate_schema(c, tabs, "fae_pack_cold");
     if (st != FAE_OK) return st;
-    if (!data || data->off || data->fixed_pool < 1 || n_cold < 0 || (n_cold > 0 && (!cold_ids || !cold_idx || !data->idx)))
-        return set_err(c, FAE_ERR_INVALID_ARG, "fae_pack_cold: fixed pooling and non-null buffers required");
+    st = validate_csr(c, tabs, data, "fae_pack_cold");
+    if (st != FAE_OK) return st;
+    if (n_cold < 0 || n_cold > data->n_records ||
+        (n_cold > 0 && (!cold_ids || (!cold_idx && data->n_lookups > 0) || (data->n_lookups > 0 && !data->idx))))
+        return set_err(c, FAE_ERR_INVALID_ARG, "fae_pack_cold: bad sizes or null buffers");
+    if (data->off && !cold_off) return set_err(c, FAE_ERR_INVALID_ARG, "fae_pack_cold: cold_off required with offsets");
     int64_t total = 0;
     for (int z = 0; z < tabs->n_tables; z++) total += tabs->rows[z];
-    if (total >= (1ll << 31)) return set_err(c, FAE_ERR_CAPACITY, "fae_pack_cold: global row ids >= 2^31");
-    if (n_cold == 0) return FAE_OK;
+    // the same bound as the step calls that train the cold batches (H < 2^31 - 1)
+    if (total >= (1ll << 31) - 1) return set_err(c, FAE_ERR_CAPACITY, "fae_pack_cold: global row ids >= 2^31 - 1");
+    const int Tn = tabs->n_tables;
+    if (n_cold == 0) {
+        if (cold_off) FAE_CUDA(c, cudaMemsetAsync(cold_off, 0, sizeof(int64_t), c->stream));
+        return read_latched(c);
+    }
     std::vector<int64_t> rowbase;
     st = upload_schema(c, tabs, rowbase);
     if (st != FAE_OK) return st;
-    const int64_t n = n_cold * tabs->n_tables * (int64_t)data->fixed_pool;
-    const int64_t g = std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), (int64_t)sms(c) * 16));
-    k_pack_cold<<<(unsigned)g, 256, 0, c->stream>>>(data->idx, cold_ids, n_cold, tabs->n_tables, data->fixed_pool,
-                                                    c->d_rowbase_tmp, c->d_rows_tmp, cold_idx, c->d_err);
+    if (!data->off) {
+        const int64_t n = n_cold * Tn * (int64_t)data->fixed_pool;
+        if (n > 0) {
+            const int64_t g = std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), (int64_t)sms(c) * 16));
+            k_pack_cold<<<(unsigned)g, 256, 0, c->stream>>>(data->idx, cold_ids, n_cold, data->n_records, Tn,
+                                                            data->fixed_pool, c->d_rowbase_tmp, c->d_rows_tmp,
+                                                            cold_idx, c->d_err);
+            FAE_LAUNCHED(c);
+        }
+        return read_latched(c);
+    }
+    // explicit offsets: bag sizes -> exclusive scan (cold_off) -> copy
+    const int64_t nb = n_cold * Tn;
+    const int64_t tiles = cdiv(nb, 256 * kScanItems);
+    size_t o = 0;
+    auto take = [&](size_t b) { size_t r = o; o = (o + b + 255) / 256 * 256; return r; };
+    const size_t o_sz = take(sizeof(int64_t) * nb);
+    const size_t o_st = take(sizeof(uint64_t) * tiles);
+    const size_t o_ctr = take(sizeof(uint32_t) * 4);
+    char* sc = (char*)scratch(c, o);
+    if (!sc) return set_err(c, FAE_ERR_CUDA, "fae_pack_cold: scratch allocation failed");
+    int64_t* d_sz = (int64_t*)(sc + o_sz);
+    FAE_CUDA(c, cudaMemsetAsync(sc + o_st, 0, o - o_st, c->stream));
+    const int64_t g = std::max<int64_t>(1, std::min<int64_t>(cdiv(nb, 256), (int64_t)sms(c) * 16));
+    k_cold_sizes<<<(unsigned)g, 256, 0, c->stream>>>(data->off, cold_ids, n_cold, data->n_records, Tn, d_sz,
+                                                     c->d_err);
+    FAE_LAUNCHED(c);
+    k_scan_i64<<<(unsigned)tiles, 256, 0, c->stream>>>(d_sz, nb, cold_off, (uint64_t*)(sc + o_st),
+                                                       (uint32_t*)(sc + o_ctr));
+    FAE_LAUNCHED(c);
+    const int64_t gw = std::max<int64_t>(1, std::min<int64_t>(cdiv(n_cold, 8), (int64_t)sms(c) * 16));
+    k_pack_cold_off<<<(unsigned)gw, 256, 0, c->stream>>>(data->idx, data->off, cold_ids, n_cold, data->n_records, Tn,
+                                                         c->d_rowbase_tmp, c->d_rows_tmp, cold_off, cold_idx,
+                                                         c->d_err);
     FAE_LAUNCHED(c);
     return read_latched(c);
 }

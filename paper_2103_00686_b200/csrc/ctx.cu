@@ -43,7 +43,7 @@ fae_status read_latched(Ctx* c) {
         FAE_CUDA(c, cudaMemsetAsync(c->d_err, 0, sizeof(uint32_t), c->stream));
         if (bits & kErrIndex) return set_err(c, FAE_ERR_INDEX_RANGE, "index outside its table (latched on device)");
         if (bits & kErrNonfinite) return set_err(c, FAE_ERR_NONFINITE, "non-finite value in update (latched on device)");
-        if (bits & kErrOverflow) return set_err(c, FAE_ERR_CAPACITY, "counter overflow (latched on device)");
+        if (bits & kErrOverflow) return set_err(c, FAE_ERR_CAPACITY, "capacity exceeded on device: counter overflow or a batch larger than max_batch_lookups (latched)");
         if (bits & kErrBarrier) return set_err(c, FAE_ERR_CUDA, "persistent kernel: grid barrier timed out (latched on device)");
     }
     return FAE_OK;
@@ -181,7 +181,7 @@ void fae_destroy(fae_ctx* h) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     else cudaDeviceSynchronize();
-    if (c->comm) ncclCommDestroy(c->comm);
+    coll_free(c);
     step_ws_free(c);
     group_free(c);
     cudaFree(c->d_err);
@@ -193,6 +193,7 @@ void fae_destroy(fae_ctx* h) {
     cudaFree(c->g_rows);
     cudaFree(c->g_vals);
     cudaFree(c->g_counts);
+    cudaFree(c->g_flag);
     delete h;
 }
 
@@ -234,23 +235,13 @@ fae_status fae_comm_init(fae_ctx* h, const void* id128, int32_t rank, int32_t wo
     cudaSetDevice(c->device);
     ncclUniqueId id;
     memcpy(&id, id128, sizeof(id));
-    if (c->comm) {
-        ncclCommDestroy(c->comm);
-        c->comm = nullptr;
-    }
+    coll_free(c);
     ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
     if (r != ncclSuccess)
         return set_err(c, FAE_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
     c->rank = rank;
     c->world = world;
-    const int64_t capL = c->cfg.max_batch_lookups;
-    if (!c->g_rows) {
-        c->g_cap = capL;
-        FAE_CUDA(c, cudaMalloc(&c->g_rows, sizeof(int32_t) * capL * world));
-        FAE_CUDA(c, cudaMalloc(&c->g_vals, sizeof(float) * capL * world * c->cfg.max_dim));
-        FAE_CUDA(c, cudaMalloc(&c->g_counts, sizeof(int32_t) * c->cfg.max_world));
-    }
-    return FAE_OK;
+    return comm_bufs(c);
 }
 
 }  // extern "C"

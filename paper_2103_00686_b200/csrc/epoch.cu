@@ -1035,17 +1035,24 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
     if (!h) return FAE_ERR_NOT_INIT;
     Ctx* c = &h->c;
     Group& g = c->grp;
-    if (!g.valid) return set_err(c, FAE_ERR_NOT_INIT, "fae_train_hot_batches: no grouped batches (fae_group_batches)");
-    if (!dim_ok(D) || D > c->cfg.max_dim) return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_hot_batches: unsupported dim");
-    if (H != g.H) return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_hot_batches: H differs from the grouped H");
-    if (chunk_for_dim(D) != g.chunk)
-        return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_hot_batches: D differs from the grouped tables' dim");
-    if (first < 0 || n < 0 || n_dy < 1 || (c->world == 1 && first + n > g.n_batches))
-        return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_hot_batches: batch range outside the grouped batches");
-    if (!(lr == lr)) return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_hot_batches: lr is NaN");
-    if (n > 0 && (!W_hot || !dY || !Y)) return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_hot_batches: null pointer");
-    if (((uintptr_t)W_hot | (uintptr_t)dY | (uintptr_t)Y) & 15)
-        return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_hot_batches: buffers must be 16-byte aligned");
+    auto validate = [&]() -> fae_status {
+        if (!g.valid) return set_err(c, FAE_ERR_NOT_INIT, "fae_train_hot_batches: no grouped batches (fae_group_batches)");
+        if (!dim_ok(D) || D > c->cfg.max_dim) return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_hot_batches: unsupported dim");
+        if (H != g.H) return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_hot_batches: H differs from the grouped H");
+        if (chunk_for_dim(D) != g.chunk)
+            return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_hot_batches: D differs from the grouped tables' dim");
+        if (first < 0 || n < 0 || n_dy < 1 || (c->world == 1 && first + n > g.n_batches))
+            return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_hot_batches: batch range outside the grouped batches");
+        if (!(lr == lr)) return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_hot_batches: lr is NaN");
+        if (n > 0 && (!W_hot || !dY || !Y)) return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_hot_batches: null pointer");
+        if (((uintptr_t)W_hot | (uintptr_t)dY | (uintptr_t)Y) & 15)
+            return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_hot_batches: buffers must be 16-byte aligned");
+        return FAE_OK;
+    };
+    fae_status vst = validate();
+    // ranks agree before the exchange loop (no peer left blocked)
+    if (c->world > 1 && has_comm(c)) vst = coll_agree(c, vst, "fae_train_hot_batches");
+    if (vst != FAE_OK) return vst;
     if (n == 0) return FAE_OK;
     // cursor, pad, run[0], run[1] — set by a kernel, not a host copy, so the
     // loop never queues behind a bulk host->device transfer on the copy engine
@@ -1058,7 +1065,7 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
         // exchange.  Every step's per-rank gradient size is known after the
         // grouping, so all of them are exchanged once here (one all-gather,
         // one host read) and the loop itself never synchronises the host.
-        if (!c->comm) return set_err(c, FAE_ERR_NOT_INIT, "fae_train_hot_batches: world > 1 without a communicator");
+        if (!has_comm(c)) return set_err(c, FAE_ERR_NOT_INIT, "fae_train_hot_batches: world > 1 without a communicator");
         const int world = c->world;
         if (g.cap_xcnt < 2 * n * world) {
             cudaFree(g.xcnt);
@@ -1073,8 +1080,9 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
         int32_t* per_step = g.xcnt + n * world;  // [n][world]
         FAE_CUDA(c, cudaMemcpyAsync(all + (int64_t)c->rank * n, mine.data(), sizeof(int32_t) * n,
                                     cudaMemcpyHostToDevice, c->stream));
-        ncclResult_t r = ncclAllGather(all + (int64_t)c->rank * n, all, n, ncclInt32, c->comm, c->stream);
-        if (r != ncclSuccess) return set_err(c, FAE_ERR_NCCL, std::string("ncclAllGather counts: ") + ncclGetErrorString(r));
+        fae_status cs = coll_allgather(c, all + (int64_t)c->rank * n, all, n, CollT::I32,
+                                       "fae_train_hot_batches: allgather counts");
+        if (cs != FAE_OK) return cs;
         std::vector<int32_t> hall((size_t)n * world), ht((size_t)n * world);
         FAE_CUDA(c, cudaMemcpyAsync(hall.data(), all, sizeof(int32_t) * n * world, cudaMemcpyDeviceToHost, c->stream));
         FAE_CUDA(c, cudaStreamSynchronize(c->stream));

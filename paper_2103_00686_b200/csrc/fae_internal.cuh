@@ -55,6 +55,10 @@ constexpr uint64_t kFlagAgg = 1ull << 62;
 constexpr uint64_t kFlagPre = 2ull << 62;
 constexpr uint64_t kValMask = (1ull << 62) - 1;
 
+// Collectives (coll.cu): NCCL or the test-only loopback transport.
+enum class CollT { U32, I32, I64, U64, F32 };
+struct LbMember;
+
 // Step workspace: everything fae_emb_bwd_update needs, allocated at create.
 struct StepWs {
     int64_t cap_L = 0;                  // lookups capacity
@@ -210,9 +214,11 @@ struct Ctx {
     size_t scratch_bytes = 0;
     int64_t* d_rowbase_tmp = nullptr;           // [max_tables+1]
     int64_t* d_rows_tmp = nullptr;              // [max_tables]
-    // NCCL
+    // collectives: NCCL communicator or loopback virtual-rank group (tests)
     ncclComm_t comm = nullptr;
+    LbMember* lb = nullptr;
     int rank = 0, world = 1;
+    int64_t* g_flag = nullptr;                  // [2] coll_agree scratch
     // sync scratch
     int32_t* g_rows = nullptr;                  // [max_world * cap_L]
     float* g_vals = nullptr;                    // [max_world * cap_L * max_dim]
@@ -262,6 +268,17 @@ fae_status read_latched(Ctx* c);       // sync + read/clear device error word
     } while (0)
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// collectives (coll.cu)
+inline bool has_comm(const Ctx* c) { return c->comm != nullptr || c->lb != nullptr; }
+fae_status coll_allreduce_sum(Ctx* c, void* buf, int64_t count, CollT t, const char* who);
+fae_status coll_allgather(Ctx* c, const void* send, void* recv, int64_t count, CollT t, const char* who);
+void coll_group_start(Ctx* c);
+fae_status coll_group_end(Ctx* c, const char* who);
+fae_status coll_async_error(Ctx* c, const char* who);
+fae_status coll_agree(Ctx* c, fae_status local, const char* who);
+fae_status comm_bufs(Ctx* c);
+void coll_free(Ctx* c);
 
 // step internals (step.cu), used by sync
 fae_status bwd_group_and_reduce(Ctx* c, float* W_hot, int64_t H, int32_t D,

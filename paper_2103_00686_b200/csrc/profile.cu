@@ -304,13 +304,17 @@ extern "C" fae_status fae_profile(fae_ctx* h, const fae_tables* tabs, const fae_
                                   int64_t* sampled_ids, int64_t* n_sampled) {
     if (!h) return FAE_ERR_NOT_INIT;
     Ctx* c = &h->c;
+    const bool multi = c->world > 1 && has_comm(c);
     fae_status st = validate_schema(c, tabs, "fae_profile");
+    if (st == FAE_OK) st = validate_csr(c, tabs, data, "fae_profile");
+    if (st == FAE_OK && !(x_pct > 0.0 && x_pct <= 100.0))
+        st = set_err(c, FAE_ERR_INVALID_ARG, "fae_profile: x must be in (0, 100]");
+    if (st == FAE_OK && (!counts || !T_host || !n_sampled))
+        st = set_err(c, FAE_ERR_INVALID_ARG, "fae_profile: null output");
+    // with a comm every rank must take the same early exit (no peer left
+    // blocked in a collective)
+    if (multi) st = coll_agree(c, st, "fae_profile");
     if (st != FAE_OK) return st;
-    st = validate_csr(c, tabs, data, "fae_profile");
-    if (st != FAE_OK) return st;
-    if (!(x_pct > 0.0 && x_pct <= 100.0)) return set_err(c, FAE_ERR_INVALID_ARG, "fae_profile: x must be in (0, 100]");
-    if (!counts || !T_host || !n_sampled) return set_err(c, FAE_ERR_INVALID_ARG, "fae_profile: null output");
-    const bool multi = c->world > 1 && c->comm;
     const int Tn = tabs->n_tables;
     std::vector<int64_t> rowbase;
     st = upload_schema(c, tabs, rowbase);
@@ -365,8 +369,8 @@ extern "C" fae_status fae_profile(fae_ctx* h, const fae_tables* tabs, const fae_
             k_sel_hist<<<(unsigned)gridn, 256, 0, c->stream>>>(n, gbase, seed, prefix, pbits, hist);
             FAE_LAUNCHED(c);
             if (multi) {
-                ncclResult_t r = ncclAllReduce(hist, hist, 256, ncclUint32, ncclSum, c->comm, c->stream);
-                if (r != ncclSuccess) return set_err(c, FAE_ERR_NCCL, "fae_profile: allreduce hist");
+                st = coll_allreduce_sum(c, hist, 256, CollT::U32, "fae_profile: allreduce hist");
+                if (st != FAE_OK) return st;
             }
             FAE_CUDA(c, cudaMemcpyAsync(h_hist, hist, sizeof(h_hist), cudaMemcpyDeviceToHost, c->stream));
             FAE_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -395,14 +399,17 @@ extern "C" fae_status fae_profile(fae_ctx* h, const fae_tables* tabs, const fae_
         uint32_t n_c = 0;
         FAE_CUDA(c, cudaMemcpyAsync(&n_c, ccnt, sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
         FAE_CUDA(c, cudaStreamSynchronize(c->stream));
-        if (n_c > (uint32_t)kCandCap) return set_err(c, FAE_ERR_CAPACITY, "fae_profile: selection candidates overflow");
+        st = n_c > (uint32_t)kCandCap ? set_err(c, FAE_ERR_CAPACITY, "fae_profile: selection candidates overflow")
+                                      : FAE_OK;
+        if (multi) st = coll_agree(c, st, "fae_profile: candidates");
+        if (st != FAE_OK) return st;
         if (multi) {
-            ncclResult_t r;
-            ncclGroupStart();
-            ncclAllGather(myk, ck, kCandCap, ncclUint64, c->comm, c->stream);
-            ncclAllGather(myi, ci, kCandCap, ncclInt64, c->comm, c->stream);
-            r = ncclGroupEnd();
-            if (r != ncclSuccess) return set_err(c, FAE_ERR_NCCL, "fae_profile: allgather candidates");
+            coll_group_start(c);
+            st = coll_allgather(c, myk, ck, kCandCap, CollT::U64, "fae_profile: allgather candidate keys");
+            if (st == FAE_OK) st = coll_allgather(c, myi, ci, kCandCap, CollT::I64, "fae_profile: allgather candidate ids");
+            fae_status st2 = coll_group_end(c, "fae_profile: allgather candidates");
+            if (st != FAE_OK) return st;
+            if (st2 != FAE_OK) return st2;
         }
         const int n_all = multi ? W * kCandCap : (int)n_c;
         const unsigned long long* pk = ck;
@@ -463,11 +470,11 @@ extern "C" fae_status fae_profile(fae_ctx* h, const fae_tables* tabs, const fae_
         for (int z = 0; z < Tn; z++) T[z] = n * (int64_t)data->fixed_pool;
     }
     if (multi) {
-        ncclResult_t r = ncclAllReduce(counts, counts, total_rows, ncclUint32, ncclSum, c->comm, c->stream);
-        if (r != ncclSuccess) return set_err(c, FAE_ERR_NCCL, "fae_profile: allreduce counts");
+        st = coll_allreduce_sum(c, counts, total_rows, CollT::U32, "fae_profile: allreduce counts");
+        if (st != FAE_OK) return st;
         FAE_CUDA(c, cudaMemcpyAsync(dT, T.data(), sizeof(int64_t) * Tn, cudaMemcpyHostToDevice, c->stream));
-        r = ncclAllReduce(dT, dT, Tn, ncclInt64, ncclSum, c->comm, c->stream);
-        if (r != ncclSuccess) return set_err(c, FAE_ERR_NCCL, "fae_profile: allreduce T");
+        st = coll_allreduce_sum(c, dT, Tn, CollT::I64, "fae_profile: allreduce T");
+        if (st != FAE_OK) return st;
         FAE_CUDA(c, cudaMemcpyAsync(T.data(), dT, sizeof(int64_t) * Tn, cudaMemcpyDeviceToHost, c->stream));
     }
     if (sampled_ids && ns > 0)

@@ -52,7 +52,7 @@ __device__ __forceinline__ int32_t find_bag(const int64_t* __restrict__ off, int
 
 __global__ void __launch_bounds__(256)
 k_bwd_prep(const int32_t* __restrict__ idx, const int64_t* __restrict__ off, int P,
-           int64_t n_bags, int64_t H, int passes, uint32_t* __restrict__ keys,
+           int64_t n_bags, int64_t H, int passes, int64_t cap, uint32_t* __restrict__ keys,
            int32_t* __restrict__ vals, uint32_t* __restrict__ ghist,
            int64_t* __restrict__ scalars, uint32_t* err) {
     __shared__ uint32_t sh[kMaxSortPasses][kSortBins];
@@ -60,6 +60,17 @@ k_bwd_prep(const int32_t* __restrict__ idx, const int64_t* __restrict__ off, int
     __syncthreads();
     const int64_t base = off ? off[0] : 0;
     const int64_t n = off ? off[n_bags] - base : n_bags * (int64_t)P;
+    // a multi-hot batch larger than the workspace (cap = the sort's tile
+    // capacity, max_batch_lookups): latch CAPACITY and apply nothing (every
+    // later kernel of the step sees n_items = 0), never write past the
+    // workspace
+    if (n > cap || n < 0) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            scalars[3] = 0;
+            atomicOr(err, kErrOverflow);
+        }
+        return;
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) scalars[3] = n;
     int nvalid = 0;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
@@ -460,7 +471,8 @@ fae_status bwd_group_and_reduce(Ctx* c, float* W_hot, int64_t H, int32_t D,
     if (st != FAE_OK) return st;
     const int passes = (key_bits(H) + kSortBits - 1) / kSortBits;
     int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(cdiv(n_hint, 256), (int64_t)sm_count(c) * 8));
-    k_bwd_prep<<<(unsigned)blocks, 256, 0, c->stream>>>(idx, off, P, n_bags, H, passes, w.keys[0],
+    k_bwd_prep<<<(unsigned)blocks, 256, 0, c->stream>>>(idx, off, P, n_bags, H, passes,
+                                                        std::min<int64_t>(n_hint, w.cap_L), w.keys[0],
                                                         w.vals[0], w.ghist, w.scalars, c->d_err);
     FAE_LAUNCHED(c);
     return sort_pieces_reduce(c, n_hint, H, D, dY, W_hot, lr, emit);
@@ -504,10 +516,11 @@ fae_status fae_emb_bwd_update(fae_ctx* h, float* W_hot, int64_t H, int32_t D, co
     if (!h) return FAE_ERR_NOT_INIT;
     Ctx* c = &h->c;
     fae_status st = validate_step(c, W_hot, H, D, idx, off, fixed_pool, n_bags, dY, "fae_emb_bwd_update");
-    if (st != FAE_OK) return st;
-    if (!(lr == lr)) return set_err(c, FAE_ERR_INVALID_ARG, "fae_emb_bwd_update: lr is NaN");
-    const int64_t n_hint = off ? c->cfg.max_batch_lookups : n_bags * (int64_t)fixed_pool;
+    if (st == FAE_OK && !(lr == lr)) st = set_err(c, FAE_ERR_INVALID_ARG, "fae_emb_bwd_update: lr is NaN");
     const bool multi = c->world > 1;
+    if (multi) st = coll_agree(c, st, "fae_emb_bwd_update");   // no peer left blocked in the exchange
+    if (st != FAE_OK) return st;
+    const int64_t n_hint = off ? c->cfg.max_batch_lookups : n_bags * (int64_t)fixed_pool;
     if (n_bags == 0 && !multi) return FAE_OK;
     st = bwd_group_and_reduce(c, W_hot, H, D, nullptr, idx, off, fixed_pool, n_bags, n_hint, dY, lr, multi);
     if (st != FAE_OK || !multi) return st;
@@ -610,18 +623,17 @@ fae_status sync_merge_apply(Ctx* c, const int32_t* rows, const float* vals, int6
                             float* W, int64_t H, float lr, int32_t* out_rows, float* out_vals,
                             int64_t* out_count, int64_t out_cap, const int32_t* known_counts,
                             int64_t known_cap) {
-    if (!c->comm) return set_err(c, FAE_ERR_NOT_INIT, "sync: no communicator");
+    if (!has_comm(c)) return set_err(c, FAE_ERR_NOT_INIT, "sync: no communicator");
     const int world = c->world;
-    if (U > c->g_cap) return set_err(c, FAE_ERR_CAPACITY, "sync: local U exceeds capacity");
-    ncclResult_t r;
     int64_t cap = 0;
     const int32_t* dcounts = known_counts;
     if (!known_counts) {
-        // 1. counts
-        int32_t Ui = (int32_t)U;
+        // 1. counts (a local U beyond capacity is exchanged as-is: every rank
+        //    then sees the same maximum and returns the same error below)
+        const int32_t Ui = (int32_t)std::min<int64_t>(U, INT32_MAX);
         FAE_CUDA(c, cudaMemcpyAsync(c->g_counts + c->rank, &Ui, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
-        r = ncclAllGather(c->g_counts + c->rank, c->g_counts, 1, ncclInt32, c->comm, c->stream);
-        if (r != ncclSuccess) return set_err(c, FAE_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+        fae_status cs = coll_allgather(c, c->g_counts + c->rank, c->g_counts, 1, CollT::I32, "sync: allgather counts");
+        if (cs != FAE_OK) return cs;
         std::vector<int32_t> counts(world);
         FAE_CUDA(c, cudaMemcpyAsync(counts.data(), c->g_counts, sizeof(int32_t) * world, cudaMemcpyDeviceToHost, c->stream));
         FAE_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -634,6 +646,7 @@ fae_status sync_merge_apply(Ctx* c, const int32_t* rows, const float* vals, int6
         if (out_count) *out_count = 0;
         return FAE_OK;
     }
+    if (cap > c->g_cap) return set_err(c, FAE_ERR_CAPACITY, "sync: a rank's U exceeds capacity");
     if (cap * world > c->ws.cap_L) return set_err(c, FAE_ERR_CAPACITY, "sync: gathered size exceeds workspace");
     // 2. padded payloads (rows, vals) — grouped all-gathers
     int32_t* my_rows = c->g_rows + (int64_t)c->rank * cap;
@@ -642,11 +655,14 @@ fae_status sync_merge_apply(Ctx* c, const int32_t* rows, const float* vals, int6
         FAE_CUDA(c, cudaMemcpyAsync(my_rows, rows, sizeof(int32_t) * U, cudaMemcpyDeviceToDevice, c->stream));
         FAE_CUDA(c, cudaMemcpyAsync(my_vals, vals, sizeof(float) * U * D, cudaMemcpyDeviceToDevice, c->stream));
     }
-    ncclGroupStart();
-    ncclAllGather(my_rows, c->g_rows, cap, ncclInt32, c->comm, c->stream);
-    ncclAllGather(my_vals, c->g_vals, cap * D, ncclFloat32, c->comm, c->stream);
-    r = ncclGroupEnd();
-    if (r != ncclSuccess) return set_err(c, FAE_ERR_NCCL, std::string("ncclAllGather payload: ") + ncclGetErrorString(r));
+    {
+        coll_group_start(c);
+        fae_status a = coll_allgather(c, my_rows, c->g_rows, cap, CollT::I32, "sync: allgather rows");
+        if (a == FAE_OK) a = coll_allgather(c, my_vals, c->g_vals, cap * D, CollT::F32, "sync: allgather grads");
+        fae_status b = coll_group_end(c, "sync: allgather payload");
+        if (a != FAE_OK) return a;
+        if (b != FAE_OK) return b;
+    }
     // 3. deterministic merge.  Applying to W: the rank-ordered merge of the
     //    sorted lists (one kernel).  Emitting the merged list: a stable sort by
     //    row over the rank-ordered concatenation, segment sums in fixed order.
@@ -654,10 +670,7 @@ fae_status sync_merge_apply(Ctx* c, const int32_t* rows, const float* vals, int6
     if (W && !c->merge_sort) {
         st = merge_apply(c, dcounts, cap, D, W, lr);
         if (st != FAE_OK) return st;
-        ncclResult_t ae;
-        if (ncclCommGetAsyncError(c->comm, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress)
-            return set_err(c, FAE_ERR_NCCL, std::string("nccl async: ") + ncclGetErrorString(ae));
-        return FAE_OK;
+        return coll_async_error(c, "sync");
     }
     const int64_t n = cap * world;
     st = zero_ws(c, n);
@@ -685,10 +698,7 @@ fae_status sync_merge_apply(Ctx* c, const int32_t* rows, const float* vals, int6
         FAE_CUDA(c, cudaStreamSynchronize(c->stream));
         *out_count = Ug;
     }
-    ncclResult_t ae;
-    if (ncclCommGetAsyncError(c->comm, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress)
-        return set_err(c, FAE_ERR_NCCL, std::string("nccl async: ") + ncclGetErrorString(ae));
-    return FAE_OK;
+    return coll_async_error(c, "sync");
 }
 
 }  // namespace fae
@@ -701,6 +711,6 @@ extern "C" fae_status fae_sync_hot_grads(fae_ctx* h, int32_t* rows, float* vals,
         return set_err(c, FAE_ERR_INVALID_ARG, "fae_sync_hot_grads: bad arguments");
     if (*count_host < 0 || *count_host > cap)
         return set_err(c, FAE_ERR_INVALID_ARG, "fae_sync_hot_grads: count outside [0, cap]");
-    if (c->world == 1 && !c->comm) return FAE_OK;   // identity
+    if (c->world == 1 && !has_comm(c)) return FAE_OK;   // identity
     return sync_merge_apply(c, rows, vals, *count_host, D, nullptr, 0, 0.f, rows, vals, count_host, cap);
 }

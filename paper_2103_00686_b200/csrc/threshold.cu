@@ -517,13 +517,17 @@ extern "C" fae_status fae_threshold(fae_ctx* h, const fae_tables* tabs, const ui
         for (int z = 0; z < Tn; z++) kmin[z] = large[z] ? cut_of(K, T_host[z], Tref) : 0;
         t_final = (double)K / ((double)Tref * x_pct / 100.0);
     }
-    // hot set: bitmap + rank directory
+    // hot set: bitmap + rank directory.  The ctx's previous hot set is
+    // invalid from here until every check below has passed: a
+    // failure leaves no half-rebuilt set for fae_classify / fae_extract.
     HotSet& hs = c->hs;
+    hs.valid = false;
     const int64_t words = cdiv(total, 64);
     if (hs.dir_cap < words) {
         cudaStreamSynchronize(c->stream);
         cudaFree(hs.dir);
         hs.dir = nullptr;
+        hs.dir_cap = 0;
         FAE_CUDA(c, cudaMalloc(&hs.dir, sizeof(uint4) * (words + 32)));
         hs.dir_cap = words;
     }

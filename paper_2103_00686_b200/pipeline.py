@@ -61,9 +61,13 @@ class FaePipeline:
                    budget_bytes: int = 0, small_table_bytes: int = 1 << 20,
                    want_estimate: bool = False,
                    bufs: Optional[Prepared] = None,
-                   times: Optional[dict] = None) -> Prepared:
+                   times: Optional[dict] = None, record_base: int = 0,
+                   n_records_global: Optional[int] = None) -> Prepared:
         """times: optional dict accumulating ms per call (the calls return
-        host values, so each has synchronised the stream)."""
+        host values, so each has synchronised the stream).  record_base /
+        n_records_global: this rank's shard of a sharded dataset (global id
+        of local record 0, records over all ranks), so the sample is drawn
+        from global record ids and equals the unsharded one (fae.h fae_csr)."""
         import time as _t
         dev = self.dev
         t0 = _t.perf_counter()
@@ -76,7 +80,8 @@ class FaePipeline:
                 t0 = t1
         counts = bufs.counts if bufs else torch.empty(sum(self.rows), dtype=torch.int32, device=dev)
         T, ns = fae_profile(self.ctx, self.rows, self.dim, idx, off, self.pool,
-                            n_records, x_pct, seed, counts)
+                            n_records, x_pct, seed, counts,
+                            record_base=record_base, n_records_global=n_records_global)
         lap("profile")
         th = fae_threshold(self.ctx, self.rows, self.dim, counts, T, x_pct,
                            mode=mode, t=t, budget_bytes=budget_bytes,

@@ -570,34 +570,57 @@ def test_scatter_hot_swap_sync(dev, host):
     assert np.array_equal(Wm.cpu().numpy(), ref)
 
 
-def test_mixed_hot_cold_schedule(dev):
+ALI_SMALL = gen.Config("ali-small", gen.ALIBABA_ROWS, 16, 128, 0, 20, 100, records=20_000, t=1e-7)
+
+
+@pytest.mark.parametrize("cfgname,R,t,small", [("tiny", 10_000, 1e-2, 0), ("ali-small", 20_000, 1e-7, 1 << 20)])
+def test_mixed_hot_cold_schedule(dev, cfgname, R, t, small):
     """NEXT-1 end to end: hot batches on the replicated hot table, swap sync
     (fae_scatter_hot), cold batches on the full tables through the cold CSR in
-    global row ids (fae_pack_cold + the standalone step calls), re-extract,
-    more hot batches == the oracle's sequential SGD over the same schedule
-    (the swaps; 1e-5 / 1e-6)."""
+    global row ids (fae_pack_cold + the standalone step calls; fixed pooling
+    and explicit offsets), re-extract, more hot batches == the oracle's
+    sequential SGD over the same schedule (P:L299-302, L540: the swaps;
+    1e-5 / 1e-6)."""
     m = fae()
     from paper_2103_00686_b200.pipeline import FaePipeline
-    c = gen.CONFIGS["tiny"]
-    R, x, seed, t = 10_000, 5.0, 7, 1e-2
+    c = ALI_SMALL if cfgname == "ali-small" else gen.CONFIGS[cfgname]
+    x, seed = 5.0, 7
     ds = gen.make_dataset(c, n_records=R, seed=3)
     dd = ds.to(dev)
     Tn, D, B = c.n_tables, c.dim, c.batch
-    pipe = FaePipeline(ds.rows, D, B, 1)
-    prep = pipe.preprocess(dd.idx, None, R, x_pct=x, seed=seed, t=t, small_table_bytes=0)
+    pipe = FaePipeline(ds.rows, D, B, c.pool, max_pool=max(c.pool_hi, 1))
+    prep = pipe.preprocess(dd.idx, dd.off, R, x_pct=x, seed=seed, t=t, small_table_bytes=small)
     W0 = gen.make_weights(sum(ds.rows), D)
     Wd = W0.to(dev).clone()
     W_hot = pipe.extract(Wd, prep).clone()
     n_cold = prep.packed["n_cold"]
-    cold_idx = torch.empty(max(n_cold, 1) * Tn, dtype=torch.int32, device=dev)
-    m.fae_pack_cold(pipe.ctx, ds.rows, D, dd.idx, 1, R, prep.cold_ids, n_cold, cold_idx)
-    # oracle side
-    ref = _prep_ref(ds, x, seed, "t", t=t, small=0, dim=D)
+    assert n_cold > B, "the schedule trains two cold batches"
+    assert prep.packed["n_hot_batches"] >= 3, "the schedule trains three hot batches"
+    cold_idx = torch.empty(max(ds.n_lookups, 1), dtype=torch.int32, device=dev)
+    cold_off = torch.empty(n_cold * Tn + 1, dtype=torch.int64, device=dev) if ds.off is not None else None
+    m.fae_pack_cold(pipe.ctx, ds.rows, D, dd.idx, ds.fixed_pool, R, prep.cold_ids, n_cold, cold_idx,
+                    off=dd.off, cold_off=cold_off)
+    # oracle side: the cold CSR by its definition (base_z + local id, bag order)
+    ref = _prep_ref(ds, x, seed, "t", t=t, small=small, dim=D)
     pk, rm, H = ref["pack"], ref["remap"], ref["H"]
     assert prep.packed["n_cold"] == pk["n_cold"]
     base = np.concatenate([[0], np.cumsum(ds.rows)])
-    cold_ref = (ds.idx.numpy().reshape(R, Tn)[pk["cold_ids"]] + base[:Tn]).reshape(-1).astype(np.int32)
-    assert np.array_equal(cold_idx[:n_cold * Tn].cpu().numpy(), cold_ref)
+    idx_np = ds.idx.numpy()
+    if ds.off is None:
+        cold_ref = (idx_np.reshape(R, Tn)[pk["cold_ids"]] + base[:Tn]).reshape(-1).astype(np.int32)
+        cold_off_ref = None
+    else:
+        off_np = ds.off.numpy()
+        parts, sizes = [], []
+        for r in pk["cold_ids"]:
+            for z in range(Tn):
+                lo, hi = off_np[r * Tn + z], off_np[r * Tn + z + 1]
+                parts.append(idx_np[lo:hi] + base[z])
+                sizes.append(hi - lo)
+        cold_ref = np.concatenate(parts).astype(np.int32)
+        cold_off_ref = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        assert np.array_equal(cold_off.cpu().numpy(), cold_off_ref)
+    assert np.array_equal(cold_idx[:len(cold_ref)].cpu().numpy(), cold_ref)
     Wr_full = W0.numpy().copy()
     Wr_hot = oracle.extract(Wr_full, rm, H)
     lr = 0.05
@@ -613,24 +636,48 @@ def test_mixed_hot_cold_schedule(dev):
                 m.fae_scatter_hot(pipe.ctx, W_hot, Wd)
                 Wr_full = oracle.scatter_hot(Wr_full, Wr_hot, rm)
             else:
-                pipe.extract(Wd, prep)   # refresh the replica from the master
-                W_hot.copy_(pipe.extract(Wd, prep))
+                W_hot.copy_(pipe.extract(Wd, prep))   # refresh the replica from the master
                 Wr_hot = oracle.extract(Wr_full, rm, H)
             prev = kind
         if kind == "hot":
-            idx, _, nb_ = pipe.batch_args(prep, i)
+            idx, off, nb_ = pipe.batch_args(prep, i)
             pipe.step(W_hot, prep, i, Y[:nb_], dY[:nb_].to(dev), lr)
-            bi = pk["hot_idx"][i * B * Tn: i * B * Tn + nb_]
-            Wr_hot, _ = oracle.emb_bwd_sgd(Wr_hot, bi, None, 1, nb_, dY[:nb_], lr)
+            r0, r1 = i * B, min((i + 1) * B, pk["n_hot"])
+            if ds.off is None:
+                bi, boff, P = pk["hot_idx"][r0 * Tn: r1 * Tn], None, 1
+            else:
+                bi, boff, P = pk["hot_idx"], pk["hot_off"][r0 * Tn: r1 * Tn + 1], 0
+            Wr_hot, _ = oracle.emb_bwd_sgd(Wr_hot, bi, boff, P, nb_, dY[:nb_], lr)
         else:
             r0, r1 = i * B, min((i + 1) * B, n_cold)
             nb_ = (r1 - r0) * Tn
-            ci = cold_idx[r0 * Tn: r1 * Tn]
-            m.fae_emb_fwd(pipe.ctx, Wd, ci, None, 1, nb_, Y[:nb_])
-            m.fae_emb_bwd_update(pipe.ctx, Wd, ci, None, 1, nb_, dY[:nb_].to(dev), lr)
-            Wr_full, _ = oracle.emb_bwd_sgd(Wr_full, cold_ref[r0 * Tn: r1 * Tn], None, 1, nb_, dY[:nb_], lr)
+            if ds.off is None:
+                ci, coff, P = cold_idx[r0 * Tn: r1 * Tn], None, 1
+                bi, boff = cold_ref[r0 * Tn: r1 * Tn], None
+            else:
+                ci, coff, P = cold_idx, cold_off[r0 * Tn: r1 * Tn + 1], 0
+                bi, boff = cold_ref, cold_off_ref[r0 * Tn: r1 * Tn + 1]
+            m.fae_emb_fwd(pipe.ctx, Wd, ci, coff, P, nb_, Y[:nb_])
+            m.fae_emb_bwd_update(pipe.ctx, Wd, ci, coff, P, nb_, dY[:nb_].to(dev), lr)
+            Wr_full, _ = oracle.emb_bwd_sgd(Wr_full, bi, boff, P, nb_, dY[:nb_], lr)
     m.fae_scatter_hot(pipe.ctx, W_hot, Wd)
     Wr_full = oracle.scatter_hot(Wr_full, Wr_hot, rm)
     pipe.ctx.check()
     ok, worst = close(Wd.cpu().numpy(), Wr_full)
     assert ok, worst
+
+
+def test_bwd_oversized_offsets_batch_latches_capacity(dev):
+    """a multi-hot batch with more lookups than max_batch_lookups
+    must not write past the workspace: CAPACITY is latched and W untouched."""
+    m = fae()
+    ctx = mkctx([1000], 16, 256, 64)
+    W = gen.make_weights(1000, 16).to(dev)
+    W0 = W.clone()
+    off = torch.arange(0, 65 * 10, 10, dtype=torch.int64, device=dev)    # 64 bags x 10 = 640 > 256
+    idx = torch.randint(0, 1000, (640,), dtype=torch.int32, device=dev)
+    m.fae_emb_bwd_update(ctx, W, idx, off, 0, 64, torch.ones(64, 16, device=dev), 0.1)
+    with pytest.raises(m.FaeError) as e:
+        ctx.check()
+    assert e.value.name == "CAPACITY"
+    assert torch.equal(W, W0)
