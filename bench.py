@@ -8,7 +8,7 @@ batch of synthetic input = this rank's dataset shard:
   fae_emb_bwd_update (+ hot-grad sync over NCCL when N > 1).
 value = hot lookups trained by all ranks / max-over-ranks step time.
 
-Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config kaggle]
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config terabyte]
        python bench.py --impl reference ...   (CPU oracle arm)
 """
 from __future__ import annotations
@@ -117,14 +117,39 @@ def ncu_traffic(kernel, workload):
 
 
 def fwd_bytes(L, S, D, explicit_off):
-    """a8 per batch: idx (4L) [+ offsets 8(S+1)] + row gathers 4DL + Y 4DS."""
-    return 4 * L + (8 * (S + 1) if explicit_off else 0) + 4 * D * L + 4 * D * S
+    """SURVEY §8(d) algorithmic bytes of a8 per batch: idx 4L [+ offsets
+    4(S+1)] + row gathers 4DL + Y write 4DS."""
+    return 4 * L + (4 * (S + 1) if explicit_off else 0) + 4 * D * L + 4 * D * S
 
 
-def red_bytes(L, S, U, D):
-    """a9+a10 per batch with the grouping precomputed: sorted bag ids (4L),
-    32-byte segment records (32U), dY rows 4DL, W rows read+write 8DU."""
+def bwd_bytes(L, S, U, D, explicit_off):
+    """SURVEY §8(d) algorithmic bytes of a9+a10 per batch: idx 4L [+ offsets
+    4(S+1)] + dY read once 4DS + one write + read of the 8-byte (key, pos)
+    sort pairs 16L + W rows read + write 8DU."""
+    return 4 * L + (4 * (S + 1) if explicit_off else 0) + 4 * D * S + 16 * L + 8 * D * U
+
+
+def design_red_bytes(L, S, U, D):
+    """What this design's reduce kernel itself must move (the sort is hoisted
+    into the grouping): sorted bag ids 4L, 32-byte segment records 32U, a dY
+    row per lookup 4DL, W rows read + write 8DU (reported beside the §8(d)
+    figure, never used for frac)."""
     return 4 * L + 32 * U + 4 * D * L + 8 * D * U
+
+
+def host_info():
+    """lscpu-equivalent facts of this host (cpu_baseline's `cores` context)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    aff = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(), "usable_cpus": aff}
 
 
 def pipe_stats(pipe):
@@ -220,15 +245,19 @@ def run_fae(args):
     fae.fae_set_kernel_timing(pipe.ctx, 0 if args.no_ktiming else 1)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    sev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     wall0 = time.perf_counter()
     t0.record()
+    sev[0].record()
     hot_lookups = 0
     prep = None
-    for _ in range(args.steps):
+    for k in range(args.steps):
         n, prep = one_step()
+        sev[k + 1].record()
         hot_lookups += n
     t1.record()
     torch.cuda.synchronize()
+    per_step_ms = [sev[k].elapsed_time(sev[k + 1]) for k in range(args.steps)]
     wall = time.perf_counter() - wall0
     ck = clocks.stop()
     pipe.ctx.check()
@@ -260,14 +289,18 @@ def run_fae(args):
         gi = pipe_stats(pipe)
         U_b = gi["segs_per_batch"]
         F_b = gi["free_segments"] / max(gi["n_batches"], 1)
+        expl = cfg.pool == 0
         if fused or persist:   # backward+SGD of one batch + forward of the next
-            kb = red_bytes(L_b, S_b, U_b, D) + 4 * L_b + 4 * D * S_b + (16 + 4 * D) * F_b
+            kb = bwd_bytes(L_b, S_b, U_b, D, expl) + fwd_bytes(L_b, S_b, D, expl)
+            kdesign = design_red_bytes(L_b, S_b, U_b, D) + 4 * L_b + 4 * D * S_b + (16 + 4 * D) * F_b
             if persist:        # one launch trains every batch of the call
                 kb *= kt["persist_batches"] / max(kn, 1)
+                kdesign *= kt["persist_batches"] / max(kn, 1)
         elif kname == "fwd":
-            kb = fwd_bytes(L_b, S_b, D, cfg.pool == 0)
+            kb = kdesign = fwd_bytes(L_b, S_b, D, expl)
         else:
-            kb = red_bytes(L_b, S_b, U_b, D)
+            kb = bwd_bytes(L_b, S_b, U_b, D, expl)
+            kdesign = design_red_bytes(L_b, S_b, U_b, D)
         achieved = kb / avg_s / 1e9 if avg_s > 0 else 0.0
         kname_full = ("k_train_persist" if persist else "k_grp_fused_pdl" if fused else
                       {"fwd": "k_grp_fwd_pdl", "reduce": "k_grp_reduce_pdl"}[kname])
@@ -275,6 +308,7 @@ def run_fae(args):
             "metric": METRIC, "value": lookups_all / (ms_max / 1e3), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "ms_per_step_median": statistics.median(per_step_ms), "per_step_ms": per_step_ms,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded Zipf s=1.1, Feistel-scattered rows; gen/)",
             "config": {"workload": f"{cfg.name}-shaped", "records_per_gpu": R,
@@ -298,7 +332,13 @@ def run_fae(args):
                          "peak": peak, "peak_kind": kind, "unit": "GB/s",
                          "frac": achieved / peak,
                          "traffic": ncu_traffic(kname_full, f"{cfg.name}-shaped"),
-                         "bytes_per_launch": kb, "avg_launch_us": avg_s * 1e6,
+                         "bytes_per_launch": kb,
+                         "bytes_formula": ("SURVEY §8(d): fwd 4L+4DL+4DS [+4(S+1)], bwd+update "
+                                           "4L+4DS+16L+8DU [+4(S+1)]; per-batch L, S, U measured"),
+                         "per_batch": {"L": L_b, "S": S_b, "U": U_b, "F": F_b},
+                         "design_bytes_per_launch": kdesign,
+                         "design_frac": (kdesign / avg_s / 1e9) / peak if avg_s > 0 else 0.0,
+                         "avg_launch_us": avg_s * 1e6,
                          "kernels_us": {k: (kt[k][0] / max(kt[k][1], 1)) * 1e3 for k in ("fwd", "reduce")},
                          "launches_timed": kn,
                          **({"batches_per_launch": kt["persist_batches"] / max(kn, 1),
@@ -423,10 +463,14 @@ def run_e2e(args, ctxs):
 # ----------------------------------------------------------------------------
 # CPU oracle arm (cpu_baseline and --impl reference)
 # ----------------------------------------------------------------------------
-def oracle_step(cfg, R_s, max_batches, seed, lr, ds=None, W=None):
+def oracle_step(cfg, R_s, max_batches, seed, lr, ds):
     """The oracle, as it stands, over a bounded sample of the workload:
-    the full a1-a10 pipeline on the first R_s records, training at most
-    max_batches hot batches.  Returns (hot lookups trained, seconds)."""
+    the full a1-a10 pipeline on the first R_s records (sample, loggers,
+    threshold, remap, classify, pack, then at most max_batches hot batches of
+    fwd + bwd + SGD).  The hot table's rows are drawn by counter
+    (gen.make_weight_rows: the same bits as extracting them from the full
+    table, which at Terabyte shape is 48 GB).  Returns (hot lookups trained,
+    seconds)."""
     import numpy as np
     import oracle
     t0 = time.perf_counter()
@@ -443,9 +487,12 @@ def oracle_step(cfg, R_s, max_batches, seed, lr, ds=None, W=None):
     rm, base, H = oracle.remap(ds.rows, hot)
     flag = oracle.classify(ds.rows, ds.idx, ds.off, ds.fixed_pool, R_s, rm)
     pk = oracle.pack(ds.rows, ds.idx, ds.off, ds.fixed_pool, R_s, rm, flag)
-    W_hot = oracle.extract(W, rm, H)
     B, Tn = cfg.batch, cfg.n_tables
     nb = min(max_batches, -(-pk["n_hot"] // B))
+    t_gen = time.perf_counter()                  # input generation: not timed
+    W_hot = gen.make_weight_rows(torch.from_numpy(np.nonzero(rm >= 0)[0]), cfg.dim).numpy()
+    dys = [gen.make_dy(B * Tn, cfg.dim, seed=1000 + i).numpy() for i in range(max(1, min(nb, 8)))]
+    t_gen = time.perf_counter() - t_gen
     slot = np.full(max(H, 1), -1, np.int32)
     done = 0
     for i in range(nb):
@@ -459,27 +506,52 @@ def oracle_step(cfg, R_s, max_batches, seed, lr, ds=None, W=None):
             P = 0
             off = pk["hot_off"][r0 * Tn: r1 * Tn + 1]
             bi = pk["hot_idx"]
-        dY = gen.make_dy(n_bags, cfg.dim, seed=1000 + i).numpy()
+        dY = dys[i % len(dys)][:n_bags]
         oracle.emb_fwd(W_hot, bi, off, P, n_bags)
         W_hot, _ = oracle.emb_bwd_sgd(W_hot, bi, off, P, n_bags, dY, lr, slot)
-        done += (r1 - r0) * Tn * (P if P else 0) if off is None else int(off[-1] - off[0])
-    return done, time.perf_counter() - t0
+        done += (r1 - r0) * Tn * P if off is None else int(off[-1] - off[0])
+    return done, time.perf_counter() - t0 - t_gen
+
+
+CPU_DEFAULTS = {   # records / hot batches of the bounded oracle sample (~10-30 s)
+    "tiny": (10_000, 1000), "kaggle": (4_000_000, 400), "terabyte": (1_000_000, 40),
+    "alibaba": (1_000_000, 200)}
 
 
 def oracle_sample_setup(cfg, R_s):
-    ds = gen.make_dataset(cfg, n_records=R_s)
-    W = gen.make_weights(sum(cfg.rows), cfg.dim).numpy()
-    return ds, W
+    """The first R_s records of the workload (drawn on the GPU when there is
+    one — the generators give the same bits on either device)."""
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    ds = gen.make_dataset(cfg, n_records=R_s, device=dev)
+    return ds.to("cpu")
+
+
+def cpu_runs(cfg, args, variants=("serial", "omp")):
+    import oracle
+    R_s = min(args.cpu_records or CPU_DEFAULTS[cfg.name][0], cfg.records)
+    nbat = args.cpu_batches or CPU_DEFAULTS[cfg.name][1]
+    ds = oracle_sample_setup(cfg, R_s)
+    out = {}
+    for v in variants:
+        oracle.use_omp(v == "omp")
+        try:
+            n, dt = oracle_step(cfg, R_s, nbat, args.seed, args.lr, ds)
+        finally:
+            oracle.use_omp(False)
+        out[v] = (n, dt, oracle.omp_threads() if v == "omp" else 1)
+    return R_s, nbat, out
 
 
 def cpu_baseline(cfg, args):
-    R_s = min(args.cpu_records, cfg.records)
-    ds, W = oracle_sample_setup(cfg, R_s)
-    n, dt = oracle_step(cfg, R_s, args.cpu_batches, args.seed, args.lr, ds, W)
-    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"full a1-a10 oracle pipeline on the first {R_s} records of the "
-                      f"{cfg.name}-shaped workload, <= {args.cpu_batches} hot batches trained "
-                      f"({n} hot lookups in {dt:.1f} s, single-threaded C, fp64)"}
+    R_s, nbat, runs = cpu_runs(cfg, args)
+    n, dt, cores = runs["omp"]
+    n1, dt1, _ = runs["serial"]
+    return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"full a1-a10 oracle pipeline (fp64 C, OpenMP build, {cores} threads) on the first "
+                      f"{R_s} records of the {cfg.name}-shaped workload, <= {nbat} hot batches trained "
+                      f"({n} hot lookups in {dt:.1f} s)",
+            "single_thread": {"value": n1 / dt1, "cores": 1, "seconds": dt1},
+            "host": host_info()}
 
 
 def run_reference(args):
@@ -487,28 +559,100 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
+    import oracle
     cfg = gen.CONFIGS[args.config]
-    # each step a bounded sample (about 2 s of oracle work) so that the whole
-    # --steps K --warmup W run ends within a few minutes
+    # each step a bounded sample so that the whole --steps K --warmup W run
+    # ends within a few minutes
     R_s = min(args.ref_records, cfg.records)
-    ds, W = oracle_sample_setup(cfg, R_s)
-    for _ in range(args.warmup):
-        oracle_step(cfg, R_s, args.ref_batches, args.seed, args.lr, ds, W)
-    n_tot, t_tot = 0, 0.0
-    for _ in range(args.steps):
-        n, dt = oracle_step(cfg, R_s, args.ref_batches, args.seed, args.lr, ds, W)
-        n_tot += n
-        t_tot += dt
+    ds = oracle_sample_setup(cfg, R_s)
+    oracle.use_omp(True)
+    try:
+        for _ in range(args.warmup):
+            oracle_step(cfg, R_s, args.ref_batches, args.seed, args.lr, ds)
+        n_tot, t_tot = 0, 0.0
+        for _ in range(args.steps):
+            n, dt = oracle_step(cfg, R_s, args.ref_batches, args.seed, args.lr, ds)
+            n_tot += n
+            t_tot += dt
+    finally:
+        oracle.use_omp(False)
+    cores = oracle.omp_threads()
     v = n_tot / t_tot
     samp = (f"full a1-a10 oracle pipeline on the first {R_s} records, <= {args.ref_batches} "
-            f"hot batches per step, single-threaded C fp64")
+            f"hot batches per step, fp64 C (OpenMP build, {cores} threads)")
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_tot * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Zipf s=1.1; gen/)",
             "config": {"workload": f"{cfg.name}-shaped", "records_per_step": R_s},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": samp},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": samp,
+                             "host": host_info()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def run_sweep(args):
+    """Threshold sweep (BASELINE.json configs[4]; P:L331-342
+    fig:hotinputembsize): BUDGET_EXACT with L = f * sum N_z * D * 4
+    for hot-row fractions f, on one GPU.  Per point: the hot set actually
+    chosen (the 5% sample bounds it: a row never sampled is never hot, R25),
+    the hot-input share, the per-batch distinct rows U, the training loop's
+    lookups/s, and the a11 exchange each GPU would receive per step at
+    G = 2 / 4 / 8 (padded all-gather: (G-1) * U * (4 + 4D) bytes) with its
+    NVLink lower bound at 900 GB/s.  Prints one JSON line."""
+    import paper_2103_00686_b200 as fae
+    from paper_2103_00686_b200.pipeline import FaePipeline
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    out = []
+    for name in args.sweep_configs.split(","):
+        cfg = gen.CONFIGS[name]
+        R = args.records or cfg.records
+        Tn, D, B = cfg.n_tables, cfg.dim, cfg.batch
+        ds = gen.make_dataset(cfg, n_records=R, device=dev)
+        W = gen.make_weights(sum(cfg.rows), D, device=dev)
+        S = B * Tn
+        n_dy = max(1, math.ceil((args.dy_pool_mb << 20) / (S * D * 4)))
+        dY = gen.make_dy(n_dy * S, D, device=dev).view(n_dy, S, D)
+        Y = torch.empty(S, D, device=dev)
+        pipe = FaePipeline(cfg.rows, D, B, cfg.pool, max_pool=max(cfg.pool_hi, 1), device=0)
+        rows_total = sum(cfg.rows)
+        for f in [float(v) for v in args.sweep_fracs.split(",")]:
+            budget = int(f / 100.0 * rows_total * D * 4)
+            t0 = time.perf_counter()
+            prep = pipe.preprocess(ds.idx, ds.off, R, x_pct=5.0, seed=args.seed, mode=fae.BUDGET_EXACT,
+                                   budget_bytes=budget, small_table_bytes=cfg.small_bytes)
+            pipe.group(prep)
+            W_hot = pipe.extract(W, prep)
+            torch.cuda.synchronize()
+            pre_ms = (time.perf_counter() - t0) * 1e3
+            nb = prep.packed["n_hot_batches"]
+            pipe.train(W_hot, 0, nb, dY, Y, args.lr)            # warm-up (graph capture)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            pipe.train(W_hot, 0, nb, dY, Y, args.lr)
+            e1.record()
+            torch.cuda.synchronize()
+            pipe.ctx.check()
+            tr_ms = e0.elapsed_time(e1)
+            gi = fae.fae_group_info(pipe.ctx)
+            U = gi["segments"] / max(gi["n_batches"], 1)
+            H = prep.thresh["H_total"]
+            sync = {str(G): {"bytes_per_gpu_per_step": (G - 1) * U * (4 + 4 * D),
+                             "nvlink_floor_us": (G - 1) * U * (4 + 4 * D) / 900e9 * 1e6} for G in (2, 4, 8)}
+            out.append({"workload": f"{name}-shaped", "f_pct": f, "budget_bytes": budget,
+                        "hot_rows": H, "hot_rows_pct": 100.0 * H / rows_total,
+                        "budget_slack": prep.thresh["budget_slack"], "K": prep.thresh["K"],
+                        "hot_records_pct": 100.0 * prep.packed["n_hot"] / R,
+                        "hot_lookups_pct": 100.0 * prep.packed["n_hot_lookups"] / max(ds.n_lookups, 1),
+                        "hot_batches": nb, "U_per_batch": U,
+                        "preprocess_ms": pre_ms, "train_ms": tr_ms,
+                        "train_lookups_per_s": prep.packed["n_hot_lookups"] / (tr_ms / 1e3) if tr_ms else None,
+                        "us_per_batch": tr_ms * 1e3 / max(nb, 1), "sync": sync})
+            print(json.dumps(out[-1]), file=sys.stderr, flush=True)
+        del ds, W, dY, pipe
+        torch.cuda.empty_cache()
+    print(json.dumps({"sweep": out, "records_per_gpu": {n: args.records or gen.CONFIGS[n].records
+                                                        for n in args.sweep_configs.split(",")}}), flush=True)
 
 
 def main():
@@ -516,21 +660,28 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="kaggle", choices=sorted(gen.CONFIGS))
+    # default: the largest single-GPU configuration (Terabyte-shaped, RMC3)
+    ap.add_argument("--config", default="terabyte", choices=sorted(gen.CONFIGS))
     ap.add_argument("--records", type=int, default=0, help="records per GPU (default: config)")
     ap.add_argument("--batch", type=int, default=0, help="hot mini-batch size B (default: config; batch sweeps)")
     ap.add_argument("--impl", default="fae", choices=["fae", "reference"])
     ap.add_argument("--lr", type=float, default=0.01)
     ap.add_argument("--seed", type=int, default=1)
-    ap.add_argument("--cpu-records", type=int, default=12_000_000)
-    ap.add_argument("--cpu-batches", type=int, default=1024)
+    ap.add_argument("--cpu-records", type=int, default=0, help="cpu_baseline sample records (default per config)")
+    ap.add_argument("--cpu-batches", type=int, default=0, help="cpu_baseline hot batches (default per config)")
     ap.add_argument("--ref-records", type=int, default=1_000_000, help="--impl reference: records per step")
-    ap.add_argument("--ref-batches", type=int, default=32, help="--impl reference: hot batches per step")
+    ap.add_argument("--ref-batches", type=int, default=16, help="--impl reference: hot batches per step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ktiming", action="store_true", help="no in-kernel stamps (overhead check; no roofline)")
     ap.add_argument("--dy-pool-mb", type=int, default=256, help="upstream-gradient pool (> L2 by default)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="threshold sweep (one JSON line; not the driver's bench)")
+    ap.add_argument("--sweep-configs", default="kaggle,terabyte")
+    ap.add_argument("--sweep-fracs", default="1,2,5,10,20")
     args = ap.parse_args()
+    if args.sweep:
+        run_sweep(args)
+        return
     if args.impl == "reference":
         r = run_reference(args)
         if r is not None:

@@ -101,8 +101,11 @@ CONFIGS = {
     "terabyte": Config("terabyte", TERABYTE_ROWS, 64, 4096, 1,
                        records=80_000_000, t=1e-9,
                        budget_bytes=180 * 10**9),
+    # L = 512 MB is slack for the 330 MB Alibaba-shaped tables: every
+    # row seen in the 5 % sample is hot (the sample-bounded maximum, 16 % of
+    # the records; profiles/r2/sweep_threshold.md)
     "alibaba": Config("alibaba", ALIBABA_ROWS, 16, 1024, 0, 20, 100,
-                      records=10_000_000, t=1e-7),
+                      records=10_000_000, t=1e-7, budget_bytes=512 << 20),
 }
 
 
@@ -279,6 +282,16 @@ def make_weights(n_rows: int, dim: int, seed: int = BASE_SEED + 2000,
         ctr = torch.arange(c0, c1, device=dev, dtype=torch.int64)
         W[c0:c1] = (lo + (hi - lo) * uniform01(seed, ctr)).float()
     return W.view(n_rows, dim)
+
+
+def make_weight_rows(rows: torch.Tensor, dim: int, seed: int = BASE_SEED + 2000,
+                     lo=-0.05, hi=0.05) -> torch.Tensor:
+    """Rows `rows` (int64 global row ids) of make_weights(n, dim, seed), bit
+    for bit, without drawing the others (a 48 GB Terabyte-shaped table's hot
+    rows on the host)."""
+    rows = torch.as_tensor(rows, dtype=torch.int64)
+    ctr = (rows.unsqueeze(1) * dim + torch.arange(dim, dtype=torch.int64, device=rows.device)).reshape(-1)
+    return (lo + (hi - lo) * uniform01(seed, ctr)).float().view(-1, dim)
 
 
 def make_dy(n_bags: int, dim: int, seed: int = BASE_SEED + 1000,

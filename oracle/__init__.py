@@ -19,26 +19,48 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "fae_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle_fae.so")
+_LIB_OMP = os.path.join(_HERE, "liboracle_fae_omp.so")   # the same file, -fopenmp
 _lib = None
+_lib_omp = None
+_use_omp = False
 
 OK, INVALID_ARG, BUDGET_INFEASIBLE, INDEX_RANGE = 0, 1, 3, 4
 
 
 def build(force: bool = False) -> str:
-    if force or not os.path.exists(_LIB) or \
-            os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(
-            ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fPIC", "-shared",
-             "-o", _LIB, _SRC, "-lm"])
+    for out, extra in ((_LIB, []), (_LIB_OMP, ["-fopenmp"])):
+        if force or not os.path.exists(out) or \
+                os.path.getmtime(out) < os.path.getmtime(_SRC):
+            subprocess.check_call(
+                ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fPIC", "-shared", *extra,
+                 "-o", out, _SRC, "-lm"])
     return _LIB
 
 
+def use_omp(flag: bool) -> None:
+    """Route the calls below to the all-cores build (-fopenmp; bit-identical
+    results, tests/test_oracle.py) or back to the serial one."""
+    global _use_omp
+    _use_omp = bool(flag)
+
+
+def omp_threads() -> int:
+    """Threads the all-cores build uses (OMP_NUM_THREADS or all cores)."""
+    n = os.environ.get("OMP_NUM_THREADS")
+    return int(n) if n else (len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count())
+
+
 def lib():
-    global _lib
+    global _lib, _lib_omp
     if _lib is None:
         build()
         _lib = ctypes.CDLL(_LIB)
         _declare(_lib)
+    if _use_omp:
+        if _lib_omp is None:
+            _lib_omp = ctypes.CDLL(_LIB_OMP)
+            _declare(_lib_omp)
+        return _lib_omp
     return _lib
 
 

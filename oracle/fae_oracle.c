@@ -22,11 +22,28 @@
  * 302.5, brute force on tiny inputs, closed forms (A.W and A^T.dY
  * as sparse-dense products, p^B), invariants (partition, purity, conservation,
  * rank remap, monotonicity, untouched rows).  Parity unpinned: none.
+ *
+ * All-cores variant (the cpu_baseline's multi-thread figure):
+ * the same file compiled with -fopenmp.  The pragmas only split loops whose
+ * iterations are independent (keys, per-record classification, per-bag
+ * forward) or integer counts (atomic increments); the backward splits by row
+ * ownership (row r belongs to thread r mod nthreads, which scans the lookups
+ * in ascending p), so every fp64 sum keeps its serial order and the results
+ * are bit-identical to the serial build (tested).  Without -fopenmp the
+ * pragmas are ignored.
  */
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 #include <math.h>
+#ifdef _OPENMP
+#include <omp.h>
+static int or_nthreads(void) { return omp_get_num_threads(); }
+static int or_thread(void) { return omp_get_thread_num(); }
+#else
+static int or_nthreads(void) { return 1; }
+static int or_thread(void) { return 0; }
+#endif
 
 /* status codes, same numeric meaning as the product ABI (documented, not shared) */
 #define OR_OK 0
@@ -83,6 +100,7 @@ int64_t or_sample(int64_t R, double x_pct, uint64_t seed, int64_t* out_ids)
     if (k == 0) return 0;
     or_pair* v = (or_pair*)malloc(sizeof(or_pair) * (size_t)R);
     uint8_t* chosen = (uint8_t*)calloc((size_t)R, 1);
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < R; i++) { v[i].key = or_key(seed, (uint64_t)i); v[i].i = i; }
     qsort(v, (size_t)R, sizeof(or_pair), cmp_pair);
     for (int64_t j = 0; j < k; j++) chosen[v[j].i] = 1;
@@ -121,12 +139,14 @@ int or_histogram(int32_t n_tables, const int64_t* rows, const int32_t* idx,
     memset(counts, 0, sizeof(uint32_t) * (size_t)total_rows);
     int st = OR_OK;
     for (int32_t z = 0; z < n_tables; z++) T[z] = 0;
+#pragma omp parallel for schedule(static) reduction(+ : T[:n_tables])
     for (int64_t r = 0; r < n_records; r++)
         for (int32_t z = 0; z < n_tables; z++) {
             int64_t lo, hi;
             bag_range(off, fixed_pool, n_tables, r, z, &lo, &hi);
             T[z] += hi - lo;
         }
+#pragma omp parallel for schedule(static) reduction(max : st)
     for (int64_t s = 0; s < n_sampled; s++) {
         int64_t r = sampled[s];
         for (int32_t z = 0; z < n_tables; z++) {
@@ -135,6 +155,7 @@ int or_histogram(int32_t n_tables, const int64_t* rows, const int32_t* idx,
             for (int64_t p = lo; p < hi; p++) {
                 int32_t j = idx[p];
                 if (j < 0 || j >= rows[z]) { st = OR_INDEX_RANGE; continue; }
+#pragma omp atomic
                 counts[base[z] + j] += 1;
             }
         }
@@ -177,8 +198,10 @@ void or_tag_rows(int32_t n_tables, const int64_t* rows, int32_t dim,
     int64_t g = 0;
     for (int32_t z = 0; z < n_tables; z++) {
         int small = is_small(rows[z], dim, small_bytes);
-        for (int64_t j = 0; j < rows[z]; j++, g++)
-            hot[g] = small ? 1 : ((int64_t)counts[g] >= kmin[z] ? 1 : 0);
+#pragma omp parallel for schedule(static)
+        for (int64_t j = 0; j < rows[z]; j++)
+            hot[g + j] = small ? 1 : ((int64_t)counts[g + j] >= kmin[z] ? 1 : 0);
+        g += rows[z];
     }
 }
 
@@ -236,16 +259,22 @@ int or_budget_exact(int32_t n_tables, const int64_t* rows, int32_t dim,
 {
     int64_t small_total = 0, Tref = 0, g0 = 0;
     uint32_t** sorted = (uint32_t**)calloc((size_t)n_tables, sizeof(uint32_t*));
+    int64_t* start = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_tables + 1));
     for (int32_t z = 0; z < n_tables; z++) {
+        start[z] = g0;
         if (is_small(rows[z], dim, small_bytes)) small_total += rows[z] * (int64_t)dim * 4;
-        else {
-            if (T[z] > Tref) Tref = T[z];
-            sorted[z] = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)rows[z]);
-            memcpy(sorted[z], counts + g0, sizeof(uint32_t) * (size_t)rows[z]);
-            qsort(sorted[z], (size_t)rows[z], sizeof(uint32_t), cmp_u32_desc);
-        }
+        else if (T[z] > Tref) Tref = T[z];
         g0 += rows[z];
     }
+    /* each large table's loggers sorted descending (independent per table) */
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int32_t z = 0; z < n_tables; z++) {
+        if (is_small(rows[z], dim, small_bytes)) continue;
+        sorted[z] = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)rows[z]);
+        memcpy(sorted[z], counts + start[z], sizeof(uint32_t) * (size_t)rows[z]);
+        qsort(sorted[z], (size_t)rows[z], sizeof(uint32_t), cmp_u32_desc);
+    }
+    free(start);
     *slack = 0;
     if (small_total > budget_bytes) {
         for (int32_t z = 0; z < n_tables; z++) free(sorted[z]);
@@ -484,6 +513,7 @@ void or_classify(int32_t n_tables, const int64_t* rows, const int32_t* idx,
     int64_t* base = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_tables + 1));
     int64_t tot = 0;
     for (int32_t z = 0; z < n_tables; z++) { base[z] = tot; tot += rows[z]; }
+#pragma omp parallel for schedule(static)
     for (int64_t r = 0; r < n_records; r++) {
         int hotr = 1;
         for (int32_t z = 0; z < n_tables; z++) {
@@ -567,20 +597,24 @@ void or_scatter_hot(int64_t total_rows, int32_t dim, const float* W_hot,
 int or_emb_fwd(const float* W_hot, int64_t H, int32_t dim, const int32_t* idx,
                const int64_t* off, int32_t fixed_pool, int64_t n_bags, float* Y)
 {
-    double* acc = (double*)malloc(sizeof(double) * (size_t)dim);
     int st = OR_OK;
-    for (int64_t b = 0; b < n_bags; b++) {
-        int64_t lo = off ? off[b] : b * fixed_pool;
-        int64_t hi = off ? off[b + 1] : (b + 1) * fixed_pool;
-        for (int32_t d = 0; d < dim; d++) acc[d] = 0.0;
-        for (int64_t p = lo; p < hi; p++) {
-            int32_t r = idx[p];
-            if (r < 0 || r >= H) { st = OR_INDEX_RANGE; continue; }
-            for (int32_t d = 0; d < dim; d++) acc[d] += (double)W_hot[(int64_t)r * dim + d];
+#pragma omp parallel reduction(max : st)
+    {
+        double* acc = (double*)malloc(sizeof(double) * (size_t)dim);
+#pragma omp for schedule(static)
+        for (int64_t b = 0; b < n_bags; b++) {
+            int64_t lo = off ? off[b] : b * fixed_pool;
+            int64_t hi = off ? off[b + 1] : (b + 1) * fixed_pool;
+            for (int32_t d = 0; d < dim; d++) acc[d] = 0.0;
+            for (int64_t p = lo; p < hi; p++) {
+                int32_t r = idx[p];
+                if (r < 0 || r >= H) { st = OR_INDEX_RANGE; continue; }
+                for (int32_t d = 0; d < dim; d++) acc[d] += (double)W_hot[(int64_t)r * dim + d];
+            }
+            for (int32_t d = 0; d < dim; d++) Y[b * dim + d] = (float)acc[d];
         }
-        for (int32_t d = 0; d < dim; d++) Y[b * dim + d] = (float)acc[d];
+        free(acc);
     }
-    free(acc);
     return st;
 }
 
@@ -603,6 +637,7 @@ int or_emb_bwd_sgd(float* W_hot, int64_t H, int32_t dim, const int32_t* idx,
     double* G = (double*)malloc(sizeof(double) * (size_t)(L > 0 ? L : 1) * (size_t)dim);
     int64_t U = 0;
     int st = OR_OK;
+    /* touched rows, in first-touch order (integer bookkeeping) */
     for (int64_t b = 0; b < n_bags; b++) {
         int64_t lo = off ? off[b] : b * fixed_pool;
         int64_t hi = off ? off[b + 1] : (b + 1) * fixed_pool;
@@ -615,11 +650,26 @@ int or_emb_bwd_sgd(float* W_hot, int64_t H, int32_t dim, const int32_t* idx,
                 for (int32_t d = 0; d < dim; d++) G[U * dim + d] = 0.0;
                 U++;
             }
-            double* g = G + (int64_t)slot[r] * dim;
-            for (int32_t d = 0; d < dim; d++) g[d] += (double)dY[b * dim + d];
+        }
+    }
+    /* G[r] += dY[bag(p)] for p ascending; with OpenMP row r is summed by
+     * thread r mod nthreads only, in the same ascending-p order */
+#pragma omp parallel
+    {
+        const int nt = or_nthreads(), me = or_thread();
+        for (int64_t b = 0; b < n_bags; b++) {
+            int64_t lo = off ? off[b] : b * fixed_pool;
+            int64_t hi = off ? off[b + 1] : (b + 1) * fixed_pool;
+            for (int64_t p = lo; p < hi; p++) {
+                int32_t r = idx[p];
+                if (r < 0 || r >= H || r % nt != me) continue;
+                double* g = G + (int64_t)slot[r] * dim;
+                for (int32_t d = 0; d < dim; d++) g[d] += (double)dY[b * dim + d];
+            }
         }
     }
     (void)p0;
+#pragma omp parallel for schedule(static)
     for (int64_t u = 0; u < U; u++) {
         int32_t r = rowlist[u];
         for (int32_t d = 0; d < dim; d++) {

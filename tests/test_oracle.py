@@ -654,3 +654,47 @@ def test_scatter_hot_inverse_of_extract():
     assert np.array_equal(W2[g_hot], W_hot[rm[g_hot]])           # brute force
     cold = rm < 0
     assert np.array_equal(W2[cold], W[cold])
+
+
+# ----------------------------------------------------------------------------
+# the all-cores build (cpu_baseline's multi-thread figure) == the serial build
+# ----------------------------------------------------------------------------
+def test_openmp_build_bit_identical(monkeypatch):
+    """oracle.use_omp(True) routes to the same C file compiled with -fopenmp;
+    every result must be bit-identical to the serial build (the pragmas split
+    independent iterations, integer counts and the backward by row ownership,
+    keeping every fp64 sum in its serial order)."""
+    monkeypatch.setenv("OMP_NUM_THREADS", "4")
+    c = gen.Config("k-small", [max(3, r // 1000) for r in gen.KAGGLE_ROWS], 16, 256, 1, records=20_000)
+    ali = gen.Config("a-small", [900, 4000, 90], 8, 64, 0, 5, 40, records=2_000)
+    outs = []
+    for omp in (False, True):
+        oracle.use_omp(omp)
+        try:
+            res = []
+            for cfg, R in ((c, 20_000), (ali, 2_000)):
+                ds = gen.make_dataset(cfg, n_records=R, seed=31)
+                samp = oracle.sample(R, 5.0, 9)
+                counts, T, _ = oracle.histogram(ds.rows, ds.idx, ds.off, ds.fixed_pool, R, samp)
+                kmin = oracle.kmin_fixed_t(ds.rows, cfg.dim, 0, T, 1e-4, 5.0)
+                hot = oracle.tag_rows(ds.rows, cfg.dim, 0, counts, kmin)
+                rm, base, H = oracle.remap(ds.rows, hot)
+                flag = oracle.classify(ds.rows, ds.idx, ds.off, ds.fixed_pool, R, rm)
+                pk = oracle.pack(ds.rows, ds.idx, ds.off, ds.fixed_pool, R, rm, flag)
+                W = gen.make_weights(max(H, 1), cfg.dim).numpy()
+                n = min(pk["n_hot"], cfg.batch * 3)
+                Tn = ds.n_tables
+                if ds.off is None:
+                    bi, off, P = pk["hot_idx"][:n * Tn], None, 1
+                else:
+                    bi, off, P = pk["hot_idx"], pk["hot_off"][:n * Tn + 1], 0
+                dY = gen.make_dy(n * Tn, cfg.dim, seed=4).numpy()
+                Y, _ = oracle.emb_fwd(W, bi, off, P, n * Tn)
+                W2, _ = oracle.emb_bwd_sgd(W, bi, off, P, n * Tn, dY, 0.05)
+                res.append((samp, counts, T, flag, pk["hot_idx"], Y, W2))
+            outs.append(res)
+        finally:
+            oracle.use_omp(False)
+    for a, b in zip(outs[0], outs[1]):
+        for x, y in zip(a, b):
+            assert np.array_equal(np.asarray(x), np.asarray(y))
