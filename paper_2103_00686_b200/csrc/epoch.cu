@@ -283,7 +283,9 @@ __device__ __forceinline__ void long_chunk(const SegRec* __restrict__ lrec, int6
             if (bad) atomicOr(err, kErrNonfinite);
         }
     }
-    if (kFused && r2.x >= 0) {
+    // no link when the next batch is outside this run (perm_b == nullptr: the
+    // last step of a run that ends before the grouping's last batch)
+    if (kFused && r2.x >= 0 && perm_b) {
         __syncthreads();
         float4 v[NV];
 #pragma unroll
@@ -535,7 +537,7 @@ __device__ __forceinline__ void fused_reduce(const SegRec* __restrict__ rec, int
             pdl_wait();
             float4 v[NV];
             if (gi == 0) sgd_row<LPB, NV>(ps.tot, lane, r.z, W, D, lr, err, v);
-            if (nx.x >= 0) {
+            if (nx.x >= 0 && perm_b) {
 #pragma unroll
                 for (int k = 0; k < NV; k++) {   // broadcast group 0's new row to the warp
                     v[k].x = __shfl_sync(0xffffffffu, v[k].x, lane);
@@ -557,11 +559,12 @@ __device__ __forceinline__ void fused_reduce(const SegRec* __restrict__ rec, int
         float4 g[NV];
         sum_rows16<LPB, NV>(perm_a, r.x, r.y, src, D, lane, g);
         int32_t bg[16];
-        prefetch_bags(perm_b, nx.x, nx.x >= 0 ? nx.y : 0, bg);
+        const bool link = nx.x >= 0 && perm_b;   // the next batch is in this run
+        prefetch_bags(perm_b, nx.x, link ? nx.y : 0, bg);
         pdl_wait();
         float4 v[NV];
         sgd_row<LPB, NV>(g, lane, r.z, W, D, lr, err, v);
-        if (nx.x >= 0) write_y_pf<LPB, NV>(v, bg, perm_b, nx.x, nx.y, Y, D, lane);
+        if (link) write_y_pf<LPB, NV>(v, bg, perm_b, nx.x, nx.y, Y, D, lane);
         return;
     }
     long_chunk<LPB, NV, true, true>(rec + n_short + n_med, n_long, b, false, perm_a, perm_b, src, D, W, lr,

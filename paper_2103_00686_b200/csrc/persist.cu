@@ -227,7 +227,7 @@ __device__ __forceinline__ void prefetch(Pre& p, const BatchDesc* __restrict__ d
             if (rp) {
                 p.r = __ldg(reinterpret_cast<const int4*>(rp));
                 const int4 r2 = __ldg(reinterpret_cast<const int4*>(rp) + 1);
-                p.nx = make_int2(r2.x, r2.y);
+                p.nx = has_b ? make_int2(r2.x, r2.y) : make_int2(-1, 0);   // no link past the run
                 if (cta) {
                     p.kind = kCta;
                     p.c0 = direct ? (int)lb : r2.z;
