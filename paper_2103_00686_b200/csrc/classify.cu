@@ -148,6 +148,204 @@ k_classify_fixed(const int32_t* __restrict__ idx, int64_t n_rec, int Tn, int P, 
     }
 }
 
+// Fixed pooling, persistent and TMA-staged (the default when idx is 16-byte
+// aligned).  Each CTA loops over tiles of TR records claimed in order from a
+// counter, through a 3-slot shared-memory ring: while it classifies tile i,
+// the async (TMA) engine already holds the copy of tile i+1 in flight (one
+// 1-D bulk copy of TR*Tn*P ids per tile), and tile i-1 waits, classified, for
+// its output offsets.  One thread per record walks its Tn*P lookups in table
+// order (table parameters are shared-memory broadcasts): a lookup into a
+// table whose rows are ALL hot (the small tables) gets its hot id
+// base_z + j without touching the rank directory; the others issue their
+// 16-byte directory loads 8 at a time.  Hot ids overwrite the staged ids in
+// place.  A tile publishes its hot-record count right after classifying and
+// finishes its decoupled look-back one tile LATER (after classifying the
+// next one), so the walk finds its predecessors already published instead of
+// stalling the CTA; then its hot_ids / cold_ids and hot CSR are written with
+// coalesced stores.
+constexpr int kBulkRec = 256;          // threads per CTA (>= records per tile)
+constexpr int kBulkSlots = 3;
+#ifndef FAE_CLS_MINB
+#define FAE_CLS_MINB 4      // CTAs per SM (registers capped at 64)
+#endif
+#ifndef FAE_CLS_SMEM_KB
+#define FAE_CLS_SMEM_KB 50  // the three tiles' shared memory per CTA
+#endif
+__global__ void __launch_bounds__(kBulkRec, FAE_CLS_MINB)
+k_classify_bulk(const int32_t* __restrict__ idx, int64_t n_rec, int Tn, int P, int TR, int64_t n_tiles,
+                const int64_t* __restrict__ rowbase, const int64_t* __restrict__ rows,
+                const int64_t* __restrict__ hbase, const uint4* __restrict__ dir,
+                int64_t* __restrict__ hot_ids, int64_t* __restrict__ cold_ids, int32_t* __restrict__ hot_idx,
+                uint64_t* __restrict__ status, uint32_t* __restrict__ ctr, int64_t* __restrict__ result,
+                uint32_t* err, uint32_t div_magic) {
+    extern __shared__ __align__(128) unsigned char s_raw[];
+    const int TnP = Tn * P;
+    const int tile_items = TR * TnP;                      // multiple of 4 (TR % 32 == 0)
+    int32_t* bufs = reinterpret_cast<int32_t*>(s_raw);     // [kBulkSlots][tile_items]
+    int64_t* s_rb = reinterpret_cast<int64_t*>(bufs + kBulkSlots * tile_items);   // [Tn] global row base
+    int64_t* s_hb = s_rb + Tn;                                       // [Tn] hot-id base, or -1
+    int32_t* s_rows = reinterpret_cast<int32_t*>(s_hb + Tn);         // [Tn]
+    int32_t* s_pq = s_rows + Tn;                                     // [TnP] items needing a probe
+    __shared__ int s_np;
+    __shared__ uint64_t s_bar[kBulkSlots];
+    __shared__ int64_t s_tile[kBulkSlots];
+    __shared__ int s_tot[kBulkSlots];
+    __shared__ int s_rk[kBulkSlots][kBulkRec];             // rank among the tile's hot (>= 0) / cold (< 0) records
+    __shared__ int s_list[kBulkSlots][kBulkRec];           // hot records of the tile, in order
+    __shared__ int s_wsum[kBulkRec / 32];
+    __shared__ uint64_t s_ex;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int z = tid; z < Tn; z += blockDim.x) {
+        s_rb[z] = rowbase[z];
+        s_rows[z] = (int32_t)rows[z];
+        s_hb[z] = hbase[z];
+    }
+    if (tid == 0) {   // the items of a record that probe the rank directory, in item order
+        int np = 0;
+        for (int q = 0; q < TnP; q++)
+            if (hbase[q / P] < 0) s_pq[np++] = q;
+        s_np = np;
+    }
+    const int64_t last_full = n_rec / TR;   // tiles [0, last_full) are full (bulk-copied)
+    auto claim = [&](int slot) {            // thread 0
+        const int64_t t = (int64_t)atomicAdd(ctr, 1u);
+        s_tile[slot] = t;
+        if (t < last_full) {
+            fence_proxy_async_smem();
+            bulk_load(bufs + slot * tile_items, idx + t * tile_items, (uint32_t)tile_items * 4u, &s_bar[slot]);
+        }
+    };
+    if (tid == 0) {
+        for (int k = 0; k < kBulkSlots; k++) mbar_init(&s_bar[k], 1);
+        mbar_init_fence();
+        claim(0);
+        claim(1);
+    }
+    __syncthreads();
+    uint32_t phase_bits = 0u;                 // bit k: parity of slot k's next completion
+    int prev = -1;                            // slot of the classified tile awaiting its writes
+    for (int i = 0;; i++) {
+        const int cur = i % kBulkSlots;
+        const int64_t tile = s_tile[cur];
+        const bool have = tile < n_tiles;
+        if (have) {
+            int32_t* buf = bufs + cur * tile_items;
+            const int64_t r0 = tile * TR;
+            const int nrec = (int)(n_rec - r0 < (int64_t)TR ? n_rec - r0 : (int64_t)TR);
+            if (tile < last_full) {
+                mbar_wait(&s_bar[cur], (phase_bits >> cur) & 1u);
+                phase_bits ^= 1u << cur;
+            } else {   // the partial last tile: plain loads
+                const int32_t* src = idx + r0 * TnP;
+                for (int q = tid; q < nrec * TnP; q += blockDim.x) buf[q] = __ldg(src + q);
+                __syncthreads();
+            }
+            bool cold = true;
+            if (tid < nrec) {
+                cold = false;
+                int32_t* my = buf + tid * TnP;
+                // all-hot tables: hot id = base_z + j, no probe
+                for (int q = 0; q < TnP; q++) {
+                    const int z = P == 1 ? q : q / P;
+                    if (s_hb[z] < 0) continue;
+                    const int32_t j = my[q];
+                    if (j < 0 || j >= s_rows[z]) {
+                        atomicOr(err, kErrIndex);
+                        cold = true;
+                        my[q] = -1;
+                    } else {
+                        my[q] = (int32_t)(s_hb[z] + j);
+                    }
+                }
+                // the others: rank-directory probes, 8 in flight
+                const int np = s_np;
+                for (int k0 = 0; k0 < np; k0 += 8) {
+                    uint4 e[8];
+                    int64_t gv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; u++) {
+                        gv[u] = -1;
+                        if (k0 + u < np) {
+                            const int q = s_pq[k0 + u];
+                            const int z = P == 1 ? q : q / P;
+                            const int32_t j = my[q];
+                            if (j < 0 || j >= s_rows[z]) {
+                                atomicOr(err, kErrIndex);
+                                cold = true;
+                            } else {
+                                gv[u] = s_rb[z] + j;
+                                e[u] = __ldg(dir + (gv[u] >> 6));
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; u++) {
+                        if (k0 + u >= np) break;
+                        int32_t hid = -1;
+                        if (gv[u] >= 0) {
+                            uint32_t rk;
+                            if (hs_test(e[u], gv[u], &rk)) hid = (int32_t)rk;
+                            else cold = true;
+                        }
+                        my[s_pq[k0 + u]] = hid;
+                    }
+                }
+            }
+            const bool hot = tid < nrec && !cold;
+            const uint32_t bal = __ballot_sync(0xffffffffu, hot);
+            if (lane == 0) s_wsum[warp] = __popc(bal);
+            __syncthreads();
+            int wp = 0, tot = 0;
+#pragma unroll
+            for (int w = 0; w < kBulkRec / 32; w++) {
+                if (w < warp) wp += s_wsum[w];
+                tot += s_wsum[w];
+            }
+            const int rank = wp + __popc(bal & lanemask_lt());
+            if (tid < nrec) {
+                s_rk[cur][tid] = hot ? rank : -1 - (tid - rank);
+                if (hot) s_list[cur][rank] = tid;
+            }
+            if (tid == 0) {
+                s_tot[cur] = tot;
+                lookback_publish(status, tile, (uint64_t)tot);
+            }
+        }
+        __syncthreads();
+        if (prev >= 0) {   // the previous tile: finish its look-back, write it out
+            const int64_t pt = s_tile[prev];
+            const int ptot = s_tot[prev];
+            if (warp == 0) {
+                const uint64_t ex = lookback_finish_warp(status, pt, (uint64_t)ptot);
+                if (lane == 0) {
+                    s_ex = ex;
+                    if (pt == n_tiles - 1) result[0] = (int64_t)(ex + ptot);
+                }
+            }
+            __syncthreads();
+            const int64_t ex = (int64_t)s_ex;
+            const int64_t r0 = pt * TR;
+            const int nrec = (int)(n_rec - r0 < (int64_t)TR ? n_rec - r0 : (int64_t)TR);
+            if (tid < nrec) {
+                const int rk = s_rk[prev][tid];
+                if (rk >= 0) hot_ids[ex + rk] = r0 + tid;
+                else cold_ids[(r0 - ex) + (-1 - rk)] = r0 + tid;
+            }
+            const int32_t* pbuf = bufs + prev * tile_items;
+            int32_t* dst = hot_idx + ex * (int64_t)TnP;
+            const int nout = ptot * TnP;
+            for (int jx = tid; jx < nout; jx += blockDim.x) {
+                const int k = (int)__umulhi((uint32_t)jx, div_magic);   // jx / TnP
+                dst[jx] = pbuf[s_list[prev][k] * TnP + (jx - k * TnP)];
+            }
+            __syncthreads();   // slot `prev` is free again
+        }
+        if (!have) break;
+        if (tid == 0) claim((i + 2) % kBulkSlots);   // == prev (or the untouched third slot at i = 0)
+        prev = cur;
+    }
+}
+
 // General (offsets or large Tn*P): warp per record, hot ids recomputed in the
 // write phase (L1/L2 hits).  Look-back value = records | lookups << 28.
 constexpr int kGenRec = 64;   // records per tile
@@ -344,6 +542,52 @@ extern "C" fae_status fae_classify(fae_ctx* h, const fae_tables* tabs, const fae
         return set_err(c, FAE_ERR_CAPACITY, "fae_classify: > 2^28 records or > 2^34 lookups per shard");
     FAE_CUDA(c, cudaMemcpyAsync(c->d_rows_tmp, tabs->rows, sizeof(int64_t) * Tn, cudaMemcpyHostToDevice, c->stream));
     const int P = data->fixed_pool;
+    // the persistent TMA-staged kernel: fixed pooling, 16-byte aligned ids,
+    // two tiles of >= 32 records in shared memory
+    const int64_t TnP64 = (int64_t)Tn * P;
+    // three tiles in shared memory, <= 64 KB: 3 CTAs per SM (the register limit)
+    int TRb = TnP64 > 0 ? (int)std::min<int64_t>(kBulkRec, (FAE_CLS_SMEM_KB * 1024 / 4 / kBulkSlots / TnP64) & ~31ll) : 0;
+    const bool bulk = !data->off && TnP64 > 0 && TRb >= 32 && (((uintptr_t)data->idx) & 15) == 0 && n > 0 &&
+                      !c->cls_legacy;
+    if (bulk) {
+        std::vector<int64_t> hb(Tn);
+        for (int z = 0; z < Tn; z++)   // tables whose rows are all hot: hot id = base_z + j
+            hb[z] = (hs.base[z + 1] - hs.base[z] == tabs->rows[z]) ? hs.base[z] : -1;
+        const int64_t tiles = cdiv(n, TRb);
+        size_t o = 0;
+        auto take = [&](size_t b) { size_t r = o; o = (o + b + 255) / 256 * 256; return r; };
+        const size_t o_st = take(sizeof(uint64_t) * tiles);
+        const size_t o_ctr = take(sizeof(uint32_t) * 4);
+        const size_t o_res = take(sizeof(int64_t) * 4);
+        const size_t o_hb = take(sizeof(int64_t) * Tn);
+        char* sc = (char*)scratch(c, o);
+        if (!sc) return set_err(c, FAE_ERR_CUDA, "fae_classify: scratch allocation failed");
+        int64_t* d_res = (int64_t*)(sc + o_res);
+        int64_t* d_hb = (int64_t*)(sc + o_hb);
+        FAE_CUDA(c, cudaMemsetAsync(sc, 0, o_hb, c->stream));
+        FAE_CUDA(c, cudaMemcpyAsync(d_hb, hb.data(), sizeof(int64_t) * Tn, cudaMemcpyHostToDevice, c->stream));
+        const size_t smem = sizeof(int32_t) * kBulkSlots * (size_t)TRb * TnP64 + sizeof(int64_t) * 2 * Tn +
+                            sizeof(int32_t) * (Tn + TnP64);
+        FAE_CUDA(c, cudaFuncSetAttribute(k_classify_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 1;
+        FAE_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_classify_bulk, kBulkRec, smem));
+        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sms(c) * std::max(per_sm, 1)));
+        const uint32_t magic = (uint32_t)((0xFFFFFFFFull + (uint64_t)TnP64) / (uint64_t)TnP64);   // ceil(2^32 / TnP)
+        k_classify_bulk<<<(unsigned)grid, kBulkRec, smem, c->stream>>>(
+            data->idx, n, Tn, P, TRb, tiles, hs.d_rowbase, c->d_rows_tmp, d_hb, hs.dir, out->hot_ids, out->cold_ids,
+            out->hot_idx, (uint64_t*)(sc + o_st), (uint32_t*)(sc + o_ctr), d_res, c->d_err, magic);
+        FAE_LAUNCHED(c);
+        int64_t res[2] = {0, 0};
+        FAE_CUDA(c, cudaMemcpyAsync(res, d_res, sizeof(int64_t) * 2, cudaMemcpyDeviceToHost, c->stream));
+        st = read_latched(c);
+        const int64_t nh = res[0];
+        out->n_hot = nh;
+        out->n_cold = n - nh;
+        out->n_hot_lookups = nh * TnP64;
+        out->n_hot_batches = cdiv(nh, batch);
+        out->n_cold_batches = cdiv(n - nh, batch);
+        return st;
+    }
     const bool fast = !data->off && (int64_t)Tn * P <= kClsItems && Tn * P > 0;
     const int TR = fast ? std::min(kClsFix, std::max(1, kClsItems / (Tn * P))) : kGenRec;
     const int64_t tiles = std::max<int64_t>(1, cdiv(n, TR));

@@ -154,6 +154,8 @@ fae_status fae_create(const fae_config* cfg, fae_ctx** out) {
         c->force_merge = fm && fm[0] == '1';
         const char* gg = getenv("FAE_GS_GENERIC");
         c->gs_generic = gg && gg[0] == '1';
+        const char* cl = getenv("FAE_CLS_LEGACY");
+        c->cls_legacy = cl && cl[0] == '1';
         const char* pm = getenv("FAE_PERSIST_MB");
         c->persist_mb = pm ? atoi(pm) : 0;
     }

@@ -242,6 +242,7 @@ struct Ctx {
     bool merge_sort = false;          // FAE_MERGE_SORT=1: sort-based merge of the exchanged gradients
     bool force_merge = false;         // FAE_FORCE_MERGE=1: the multi-rank exchange loop even at world 1 (tests)
     bool gs_generic = false;          // FAE_GS_GENERIC=1: radix-pass grouping even where the unit path applies
+    bool cls_legacy = false;          // FAE_CLS_LEGACY=1: the round-1 one-tile-per-CTA classify kernel
     int red_mb = 4;                   // FAE_RED_MB: min resident reduce CTAs per SM (4/6/8)
     int pdl_trig = 0;                 // FAE_PDL_TRIG bit0: reduce triggers after its wait, bit1: fwd too
 };
@@ -356,6 +357,95 @@ __device__ __forceinline__ uint64_t lookback_u64(uint64_t* status, int64_t tile,
         --t;
     }
     st_relaxed_u64(&status[tile], kFlagPre | (excl + agg));
+    return excl;
+}
+
+// 1-D bulk copies global -> shared through the async (TMA) engine, completion
+// counted on an mbarrier (cp.async.bulk ... mbarrier::complete_tx::bytes).
+// dst / src 16-byte aligned, bytes a multiple of 16.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+// make mbarrier inits visible to the async proxy
+__device__ __forceinline__ void mbar_init_fence() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// order this thread's (and, after a __syncthreads, the block's) generic-proxy
+// shared-memory accesses before later async-proxy writes to the same buffer
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+    }
+}
+
+// Split look-back: publish a tile's aggregate now (tile 0: its inclusive
+// prefix), finish the walk later — a CTA can do other work in between, so by
+// the time it walks, its predecessors have published.
+__device__ __forceinline__ void lookback_publish(uint64_t* status, int64_t tile, uint64_t agg) {
+    st_relaxed_u64(&status[tile], (tile == 0 ? kFlagPre : kFlagAgg) | agg);
+}
+__device__ __forceinline__ uint64_t lookback_finish(uint64_t* status, int64_t tile, uint64_t agg) {
+    if (tile == 0) return 0;
+    uint64_t excl = 0;
+    int64_t t = tile - 1;
+    while (true) {
+        uint64_t s;
+        do {
+            s = ld_relaxed_u64(&status[t]);
+        } while ((s >> 62) == 0);
+        excl += s & kValMask;
+        if ((s >> 62) == 2) break;
+        --t;
+    }
+    st_relaxed_u64(&status[tile], kFlagPre | (excl + agg));
+    return excl;
+}
+
+// lookback_finish by a whole warp: 32 predecessors per step (the walk from a
+// tile back to the nearest published inclusive prefix is up to a few hundred
+// tiles when hundreds of CTAs classify concurrently).  All 32 lanes call it;
+// every lane returns the exclusive prefix.
+__device__ __forceinline__ uint64_t lookback_finish_warp(uint64_t* status, int64_t tile, uint64_t agg) {
+    if (tile == 0) return 0;
+    const int lane = threadIdx.x & 31;
+    uint64_t excl = 0;
+    int64_t base = tile - 1;
+    while (true) {
+        const int64_t t = base - lane;
+        uint64_t s = t >= 0 ? ld_relaxed_u64(&status[t]) : kFlagPre;   // before tile 0: inclusive 0
+        while (__any_sync(0xffffffffu, (s >> 62) == 0))
+            if ((s >> 62) == 0) s = ld_relaxed_u64(&status[t]);
+        const uint32_t pm = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+        uint64_t v = s & kValMask;
+        const int first = pm ? __ffs(pm) - 1 : 32;   // nearest inclusive prefix in the window
+        if (lane > first) v = 0;
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (pm) break;
+        base -= 32;
+    }
+    if (lane == 0) st_relaxed_u64(&status[tile], kFlagPre | (excl + agg));
     return excl;
 }
 

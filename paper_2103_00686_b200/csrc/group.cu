@@ -322,12 +322,13 @@ constexpr int kUnitIPT = 16;
 constexpr int kUnitMax = kUnitThreads * kUnitIPT;   // 4096 lookups per unit
 constexpr int kMaxUnitTables = 1024;                 // unit path: tables per batch
 
-template <int IPT>
+template <int IPT, bool kP1>
 __global__ void __launch_bounds__(kUnitThreads, IPT <= 8 ? 5 : 2)
-k_gs_units(const int32_t* __restrict__ hot_idx, int64_t H, int Tn, int P, const BatchDesc* __restrict__ desc,
+k_gs_units(const int32_t* __restrict__ hot_idx, int64_t H, int Tn, int P_, const BatchDesc* __restrict__ desc,
            int32_t* __restrict__ perm, int32_t* __restrict__ useg_pos, int32_t* __restrict__ useg_row,
            uint32_t* __restrict__ ucnt, uint32_t* err) {
     constexpr int NW = kUnitThreads / 32;
+    const int P = kP1 ? 1 : P_;   // single-lookup bags: no divisions below
     __shared__ uint32_t s_k[kUnitThreads * IPT];
     __shared__ int32_t s_v[kUnitThreads * IPT];
     __shared__ uint32_t s_w[NW][kSortBins];
@@ -685,7 +686,7 @@ k_gs_records(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __r
             r.nlen = 0;
             r.c0 = 0;
             r.nc = 1;
-            const int32_t t = nxt[s];
+            const int32_t t = nxt ? nxt[s] : -1;
             if (t >= 0 && has_next) {
                 const int64_t sn = dn.sb0 + t;
                 const int64_t en = sn + 1 < dn.sb1 ? seg_start[sn + 1] : dn.lk1;
@@ -960,7 +961,9 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
         if (unit_path) {
             // fixed pooling, every (batch, table) unit <= kUnitMax lookups:
             // one in-shared-memory sort per unit (k_gs_units)
-            auto ku = (int64_t)batch * fixed_pool <= kUnitThreads * 8 ? k_gs_units<8> : k_gs_units<kUnitIPT>;
+            const bool small_unit = (int64_t)batch * fixed_pool <= kUnitThreads * 8;
+            auto ku = fixed_pool == 1 ? (small_unit ? k_gs_units<8, true> : k_gs_units<kUnitIPT, true>)
+                                      : (small_unit ? k_gs_units<8, false> : k_gs_units<kUnitIPT, false>);
             ku<<<(unsigned)n_units, kUnitThreads, 0, c->stream>>>(g.hot_idx, H, Tn, fixed_pool, g.desc, g.perm,
                                                                   (int32_t*)g.keys[0], (int32_t*)g.keys[1],
                                                                   (uint32_t*)g.vals, c->d_err);
@@ -1027,8 +1030,12 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
         }
         FAE_CUDA(c, cudaMemcpyAsync(g.desc, g.hdesc.data(), sizeof(BatchDesc) * nb, cudaMemcpyHostToDevice, c->stream));
         const int64_t gr = std::max<int64_t>(1, std::min<int64_t>(nb, (int64_t)sm_count(c) * 8));
-        FAE_CUDA(c, cudaMemsetAsync(g.nxt, 0xFF, sizeof(int32_t) * std::max<int64_t>(g.S_total, 1), c->stream));
-        {
+        // the links to the next batch (SegRec npos/nlen) and the free lists are
+        // read only by the fused one-kernel step (and the persistent kernel);
+        // the two-kernel step (D > 16, multi-hot, world > 1) never needs them
+        const bool links = fused_step(c) || (g.P == 1 && !g.hot_off && c->world == 1 && c->persist);
+        if (links) {
+            FAE_CUDA(c, cudaMemsetAsync(g.nxt, 0xFF, sizeof(int32_t) * std::max<int64_t>(g.S_total, 1), c->stream));
             int64_t ms = 0;
             for (const BatchDesc& d : g.hdesc) ms = std::max<int64_t>(ms, d.sb1 - d.sb0);
             const int smem_rows = (int)std::min<int64_t>(ms, 40 * 1024);   // <= 160 KB
@@ -1037,11 +1044,11 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
                 FAE_CUDA(c, cudaFuncSetAttribute(k_gs_links, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
             k_gs_links<<<(unsigned)gr, 256, lsm, c->stream>>>(g.desc, nb, g.seg_start, g.seg_row, g.nxt, g.freer,
                                                                smem_rows);
+            FAE_LAUNCHED(c);
         }
-        FAE_LAUNCHED(c);
         g.chunk = chunk_for_dim(tabs->dim);
-        k_gs_records<<<(unsigned)gr, 256, 0, c->stream>>>(g.desc, nb, g.seg_start, g.seg_row, g.nxt, g.rec, g.chunk,
-                                                          g.lmap);
+        k_gs_records<<<(unsigned)gr, 256, 0, c->stream>>>(g.desc, nb, g.seg_start, g.seg_row, links ? g.nxt : nullptr,
+                                                          g.rec, g.chunk, g.lmap);
         FAE_LAUNCHED(c);
         FAE_CUDA(c, cudaMemcpyAsync(g.hdesc.data(), g.desc, sizeof(BatchDesc) * nb, cudaMemcpyDeviceToHost, c->stream));
         st = read_latched(c);

@@ -40,23 +40,64 @@ __device__ __forceinline__ int table_of(const int64_t* s_rb, int Tn, int64_t g) 
     return lo;
 }
 
-// per-table max count (large tables only matter; computed for all)
+// Per-table max count (large tables only matter; computed for all).  Each
+// thread streams 4 consecutive loggers per 16-byte load; the table of a
+// position is tracked incrementally (tables are contiguous), the running max
+// kept in a register and flushed to shared memory only when the table
+// changes, then one global atomic per table per block.
+__device__ __forceinline__ int table_from(const int64_t* s_rb, int Tn, int64_t g, int z) {
+    while (z + 1 < Tn && g >= s_rb[z + 1]) z++;
+    return z;
+}
+
 __global__ void __launch_bounds__(256)
 k_table_max(const uint32_t* __restrict__ counts, int64_t total, const int64_t* __restrict__ rowbase,
             int Tn, uint32_t* __restrict__ tmax) {
     extern __shared__ int64_t s_rb[];
+    uint32_t* s_max = reinterpret_cast<uint32_t*>(s_rb + Tn + 1);
     for (int z = threadIdx.x; z <= Tn; z += blockDim.x) s_rb[z] = rowbase[z];
+    for (int z = threadIdx.x; z < Tn; z += blockDim.x) s_max[z] = 0u;
     __syncthreads();
-    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
-         g += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t v = counts[g];
-        if (v) atomicMax(&tmax[table_of(s_rb, Tn, g)], v);
+    const int64_t n4 = (((uintptr_t)counts & 15) == 0) ? total / 4 : 0;   // 16-byte loads when aligned
+    const uint4* c4 = reinterpret_cast<const uint4*>(counts);
+    int zc = -1;
+    uint32_t m = 0;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4 + (total - 4 * n4);
+         q += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t v[4];
+        int64_t g0;
+        int nv;
+        if (q < n4) {
+            const uint4 x = __ldcs(c4 + q);
+            v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+            g0 = q * 4;
+            nv = 4;
+        } else {   // the < 4 trailing loggers
+            g0 = n4 * 4 + (q - n4);
+            v[0] = counts[g0];
+            nv = 1;
+        }
+        int z = table_of(s_rb, Tn, g0);
+        for (int k = 0; k < nv; k++) {
+            z = table_from(s_rb, Tn, g0 + k, z);
+            if (z != zc) {
+                if (zc >= 0 && m) atomicMax(&s_max[zc], m);
+                zc = z;
+                m = 0;
+            }
+            m = max(m, v[k]);
+        }
     }
+    if (zc >= 0 && m) atomicMax(&s_max[zc], m);
+    __syncthreads();
+    for (int z = threadIdx.x; z < Tn; z += blockDim.x)
+        if (s_max[z]) atomicMax(&tmax[z], s_max[z]);
 }
 
 // For each large row: m = #{candidates c : cut[z][c] <= k}; hist[m]++ .
-// cut is [Tn][kNCand] ascending in c (uint64); small tables have cut = 0
-// and are skipped via the `large` mask.
+// cut is [Tn][kNCand] ascending in c (uint64; >= 1 for large tables, so a
+// zero logger counts for no candidate); small tables have cut = 0 and are
+// skipped via the `large` mask.  16-byte loads, incremental table tracking.
 __global__ void __launch_bounds__(256)
 k_count_ge_multi(const uint32_t* __restrict__ counts, int64_t total,
                  const int64_t* __restrict__ rowbase, int Tn,
@@ -67,19 +108,38 @@ k_count_ge_multi(const uint32_t* __restrict__ counts, int64_t total,
     for (int z = threadIdx.x; z <= Tn; z += blockDim.x) s_rb[z] = rowbase[z];
     for (int i = threadIdx.x; i <= kNCand; i += blockDim.x) sh[i] = 0;
     __syncthreads();
-    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total;
-         g += (int64_t)gridDim.x * blockDim.x) {
-        const int z = table_of(s_rb, Tn, g);
-        if (!large[z]) continue;
-        const uint64_t v = counts[g];
-        const unsigned long long* cz = cut + (int64_t)z * kNCand;
-        int lo = 0, hi = ncand;   // first c with cut > v
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (cz[mid] <= v) lo = mid + 1;
-            else hi = mid;
+    const int64_t n4 = (((uintptr_t)counts & 15) == 0) ? total / 4 : 0;   // 16-byte loads when aligned
+    const uint4* c4 = reinterpret_cast<const uint4*>(counts);
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4 + (total - 4 * n4);
+         q += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t v[4];
+        int64_t g0;
+        int nv;
+        if (q < n4) {
+            const uint4 x = __ldcs(c4 + q);
+            v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+            g0 = q * 4;
+            nv = 4;
+        } else {
+            g0 = n4 * 4 + (q - n4);
+            v[0] = counts[g0];
+            nv = 1;
         }
-        if (lo) atomicAdd(&sh[lo], 1u);
+        if ((v[0] | (nv > 1 ? v[1] | v[2] | v[3] : 0u)) == 0u) continue;   // the common case
+        int z = table_of(s_rb, Tn, g0);
+        for (int k = 0; k < nv; k++) {
+            z = table_from(s_rb, Tn, g0 + k, z);
+            if (!v[k] || !large[z]) continue;
+            const uint64_t vv = v[k];
+            const unsigned long long* cz = cut + (int64_t)z * kNCand;
+            int lo = 0, hi = ncand;   // first c with cut > v
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (cz[mid] <= vv) lo = mid + 1;
+                else hi = mid;
+            }
+            if (lo) atomicAdd(&sh[lo], 1u);
+        }
     }
     __syncthreads();
     for (int i = threadIdx.x; i <= kNCand; i += blockDim.x)
@@ -103,13 +163,21 @@ k_build_dir(const uint32_t* __restrict__ counts, int64_t total, const int64_t* _
     const int64_t tile = s_tile;
     const int64_t tbase = tile * kDirTileRows;
     if (tbase >= total) return;
+    const int zt = table_of(s_rb, Tn, tbase);   // tables are contiguous: track from the tile's first
+    uint32_t cv[kDirIters];
+#pragma unroll
+    for (int it = 0; it < kDirIters; it++) {   // all loads in flight first
+        const int64_t g = tbase + it * kDirThreads + tid;
+        cv[it] = g < total ? __ldcs(counts + g) : 0u;
+    }
+    int z = zt;
 #pragma unroll
     for (int it = 0; it < kDirIters; it++) {
         const int64_t g = tbase + it * kDirThreads + tid;
         bool hot = false;
         if (g < total) {
-            const int z = table_of(s_rb, Tn, g);
-            hot = (unsigned long long)counts[g] >= kmin_eff[z];
+            z = table_from(s_rb, Tn, g, z);
+            hot = (unsigned long long)cv[it] >= kmin_eff[z];
         }
         const uint32_t m = __ballot_sync(0xffffffffu, hot);
         if (lane == 0) s_half[it * (kDirThreads / 32) + warp] = m;
@@ -447,7 +515,8 @@ extern "C" fae_status fae_threshold(fae_ctx* h, const fae_tables* tabs, const ui
         if (Tref == 0) Tref = 1;
         // K_hi: first K at which no large row can be hot
         FAE_CUDA(c, cudaMemsetAsync(d_tmax, 0, sizeof(uint32_t) * Tn, c->stream));
-        k_table_max<<<(unsigned)grid, 256, rb_smem, c->stream>>>(counts, total, c->d_rowbase_tmp, Tn, d_tmax);
+        k_table_max<<<(unsigned)grid, 256, rb_smem + sizeof(uint32_t) * Tn, c->stream>>>(counts, total,
+                                                                                        c->d_rowbase_tmp, Tn, d_tmax);
         FAE_LAUNCHED(c);
         std::vector<uint32_t> tmax(Tn);
         FAE_CUDA(c, cudaMemcpyAsync(tmax.data(), d_tmax, sizeof(uint32_t) * Tn, cudaMemcpyDeviceToHost, c->stream));
