@@ -186,11 +186,15 @@ def run_fae(args):
     R = args.records or cfg.records
     Tn, D, B = cfg.n_tables, cfg.dim, cfg.batch
     ds = gen.make_dataset(cfg, n_records=R, device=dev, record_base=rank * R)
+    if args.exchange:
+        os.environ["FAE_FORCE_MERGE"] = "1"      # read at fae_create
     pipe = FaePipeline(cfg.rows, D, B, cfg.pool, max_pool=max(cfg.pool_hi, 1), device=local,
                        max_world=world)
     if world > 1:
         from paper_2103_00686_b200 import dist as fdist
         fdist.init_comm(pipe.ctx, dev)
+    elif args.exchange:                           # the exchange loop on a 1-rank communicator
+        fae.fae_comm_init(pipe.ctx, fae.fae_get_nccl_id(), 0, 1)
     W = gen.make_weights(sum(cfg.rows), D, device=dev)
     S_max = B * Tn
     dy_bytes = S_max * D * 4
@@ -264,6 +268,7 @@ def run_fae(args):
     ms = t0.elapsed_time(t1)
     launches = pipe.ctx.launches - l0
     kt = fae.fae_get_kernel_timing(pipe.ctx)
+    xt = fae.fae_get_exchange_timing(pipe.ctx) if (world > 1 or args.exchange) else None
     fae.fae_set_kernel_timing(pipe.ctx, 0)
     tot = torch.tensor([ms, float(hot_lookups)], dtype=torch.float64, device=dev)
     if dist is not None:
@@ -347,12 +352,35 @@ def run_fae(args):
             "clocks": ck,
             "wall_s": wall,
             "phases_ms_per_step": {k: v / args.steps for k, v in phases.items()},
+            **({"sync": sync_report(xt, world, D, kt)} if xt else {}),
             # the a8-a10 training loop alone (the value above times the whole
             # hot path a1-a10 per step)
             "train_only_lookups_per_s": (lookups_all / (phases["train"] / 1e3)
                                          if phases.get("train") else None),
         }
     return res, (pipe, ds, W, cfg, R, dist, rank, world, dev, dY, Y)
+
+
+def sync_report(xt, world, D, kt):
+    """a11 exchange per training step, device-timed on rank 0:
+    every rank contributes xcap (row, G) entries of 4 + 4D bytes (xcap = the
+    largest U of any rank and step) and receives world-1 of them; nccl-tests
+    conventions: allgather algBW = world * slot bytes / time, busBW = algBW *
+    (world-1)/world, against NVLink 5's 900 GB/s per direction."""
+    st = max(xt["steps_timed"], 1)
+    slot = xt["slot_bytes"] / max(xt["steps"], 1)
+    ag_s = xt["allgather_ms"] / st / 1e3
+    algbw = world * slot / ag_s / 1e9 if ag_s > 0 else None
+    busbw = algbw * (world - 1) / world if algbw else None
+    step_us = ((kt["fwd"][0] + kt["reduce"][0]) / max(kt["reduce"][1], 1)) * 1e3 + \
+        (xt["allgather_ms"] + xt["merge_ms"]) / st * 1e3
+    return {"transport": "nccl", "xcap_entries": xt["xcap"],
+            "slot_bytes_per_step": slot, "recv_bytes_per_gpu_per_step": (world - 1) * slot,
+            "allgather_us_per_step": ag_s * 1e6, "merge_us_per_step": xt["merge_ms"] / st * 1e3,
+            "train_step_us": step_us,
+            "algbw_GBs": algbw, "busbw_GBs": busbw,
+            "busbw_frac_of_900": (busbw / 900.0) if busbw else None,
+            "timing": "in-kernel globaltimer: reduce-emit end -> first merge CTA (all-gather), merge CTAs"}
 
 
 def run_e2e(args, ctxs):
@@ -675,6 +703,8 @@ def main():
     ap.add_argument("--no-ktiming", action="store_true", help="no in-kernel stamps (overhead check; no roofline)")
     ap.add_argument("--dy-pool-mb", type=int, default=256, help="upstream-gradient pool (> L2 by default)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--exchange", action="store_true",
+                    help="N=1: run the multi-rank exchange loop on a 1-rank NCCL communicator (sync cost)")
     ap.add_argument("--sweep", action="store_true", help="threshold sweep (one JSON line; not the driver's bench)")
     ap.add_argument("--sweep-configs", default="kaggle,terabyte")
     ap.add_argument("--sweep-fracs", default="1,2,5,10,20")

@@ -411,8 +411,17 @@ fae_status fae_group_batches(fae_ctx* ctx, const fae_tables* tabs,
  * SGD), chained by programmatic dependent launch; bit-identical either way.
  * FAE_FUSED=0/1 forces the choice; FAE_PERSIST=1 selects a cooperative
  * persistent kernel with a grid barrier per step (single-lookup bags; slower
- * on B200, kept for measurement).  World > 1: the
- * sparse gradient is exchanged every step (fae_sync_hot_grads semantics).
+ * on B200, kept for measurement).  World > 1 (or FAE_FORCE_MERGE=1 on a
+ * 1-rank communicator): the sparse gradient is exchanged every step
+ * (fae_sync_hot_grads semantics): per step, the forward, a reduce that
+ * writes this rank's (row, G) list straight into its slot of the exchange
+ * buffer, an in-place NCCL all-gather of xcap entries per rank (xcap = the
+ * call's largest per-step U over ranks, known after one up-front count
+ * exchange), and a rank-ordered merge + SGD kernel (world > 2: via a
+ * [world][H] int32 row-position table allocated here); replayed from a
+ * captured graph of 128 steps (NCCL transport) or a host loop (loopback
+ * test transport).  Every rank passes the same n; a rank with fewer
+ * batches than first + n contributes empty gradients.
  * H must equal the H given to fae_group_batches and D the tabs->dim given
  * to it (the long-segment chunking is sized for that row width).
  * ------------------------------------------------------------------------ */
@@ -445,6 +454,21 @@ fae_status fae_set_kernel_timing(fae_ctx* ctx, int32_t enable);
  * batch absent from the previous batch, summed), fused step in use}. */
 fae_status fae_group_info(const fae_ctx* ctx, int64_t* info);
 fae_status fae_get_kernel_timing(const fae_ctx* ctx, double* ms, int64_t* n);
+/* Exchange-loop timing (a11; world > 1 or FAE_FORCE_MERGE),
+ * accumulated by fae_train_hot_batches under fae_set_kernel_timing(1) and
+ * reset by it.  out[6] (host):
+ *  out[0] ms in the all-gather: from this rank's reduce-emit end (or the
+ *         previous merge's end on a step with no local batch) to the first
+ *         merge CTA's start, summed over timed steps;
+ *  out[1] ms in the rank-ordered merge + SGD kernel, summed;
+ *  out[2] steps timed;
+ *  out[3] bytes one rank contributes to the all-gathers, summed over the
+ *         call's steps: xcap * (4 + 4D) per step (xcap = the largest U of
+ *         any rank and step of the call; every rank receives (world-1) times
+ *         this);
+ *  out[4] steps run; out[5] xcap of the last call.
+ * Errors: INVALID_ARG (null). */
+fae_status fae_get_exchange_timing(const fae_ctx* ctx, double* out);
 
 #ifdef __cplusplus
 }

@@ -31,7 +31,7 @@ EXPORTS = ["fae_create", "fae_destroy", "fae_set_stream", "fae_last_error",
            "fae_kernel_launches", "fae_profile", "fae_threshold",
            "fae_classify", "fae_extract", "fae_scatter_hot", "fae_pack_cold", "fae_emb_fwd", "fae_emb_bwd_update",
            "fae_sync_hot_grads", "fae_group_batches", "fae_train_hot_batches",
-           "fae_set_kernel_timing", "fae_get_kernel_timing", "fae_group_info"]
+           "fae_set_kernel_timing", "fae_get_kernel_timing", "fae_get_exchange_timing", "fae_group_info"]
 
 
 class FaeError(RuntimeError):
@@ -123,6 +123,7 @@ def lib():
                                        ctypes.c_float], c_i32),
             "fae_set_kernel_timing": ([P, c_i32], c_i32),
             "fae_get_kernel_timing": ([P, P, P], c_i32),
+            "fae_get_exchange_timing": ([P, P], c_i32),
             "fae_group_info": ([P, P], c_i32),
         }
         for name, (args, res) in sig.items():
@@ -382,6 +383,16 @@ def fae_get_kernel_timing(ctx: Ctx) -> dict:
     return {"fwd": (ms[0], n[0]), "reduce": (ms[1], n[1]),
             "overlap": (ms[2], n[2]), "fused": n[3] == 1, "persist": n[3] == 2,
             "persist_batches": int(ms[3])}
+
+
+def fae_get_exchange_timing(ctx: Ctx) -> dict:
+    """Exchange loop (world > 1): all-gather / merge ms summed over the timed
+    steps, steps timed, slot bytes this rank contributed, steps run, and the
+    last call's padded per-rank entries xcap."""
+    out = (c_dbl * 6)()
+    ctx._ok(lib().fae_get_exchange_timing(ctx.h, ctypes.cast(out, c_ptr)))
+    return {"allgather_ms": out[0], "merge_ms": out[1], "steps_timed": int(out[2]),
+            "slot_bytes": out[3], "steps": int(out[4]), "xcap": int(out[5])}
 
 
 def fae_group_info(ctx: Ctx) -> dict:

@@ -156,6 +156,10 @@ fae_status fae_create(const fae_config* cfg, fae_ctx** out) {
         c->gs_generic = gg && gg[0] == '1';
         const char* cl = getenv("FAE_CLS_LEGACY");
         c->cls_legacy = cl && cl[0] == '1';
+        // exchange merge: FAE_MERGE_TABLE=1 / 0 forces the row-position
+        // table / the binary searches (default: table for world > 2)
+        const char* mt = getenv("FAE_MERGE_TABLE");
+        c->merge_table = mt ? (mt[0] == '1' ? 1 : 0) : -1;
         const char* pm = getenv("FAE_PERSIST_MB");
         c->persist_mb = pm ? atoi(pm) : 0;
     }

@@ -721,6 +721,7 @@ k_grp_fwd_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ ru
     const int64_t rel = *base + s;
     if (rel >= run[1]) {
         if (trig & 2) pdl_trigger();
+        if (trig & 4) pdl_wait();   // exchange loop: completion implies the previous merge's
         return;
     }
     if (stamps && threadIdx.x == 0) {
@@ -736,6 +737,7 @@ k_grp_fwd_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ ru
     if (hot_off) fwd_bags<LPB, NV, true>(W, H, D, hot_idx, hot_off + d.bag0, 0, d.n_bags, Y, err);
     else if (P == 1) fwd_gather1<LPB, NV, true>(W, H, D, hot_idx + d.lk0, d.n_bags, Y, err);
     else fwd_bags<LPB, NV, true>(W, H, D, hot_idx + d.lk0, nullptr, P, d.n_bags, Y, err);
+    if (trig & 4) pdl_wait();       // (threads without a bag never waited above)
     if (stamps) {
         __syncthreads();
         if (threadIdx.x == 0) atomicMax(&stamps[rel * kSt + 1], (unsigned long long)gtimer());
@@ -794,12 +796,170 @@ k_grp_reduce_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__
     }
 }
 
-__global__ void k_set_run(int64_t* cursor, int64_t first, int64_t n) {
+__global__ void k_set_run(int64_t* cursor, int64_t first, int64_t n, int64_t n_total) {
     if (threadIdx.x == 0) {
         cursor[0] = 0;
         cursor[1] = 0;
         cursor[2] = first;
         cursor[3] = n;
+        cursor[4] = n_total;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// world > 1 exchange step (a11: the hot gradients of every GPU are
+// summed after each mini-batch), graph-replayed like the world-1 loop:
+//   k_grp_fwd_pdl   a8 of this rank's batch rel = *base + s
+//   k_grp_xreduce   a9 sums of the batch, emitted straight into this rank's
+//                   slot of the exchange buffers: rows -> xrows[rank][seg],
+//                   G -> xvals[rank][seg] (no staging copies)
+//   allgather       every slot to every rank, xcap entries per rank (the
+//                   call's largest per-step U; ncclAllGather in place)
+//   [k_xscatter]    world > 2: ptab[q][row] = j for entry j of rank q
+//   k_xmerge        the owner of a row (lowest rank holding it) sums the
+//                   ranks' G in rank order and applies a10; the last step of
+//                   a replay advances *base.
+// Steps past this rank's last batch (run[1]) emit nothing (count 0 in
+// per_step, exchanged up front), the exchange and merge still run.
+// ---------------------------------------------------------------------------
+template <int LPB, int NV, int MB>
+__global__ void __launch_bounds__(256, MB)
+k_grp_xreduce(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ run, const int64_t* __restrict__ base,
+              int s, const SegRec* __restrict__ rec, const int32_t* __restrict__ perm,
+              const int32_t* __restrict__ seg_row, const float* __restrict__ dY, int64_t n_dy, int64_t dy_stride,
+              int D, float* lpart, uint32_t* lcnt, const int32_t* __restrict__ lmap, int32_t* __restrict__ xrows,
+              float* __restrict__ xvals, uint32_t* err, unsigned long long* stamps) {
+    pdl_trigger();
+    const int64_t rel = *base + s;
+    if (rel >= run[1]) {
+        pdl_wait();   // completion implies the forward's, hence the previous merge's
+        return;
+    }
+    if (stamps && threadIdx.x == 0) atomicMin(&stamps[rel * kSt + 4], (unsigned long long)gtimer());
+    const BatchDesc d = desc[run[0] + rel];
+    const int64_t U = d.sb1 - d.sb0;
+    const int64_t n_long = U - d.n_short - d.n_med;
+    reduce_segments<LPB, NV, true>(rec + d.sb0, d.n_tiny, d.n_short, d.n_med, n_long, d.n_lchunk, perm + d.lk0,
+                                   dY + (rel % n_dy) * dy_stride, D, nullptr, 0.f, lpart, lcnt,
+                                   lmap + lmap_base(d, run[0] + rel), 1, xvals, err);
+    // the batch's rows (static, ascending) into the slot; the previous
+    // step's readers of the slot finished before this batch's forward began
+    pdl_wait();
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < U; j += (int64_t)gridDim.x * blockDim.x)
+        xrows[j] = __ldg(seg_row + d.sb0 + j);
+    if (stamps) {
+        __syncthreads();
+        if (threadIdx.x == 0) atomicMax(&stamps[rel * kSt + 3], (unsigned long long)gtimer());
+    }
+}
+
+// world > 2: position of every gathered row in its rank's list
+__global__ void k_xscatter(const int32_t* __restrict__ xrows, const int32_t* __restrict__ per_step,
+                           const int64_t* __restrict__ base, int s, int world, int64_t xcap, int64_t H,
+                           int32_t* __restrict__ ptab) {
+    const int64_t rel = *base + s;
+    const int64_t n_total = base[4];
+    if (rel >= n_total) return;
+    const int32_t* cnt = per_step + rel * world;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < xcap * world;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int q = (int)(e / xcap);
+        const int64_t j = e - (int64_t)q * xcap;
+        if (j < __ldg(cnt + q)) ptab[(int64_t)q * H + __ldg(xrows + e)] = (int32_t)j;
+    }
+}
+
+// entry j of rank q holds row x?  (ptab values of earlier steps may be stale:
+// a position is trusted only if it is inside q's list and holds x)
+__device__ __forceinline__ int64_t xfind(const int32_t* __restrict__ xrows, const int32_t* __restrict__ ptab,
+                                         int64_t H, int64_t xcap, int32_t cnt_q, int q, int32_t x) {
+    const int32_t j = __ldcg(ptab + (int64_t)q * H + x);
+    if (j < 0 || j >= cnt_q) return -1;
+    return __ldg(xrows + (int64_t)q * xcap + j) == x ? j : -1;
+}
+
+// binary search of x in rank q's sorted list (world <= 2: no table)
+__device__ __forceinline__ int64_t xsearch(const int32_t* __restrict__ rows, int64_t n, int32_t x) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(rows + mid) < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo < n && __ldg(rows + lo) == x ? lo : -1;
+}
+
+// The owner of row x (the lowest rank holding it) sums 0 + G_r + G_r' + ...
+// over the ranks holding x in rank order — the order of the standalone
+// sync's sort-based merge (one piece of <= world terms) — and applies
+// W[x] = fmaf(-lr, G, W[x]); every rank computes identical bits.
+template <int LPB, int NV, bool kTable>
+__global__ void __launch_bounds__(256)
+k_xmerge(const int32_t* __restrict__ xrows, const float* __restrict__ xvals, const int32_t* __restrict__ per_step,
+         int64_t* base, int s, int last_step, uint32_t* done_ctr, int world, int64_t xcap, int D, float* W, float lr,
+         const int32_t* __restrict__ ptab, int64_t H, uint32_t* err, unsigned long long* stamps) {
+    pdl_trigger();   // the next forward's index loads overlap this merge (it waits before reading W)
+    const int64_t b0 = *base;
+    const int64_t rel = b0 + s;
+    if (rel < base[4]) {
+        if (stamps && threadIdx.x == 0) atomicMin(&stamps[rel * kSt + 10], (unsigned long long)gtimer());
+        const int32_t* cnt = per_step + rel * world;
+        const int lane = threadIdx.x % LPB;
+        const int64_t gpb = blockDim.x / LPB;
+        for (int64_t e = blockIdx.x * gpb + threadIdx.x / LPB; e < xcap * world; e += (int64_t)gridDim.x * gpb) {
+            const int r = (int)(e / xcap);
+            const int64_t j = e - (int64_t)r * xcap;
+            if (j >= __ldg(cnt + r)) continue;
+            const int32_t x = __ldg(xrows + e);
+            bool owner = true;
+            for (int q = 0; q < r && owner; q++) {
+                const int64_t t = kTable ? xfind(xrows, ptab, H, xcap, __ldg(cnt + q), q, x)
+                                         : xsearch(xrows + (int64_t)q * xcap, __ldg(cnt + q), x);
+                if (t >= 0) owner = false;
+            }
+            if (!owner) continue;
+            float4 acc[NV];
+#pragma unroll
+            for (int k = 0; k < NV; k++) acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int q = r; q < world; q++) {
+                const int64_t t = q == r ? j
+                                : (kTable ? xfind(xrows, ptab, H, xcap, __ldg(cnt + q), q, x)
+                                          : xsearch(xrows + (int64_t)q * xcap, __ldg(cnt + q), x));
+                if (t < 0) continue;
+                const float4* v = reinterpret_cast<const float4*>(xvals + ((int64_t)q * xcap + t) * D) + lane;
+#pragma unroll
+                for (int k = 0; k < NV; k++) add4(acc[k], __ldcg(v + k * LPB));
+            }
+            float4* w = reinterpret_cast<float4*>(W + (int64_t)x * D) + lane;
+            bool bad = false;
+#pragma unroll
+            for (int k = 0; k < NV; k++) {
+                float4 y = w[k * LPB];
+                y.x = __fmaf_rn(-lr, acc[k].x, y.x);
+                y.y = __fmaf_rn(-lr, acc[k].y, y.y);
+                y.z = __fmaf_rn(-lr, acc[k].z, y.z);
+                y.w = __fmaf_rn(-lr, acc[k].w, y.w);
+                bad |= !(isfinite(y.x) && isfinite(y.y) && isfinite(y.z) && isfinite(y.w));
+                w[k * LPB] = y;
+            }
+            if (bad) atomicOr(err, kErrNonfinite);
+        }
+        if (stamps) {
+            __syncthreads();
+            if (threadIdx.x == 0) atomicMax(&stamps[rel * kSt + 11], (unsigned long long)gtimer());
+        }
+    }
+    if (last_step) {   // the last CTA of the replay's last merge advances the base
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const uint32_t old = atomicAdd(done_ctr, 1u);
+            if (old == gridDim.x - 1) {
+                *done_ctr = 0u;
+                *base = b0 + last_step;
+                __threadfence();
+            }
+        }
     }
 }
 
@@ -815,6 +975,9 @@ void drop_graphs(Group& g) {
         g.tgraph[v] = nullptr;
     }
     g.tgraph_key = 0;
+    if (g.xgraph) cudaGraphExecDestroy(g.xgraph);
+    g.xgraph = nullptr;
+    g.xgraph_key = 0;
 }
 
 // blocks of the reduce kernel for the largest batch
@@ -925,6 +1088,86 @@ static fae_status launch_fused(Ctx* c, cudaStream_t st, int s, float* W, int64_t
     return FAE_OK;
 }
 
+// One exchange step (world > 1) on stream st: forward, reduce-emit into this
+// rank's slot, in-place all-gather of every slot, [position table], merge +
+// SGD.  s: step within a replay; last: base increment by this step's merge.
+template <int LPB, int NV>
+static fae_status launch_x_step(Ctx* c, cudaStream_t st, int s, int last, float* W, int64_t H, int D,
+                                const float* dY, int64_t n_dy, float* Y, float lr, int64_t xcap,
+                                const int32_t* per_step, bool table, unsigned long long* stamps) {
+    Group& g = c->grp;
+    const int threads = 256;
+    const int64_t gpb = threads / LPB;
+    const int world = c->world;
+    int32_t* xrows = c->g_rows;
+    float* xvals = c->g_vals;
+    int32_t* my_rows = xrows + (int64_t)c->rank * xcap;
+    float* my_vals = xvals + (int64_t)c->rank * xcap * D;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(threads);
+    cfg.stream = st;
+    // PDL chain merge -> forward -> reduce: the forward reads W and the reduce
+    // writes this rank's slot only after griddepcontrol.wait, and both wait
+    // on every path (trig bit 2 for the forward), so the reduce's completion
+    // implies the previous merge's and the next all-gather cannot overwrite
+    // a slot the merge still reads
+    cfg.attrs = attr;
+    cfg.numAttrs = c->no_pdl ? 0 : 1;
+    const int64_t fu = g.P == 1 ? cdiv(g.max_bags, 4)
+                     : (g.hot_off || g.P >= kWarpBagMinP) ? g.max_bags * (32 / LPB) : g.max_bags;
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(fu, gpb), (int64_t)sm_count(c) * 4)));
+    FAE_CUDA(c, cudaLaunchKernelEx(&cfg, k_grp_fwd_pdl<LPB, NV>, (const BatchDesc*)g.desc, (const int64_t*)g.run,
+                                   (const int64_t*)g.cursor, s, g.hot_idx, g.hot_off, (int)g.P, (const float*)W, H, D,
+                                   Y, c->d_err, stamps, 4));
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, red_grid(g, gpb)));
+    auto kern = c->red_mb >= 8 ? k_grp_xreduce<LPB, NV, 8>
+              : (c->red_mb >= 6 ? k_grp_xreduce<LPB, NV, 6> : k_grp_xreduce<LPB, NV, 4>);
+    FAE_CUDA(c, cudaLaunchKernelEx(&cfg, kern, (const BatchDesc*)g.desc, (const int64_t*)g.run,
+                                   (const int64_t*)g.cursor, s, (const SegRec*)g.rec, (const int32_t*)g.perm,
+                                   (const int32_t*)g.seg_row, dY, n_dy, g.max_bags * (int64_t)D, D,
+                                   g.lpart + (int64_t)s * std::max<int64_t>(g.max_lchunk, 1) * 8 * D,
+                                   g.lcnt + (int64_t)s * std::max<int64_t>(g.max_long, 1), (const int32_t*)g.lmap,
+                                   my_rows, my_vals, c->d_err, stamps));
+    FAE_LAUNCHED(c);
+    c->launches++;   // the forward
+    {
+        cudaStream_t keep = c->stream;
+        c->stream = st;
+        coll_group_start(c);
+        fae_status a = coll_allgather(c, my_rows, xrows, xcap, CollT::I32, "exchange: allgather rows");
+        if (a == FAE_OK) a = coll_allgather(c, my_vals, xvals, xcap * D, CollT::F32, "exchange: allgather grads");
+        fae_status b = coll_group_end(c, "exchange: allgather");
+        c->stream = keep;
+        if (a != FAE_OK) return a;
+        if (b != FAE_OK) return b;
+    }
+    const int64_t n = xcap * world;
+    if (table) {
+        const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), (int64_t)sm_count(c) * 8));
+        k_xscatter<<<(unsigned)blocks, 256, 0, st>>>(xrows, per_step, g.cursor, s, world, xcap, H, g.ptab);
+        FAE_LAUNCHED(c);
+    }
+    const int64_t mb = std::max<int64_t>(1, std::min<int64_t>(cdiv(n, gpb), (int64_t)sm_count(c) * 16));
+    if (table)
+        k_xmerge<LPB, NV, true><<<(unsigned)mb, 256, 0, st>>>(xrows, xvals, per_step, g.cursor, s, last, g.done_ctr,
+                                                              world, xcap, D, W, lr, g.ptab, H, c->d_err, stamps);
+    else
+        k_xmerge<LPB, NV, false><<<(unsigned)mb, 256, 0, st>>>(xrows, xvals, per_step, g.cursor, s, last, g.done_ctr,
+                                                               world, xcap, D, W, lr, nullptr, H, c->d_err, stamps);
+    FAE_LAUNCHED(c);
+    return FAE_OK;
+}
+
+static fae_status launch_x(Ctx* c, cudaStream_t st, int s, int last, float* W, int64_t H, int D, const float* dY,
+                           int64_t n_dy, float* Y, float lr, int64_t xcap, const int32_t* per_step, bool table,
+                           unsigned long long* stamps) {
+    FAE_DISPATCH_D(D, return launch_x_step, c, st, s, last, W, H, D, dY, n_dy, Y, lr, xcap, per_step, table, stamps);
+    return FAE_OK;
+}
+
 static bool use_persist(Ctx* c) {
     const Group& g = c->grp;
     return g.P == 1 && !g.hot_off && c->world == 1 && c->persist;
@@ -995,7 +1238,7 @@ void group_free(Ctx* c) {
     for (int v = 0; v < 2; v++)
         for (int e = 0; e < 3 * kUnroll; e++)
             if (g.tev[v][e]) cudaEventDestroy(g.tev[v][e]);
-    void* ptrs[] = {g.desc, g.perm, g.rec, g.freer, g.nxt, g.lpart, g.lcnt, g.lmap, g.xcnt, g.keys[0], g.keys[1], g.vals, g.seg_start,
+    void* ptrs[] = {g.desc, g.perm, g.rec, g.freer, g.nxt, g.lpart, g.lcnt, g.lmap, g.xcnt, g.ptab, g.keys[0], g.keys[1], g.vals, g.seg_start,
                     g.seg_row, g.tile_start, g.tile_batch, g.sstatus, g.pstatus, g.ghist, g.cursor, g.done_ctr, g.pbar,
                     g.stamps};
     for (void* p : ptrs) cudaFree(p);
@@ -1005,6 +1248,42 @@ void group_free(Ctx* c) {
 }  // namespace fae
 
 using namespace fae;
+
+// Exchange-loop stamps of one call (n steps): per step, the forward from the
+// previous merge's end, the reduce-emit from the forward's end, the exchange
+// from the reduce's end (this rank's; its own last step: the previous merge)
+// to the first merge CTA, and the merge itself.
+static fae_status harvest_x(Ctx* c, int64_t n, int64_t xcap) {
+    Group& g = c->grp;
+    std::vector<unsigned long long> st(kSt * (n + 1));
+    FAE_CUDA(c, cudaMemcpyAsync(st.data(), g.stamps, sizeof(unsigned long long) * kSt * (n + 1),
+                                cudaMemcpyDeviceToHost, c->stream));
+    FAE_CUDA(c, cudaStreamSynchronize(c->stream));
+    unsigned long long prev_end = 0;
+    for (int64_t i = 0; i < n; i++) {
+        const unsigned long long fe = st[kSt * i + 1], fs = st[kSt * i + 5], re = st[kSt * i + 3];
+        const unsigned long long me0 = st[kSt * i + 10], me1 = st[kSt * i + 11];
+        if (me1 == 0 || me0 == ~0ull) continue;
+        unsigned long long x0 = prev_end;
+        if (fe && re) {
+            const unsigned long long f0 = prev_end ? prev_end : fs;
+            c->t_ms[0] += fe > f0 ? (double)(fe - f0) * 1e-6 : 0.0;
+            c->t_ms[1] += re > fe ? (double)(re - fe) * 1e-6 : 0.0;
+            c->t_n[0]++;
+            c->t_n[1]++;
+            x0 = re;
+        }
+        if (x0) {
+            c->t_x_ms[0] += me0 > x0 ? (double)(me0 - x0) * 1e-6 : 0.0;
+            c->t_x_ms[1] += me1 > me0 ? (double)(me1 - me0) * 1e-6 : 0.0;
+            c->t_x_n++;
+        }
+        prev_end = me1;
+    }
+    c->t_x_bytes += (double)n * xcap * (4.0 + 4.0 * g.dim);
+    c->t_x_steps += n;
+    return FAE_OK;
+}
 
 extern "C" fae_status fae_set_kernel_timing(fae_ctx* h, int32_t enable) {
     if (!h) return FAE_ERR_NOT_INIT;
@@ -1017,6 +1296,22 @@ extern "C" fae_status fae_set_kernel_timing(fae_ctx* h, int32_t enable) {
     h->c.t_persist = false;
     h->c.t_persist_batches = 0;
     h->c.t_red_entry_lead_ms = 0.0;
+    h->c.t_x_ms[0] = h->c.t_x_ms[1] = 0.0;
+    h->c.t_x_n = 0;
+    h->c.t_x_bytes = 0.0;
+    h->c.t_x_steps = 0;
+    return FAE_OK;
+}
+
+extern "C" fae_status fae_get_exchange_timing(const fae_ctx* h, double* out) {
+    if (!h || !out) return FAE_ERR_INVALID_ARG;
+    const Ctx* c = &h->c;
+    out[0] = c->t_x_ms[0];
+    out[1] = c->t_x_ms[1];
+    out[2] = (double)c->t_x_n;
+    out[3] = c->t_x_bytes;
+    out[4] = (double)c->t_x_steps;
+    out[5] = (double)c->grp.xcap_last;
     return FAE_OK;
 }
 
@@ -1059,17 +1354,52 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
     if (n == 0) return FAE_OK;
     // cursor, pad, run[0], run[1] — set by a kernel, not a host copy, so the
     // loop never queues behind a bulk host->device transfer on the copy engine
-    k_set_run<<<1, 32, 0, c->stream>>>(g.cursor, first, n);
-    FAE_LAUNCHED(c);
-    if (c->world > 1 || c->force_merge) {
+    // timing stamps (fae_set_kernel_timing(1)): kSt slots per step, reset here
+    auto stamps_init = [&](int64_t steps) -> fae_status {
+        if (g.stamp_cap < steps + 1) {
+            cudaFree(g.stamps);
+            g.stamps = nullptr;
+            g.stamp_cap = steps + steps / 4 + 64;
+            FAE_CUDA(c, cudaMalloc(&g.stamps, sizeof(unsigned long long) * kSt * g.stamp_cap));
+        }
+        std::vector<unsigned long long> init(kSt * (steps + 1));
+        for (int64_t i = 0; i <= steps; i++) {
+            init[kSt * i + 0] = ~0ull;
+            init[kSt * i + 1] = 0;
+            init[kSt * i + 2] = ~0ull;
+            init[kSt * i + 3] = 0;
+            init[kSt * i + 4] = ~0ull;
+            init[kSt * i + 5] = ~0ull;
+            init[kSt * i + 6] = 0;
+            init[kSt * i + 7] = 0;   // tier ends
+            for (int q = 8; q < kSt; q++) init[kSt * i + q] = 0;   // maxima
+            init[kSt * i + 10] = ~0ull;                             // merge entry (min)
+        }
+        FAE_CUDA(c, cudaMemcpyAsync(g.stamps, init.data(), sizeof(unsigned long long) * kSt * (steps + 1),
+                                    cudaMemcpyHostToDevice, c->stream));
+        FAE_CUDA(c, cudaStreamSynchronize(c->stream));
+        return FAE_OK;
+    };
+    const bool xpath = c->world > 1 || c->force_merge;
+    if (!xpath) {
+        // cursor, pad, run[0], run[1] — set by a kernel, not a host copy, so
+        // the loop never queues behind a bulk host->device transfer on the copy engine
+        k_set_run<<<1, 32, 0, c->stream>>>(g.cursor, first, n, n);
+        FAE_LAUNCHED(c);
+    }
+    if (xpath) {
         // a11 each step: emit the local sparse gradient, exchange, merge, apply.
         // Ranks may hold different numbers of hot batches: a rank past its
         // last batch contributes an empty gradient to every remaining
         // exchange.  Every step's per-rank gradient size is known after the
         // grouping, so all of them are exchanged once here (one all-gather,
-        // one host read) and the loop itself never synchronises the host.
+        // one host read); the loop itself is a replayed graph (NCCL) or a
+        // host loop of the same kernels (loopback test transport).
         if (!has_comm(c)) return set_err(c, FAE_ERR_NOT_INIT, "fae_train_hot_batches: world > 1 without a communicator");
         const int world = c->world;
+        const int64_t n_loc = std::max<int64_t>(0, std::min<int64_t>(n, g.n_batches - first));
+        k_set_run<<<1, 32, 0, c->stream>>>(g.cursor, first, n_loc, n);
+        FAE_LAUNCHED(c);
         if (g.cap_xcnt < 2 * n * world) {
             cudaFree(g.xcnt);
             g.xcnt = nullptr;
@@ -1077,8 +1407,7 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
             FAE_CUDA(c, cudaMalloc(&g.xcnt, sizeof(int32_t) * g.cap_xcnt));
         }
         std::vector<int32_t> mine(n, 0);
-        for (int64_t i = 0; i < n; i++)
-            if (first + i < g.n_batches) mine[i] = (int32_t)(g.hdesc[first + i].sb1 - g.hdesc[first + i].sb0);
+        for (int64_t i = 0; i < n_loc; i++) mine[i] = (int32_t)(g.hdesc[first + i].sb1 - g.hdesc[first + i].sb0);
         int32_t* all = g.xcnt;                 // [world][n]
         int32_t* per_step = g.xcnt + n * world;  // [n][world]
         FAE_CUDA(c, cudaMemcpyAsync(all + (int64_t)c->rank * n, mine.data(), sizeof(int32_t) * n,
@@ -1089,33 +1418,99 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
         std::vector<int32_t> hall((size_t)n * world), ht((size_t)n * world);
         FAE_CUDA(c, cudaMemcpyAsync(hall.data(), all, sizeof(int32_t) * n * world, cudaMemcpyDeviceToHost, c->stream));
         FAE_CUDA(c, cudaStreamSynchronize(c->stream));
-        std::vector<int64_t> cap(n, 0);
+        int64_t xcap = 1;
         for (int64_t i = 0; i < n; i++)
             for (int rk = 0; rk < world; rk++) {
                 const int32_t v = hall[(size_t)rk * n + i];
                 ht[(size_t)i * world + rk] = v;
-                cap[i] = std::max<int64_t>(cap[i], v);
+                xcap = std::max<int64_t>(xcap, v);
             }
+        // every rank saw the same counts, so every rank takes the same exit
+        if (xcap > c->g_cap) return set_err(c, FAE_ERR_CAPACITY, "fae_train_hot_batches: a rank's U exceeds capacity");
         FAE_CUDA(c, cudaMemcpyAsync(per_step, ht.data(), sizeof(int32_t) * n * world, cudaMemcpyHostToDevice,
                                     c->stream));
         FAE_CUDA(c, cudaStreamSynchronize(c->stream));   // ht is pageable and goes out of scope
-        for (int64_t i = 0; i < n; i++) {
-            int64_t U = 0;
-            const int32_t* rows = g.seg_row;
-            if (first + i < g.n_batches) {
-                fae_status st = launch_step(c, c->stream, W_hot, H, D, dY, n_dy, Y, lr, 1);
-                if (st != FAE_OK) return st;
-                FAE_LAUNCHED(c);
-                c->launches++;
-                const BatchDesc& d = g.hdesc[first + i];
-                rows = g.seg_row + d.sb0;
-                U = d.sb1 - d.sb0;
-            }
-            fae_status st = sync_merge_apply(c, rows, c->ws.grad, U, D, W_hot, H, lr, nullptr, nullptr, nullptr, 0,
-                                             per_step + i * world, cap[i]);
-            if (st != FAE_OK) return st;
+        g.xcap_last = xcap;
+        const bool table = c->merge_table >= 0 ? c->merge_table == 1 : world > 2;
+        if (table && g.cap_ptab < (int64_t)world * H) {
+            cudaFree(g.ptab);
+            g.ptab = nullptr;
+            g.cap_ptab = 0;
+            FAE_CUDA(c, cudaMalloc(&g.ptab, sizeof(int32_t) * world * std::max<int64_t>(H, 1)));
+            FAE_CUDA(c, cudaMemsetAsync(g.ptab, 0xff, sizeof(int32_t) * world * std::max<int64_t>(H, 1), c->stream));
+            g.cap_ptab = (int64_t)world * H;
         }
-        return FAE_OK;
+        unsigned long long* xst = nullptr;
+        if (c->timing == 1) {
+            fae_status sst = stamps_init(n);
+            if (sst != FAE_OK) return sst;
+            xst = g.stamps;
+        }
+        if (c->lb) {
+            // loopback (tests): host loop of the same kernels, step s of a
+            // kUnroll-step "replay" as in the graph (the next forward may read
+            // the base before a merge finishes, so only a replay's last merge
+            // advances it)
+            for (int64_t i = 0; i < n; i++) {
+                const int sidx = (int)(i % kUnroll);
+                fae_status st = launch_x(c, c->stream, sidx, sidx == kUnroll - 1 ? kUnroll : 0, W_hot, H, D, dY,
+                                         n_dy, Y, lr, xcap, per_step, table, xst);
+                if (st != FAE_OK) return st;
+            }
+            if (xst) {
+                fae_status hs = harvest_x(c, n, xcap);
+                if (hs != FAE_OK) return hs;
+            }
+            return coll_async_error(c, "fae_train_hot_batches");
+        }
+        uint64_t xkey = 1469598103934665603ull;
+        auto xmix = [&](uint64_t v) { xkey = (xkey ^ v) * 1099511628211ull; };
+        for (uint64_t v : {(uint64_t)(uintptr_t)W_hot, (uint64_t)H, (uint64_t)D, (uint64_t)(uintptr_t)dY,
+                           (uint64_t)n_dy, (uint64_t)(uintptr_t)Y, (uint64_t)xcap, (uint64_t)(uintptr_t)per_step,
+                           (uint64_t)table, (uint64_t)(uintptr_t)g.ptab, (uint64_t)(uintptr_t)g.perm,
+                           (uint64_t)(uintptr_t)g.rec, (uint64_t)(uintptr_t)g.desc, (uint64_t)(uintptr_t)g.lpart,
+                           (uint64_t)g.max_bags, (uint64_t)g.max_lchunk, (uint64_t)g.max_long,
+                           (uint64_t)(uintptr_t)c->comm, (uint64_t)(uintptr_t)g.seg_row,
+                           (uint64_t)(uintptr_t)g.lmap, (uint64_t)(uintptr_t)g.lcnt, (uint64_t)(uintptr_t)g.hot_idx,
+                           (uint64_t)(uintptr_t)g.hot_off, (uint64_t)c->rank, (uint64_t)world,
+                           (uint64_t)(uintptr_t)xst})
+            xmix(v);
+        uint32_t lb32;
+        memcpy(&lb32, &lr, 4);
+        xmix(lb32);
+        if (!g.xgraph || g.xgraph_key != xkey) {
+            if (g.xgraph) cudaGraphExecDestroy(g.xgraph);
+            g.xgraph = nullptr;
+            cudaStream_t cs2;
+            FAE_CUDA(c, cudaStreamCreateWithFlags(&cs2, cudaStreamNonBlocking));
+            cudaGraph_t graph;
+            const int64_t launches0 = c->launches;
+            FAE_CUDA(c, cudaStreamBeginCapture(cs2, cudaStreamCaptureModeThreadLocal));
+            fae_status st = FAE_OK;
+            for (int s = 0; s < kUnroll && st == FAE_OK; s++)
+                st = launch_x(c, cs2, s, s == kUnroll - 1 ? kUnroll : 0, W_hot, H, D, dY, n_dy, Y, lr, xcap, per_step,
+                              table, xst);
+            cudaError_t e = cudaStreamEndCapture(cs2, &graph);
+            c->launches = launches0;
+            if (st != FAE_OK || e != cudaSuccess) {
+                if (e == cudaSuccess) cudaGraphDestroy(graph);
+                cudaStreamDestroy(cs2);
+                return st != FAE_OK ? st : cuda_err(c, e, "cudaStreamEndCapture (exchange)");
+            }
+            e = cudaGraphInstantiate(&g.xgraph, graph, 0);
+            cudaGraphDestroy(graph);
+            cudaStreamDestroy(cs2);
+            if (e != cudaSuccess) return cuda_err(c, e, "cudaGraphInstantiate (exchange)");
+            g.xgraph_key = xkey;
+        }
+        const int64_t reps = cdiv(n, kUnroll);
+        for (int64_t r = 0; r < reps; r++) FAE_CUDA(c, cudaGraphLaunch(g.xgraph, c->stream));
+        c->launches += reps * kUnroll * (table ? 4 : 3);
+        if (xst) {
+            fae_status hs = harvest_x(c, n, xcap);
+            if (hs != FAE_OK) return hs;
+        }
+        return coll_async_error(c, "fae_train_hot_batches");
     }
     if (use_persist(c) && c->timing != 2) {
         cudaEvent_t* ev = nullptr;
@@ -1207,28 +1602,9 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
     }
     unsigned long long* stamps = nullptr;
     if (c->timing == 1) {
-        if (g.stamp_cap < n + 1) {
-            cudaFree(g.stamps);
-            g.stamps = nullptr;
-            g.stamp_cap = n + n / 4 + 64;
-            FAE_CUDA(c, cudaMalloc(&g.stamps, sizeof(unsigned long long) * kSt * g.stamp_cap));
-        }
+        fae_status sst = stamps_init(n);
+        if (sst != FAE_OK) return sst;
         stamps = g.stamps;
-        std::vector<unsigned long long> init(kSt * (n + 1));
-        for (int64_t i = 0; i <= n; i++) {
-            init[kSt * i + 0] = ~0ull;
-            init[kSt * i + 1] = 0;
-            init[kSt * i + 2] = ~0ull;
-            init[kSt * i + 3] = 0;
-            init[kSt * i + 4] = ~0ull;
-            init[kSt * i + 5] = ~0ull;
-            init[kSt * i + 6] = 0;
-            init[kSt * i + 7] = 0;   // tier ends
-            for (int q = 8; q < kSt; q++) init[kSt * i + q] = 0;   // maxima
-        }
-        FAE_CUDA(c, cudaMemcpyAsync(stamps, init.data(), sizeof(unsigned long long) * kSt * (n + 1),
-                                    cudaMemcpyHostToDevice, c->stream));
-        FAE_CUDA(c, cudaStreamSynchronize(c->stream));
     }
     mix((uint64_t)(uintptr_t)stamps);
     if (!g.graph || g.graph_key != key) {

@@ -181,12 +181,17 @@ struct Group {
     uint32_t* ghist = nullptr;        // [n_batches][kMaxSortPasses][256]
     int64_t cap_T = 0, cap_Hh = 0;
     // epoch runner
-    int64_t* cursor = nullptr;        // device: [0] base / cursor, [2] first, [3] n
+    int64_t* cursor = nullptr;        // device: [0] base / cursor, [2] first, [3] n, [4] exchange steps
     int64_t* run = nullptr;
     uint32_t* done_ctr = nullptr;
     int32_t* lmap = nullptr;          // long chunk -> long record index (lmap_base per batch)
     int32_t* xcnt = nullptr;          // world > 1: every step's per-rank gradient sizes
     int64_t cap_xcnt = 0;
+    int32_t* ptab = nullptr;          // world > 2: [world][H] row -> position in a rank's gathered list
+    int64_t cap_ptab = 0;
+    cudaGraphExec_t xgraph = nullptr; // world > 1 (NCCL): kUnroll exchange steps
+    uint64_t xgraph_key = 0;
+    int64_t xcap_last = 0;            // entries per rank of the last call's exchange (padded)
     int64_t cap_lmap = 0;
     uint32_t* pbar = nullptr;         // persistent kernel: [0] arrivals, [1] abort, [2 + 32 c] CTA c's flag
 
@@ -232,6 +237,10 @@ struct Ctx {
     int64_t t_overlap_n = 0;          // steps whose reduce entered before the fwd ended
     double t_red_entry_lead_ms = 0.0; // sum of (fwd end - reduce entry)
     double t_tier_ms[2] = {0.0, 0.0}; // reduce tiers' completion after fwd end
+    double t_x_ms[2] = {0.0, 0.0};    // exchange loop: [0] all-gather (reduce end -> merge entry), [1] merge
+    int64_t t_x_n = 0;                // steps timed by t_x_ms
+    double t_x_bytes = 0.0;           // slot bytes one rank contributes, summed over timed steps
+    int64_t t_x_steps = 0;
     bool no_pdl = false;              // FAE_NO_PDL=1: plain serialized launches
     int fused_mode = -1;              // FAE_FUSED: -1 auto (D <= 16), 1 on, 0 off (P = 1, world 1)
     bool t_fused = false;             // timing came from the fused kernel
@@ -240,6 +249,7 @@ struct Ctx {
     bool persist = false;             // FAE_PERSIST=1: the persistent grid-barrier kernel
     int persist_mb = 0;               // FAE_PERSIST_MB: CTAs per SM (0 = occupancy limit)
     bool merge_sort = false;          // FAE_MERGE_SORT=1: sort-based merge of the exchanged gradients
+    int merge_table = -1;             // FAE_MERGE_TABLE: exchange merge by position table (1) / search (0) / auto
     bool force_merge = false;         // FAE_FORCE_MERGE=1: the multi-rank exchange loop even at world 1 (tests)
     bool gs_generic = false;          // FAE_GS_GENERIC=1: radix-pass grouping even where the unit path applies
     bool cls_legacy = false;          // FAE_CLS_LEGACY=1: the round-1 one-tile-per-CTA classify kernel

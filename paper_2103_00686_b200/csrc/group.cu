@@ -931,7 +931,7 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
     if ((st = ensure(c, &g.ghist, &g.cap_Hh, std::max<int64_t>(nb, 1) * kMaxSortPasses * kSortBins)) != FAE_OK)
         return st;
     if (!g.cursor) {
-        FAE_CUDA(c, cudaMalloc(&g.cursor, sizeof(int64_t) * 4));
+        FAE_CUDA(c, cudaMalloc(&g.cursor, sizeof(int64_t) * 8));
         g.run = g.cursor + 2;
         FAE_CUDA(c, cudaMalloc(&g.done_ctr, sizeof(uint32_t) * 16));
         FAE_CUDA(c, cudaMemset(g.done_ctr, 0, sizeof(uint32_t) * 16));

@@ -253,15 +253,19 @@ def _oracle_prep(cfg, full, R, x, seed, t, small):
     return oracle.remap(full.rows, hot)
 
 
-@pytest.mark.parametrize("world,cfgname,R,t,small,standalone", [
-    (2, "kaggle-small", 200_000, 1e-5, 1 << 20, False),
-    (4, "kaggle-small", 200_000, 1e-5, 1 << 20, False),
-    (8, "tiny", 40_000, 1e-2, 0, False),
-    (3, "ali-small", 24_000, 1e-7, 1 << 20, False),
-    (4, "tiny", 20_000, 1e-2, 0, True),            # fae_emb_fwd + fae_emb_bwd_update with a comm
+@pytest.mark.parametrize("world,cfgname,R,t,small,standalone,table", [
+    (2, "kaggle-small", 200_000, 1e-5, 1 << 20, False, None),   # merge by binary search
+    (2, "kaggle-small", 200_000, 1e-5, 1 << 20, False, "1"),    # merge by row-position table
+    (4, "kaggle-small", 200_000, 1e-5, 1 << 20, False, None),   # table (default above 2 ranks)
+    (4, "kaggle-small", 200_000, 1e-5, 1 << 20, False, "0"),
+    (8, "tiny", 40_000, 1e-2, 0, False, None),
+    (3, "ali-small", 24_000, 1e-7, 1 << 20, False, None),
+    (4, "tiny", 20_000, 1e-2, 0, True, None),            # fae_emb_fwd + fae_emb_bwd_update with a comm
 ])
-def test_train_world_equals_oracle_global_batches(world, cfgname, R, t, small, standalone):
+def test_train_world_equals_oracle_global_batches(world, cfgname, R, t, small, standalone, table, monkeypatch):
     m = fae()
+    if table is not None:
+        monkeypatch.setenv("FAE_MERGE_TABLE", table)   # read at fae_create
     cfg = config(cfgname)
     x, seed, lr = 5.0, 3, 0.05
     full = gen.make_dataset(cfg, n_records=R, seed=23)

@@ -482,33 +482,50 @@ def test_grouping_unit_path_equals_generic(dev, cfg, R, pool, monkeypatch):
 @pytest.mark.parametrize("cfg", ["kaggle", "tb-small"])
 def test_train_exchange_loop_world1(dev, cfg, monkeypatch):
     """The multi-rank training loop (per-step sparse-gradient exchange over
-    NCCL, every step's sizes exchanged once up front, rank-ordered merge)
-    run on a 1-rank communicator == the single-GPU loop, bit for bit."""
+    NCCL: reduce-emit into the rank's slot, in-place all-gather, rank-ordered
+    merge, replayed from a captured graph of 128 steps) on a 1-rank
+    communicator == the single-GPU loop, bit for bit: more than one graph
+    replay, a call split in two ranges, both merge variants (binary search /
+    row-position table)."""
     m = fae()
     from paper_2103_00686_b200.pipeline import FaePipeline
     c = TB_SMALL if cfg == "tb-small" else gen.CONFIGS[cfg]
     R = 30_000 if cfg == "tb-small" else 100_000
+    if cfg == "kaggle":
+        c = gen.Config("kaggle-b32", c.rows, c.dim, 32, 1, records=R, t=c.t)
     ds = gen.make_dataset(c, n_records=R, seed=8)
     dd = ds.to(dev)
     W = gen.make_weights(sum(ds.rows), c.dim)
     outs = []
-    for force in ("0", "1"):
+    for force, table in (("0", "0"), ("1", "0"), ("1", "1")):
         monkeypatch.setenv("FAE_FORCE_MERGE", force)   # read at fae_create
+        monkeypatch.setenv("FAE_MERGE_TABLE", table)
         pipe = FaePipeline(ds.rows, c.dim, c.batch, c.pool, max_pool=max(c.pool, 1))
         if force == "1":
             m.fae_comm_init(pipe.ctx, m.fae_get_nccl_id(), 0, 1)
         prep = pipe.preprocess(dd.idx, dd.off, R, x_pct=5.0, seed=2, t=1e-6, small_table_bytes=1 << 20)
         W_hot = pipe.extract(W.to(dev), prep).clone()
         pipe.group(prep)
-        nb = min(prep.packed["n_hot_batches"], 12)
+        nb = min(prep.packed["n_hot_batches"], 300)
+        if cfg == "kaggle":
+            assert nb > 128, "more than one replay of the captured exchange graph"
         S = c.batch * c.n_tables
         dY = gen.make_dy(nb * S, c.dim, seed=10).view(nb, S, c.dim).to(dev)
         Y = torch.zeros(S, c.dim, device=dev)
-        pipe.train(W_hot, 0, nb, dY, Y, 0.05)
+        m.fae_set_kernel_timing(pipe.ctx, 1)
+        h = nb // 3
+        pipe.train(W_hot, 0, h, dY[:max(h, 1)], Y, 0.05)
+        pipe.train(W_hot, h, nb - h, dY[h:], Y, 0.05)
         pipe.ctx.check()
+        if force == "1":
+            xt = m.fae_get_exchange_timing(pipe.ctx)
+            assert xt["steps"] == nb and xt["steps_timed"] == nb and xt["xcap"] > 0
+            assert xt["allgather_ms"] >= 0 and xt["merge_ms"] > 0
+        m.fae_set_kernel_timing(pipe.ctx, 0)
         outs.append((W_hot.cpu(), Y.cpu()))
-    assert torch.equal(outs[0][0], outs[1][0])
-    assert torch.equal(outs[0][1], outs[1][1])
+    for o in outs[1:]:
+        assert torch.equal(outs[0][0], o[0])
+        assert torch.equal(outs[0][1], o[1])
 
 
 def test_merge_apply_equals_sort_merge(dev, monkeypatch):
