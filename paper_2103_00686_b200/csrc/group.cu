@@ -1065,6 +1065,21 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
             g.max_lchunk = std::max<int64_t>(g.max_lchunk, d.n_lchunk);
             g.n_long_total += S - d.n_short;
         }
+        if (getenv("FAE_VERBOSE") && nb > 0) {
+            double a[7] = {0, 0, 0, 0, 0, 0, 0};
+            for (const BatchDesc& d : g.hdesc) {
+                a[0] += d.n_tiny;
+                a[1] += d.n_short - d.n_tiny;
+                a[2] += d.n_med;
+                a[3] += (d.sb1 - d.sb0) - d.n_short - d.n_med;
+                a[4] += d.n_lchunk;
+                a[5] += d.n_free;
+                a[6] += (double)(d.lk1 - d.lk0);
+            }
+            fprintf(stderr, "[fae_group_batches] per batch: tiny %.0f short %.0f medium %.0f long %.0f (chunks %.0f) "
+                            "free %.0f lookups %.0f\n", a[0] / nb, a[1] / nb, a[2] / nb, a[3] / nb, a[4] / nb,
+                    a[5] / nb, a[6] / nb);
+        }
     }
     if (g.max_segs > c->ws.cap_L) return set_err(c, FAE_ERR_CAPACITY, "fae_group_batches: batch segments exceed ctx capacity");
     {   // grow-only (cudaFree would synchronise the device on every call)
