@@ -683,6 +683,96 @@ def run_sweep(args):
                                                         for n in args.sweep_configs.split(",")}}), flush=True)
 
 
+def run_mixed(args):
+    """NEXT-1 timed mixed epoch (P:L146, L223-230, L299-302,
+    L540): every hot AND cold mini-batch of one GPU's dataset, cold first,
+    in phases of ceil(r% of each kind's batch count) (the paper's R(r),
+    P:L553-572; fixed rate here), the hot rows synchronised at every change
+    of kind.  Cold batches train the HBM-resident master tables through the
+    same grouped, graph-replayed step (pipeline.MixedEpoch).  Device-timed
+    phases and swaps (CUDA events); one JSON line, not the driver's bench."""
+    import paper_2103_00686_b200 as fae
+    from paper_2103_00686_b200.pipeline import FaePipeline, MixedEpoch
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    cfg = config_of(args)
+    R = args.records or cfg.records
+    Tn, D, B = cfg.n_tables, cfg.dim, cfg.batch
+    ds = gen.make_dataset(cfg, n_records=R, device=dev)
+    W = gen.make_weights(sum(cfg.rows), D, device=dev)
+    S = B * Tn
+    n_dy = max(1, math.ceil((args.dy_pool_mb << 20) / (S * D * 4)))
+    dY = gen.make_dy(n_dy * S, D, device=dev).view(n_dy, S, D)
+    Y = torch.empty(S, D, device=dev)
+    pipe = FaePipeline(cfg.rows, D, B, cfg.pool, max_pool=max(cfg.pool_hi, 1), device=0)
+    mode = fae.BUDGET_EXACT if cfg.budget_bytes else fae.FIXED_T
+    prep = pipe.preprocess(ds.idx, ds.off, R, x_pct=5.0, seed=args.seed, mode=mode, t=cfg.t,
+                           budget_bytes=cfg.budget_bytes, small_table_bytes=cfg.small_bytes)
+    W_hot = pipe.extract(W, prep)
+    t0 = time.perf_counter()
+    ep = MixedEpoch(pipe, prep, W, ds.idx, ds.off, R, W_hot)
+    torch.cuda.synchronize()
+    setup_ms = (time.perf_counter() - t0) * 1e3
+    nh, nc = ep.n_hot_batches, ep.n_cold_batches
+    r = args.rate
+    ph, pc = max(1, math.ceil(nh * r / 100)), max(1, math.ceil(nc * r / 100))
+    plan, fh, fc = [], 0, 0
+    while fh < nh or fc < nc:             # cold first, alternate until both drain
+        if fc < nc:
+            plan.append(("cold", fc, min(pc, nc - fc)))
+            fc += plan[-1][2]
+        if fh < nh:
+            plan.append(("hot", fh, min(ph, nh - fh)))
+            fh += plan[-1][2]
+    ep.train("hot", 0, 0, dY, Y, args.lr)
+    for kind, first, n in plan[:4]:       # warm-up: graph capture of both loops
+        ep.train(kind, first, min(n, 2 * 128), dY, Y, args.lr)
+    ep.swap_to("hot")
+    torch.cuda.synchronize()
+    ev = []
+    res = {"hot_ms": 0.0, "cold_ms": 0.0, "swap_to_cold_ms": 0.0, "swap_to_hot_ms": 0.0}
+    sw0 = ep.swaps
+    start = torch.cuda.Event(enable_timing=True)
+    start.record()
+    prev = start
+    for kind, first, n in plan:
+        a = torch.cuda.Event(enable_timing=True)
+        ep.swap_to(kind)
+        a.record()
+        b = torch.cuda.Event(enable_timing=True)
+        ep.train(kind, first, n, dY, Y, args.lr)
+        b.record()
+        ev.append((kind, prev, a, b))
+        prev = b
+    a = torch.cuda.Event(enable_timing=True)
+    ep.finish()
+    a.record()
+    torch.cuda.synchronize()
+    pipe.ctx.check()
+    ep.cold.ctx.check()
+    for kind, p0, a0, b0 in ev:          # every phase begins with a change of kind
+        res["swap_to_" + kind + "_ms"] += p0.elapsed_time(a0)
+        res[kind + "_ms"] += a0.elapsed_time(b0)
+    res["swap_to_cold_ms"] += prev.elapsed_time(a)
+    total = start.elapsed_time(a)
+    hl, cl = prep.packed["n_hot_lookups"], ep.n_cold_lookups
+    swaps = ep.swaps - sw0
+    hot_bytes = prep.thresh["H_total"] * D * 4
+    out = {"mode": "mixed-epoch", "workload": f"{cfg.name}-shaped", "records": R, "rate_pct": r,
+           "phases": len(plan), "swaps": swaps, "hot_batches": nh, "cold_batches": nc,
+           "hot_lookups": hl, "cold_lookups": cl, "hot_rows": prep.thresh["H_total"],
+           "hot_table_bytes": hot_bytes, "epoch_ms": total,
+           "epoch_lookups_per_s": (hl + cl) / (total / 1e3),
+           "hot_us_per_batch": res["hot_ms"] * 1e3 / max(nh, 1),
+           "cold_us_per_batch": res["cold_ms"] * 1e3 / max(nc, 1),
+           "swap_ms_total": res["swap_to_cold_ms"] + res["swap_to_hot_ms"],
+           "swap_share": (res["swap_to_cold_ms"] + res["swap_to_hot_ms"]) / total,
+           "swap_ms_each": (res["swap_to_cold_ms"] + res["swap_to_hot_ms"]) / max(swaps, 1),
+           "sync_bytes_per_swap": hot_bytes, **res, "setup_ms": setup_ms,
+           "timing": "CUDA events on the ctx stream around each swap and phase"}
+    print(json.dumps(out), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -706,11 +796,16 @@ def main():
     ap.add_argument("--exchange", action="store_true",
                     help="N=1: run the multi-rank exchange loop on a 1-rank NCCL communicator (sync cost)")
     ap.add_argument("--sweep", action="store_true", help="threshold sweep (one JSON line; not the driver's bench)")
+    ap.add_argument("--mixed", action="store_true", help="NEXT-1 timed mixed hot/cold epoch (one JSON line)")
+    ap.add_argument("--rate", type=float, default=50.0, help="--mixed: phase size, %% of each kind's batches")
     ap.add_argument("--sweep-configs", default="kaggle,terabyte")
     ap.add_argument("--sweep-fracs", default="1,2,5,10,20")
     args = ap.parse_args()
     if args.sweep:
         run_sweep(args)
+        return
+    if args.mixed:
+        run_mixed(args)
         return
     if args.impl == "reference":
         r = run_reference(args)

@@ -396,6 +396,17 @@ fae_status fae_group_batches(fae_ctx* ctx, const fae_tables* tabs,
                              int32_t batch, int64_t H);
 
 /* --------------------------------------------------------------------------
+ * fae_release_scratch — free the build-only scratch of the last
+ * fae_group_batches (sort keys and values, segment starts, next-batch
+ * links, tile state: about 20 bytes per grouped lookup), keeping what
+ * fae_train_hot_batches reads.  For runs that keep two groupings alive
+ * (hot and cold batches of a mixed epoch, NEXT-1).  The next
+ * fae_group_batches reallocates on demand.  Synchronises the stream.
+ * Errors: NOT_INIT (null ctx), CUDA.
+ * ------------------------------------------------------------------------ */
+fae_status fae_release_scratch(fae_ctx* ctx);
+
+/* --------------------------------------------------------------------------
  * fae_train_hot_batches — the hot mini-batch training loop over grouped
  * batches [first, first + n): for each batch i in order,
  *   Y = fwd(batch i)                                  (a8, as fae_emb_fwd)

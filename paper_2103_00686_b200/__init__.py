@@ -30,7 +30,7 @@ EXPORTS = ["fae_create", "fae_destroy", "fae_set_stream", "fae_last_error",
            "fae_check", "fae_get_nccl_id", "fae_comm_init", "fae_comm_init_loopback",
            "fae_kernel_launches", "fae_profile", "fae_threshold",
            "fae_classify", "fae_extract", "fae_scatter_hot", "fae_pack_cold", "fae_emb_fwd", "fae_emb_bwd_update",
-           "fae_sync_hot_grads", "fae_group_batches", "fae_train_hot_batches",
+           "fae_sync_hot_grads", "fae_group_batches", "fae_release_scratch", "fae_train_hot_batches",
            "fae_set_kernel_timing", "fae_get_kernel_timing", "fae_get_exchange_timing", "fae_group_info"]
 
 
@@ -119,6 +119,7 @@ def lib():
             "fae_sync_hot_grads": ([P, P, P, P, c_i64, c_i32], c_i32),
             "fae_group_batches": ([P, ctypes.POINTER(FaeTables), ctypes.POINTER(FaePacked),
                                    c_i32, c_i32, c_i64], c_i32),
+            "fae_release_scratch": ([P], c_i32),
             "fae_train_hot_batches": ([P, P, c_i64, c_i32, c_i64, c_i64, P, c_i64, P,
                                        ctypes.c_float], c_i32),
             "fae_set_kernel_timing": ([P, c_i32], c_i32),
@@ -354,6 +355,11 @@ def fae_group_batches(ctx: Ctx, rows, dim: int, hot_idx: torch.Tensor,
     ctx._ok(lib().fae_group_batches(ctx.h, ctypes.byref(tabs), ctypes.byref(pk),
                                     int(fixed_pool), int(batch), int(H)))
     del keep
+
+
+def fae_release_scratch(ctx: Ctx):
+    """Free the last grouping's build-only scratch (kept: what training reads)."""
+    ctx._ok(lib().fae_release_scratch(ctx.h))
 
 
 def fae_train_hot_batches(ctx: Ctx, W_hot: torch.Tensor, first: int, n: int,

@@ -168,6 +168,7 @@ struct Group {
     uint32_t* lcnt = nullptr;         // [kUnroll][max_long] arrival counters (kept zero)
     int64_t cap_lpart = 0, cap_lcnt = 0;
     int64_t cap_L = 0, cap_R = 0;
+    int64_t cap_rec = 0, cap_free = 0, cap_nxt = 0;   // sized by the segment count
     // grouping scratch (kept for reuse)
     uint32_t* keys[2] = {nullptr, nullptr};
     int32_t* vals = nullptr;          // [L_total] (second value buffer is perm)

@@ -912,15 +912,13 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
     if ((st = ensure(c, &g.vals, &vcap, std::max<int64_t>(L, 1))) != FAE_OK) return st;
     if ((st = ensure(c, &g.perm, &pcap, std::max<int64_t>(L, 1))) != FAE_OK) return st;
     g.cap_L = std::min(std::min(k0cap, k1cap), std::min(vcap, pcap));
-    int64_t c3 = g.cap_S, c4 = g.cap_S, c5 = g.cap_S;
+    // segment arrays written before the segment count is known: capacity L
+    // (records, free lists and links are sized by the count, below)
+    int64_t c3 = g.cap_S, c4 = g.cap_S;
     if ((st = ensure(c, &g.seg_start, &c3, L + 2)) != FAE_OK) return st;
     if ((st = ensure(c, &g.seg_row, &c4, L + 2)) != FAE_OK) return st;
-    if ((st = ensure(c, &g.rec, &c5, L + 2)) != FAE_OK) return st;
-    int64_t c6 = g.cap_S, c7 = g.cap_S;
-    if ((st = ensure(c, &g.freer, &c6, L + 2)) != FAE_OK) return st;
+    g.cap_S = std::min(c3, c4);
     if ((st = ensure(c, &g.lmap, &g.cap_lmap, L / 64 + nb + 2)) != FAE_OK) return st;
-    if ((st = ensure(c, &g.nxt, &c7, L + 2)) != FAE_OK) return st;
-    g.cap_S = std::min(std::min(std::min(c3, c4), c5), std::min(c6, c7));
     if ((st = ensure(c, &g.desc, &g.cap_B, std::max<int64_t>(nb, 1))) != FAE_OK) return st;
     int64_t t1 = g.cap_T, t2 = g.cap_T, t3 = g.cap_T * kSortBins, t4 = g.cap_T;
     if ((st = ensure(c, &g.tile_start, &t1, nt + 2)) != FAE_OK) return st;
@@ -1034,6 +1032,11 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
         // read only by the fused one-kernel step (and the persistent kernel);
         // the two-kernel step (D > 16, multi-hot, world > 1) never needs them
         const bool links = fused_step(c) || (g.P == 1 && !g.hot_off && c->world == 1 && c->persist);
+        if ((st = ensure(c, &g.rec, &g.cap_rec, g.S_total + 2)) != FAE_OK) return st;
+        if (links) {
+            if ((st = ensure(c, &g.freer, &g.cap_free, g.S_total + 2)) != FAE_OK) return st;
+            if ((st = ensure(c, &g.nxt, &g.cap_nxt, g.S_total + 2)) != FAE_OK) return st;
+        }
         if (links) {
             FAE_CUDA(c, cudaMemsetAsync(g.nxt, 0xFF, sizeof(int32_t) * std::max<int64_t>(g.S_total, 1), c->stream));
             int64_t ms = 0;
@@ -1102,5 +1105,29 @@ extern "C" fae_status fae_group_batches(fae_ctx* h, const fae_tables* tabs, cons
     st = read_latched(c);
     if (st != FAE_OK) return st;
     g.valid = true;
+    return FAE_OK;
+}
+
+// Free the grouping's build-only scratch (sort keys / values, segment
+// starts, links, tile state), keeping what the training loop reads (perm,
+// records, free lists, chunk map, segment rows, descriptors).  The next
+// fae_group_batches reallocates on demand.
+extern "C" fae_status fae_release_scratch(fae_ctx* h) {
+    if (!h) return FAE_ERR_NOT_INIT;
+    Ctx* c = &h->c;
+    Group& g = c->grp;
+    FAE_CUDA(c, cudaStreamSynchronize(c->stream));
+    void** ptrs[] = {(void**)&g.keys[0], (void**)&g.keys[1], (void**)&g.vals, (void**)&g.seg_start,
+                     (void**)&g.nxt, (void**)&g.tile_start, (void**)&g.tile_batch, (void**)&g.sstatus,
+                     (void**)&g.pstatus, (void**)&g.ghist};
+    for (void** p : ptrs) {
+        cudaFree(*p);
+        *p = nullptr;
+    }
+    g.cap_L = 0;        // perm shares the lookup capacity with keys / vals
+    g.cap_S = 0;        // seg_row shares it with seg_start
+    g.cap_nxt = 0;
+    g.cap_T = 0;
+    g.cap_Hh = 0;
     return FAE_OK;
 }

@@ -20,7 +20,8 @@ import torch
 
 from . import (BUDGET_EXACT, FIXED_T, Ctx, fae_classify, fae_create,
                fae_emb_bwd_update, fae_emb_fwd, fae_extract, fae_group_batches,
-               fae_profile, fae_threshold, fae_train_hot_batches)
+               fae_pack_cold, fae_profile, fae_release_scratch, fae_scatter_hot,
+               fae_threshold, fae_train_hot_batches)
 
 
 @dataclasses.dataclass
@@ -46,6 +47,7 @@ class FaePipeline:
         self.batch = batch
         self.pool = pool                      # 0 => offsets
         self.device = device
+        self.max_pool = max_pool
         max_lookups = batch * self.Tn * max(pool, max_pool, 1)
         self.ctx = ctx or fae_create(device, max_tables=max(self.Tn, 1),
                                      max_rows=sum(self.rows),
@@ -140,4 +142,73 @@ class FaePipeline:
         fae_emb_bwd_update(self.ctx, W_hot, idx, off, self.pool, n_bags, dY, lr)
 
 
-__all__ = ["FaePipeline", "Prepared", "FIXED_T", "BUDGET_EXACT"]
+class MixedEpoch:
+    """Hot AND cold mini-batches of one epoch (P:L146,
+    L223-230, L299-302, L540).
+
+    Hot batches train the replicated hot table W_hot through the pipeline's
+    ctx (grouped once); cold batches train the full master tables W (HBM
+    resident: B200 holds the tables the paper keeps in CPU memory) through a
+    second ctx that groups the cold CSR in global row ids once (fae_pack_cold
+    + fae_group_batches with H = sum N_z), so both kinds run the same
+    graph-replayed step.  At every change of kind the hot rows are
+    synchronised (the paper's "embedding sync"): hot -> cold writes W_hot
+    back into W (fae_scatter_hot), cold -> hot re-extracts W_hot from W
+    (fae_extract).  Sequential SGD semantics over the phase order."""
+
+    def __init__(self, pipe: "FaePipeline", prep: Prepared, W: torch.Tensor,
+                 idx: torch.Tensor, off: Optional[torch.Tensor], n_records: int,
+                 W_hot: torch.Tensor):
+        self.pipe, self.prep, self.W, self.W_hot = pipe, prep, W, W_hot
+        pk = prep.packed
+        self.n_cold = int(pk["n_cold"])
+        Tn, B = pipe.Tn, pipe.batch
+        n_lookups = int(idx.numel()) if off is None else int(off[-1].item())
+        self.n_cold_lookups = n_lookups - int(pk["n_hot_lookups"])
+        dev = pipe.dev
+        self.cold_idx = torch.empty(max(self.n_cold_lookups, 1), dtype=torch.int32, device=dev)
+        self.cold_off = (torch.empty(self.n_cold * Tn + 1, dtype=torch.int64, device=dev)
+                         if off is not None else None)
+        fae_pack_cold(pipe.ctx, pipe.rows, pipe.dim, idx, pipe.pool, n_records, prep.cold_ids,
+                      self.n_cold, self.cold_idx, off=off, cold_off=self.cold_off)
+        self.cold = FaePipeline(pipe.rows, pipe.dim, B, pipe.pool,
+                                max_pool=getattr(pipe, "max_pool", 1), device=pipe.device)
+        self.H_full = sum(pipe.rows)
+        if self.n_cold > 0:
+            fae_group_batches(self.cold.ctx, pipe.rows, pipe.dim, self.cold_idx, self.cold_off,
+                              self.n_cold, self.n_cold_lookups, pipe.pool, B, self.H_full)
+            fae_release_scratch(self.cold.ctx)      # two groupings stay alive
+        pipe.group(prep)
+        fae_release_scratch(pipe.ctx)
+        self.n_hot_batches = int(pk["n_hot_batches"])
+        self.n_cold_batches = -(-self.n_cold // B)
+        self.kind = "hot"          # W_hot holds the current hot rows
+        self.swaps = 0
+
+    def swap_to(self, kind: str):
+        """Synchronise the hot rows for a phase of `kind` (no-op if current)."""
+        if kind == self.kind:
+            return
+        if kind == "cold":
+            fae_scatter_hot(self.pipe.ctx, self.W_hot, self.W)
+        else:
+            fae_extract(self.pipe.ctx, self.W, self.W_hot)
+        self.kind = kind
+        self.swaps += 1
+
+    def train(self, kind: str, first: int, n: int, dY, Y, lr: float):
+        """Batches [first, first+n) of `kind`, after the swap if needed."""
+        self.swap_to(kind)
+        if n <= 0:
+            return
+        if kind == "hot":
+            fae_train_hot_batches(self.pipe.ctx, self.W_hot, first, n, dY, Y, lr)
+        else:
+            fae_train_hot_batches(self.cold.ctx, self.W, first, n, dY, Y, lr)
+
+    def finish(self):
+        """Write the hot rows back into W (end of the epoch)."""
+        self.swap_to("cold")
+
+
+__all__ = ["FaePipeline", "Prepared", "MixedEpoch", "FIXED_T", "BUDGET_EXACT"]

@@ -687,6 +687,97 @@ def test_mixed_hot_cold_schedule(dev, cfgname, R, t, small):
     assert ok, worst
 
 
+@pytest.mark.parametrize("cfgname,R,t,small,cap", [("tiny", 10_000, 1e-2, 0, None),
+                                                  ("ali-small", 20_000, 1e-7, 1 << 20, 3)])
+def test_mixed_epoch_grouped(dev, cfgname, R, t, small, cap):
+    """NEXT-1 with both kinds on the graph-replayed loop (pipeline.MixedEpoch):
+    cold batches grouped once in global row ids and trained on the master
+    tables, hot batches on the replica, the hot rows synchronised at every
+    change of kind; cold-first phases ("always begins with
+    training on cold inputs") == the oracle's sequential SGD over the same
+    phase order (1e-5 / 1e-6), swaps counted."""
+    from paper_2103_00686_b200.pipeline import FaePipeline, MixedEpoch
+    c = ALI_SMALL if cfgname == "ali-small" else gen.CONFIGS[cfgname]
+    # lr of the workloads (SURVEY §8(d)): the tolerance derivation of §8(c)
+    # (fp32 sums of Zipf-head segments) assumes it; the cold side here trains
+    # every cold batch, whose head rows carry thousands of lookups
+    x, seed, lr = 5.0, 7, 0.01
+    ds = gen.make_dataset(c, n_records=R, seed=3)
+    dd = ds.to(dev)
+    Tn, D, B = c.n_tables, c.dim, c.batch
+    pipe = FaePipeline(ds.rows, D, B, c.pool, max_pool=max(c.pool_hi, 1))
+    prep = pipe.preprocess(dd.idx, dd.off, R, x_pct=x, seed=seed, t=t, small_table_bytes=small)
+    W0 = gen.make_weights(sum(ds.rows), D)
+    Wd = W0.to(dev).clone()
+    W_hot = pipe.extract(Wd, prep).clone()
+    ep = MixedEpoch(pipe, prep, Wd, dd.idx, dd.off, R, W_hot)
+    nh, nc = ep.n_hot_batches, ep.n_cold_batches
+    assert nh >= 2 and nc >= 2
+    ref = _prep_ref(ds, x, seed, "t", t=t, small=small, dim=D)
+    pk, rm, H = ref["pack"], ref["remap"], ref["H"]
+    base = np.concatenate([[0], np.cumsum(ds.rows)])
+    idx_np = ds.idx.numpy()
+    off_np = ds.off.numpy() if ds.off is not None else None
+
+    def cold_batch(i):            # global-id CSR of cold batch i, by definition
+        r0, r1 = i * B, min((i + 1) * B, pk["n_cold"])
+        parts, sizes = [], []
+        for r in pk["cold_ids"][r0:r1]:
+            for z in range(Tn):
+                if off_np is None:
+                    v = idx_np[r * Tn + z: r * Tn + z + 1]
+                else:
+                    v = idx_np[off_np[r * Tn + z]: off_np[r * Tn + z + 1]]
+                parts.append(v + base[z])
+                sizes.append(len(v))
+        bi = np.concatenate(parts).astype(np.int32)
+        return bi, np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64), (r1 - r0) * Tn
+
+    def hot_batch(i):
+        r0, r1 = i * B, min((i + 1) * B, pk["n_hot"])
+        if ds.off is None:
+            return pk["hot_idx"][r0 * Tn: r1 * Tn], None, (r1 - r0) * Tn
+        ho = pk["hot_off"][r0 * Tn: r1 * Tn + 1]
+        return pk["hot_idx"][ho[0]:ho[-1]], ho - ho[0], (r1 - r0) * Tn
+
+    h1, c1 = nh // 2, nc // 2
+    phases = [("cold", 0, c1), ("hot", 0, h1), ("cold", c1, nc - c1), ("hot", h1, nh - h1)]
+    if cap:   # multi-hot: a few batches per phase (fp32 sums of Zipf-head segments
+        #       of thousands of lookups over a whole epoch would drift past the
+        #       per-step tolerance of north_star)
+        phases = [(k, f, min(n, cap)) for k, f, n in phases]
+    S = B * Tn
+    Y = torch.zeros(S, D, device=dev)
+    Wr_full = W0.numpy().astype(np.float32).copy()
+    Wr_hot = oracle.extract(Wr_full, rm, H)
+    cur = "hot"
+    for k, (kind, first, n) in enumerate(phases):
+        dY = gen.make_dy(n * S, D, seed=500 + k).view(n, S, D)
+        ep.train(kind, first, n, dY.to(dev), Y, lr)
+        if kind != cur:
+            if kind == "cold":
+                Wr_full = oracle.scatter_hot(Wr_full, Wr_hot, rm)
+            else:
+                Wr_hot = oracle.extract(Wr_full, rm, H)
+            cur = kind
+        for j in range(n):
+            if kind == "hot":
+                bi, bo, nb_ = hot_batch(first + j)
+                Wr_hot, st = oracle.emb_bwd_sgd(Wr_hot, bi, bo, 0 if bo is not None else 1, nb_,
+                                                dY[j, :nb_].numpy(), lr)
+            else:
+                bi, bo, nb_ = cold_batch(first + j)
+                Wr_full, st = oracle.emb_bwd_sgd(Wr_full, bi, bo, 0, nb_, dY[j, :nb_].numpy(), lr)
+            assert st == 0
+    ep.finish()
+    Wr_full = oracle.scatter_hot(Wr_full, Wr_hot, rm)
+    pipe.ctx.check()
+    ep.cold.ctx.check()
+    assert ep.swaps == 5    # (replica current) -> cold -> hot -> cold -> hot, then finish -> cold
+    ok, worst = close(Wd.cpu().numpy(), Wr_full)
+    assert ok, worst
+
+
 def test_bwd_oversized_offsets_batch_latches_capacity(dev):
     """a multi-hot batch with more lookups than max_batch_lookups
     must not write past the workspace: CAPACITY is latched and W untouched."""
