@@ -481,6 +481,61 @@ fae_status fae_get_kernel_timing(const fae_ctx* ctx, double* ms, int64_t* n);
  * Errors: INVALID_ARG (null). */
 fae_status fae_get_exchange_timing(const fae_ctx* ctx, double* out);
 
+/* ==========================================================================
+ * Scheduler (§4.3 "Communication Overheads",
+ * P:L538-572, Eq. 5 `eqn:scheduler` P:L550-557): the interleaving of cold
+ * and hot mini-batches of an epoch and its loss-feedback rate.  Host-only
+ * state machine (no GPU work); the caller runs the phases (e.g. the hot
+ * loop on W_hot, the cold loop on the master tables) and reports the test
+ * loss at every swap boundary.  Readings R28-R31:
+ *  - R(r): a phase issues ceil(r% * the kind's per-epoch batch count)
+ *    batches (>= 1) of one kind; r in [1, 100].
+ *  - cold first, start R(50); once a kind is drained the
+ *    rest of the other kind is one phase.
+ *  - Eq. 5 at each swap with the post-swap test loss L_i: L_i > L_{i-1}
+ *    halves r (clamp 1); else if the last u losses each strictly decreased
+ *    (sliding window, u = 4) r doubles (clamp 100); else
+ *    unchanged.  The first loss changes nothing.
+ *  - each swap logs n_devices sync events of hot_bytes.
+ *  - the rate persists across epochs (fae_sched_new_epoch).
+ * The struct is caller-owned plain data; fields are read-only to callers.
+ * ========================================================================== */
+#define FAE_SCHED_COLD 0
+#define FAE_SCHED_HOT 1
+#define FAE_SCHED_MAX_U 64
+typedef struct fae_sched {
+    int64_t n[2];            /* batches per epoch: [COLD], [HOT] */
+    int64_t done[2];         /* issued this epoch */
+    double r;                /* current rate r(i), percent */
+    int32_t u;               /* successive-decrease window */
+    int32_t next_kind;       /* kind the next phase prefers */
+    int32_t last_kind;       /* kind of the last issued phase, -1 none */
+    int32_t n_hist;          /* losses kept (<= u + 1) */
+    double hist[FAE_SCHED_MAX_U + 1];   /* the last n_hist losses, oldest first */
+    int64_t swaps;           /* swap boundaries recorded (all epochs) */
+    int64_t sync_events;     /* n_devices per swap */
+    int64_t sync_bytes;      /* hot_bytes * n_devices per swap */
+} fae_sched;
+
+/* n_cold / n_hot >= 0 batches per epoch, r_start in [1, 100], u in
+ * [1, FAE_SCHED_MAX_U].  Errors: INVALID_ARG. */
+fae_status fae_sched_init(fae_sched* s, int64_t n_cold, int64_t n_hot,
+                          double r_start, int32_t u);
+/* Next phase: *kind (FAE_SCHED_COLD / HOT), batches [*first, *first +
+ * *count) of that kind; *count = 0 once both kinds are drained.
+ * *swap_after = 1 when a phase of the other kind will follow, i.e. the
+ * caller must synchronise the hot rows and call fae_sched_record_swap with
+ * the post-swap test loss before the next fae_sched_next.
+ * Errors: INVALID_ARG (null). */
+fae_status fae_sched_next(fae_sched* s, int32_t* kind, int64_t* first,
+                          int64_t* count, int32_t* swap_after);
+/* Swap boundary: sync accounting, then Eq. 5 with test_loss (finite).
+ * Errors: INVALID_ARG (null, non-finite loss, n_devices < 1, hot_bytes < 0). */
+fae_status fae_sched_record_swap(fae_sched* s, double test_loss,
+                                 int64_t hot_bytes, int32_t n_devices);
+/* Restart the epoch's queues (rate, history and counters persist). */
+fae_status fae_sched_new_epoch(fae_sched* s);
+
 #ifdef __cplusplus
 }
 #endif

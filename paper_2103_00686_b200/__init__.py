@@ -31,7 +31,19 @@ EXPORTS = ["fae_create", "fae_destroy", "fae_set_stream", "fae_last_error",
            "fae_kernel_launches", "fae_profile", "fae_threshold",
            "fae_classify", "fae_extract", "fae_scatter_hot", "fae_pack_cold", "fae_emb_fwd", "fae_emb_bwd_update",
            "fae_sync_hot_grads", "fae_group_batches", "fae_release_scratch", "fae_train_hot_batches",
-           "fae_set_kernel_timing", "fae_get_kernel_timing", "fae_get_exchange_timing", "fae_group_info"]
+           "fae_set_kernel_timing", "fae_get_kernel_timing", "fae_get_exchange_timing", "fae_group_info",
+           "fae_sched_init", "fae_sched_next", "fae_sched_record_swap", "fae_sched_new_epoch"]
+
+
+SCHED_MAX_U = 64
+
+
+class FaeSched(ctypes.Structure):
+    """fae_sched (include/fae.h): the scheduler's plain state (NEXT-3)."""
+    _fields_ = [("n", ctypes.c_int64 * 2), ("done", ctypes.c_int64 * 2), ("r", ctypes.c_double),
+                ("u", ctypes.c_int32), ("next_kind", ctypes.c_int32), ("last_kind", ctypes.c_int32),
+                ("n_hist", ctypes.c_int32), ("hist", ctypes.c_double * (SCHED_MAX_U + 1)),
+                ("swaps", ctypes.c_int64), ("sync_events", ctypes.c_int64), ("sync_bytes", ctypes.c_int64)]
 
 
 class FaeError(RuntimeError):
@@ -126,6 +138,10 @@ def lib():
             "fae_get_kernel_timing": ([P, P, P], c_i32),
             "fae_get_exchange_timing": ([P, P], c_i32),
             "fae_group_info": ([P, P], c_i32),
+            "fae_sched_init": ([ctypes.POINTER(FaeSched), c_i64, c_i64, c_dbl, c_i32], c_i32),
+            "fae_sched_next": ([ctypes.POINTER(FaeSched), P, P, P, P], c_i32),
+            "fae_sched_record_swap": ([ctypes.POINTER(FaeSched), c_dbl, c_i64, c_i32], c_i32),
+            "fae_sched_new_epoch": ([ctypes.POINTER(FaeSched)], c_i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -407,3 +423,45 @@ def fae_group_info(ctx: Ctx) -> dict:
     keys = ("n_batches", "lookups", "long_segments", "segments", "max_long", "max_bags",
             "free_segments", "fused")
     return dict(zip(keys, [int(v) for v in info]))
+
+
+# ---------------------------------------------------------------------------
+# scheduler (NEXT-3, host-only; §4.3 Eq. 5)
+# ---------------------------------------------------------------------------
+class Scheduler:
+    """Cold/hot phase interleaving with Eq. 5's loss-feedback rate
+    (libfae's fae_sched_*; argument marshalling only)."""
+    KINDS = ("cold", "hot")
+
+    def __init__(self, n_cold: int, n_hot: int, r_start: float = 50.0, u: int = 4):
+        self.s = FaeSched()
+        st = lib().fae_sched_init(ctypes.byref(self.s), int(n_cold), int(n_hot), float(r_start), int(u))
+        if st != 0:
+            raise FaeError(st, "fae_sched_init: bad arguments")
+
+    def next_phase(self):
+        """(kind, first, count, swap_after) or None once both kinds are drained."""
+        k, f, c, w = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
+        st = lib().fae_sched_next(ctypes.byref(self.s), ctypes.byref(k), ctypes.byref(f), ctypes.byref(c),
+                                  ctypes.byref(w))
+        if st != 0:
+            raise FaeError(st, "fae_sched_next")
+        if c.value == 0:
+            return None
+        return self.KINDS[k.value], int(f.value), int(c.value), bool(w.value)
+
+    def record_swap(self, test_loss: float, hot_bytes: int = 0, n_devices: int = 1):
+        st = lib().fae_sched_record_swap(ctypes.byref(self.s), float(test_loss), int(hot_bytes), int(n_devices))
+        if st != 0:
+            raise FaeError(st, "fae_sched_record_swap: bad arguments")
+
+    def new_epoch(self):
+        lib().fae_sched_new_epoch(ctypes.byref(self.s))
+
+    @property
+    def rate(self) -> float:
+        return float(self.s.r)
+
+    @property
+    def swaps(self) -> int:
+        return int(self.s.swaps)
