@@ -298,3 +298,56 @@ def make_dy(n_bags: int, dim: int, seed: int = BASE_SEED + 1000,
             device="cpu") -> torch.Tensor:
     """Upstream gradient dY ~ U(-1, 1), fp32 [n_bags, dim]."""
     return make_weights(n_bags, dim, seed, device, -1.0, 1.0)
+
+
+# ----------------------------------------------------------------------------
+# DLRM inputs (NEXT-2): dense features, labels, random-init MLP parameters
+# ----------------------------------------------------------------------------
+def make_dense(n_records: int, n_dense: int, seed: int = BASE_SEED + 3000,
+               device="cpu", record_base: int = 0) -> torch.Tensor:
+    """Dense features fp32 [n_records, n_dense] ~ U(0, 4) (the range of
+    Criteo's log(1 + x) dense features), counter (record, feature)."""
+    dev = torch.device(device)
+    ctr = (torch.arange(n_records, device=dev, dtype=torch.int64) + record_base).unsqueeze(1) * n_dense + \
+        torch.arange(n_dense, device=dev, dtype=torch.int64)
+    return (4.0 * uniform01(seed, ctr.reshape(-1))).float().view(n_records, n_dense)
+
+
+def make_labels(n_records: int, n_dense: int, seed: int = BASE_SEED + 4000,
+                device="cpu", record_base: int = 0, dense_seed: int = BASE_SEED + 3000) -> torch.Tensor:
+    """Click labels fp32 {0, 1} [n_records] with a planted, learnable rule:
+    P(click) = 0.7 if dense feature 0 (of make_dense(..., dense_seed)) > 2
+    else 0.1 (about 40% positives)."""
+    d0 = make_dense(n_records, n_dense, seed=dense_seed, device=device, record_base=record_base)[:, 0].double()
+    dev = torch.device(device)
+    u = uniform01(seed, torch.arange(n_records, device=dev, dtype=torch.int64) + record_base)
+    p = torch.where(d0 > 2.0, torch.full_like(d0, 0.7), torch.full_like(d0, 0.1))
+    return (u < p).float()
+
+
+def dlrm_dims(n_dense: int, bottom, top, n_tables: int, dim: int):
+    """[(in, out)] of every bottom then top layer (flat-parameter order)."""
+    dims, prev = [], n_dense
+    for w in bottom:
+        dims.append((prev, w))
+        prev = w
+    F = n_tables + 1
+    prev = dim + F * (F - 1) // 2
+    for w in top:
+        dims.append((prev, w))
+        prev = w
+    return dims
+
+
+def make_dlrm_params(dims, seed: int = BASE_SEED + 5000, device="cpu") -> torch.Tensor:
+    """Random-init flat parameters (per layer W [out][in] then b [out]),
+    U(-1/sqrt(in), 1/sqrt(in)) like PyTorch's Linear default."""
+    dev = torch.device(device)
+    parts, o = [], 0
+    for i, n in dims:
+        k = (i * n + n)
+        ctr = torch.arange(o, o + k, device=dev, dtype=torch.int64)
+        a = 1.0 / (i ** 0.5)
+        parts.append((-a + 2 * a * uniform01(seed, ctr)).float())
+        o += k
+    return torch.cat(parts)

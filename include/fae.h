@@ -536,6 +536,76 @@ fae_status fae_sched_record_swap(fae_sched* s, double test_loss,
 /* Restart the epoch's queues (rate, history and counters persist). */
 fae_status fae_sched_new_epoch(fae_sched* s);
 
+/* ==========================================================================
+ * DLRM hot step: the model a hot mini-batch trains
+ * "entirely on the GPU" — bottom MLP over the dense features,
+ * the embedding bags (a8), "dot" feature interaction, top MLP, logarithmic
+ * loss, backward, SGD; widths from tab:benchmarks
+ * (e.g. RMC2 13-512-256-64-16 / 512-256-1) or SYN-M1..M4
+ * (P:L892-914).  Readings R32-R34: ReLU after every bottom
+ * layer and every top layer but the last (linear logit, sigmoid inside the
+ * loss); interaction input T = [bottom output, Y_0 .. Y_{Tn-1}], output
+ * [bottom output, <T_i, T_j> for i > j in row-major (i, j) order]; loss =
+ * mean over the batch of the log loss; plain SGD of every weight and bias.
+ * Parameters: ONE caller-owned device fp32 buffer, per layer (bottom
+ * first, then top) W [out][in] row-major followed by b [out].
+ * GEMMs through cuBLAS (tf32 = 1: TF32 on the tensor cores; 0: pedantic
+ * fp32); everything else hand-written kernels; no allocation after create.
+ * ========================================================================== */
+#define FAE_DLRM_MAX_LAYERS 8
+typedef struct fae_dlrm_cfg {
+    int32_t n_dense;                        /* dense features per sample */
+    int32_t n_bottom;                       /* bottom layers */
+    int32_t bottom[FAE_DLRM_MAX_LAYERS];    /* widths; the last == dim */
+    int32_t n_top;                          /* top layers */
+    int32_t top[FAE_DLRM_MAX_LAYERS];       /* widths; the last == 1 */
+    int32_t n_tables;                       /* sparse features Tn */
+    int32_t dim;                            /* embedding dim D */
+    int32_t max_batch;                      /* samples per mini-batch */
+    int32_t tf32;                           /* 1: TF32 tensor-core GEMMs */
+} fae_dlrm_cfg;
+typedef struct fae_dlrm fae_dlrm;
+
+/* Parameter count of the flat buffer (-1: invalid configuration). */
+int64_t fae_dlrm_param_count(const fae_dlrm_cfg* cfg);
+/* Allocates the activations, gradients, interaction tables and a cuBLAS
+ * handle on ctx's device; uses ctx's stream.  Errors: INVALID_ARG, CUDA. */
+fae_status fae_dlrm_create(fae_ctx* ctx, const fae_dlrm_cfg* cfg,
+                           fae_dlrm** out);
+void fae_dlrm_destroy(fae_dlrm* m);
+/* One DLRM step on a batch of B <= max_batch samples (device pointers):
+ * dense [B][n_dense], label [B] (0 / 1), Y [B][Tn][D] (the a8 output);
+ * train = 1: backward + SGD of params (lr) and dY [B][Tn][D] = dL/dY (the
+ * a9 input; L = mean log loss); train = 0: forward only.  The summed
+ * per-sample loss and the sample count accumulate on the device
+ * (fae_dlrm_loss).  Asynchronous.  Errors: INVALID_ARG. */
+fae_status fae_dlrm_step(fae_dlrm* m, float* params, int32_t B,
+                         const float* dense, const float* label,
+                         const float* Y, float* dY, float lr, int32_t train);
+/* Host read of the accumulated {sum of per-sample losses, samples};
+ * reset = 1 zeroes them.  Synchronises the stream. */
+fae_status fae_dlrm_loss(fae_dlrm* m, double* sum_loss, double* n_samples,
+                         int32_t reset);
+/* The model's internal Y / dY batch buffers and loss accumulator (device),
+ * for callers that run a8 / a9 themselves. */
+fae_status fae_dlrm_buffers(fae_dlrm* m, float** Y, float** dY,
+                            double** loss_acc);
+/* The full hot step over grouped hot batches [first, first + n) (after
+ * fae_group_batches), world 1: per batch, the a8 forward of the grouped
+ * loop into the model's Y, the DLRM forward + backward + SGD (lr_mlp) of
+ * the batch's records (dense / label gathered through hot_ids: device
+ * int64 [n_hot], dense [n_records][n_dense], label [n_records], indexed by
+ * record id), then a9 + a10 on W_hot with the model's dY (lr_emb);
+ * replayed from a captured graph of 128 steps.  Sequential semantics.
+ * Errors: NOT_INIT (no grouping), INVALID_ARG (shapes differ from the
+ * grouping / model, world > 1). */
+fae_status fae_train_dlrm_batches(fae_ctx* ctx, fae_dlrm* m, float* params,
+                                  float* W_hot, int64_t H, int32_t D,
+                                  int64_t first, int64_t n,
+                                  const int64_t* hot_ids, const float* dense,
+                                  const float* label, float lr_mlp,
+                                  float lr_emb);
+
 #ifdef __cplusplus
 }
 #endif

@@ -32,7 +32,9 @@ EXPORTS = ["fae_create", "fae_destroy", "fae_set_stream", "fae_last_error",
            "fae_classify", "fae_extract", "fae_scatter_hot", "fae_pack_cold", "fae_emb_fwd", "fae_emb_bwd_update",
            "fae_sync_hot_grads", "fae_group_batches", "fae_release_scratch", "fae_train_hot_batches",
            "fae_set_kernel_timing", "fae_get_kernel_timing", "fae_get_exchange_timing", "fae_group_info",
-           "fae_sched_init", "fae_sched_next", "fae_sched_record_swap", "fae_sched_new_epoch"]
+           "fae_sched_init", "fae_sched_next", "fae_sched_record_swap", "fae_sched_new_epoch",
+           "fae_dlrm_param_count", "fae_dlrm_create", "fae_dlrm_destroy", "fae_dlrm_step", "fae_dlrm_loss",
+           "fae_dlrm_buffers", "fae_train_dlrm_batches"]
 
 
 SCHED_MAX_U = 64
@@ -44,6 +46,17 @@ class FaeSched(ctypes.Structure):
                 ("u", ctypes.c_int32), ("next_kind", ctypes.c_int32), ("last_kind", ctypes.c_int32),
                 ("n_hist", ctypes.c_int32), ("hist", ctypes.c_double * (SCHED_MAX_U + 1)),
                 ("swaps", ctypes.c_int64), ("sync_events", ctypes.c_int64), ("sync_bytes", ctypes.c_int64)]
+
+
+DLRM_MAX_LAYERS = 8
+
+
+class FaeDlrmCfg(ctypes.Structure):
+    """fae_dlrm_cfg (include/fae.h, NEXT-2)."""
+    _fields_ = [("n_dense", ctypes.c_int32), ("n_bottom", ctypes.c_int32),
+                ("bottom", ctypes.c_int32 * DLRM_MAX_LAYERS), ("n_top", ctypes.c_int32),
+                ("top", ctypes.c_int32 * DLRM_MAX_LAYERS), ("n_tables", ctypes.c_int32),
+                ("dim", ctypes.c_int32), ("max_batch", ctypes.c_int32), ("tf32", ctypes.c_int32)]
 
 
 class FaeError(RuntimeError):
@@ -142,6 +155,14 @@ def lib():
             "fae_sched_next": ([ctypes.POINTER(FaeSched), P, P, P, P], c_i32),
             "fae_sched_record_swap": ([ctypes.POINTER(FaeSched), c_dbl, c_i64, c_i32], c_i32),
             "fae_sched_new_epoch": ([ctypes.POINTER(FaeSched)], c_i32),
+            "fae_dlrm_param_count": ([ctypes.POINTER(FaeDlrmCfg)], c_i64),
+            "fae_dlrm_create": ([P, ctypes.POINTER(FaeDlrmCfg), P], c_i32),
+            "fae_dlrm_destroy": ([P], None),
+            "fae_dlrm_step": ([P, P, c_i32, P, P, P, P, ctypes.c_float, c_i32], c_i32),
+            "fae_dlrm_loss": ([P, P, P, c_i32], c_i32),
+            "fae_dlrm_buffers": ([P, P, P, P], c_i32),
+            "fae_train_dlrm_batches": ([P, P, P, P, c_i64, c_i32, c_i64, c_i64, P, P, P, ctypes.c_float,
+                                        ctypes.c_float], c_i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -465,3 +486,62 @@ class Scheduler:
     @property
     def swaps(self) -> int:
         return int(self.s.swaps)
+
+
+# ---------------------------------------------------------------------------
+# DLRM hot step (NEXT-2)
+# ---------------------------------------------------------------------------
+class Dlrm:
+    """The DLRM of a hot mini-batch (libfae's fae_dlrm_*; marshalling only).
+    Parameters live in one flat device fp32 tensor (per layer W [out][in],
+    then b [out]; bottom layers first)."""
+
+    def __init__(self, ctx: Ctx, n_dense: int, bottom, top, n_tables: int, dim: int,
+                 max_batch: int, tf32: bool = True):
+        cfg = FaeDlrmCfg()
+        cfg.n_dense, cfg.n_bottom, cfg.n_top = int(n_dense), len(bottom), len(top)
+        for i, w in enumerate(bottom):
+            cfg.bottom[i] = int(w)
+        for i, w in enumerate(top):
+            cfg.top[i] = int(w)
+        cfg.n_tables, cfg.dim, cfg.max_batch, cfg.tf32 = int(n_tables), int(dim), int(max_batch), int(bool(tf32))
+        self.cfg, self.ctx = cfg, ctx
+        self.n_params = int(lib().fae_dlrm_param_count(ctypes.byref(cfg)))
+        if self.n_params < 0:
+            raise FaeError(1, "fae_dlrm_param_count: invalid configuration")
+        h = ctypes.c_void_p()
+        ctx._ok(lib().fae_dlrm_create(ctx.h, ctypes.byref(cfg), ctypes.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                lib().fae_dlrm_destroy(self.h)
+            except Exception:
+                pass
+            self.h = None
+
+    def step(self, params: torch.Tensor, B: int, dense, label, Y, dY=None, lr: float = 0.0,
+             train: bool = True):
+        self.ctx._ok(lib().fae_dlrm_step(self.h, _p(params), int(B), _p(dense), _p(label), _p(Y), _p(dY),
+                                         ctypes.c_float(lr), int(bool(train))))
+
+    def loss(self, reset: bool = True):
+        """(sum of per-sample losses, samples) accumulated on the device."""
+        a, b = ctypes.c_double(), ctypes.c_double()
+        self.ctx._ok(lib().fae_dlrm_loss(self.h, ctypes.byref(a), ctypes.byref(b), int(bool(reset))))
+        return a.value, b.value
+
+    def buffers(self):
+        """Device pointers (Y, dY, loss accumulator) of the model's batch buffers."""
+        y, dy, acc = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        self.ctx._ok(lib().fae_dlrm_buffers(self.h, ctypes.byref(y), ctypes.byref(dy), ctypes.byref(acc)))
+        return y.value, dy.value, acc.value
+
+    def train_batches(self, params, W_hot, first: int, n: int, hot_ids, dense, label,
+                      lr_mlp: float, lr_emb: float):
+        """The full hot step over grouped hot batches [first, first + n)."""
+        self.ctx._ok(lib().fae_train_dlrm_batches(self.ctx.h, self.h, _p(params), _p(W_hot),
+                                                  int(W_hot.shape[0]), int(W_hot.shape[1]), int(first), int(n),
+                                                  _p(hot_ids), _p(dense), _p(label), ctypes.c_float(lr_mlp),
+                                                  ctypes.c_float(lr_emb)))

@@ -26,6 +26,18 @@ def nccl_paths():
     return "/usr/include", "/usr/lib/x86_64-linux-gnu"
 
 
+def cublas_paths():
+    try:
+        import nvidia.cublas as nc
+        base = list(nc.__path__)[0]
+        inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
+        if os.path.exists(os.path.join(inc, "cublas_v2.h")):
+            return inc, lib
+    except Exception:
+        pass
+    return "/usr/local/cuda/include", "/usr/local/cuda/lib64"
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
@@ -49,11 +61,12 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = OUT
         return OUT
     os.makedirs(os.path.dirname(out), exist_ok=True)
     inc, lib = nccl_paths()
+    binc, blib = cublas_paths()
     objdir = os.path.join(HERE, "_lib", "obj" + ("_" + os.path.basename(out)[:-3] if out != OUT else ""))
     os.makedirs(objdir, exist_ok=True)
     common = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
               "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
-              "-I", inc, "-I", os.path.join(ROOT, "include"), *["-D" + d for d in defines]]
+              "-I", inc, "-I", binc, "-I", os.path.join(ROOT, "include"), *["-D" + d for d in defines]]
     procs, objs = [], []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
@@ -72,7 +85,8 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = OUT
     if failed:
         raise RuntimeError("nvcc failed building libfae.so")
     cmd = ["nvcc", *ARCH, "-shared", "-o", out + ".tmp", *objs,
-           "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath," + lib]
+           "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath," + lib,
+           "-L", blib, "-l:libcublas.so.12", "-l:libcublasLt.so.12", "-Xlinker", "-rpath," + blib]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

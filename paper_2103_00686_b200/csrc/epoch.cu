@@ -1168,6 +1168,64 @@ static fae_status launch_x(Ctx* c, cudaStream_t st, int s, int last, float* W, i
     return FAE_OK;
 }
 
+// Single grouped-loop kernels for other step compositions (the DLRM hot
+// step, dlrm.cu): the forward of step s (PDL-launched: it waits before
+// reading W) and the reduce + SGD of step s launched WITHOUT the PDL
+// attribute, because its dY is produced by the kernel right before it.
+template <int LPB, int NV>
+static fae_status fwd_pdl_one(Ctx* c, cudaStream_t st, int s, float* W, int64_t H, int D, float* Y) {
+    Group& g = c->grp;
+    const int64_t gpb = 256 / LPB;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = c->no_pdl ? 0 : 1;
+    const int64_t fu = g.P == 1 ? cdiv(g.max_bags, 4)
+                     : (g.hot_off || g.P >= kWarpBagMinP) ? g.max_bags * (32 / LPB) : g.max_bags;
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(fu, gpb), (int64_t)sm_count(c) * 4)));
+    FAE_CUDA(c, cudaLaunchKernelEx(&cfg, k_grp_fwd_pdl<LPB, NV>, (const BatchDesc*)g.desc, (const int64_t*)g.run,
+                                   (const int64_t*)g.cursor, s, g.hot_idx, g.hot_off, (int)g.P, (const float*)W, H, D,
+                                   Y, c->d_err, (unsigned long long*)nullptr, 0));
+    return FAE_OK;
+}
+
+template <int LPB, int NV>
+static fae_status reduce_one(Ctx* c, cudaStream_t st, int s, int last, float* W, int64_t H, int D, const float* dY,
+                             float lr) {
+    Group& g = c->grp;
+    const int64_t gpb = 256 / LPB;
+    (void)H;
+    k_grp_reduce_pdl<LPB, NV, 4><<<(unsigned)std::max<int64_t>(1, red_grid(g, gpb)), 256, 0, st>>>(
+        (const BatchDesc*)g.desc, (const int64_t*)g.run, g.cursor, s, last, g.done_ctr, (const SegRec*)g.rec,
+        (const int32_t*)g.perm, dY, (int64_t)1, g.max_bags * (int64_t)D, D, W, lr,
+        g.lpart + (int64_t)s * std::max<int64_t>(g.max_lchunk, 1) * 8 * D,
+        g.lcnt + (int64_t)s * std::max<int64_t>(g.max_long, 1), (const int32_t*)g.lmap, c->d_err,
+        (unsigned long long*)nullptr, 0);
+    FAE_LAUNCHED(c);
+    return FAE_OK;
+}
+
+fae_status launch_set_run(Ctx* c, cudaStream_t st, int64_t first, int64_t n, int64_t n_total) {
+    k_set_run<<<1, 32, 0, st>>>(c->grp.cursor, first, n, n_total);
+    FAE_LAUNCHED(c);
+    return FAE_OK;
+}
+
+fae_status launch_grp_fwd_pdl_any(Ctx* c, cudaStream_t st, int s, float* W, int64_t H, int D, float* Y) {
+    FAE_DISPATCH_D(D, return fwd_pdl_one, c, st, s, W, H, D, Y);
+    return FAE_OK;
+}
+
+fae_status launch_grp_reduce_any(Ctx* c, cudaStream_t st, int s, int last, float* W, int64_t H, int D,
+                                 const float* dY, float lr) {
+    FAE_DISPATCH_D(D, return reduce_one, c, st, s, last, W, H, D, dY, lr);
+    return FAE_OK;
+}
+
 static bool use_persist(Ctx* c) {
     const Group& g = c->grp;
     return g.P == 1 && !g.hot_off && c->world == 1 && c->persist;

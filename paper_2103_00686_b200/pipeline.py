@@ -211,4 +211,92 @@ class MixedEpoch:
         self.swap_to("cold")
 
 
-__all__ = ["FaePipeline", "Prepared", "MixedEpoch", "FIXED_T", "BUDGET_EXACT"]
+class FaeTrainer:
+    """FAE training of the DLRM (SURVEY §8(f) NEXT-2 + NEXT-3): the epoch's
+    cold and hot mini-batches in the order of the Eq. 5 scheduler
+    (P:L538-572), every batch a full DLRM step (a8 -> MLPs / interaction /
+    log loss / SGD -> a9 + a10; fae_train_dlrm_batches) — hot batches on the
+    replicated hot table, cold batches on the master tables (MixedEpoch) —
+    and at every swap boundary the hot rows synchronised and the TEST loss
+    of the held-out records evaluated on the master tables and fed to the
+    scheduler ("post-swap testing loss", P:L559-565).
+
+    dense / label: device [n_records] inputs of the training records (record
+    id order); test_idx / test_off / n_test: the held-out records' CSR in
+    GLOBAL row ids (fae_pack_cold layout), test_dense / test_label theirs."""
+
+    def __init__(self, ep: MixedEpoch, n_dense: int, bottom, top, params: torch.Tensor,
+                 dense: torch.Tensor, label: torch.Tensor, test_idx: torch.Tensor,
+                 test_off: Optional[torch.Tensor], n_test: int, test_dense: torch.Tensor,
+                 test_label: torch.Tensor, tf32: bool = True):
+        from . import Dlrm
+        p = ep.pipe
+        self.ep, self.params = ep, params
+        self.dense, self.label = dense, label
+        self.hot_model = Dlrm(p.ctx, n_dense, bottom, top, p.Tn, p.dim, p.batch, tf32=tf32)
+        self.cold_model = Dlrm(ep.cold.ctx, n_dense, bottom, top, p.Tn, p.dim, p.batch, tf32=tf32)
+        self.test = (test_idx, test_off, int(n_test), test_dense, test_label)
+        self.Ybuf = torch.empty(p.batch * p.Tn, p.dim, device=p.dev)
+
+    def train(self, kind: str, first: int, n: int, lr_mlp: float, lr_emb: float):
+        ep = self.ep
+        ep.swap_to(kind)
+        if n <= 0:
+            return
+        if kind == "hot":
+            self.hot_model.train_batches(self.params, ep.W_hot, first, n, ep.prep.hot_ids, self.dense,
+                                         self.label, lr_mlp, lr_emb)
+        else:
+            self.cold_model.train_batches(self.params, ep.W, first, n, ep.prep.cold_ids, self.dense,
+                                          self.label, lr_mlp, lr_emb)
+
+    def train_loss(self, reset: bool = True):
+        a, n = self.hot_model.loss(reset)
+        b, m = self.cold_model.loss(reset)
+        return (a + b) / max(n + m, 1.0)
+
+    def test_loss(self) -> float:
+        """Mean log loss of the held-out records on the master tables (the
+        hot rows written back first)."""
+        ep = self.ep
+        ep.swap_to("cold")
+        idx, off, n_test, tdense, tlabel = self.test
+        p = ep.pipe
+        B, Tn = p.batch, p.Tn
+        model = self.cold_model
+        model.loss(reset=True)
+        for r0 in range(0, n_test, B):
+            r1 = min(r0 + B, n_test)
+            nb = (r1 - r0) * Tn
+            if off is None:
+                bi, bo = idx[r0 * Tn * p.pool: r1 * Tn * p.pool], None
+            else:
+                bi, bo = idx, off[r0 * Tn: r1 * Tn + 1]
+            fae_emb_fwd(ep.cold.ctx, ep.W, bi, bo, p.pool, nb, self.Ybuf[:nb])
+            model.step(self.params, r1 - r0, tdense[r0:r1], tlabel[r0:r1], self.Ybuf[:nb], None, 0.0,
+                       train=False)
+        s, n = model.loss(reset=True)
+        return s / max(n, 1.0)
+
+    def run_epoch(self, sched, lr_mlp: float, lr_emb: float, log: Optional[list] = None):
+        """One epoch in the scheduler's order; returns the phases run."""
+        ep = self.ep
+        hot_bytes = ep.prep.thresh["H_total"] * ep.pipe.dim * 4
+        phases = []
+        while True:
+            ph = sched.next_phase()
+            if ph is None:
+                break
+            kind, first, n, swap_after = ph
+            self.train(kind, first, n, lr_mlp, lr_emb)
+            phases.append((kind, first, n))
+            if swap_after:
+                tl = self.test_loss()
+                sched.record_swap(tl, hot_bytes, 1)
+                if log is not None:
+                    log.append({"swap": sched.swaps, "after": kind, "batches": n, "test_loss": tl,
+                                "rate": sched.rate})
+        return phases
+
+
+__all__ = ["FaePipeline", "Prepared", "MixedEpoch", "FaeTrainer", "FIXED_T", "BUDGET_EXACT"]
