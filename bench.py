@@ -773,6 +773,106 @@ def run_mixed(args):
     print(json.dumps(out), flush=True)
 
 
+# tab:benchmarks: RMC2 (Kaggle) / RMC3 (Terabyte) DLRM widths
+DLRM_MODELS = {"kaggle": (13, [512, 256, 64, 16], [512, 256, 1]),
+               "terabyte": (13, [512, 256, 64], [512, 512, 256, 1])}
+
+
+def run_train(args):
+    """NEXT-2 + NEXT-3: one epoch of FAE training of the paper's DLRM
+    (RMC2 Kaggle / RMC3 Terabyte widths, tab:benchmarks) on one GPU: every
+    cold and hot mini-batch of the dataset in the Eq. 5 scheduler's order
+    (cold first, R(--rate) start), each a full DLRM step (a8, MLPs on TF32
+    tensor cores, interaction, log loss, SGD, a9 + a10), hot rows
+    synchronised and the test loss of held-out records evaluated at every
+    swap.  Device-timed (CUDA events); one JSON line, not the driver's bench."""
+    import paper_2103_00686_b200 as fae
+    from paper_2103_00686_b200.pipeline import FaePipeline, FaeTrainer, MixedEpoch
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    cfg = config_of(args)
+    if cfg.name not in DLRM_MODELS:
+        raise SystemExit(f"--train: no DLRM model for {cfg.name} (RMC1 is TBSM, out of scope)")
+    n_dense, bottom, top = DLRM_MODELS[cfg.name]
+    R = args.records or cfg.records
+    Tn, D, B = cfg.n_tables, cfg.dim, cfg.batch
+    ds = gen.make_dataset(cfg, n_records=R, device=dev)
+    W = gen.make_weights(sum(cfg.rows), D, device=dev)
+    pipe = FaePipeline(cfg.rows, D, B, cfg.pool, max_pool=max(cfg.pool_hi, 1), device=0)
+    mode = fae.BUDGET_EXACT if cfg.budget_bytes else fae.FIXED_T
+    t0 = time.perf_counter()
+    prep = pipe.preprocess(ds.idx, ds.off, R, x_pct=5.0, seed=args.seed, mode=mode, t=cfg.t,
+                           budget_bytes=cfg.budget_bytes, small_table_bytes=cfg.small_bytes)
+    W_hot = pipe.extract(W, prep)
+    ep = MixedEpoch(pipe, prep, W, ds.idx, ds.off, R, W_hot)
+    torch.cuda.synchronize()
+    prep_ms = (time.perf_counter() - t0) * 1e3
+    dims = gen.dlrm_dims(n_dense, bottom, top, Tn, D)
+    params = gen.make_dlrm_params(dims, device=dev)
+    dense = gen.make_dense(R, n_dense, device=dev)
+    label = gen.make_labels(R, n_dense, device=dev)
+    n_test = args.test_records
+    tds = gen.make_dataset(cfg, n_records=n_test, device=dev, record_base=R)
+    gbase = torch.tensor([0] + list(__import__("itertools").accumulate(cfg.rows))[:-1], device=dev)
+    tidx = (tds.idx.view(n_test, Tn) + gbase).view(-1).to(torch.int32)
+    tr = FaeTrainer(ep, n_dense, bottom, top, params, dense, label, tidx, None, n_test,
+                    gen.make_dense(n_test, n_dense, device=dev, record_base=R),
+                    gen.make_labels(n_test, n_dense, device=dev, record_base=R), tf32=True)
+    nh, nc = ep.n_hot_batches, ep.n_cold_batches
+    # warm-up: capture both loops' graphs and run a few batches (then restore)
+    p_save, W_save, Wh_save = params.clone(), W.clone(), W_hot.clone()
+    tr.train("cold", 0, min(nc, 256), args.lr_mlp, args.lr)
+    tr.train("hot", 0, min(nh, 256), args.lr_mlp, args.lr)
+    tr.test_loss()
+    ep.swap_to("hot")
+    params.copy_(p_save)
+    W.copy_(W_save)
+    W_hot.copy_(Wh_save)
+    del p_save, W_save, Wh_save
+    tr.train_loss(reset=True)
+    loss0 = tr.test_loss()
+    ep.swap_to("hot")
+    sched = fae.Scheduler(nc, nh, args.rate)
+    log = []
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record()
+    phases = tr.run_epoch(sched, args.lr_mlp, args.lr, log)
+    ep.finish()
+    e1.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    pipe.ctx.check()
+    ep.cold.ctx.check()
+    ms = e0.elapsed_time(e1)
+    train_loss = tr.train_loss(reset=True)
+    loss1 = tr.test_loss()
+    hl, cl = prep.packed["n_hot_lookups"], ep.n_cold_lookups
+    fl = 6 * sum(i * o for i, o in dims) * R      # fwd 2, bwd 4 flops per weight per sample
+    peak_bf16 = None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        peak_bf16 = float(pk.get("bf16_tflops") or pk.get("bf16_dense_tflops") or 0) or None
+    except Exception:
+        pass
+    out = {"mode": "fae-train-epoch", "workload": f"{cfg.name}-shaped", "model": {
+               "n_dense": n_dense, "bottom": bottom, "top": top, "interaction": "dot",
+               "params": int(params.numel()), "gemm": "cuBLAS TF32 tensor cores, fp32 master weights"},
+           "records": R, "hot_records": prep.packed["n_hot"], "hot_batches": nh, "cold_batches": nc,
+           "batch": B, "rate_start": args.rate, "phases": len(phases), "swaps": sched.swaps,
+           "sync_bytes": int(sched.s.sync_bytes), "epoch_ms": ms, "wall_s": wall,
+           "samples_per_s": R / (ms / 1e3), "lookups_per_s": (hl + cl) / (ms / 1e3),
+           "us_per_batch": ms * 1e3 / (nh + nc), "mlp_tflops": fl / (ms / 1e3) / 1e12,
+           "mlp_peak_tf32_tflops": (peak_bf16 / 2 if peak_bf16 else None),
+           "test_loss_before": loss0, "test_loss_after": loss1, "train_loss_epoch": train_loss,
+           "swap_log": log[:64], "preprocess_ms": prep_ms, "n_test": n_test,
+           "lr_mlp": args.lr_mlp, "lr_emb": args.lr,
+           "timing": "CUDA events around the whole scheduled epoch (training, swaps, test-loss evaluations)"}
+    print(json.dumps(out), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -797,7 +897,10 @@ def main():
                     help="N=1: run the multi-rank exchange loop on a 1-rank NCCL communicator (sync cost)")
     ap.add_argument("--sweep", action="store_true", help="threshold sweep (one JSON line; not the driver's bench)")
     ap.add_argument("--mixed", action="store_true", help="NEXT-1 timed mixed hot/cold epoch (one JSON line)")
-    ap.add_argument("--rate", type=float, default=50.0, help="--mixed: phase size, %% of each kind's batches")
+    ap.add_argument("--rate", type=float, default=50.0, help="--mixed / --train: phase size (start), %% of each kind's batches")
+    ap.add_argument("--train", action="store_true", help="NEXT-2/3: one scheduled FAE epoch of the paper's DLRM (one JSON line)")
+    ap.add_argument("--lr-mlp", type=float, default=0.05)
+    ap.add_argument("--test-records", type=int, default=65536)
     ap.add_argument("--sweep-configs", default="kaggle,terabyte")
     ap.add_argument("--sweep-fracs", default="1,2,5,10,20")
     args = ap.parse_args()
@@ -806,6 +909,9 @@ def main():
         return
     if args.mixed:
         run_mixed(args)
+        return
+    if args.train:
+        run_train(args)
         return
     if args.impl == "reference":
         r = run_reference(args)
