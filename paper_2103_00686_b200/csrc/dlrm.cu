@@ -150,6 +150,101 @@ __global__ void k_interact_bwd(const float* __restrict__ xbot, const float* __re
     }
 }
 
+// Register versions (F <= 32, D in {8, 16, 32, 64}): lane i holds the row
+// T_i of its sample; row j is broadcast by shuffles, so there is no shared-
+// memory bank traffic on the rows.  Forward: lane i computes <T_i, T_j> for
+// every j < i (pair index i(i-1)/2 + j), staged in shared memory and stored
+// coalesced.  Backward: lane i accumulates dT_i = sum_{j != i} dZ_(i,j) T_j
+// in ascending j (dZ staged in shared memory).  Same arithmetic and order as
+// the shared-memory kernels above.
+template <int D>
+__global__ void __launch_bounds__(128) k_interact_fwd_reg(const float* __restrict__ xbot, const float* __restrict__ Y,
+                                                          int B, int Tn, int P, const int32_t* __restrict__ nb,
+                                                          float* __restrict__ out) {
+    extern __shared__ float s_z[];   // [warps][P]
+    const int F = Tn + 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (b >= B) return;
+    const bool valid = b < *nb;
+    float t[D];
+    const float* src = lane == 0 ? xbot + (int64_t)b * D : Y + ((int64_t)b * Tn + (lane - 1)) * D;
+#pragma unroll
+    for (int q = 0; q < D / 4; q++) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid && lane < F) v = __ldg(reinterpret_cast<const float4*>(src) + q);
+        t[4 * q] = v.x;
+        t[4 * q + 1] = v.y;
+        t[4 * q + 2] = v.z;
+        t[4 * q + 3] = v.w;
+    }
+    float* z = s_z + (int64_t)warp * P;
+    const int kb = lane * (lane - 1) / 2;
+    for (int j = 0; j < F - 1; j++) {
+        float s = 0.f;
+#pragma unroll
+        for (int d = 0; d < D; d++) s = fmaf(t[d], __shfl_sync(0xffffffffu, t[d], j), s);
+        if (lane > j && lane < F) z[kb + j] = s;
+    }
+    __syncwarp();
+    float* o = out + (int64_t)b * (D + P);
+    if (lane == 0) {
+#pragma unroll
+        for (int d = 0; d < D; d++) o[d] = t[d];
+    }
+    for (int k = lane; k < P; k += 32) o[D + k] = z[k];
+}
+
+template <int D>
+__global__ void __launch_bounds__(128) k_interact_bwd_reg(const float* __restrict__ xbot, const float* __restrict__ Y,
+                                                          int B, int Tn, int P, const int32_t* __restrict__ nb,
+                                                          const float* __restrict__ din, float* __restrict__ dxbot,
+                                                          float* __restrict__ dY) {
+    extern __shared__ float s_z[];   // [warps][P]
+    const int F = Tn + 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (b >= B) return;
+    const bool valid = b < *nb;
+    float t[D], a[D];
+    const float* src = lane == 0 ? xbot + (int64_t)b * D : Y + ((int64_t)b * Tn + (lane - 1)) * D;
+#pragma unroll
+    for (int q = 0; q < D / 4; q++) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid && lane < F) v = __ldg(reinterpret_cast<const float4*>(src) + q);
+        t[4 * q] = v.x;
+        t[4 * q + 1] = v.y;
+        t[4 * q + 2] = v.z;
+        t[4 * q + 3] = v.w;
+        a[4 * q] = a[4 * q + 1] = a[4 * q + 2] = a[4 * q + 3] = 0.f;
+    }
+    const float* g = din + (int64_t)b * (D + P);
+    float* z = s_z + (int64_t)warp * P;
+    for (int k = lane; k < P; k += 32) z[k] = valid ? g[D + k] : 0.f;
+    __syncwarp();
+    for (int j = 0; j < F; j++) {
+        const int ii = lane > j ? lane : j, jj = lane > j ? j : lane;
+        const float w = (lane != j && lane < F) ? z[ii * (ii - 1) / 2 + jj] : 0.f;
+#pragma unroll
+        for (int d = 0; d < D; d++) {
+            const float tj = __shfl_sync(0xffffffffu, t[d], j);
+            if (lane != j) a[d] = fmaf(w, tj, a[d]);
+        }
+    }
+    if (lane == 0) {
+        float* o = dxbot + (int64_t)b * D;
+#pragma unroll
+        for (int d = 0; d < D; d++) {
+            const float v = valid ? g[d] + a[d] : 0.f;
+            o[d] = t[d] > 0.f ? v : 0.f;   // bottom ReLU mask
+        }
+    } else if (lane < F) {
+        float4* o = reinterpret_cast<float4*>(dY + ((int64_t)b * Tn + (lane - 1)) * D);
+#pragma unroll
+        for (int q = 0; q < D / 4; q++) o[q] = make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
+    }
+}
+
 // Loss: one CTA.  z[b] (+ bias c) -> s = sigmoid(z); loss_b = max(z,0) -
 // z y + log1p(exp(-|z|)); dz[b] = (s - y) / nb (0 for padded rows);
 // acc[0] += sum_b loss_b (fixed-order block reduction), acc[1] += nb.
@@ -248,9 +343,18 @@ static fae_status dlrm_run(Dlrm* m, float* params, float lr, bool train, cudaStr
         FAE_LAUNCHED(c);
         if (l == nbot - 1) {     // interaction: act[nbot] = bottom output -> act[nbot + 1]
             const int wpb = 4;
-            const size_t sm = sizeof(float) * wpb * (Tn + 1) * D;
-            k_interact_fwd<<<(unsigned)cdiv(B, wpb), 32 * wpb, sm, st>>>(m->act[nbot], m->Y, B, Tn, D, m->pairs, m->P,
-                                                                         m->nb, m->act[nbot + 1]);
+            const bool reg = Tn + 1 <= 32 && (D == 8 || D == 16 || D == 32 || D == 64);
+            if (reg) {
+                const size_t sm = sizeof(float) * wpb * m->P;
+                auto kf = D == 8 ? k_interact_fwd_reg<8> : D == 16 ? k_interact_fwd_reg<16>
+                        : D == 32 ? k_interact_fwd_reg<32> : k_interact_fwd_reg<64>;
+                kf<<<(unsigned)cdiv(B, wpb), 32 * wpb, sm, st>>>(m->act[nbot], m->Y, B, Tn, m->P, m->nb,
+                                                                 m->act[nbot + 1]);
+            } else {
+                const size_t sm = sizeof(float) * wpb * (Tn + 1) * D;
+                k_interact_fwd<<<(unsigned)cdiv(B, wpb), 32 * wpb, sm, st>>>(m->act[nbot], m->Y, B, Tn, D, m->pairs,
+                                                                             m->P, m->nb, m->act[nbot + 1]);
+            }
             FAE_LAUNCHED(c);
         }
     }
@@ -278,9 +382,18 @@ static fae_status dlrm_run(Dlrm* m, float* params, float lr, bool train, cudaStr
         if (l == nbot) {
             // dX = d(interaction output) -> dT: bottom output gradient (masked) and dY
             const int wpb = 4;
-            const size_t sm = sizeof(float) * wpb * (Tn + 1) * D;
-            k_interact_bwd<<<(unsigned)cdiv(B, wpb), 32 * wpb, sm, st>>>(m->act[nbot], m->Y, B, Tn, D, m->pidx, m->P,
-                                                                         m->nb, dX, dC, m->dY);
+            const bool reg = Tn + 1 <= 32 && (D == 8 || D == 16 || D == 32 || D == 64);
+            if (reg) {
+                const size_t sm = sizeof(float) * wpb * m->P;
+                auto kb = D == 8 ? k_interact_bwd_reg<8> : D == 16 ? k_interact_bwd_reg<16>
+                        : D == 32 ? k_interact_bwd_reg<32> : k_interact_bwd_reg<64>;
+                kb<<<(unsigned)cdiv(B, wpb), 32 * wpb, sm, st>>>(m->act[nbot], m->Y, B, Tn, m->P, m->nb, dX, dC,
+                                                                 m->dY);
+            } else {
+                const size_t sm = sizeof(float) * wpb * (Tn + 1) * D;
+                k_interact_bwd<<<(unsigned)cdiv(B, wpb), 32 * wpb, sm, st>>>(m->act[nbot], m->Y, B, Tn, D, m->pidx,
+                                                                             m->P, m->nb, dX, dC, m->dY);
+            }
             FAE_LAUNCHED(c);
             continue;            // dC now holds the bottom output's gradient
         }
