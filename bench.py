@@ -542,7 +542,7 @@ def oracle_step(cfg, R_s, max_batches, seed, lr, ds):
 
 
 CPU_DEFAULTS = {   # records / hot batches of the bounded oracle sample (~10-30 s)
-    "tiny": (10_000, 1000), "kaggle": (4_000_000, 400), "terabyte": (1_000_000, 40),
+    "tiny": (10_000, 1000), "kaggle": (4_000_000, 400), "terabyte": (3_000_000, 120),
     "alibaba": (1_000_000, 200)}
 
 

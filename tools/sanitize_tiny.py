@@ -46,4 +46,49 @@ for fused in ("1", "0"):
         pipe.ctx.check()
         torch.cuda.synchronize()
         print(f"{name} fused={fused}: ok, launches={pipe.ctx.launches}", flush=True)
+# round 2: the mixed epoch (cold grouping in global ids, scratch release), the
+# DLRM hot step and a scheduled FAE epoch (cuBLAS GEMMs + interaction / loss
+# kernels + the grouped loop), and the exchange loop on a 1-rank communicator
+import numpy as np  # noqa: E402
+from paper_2103_00686_b200.pipeline import FaeTrainer, MixedEpoch  # noqa: E402
+
+os.environ["FAE_FUSED"] = "1"
+cfg = gen.CONFIGS["tiny"]
+R = 3_000
+ds = gen.make_dataset(cfg, n_records=R, seed=5).to(dev)
+pipe = FaePipeline(cfg.rows, cfg.dim, cfg.batch, cfg.pool)
+prep = pipe.preprocess(ds.idx, None, R, x_pct=5.0, seed=3, t=1e-2, small_table_bytes=0)
+W = gen.make_weights(sum(cfg.rows), cfg.dim, device=dev)
+W_hot = pipe.extract(W, prep).clone()
+ep = MixedEpoch(pipe, prep, W, ds.idx, None, R, W_hot)
+Tn, D = cfg.n_tables, cfg.dim
+dims = gen.dlrm_dims(4, [12, D], [20, 1], Tn, D)
+params = gen.make_dlrm_params(dims, device=dev)
+tds = gen.make_dataset(cfg, n_records=256, seed=5, record_base=R)
+base = torch.tensor(np.concatenate([[0], np.cumsum(cfg.rows)])[:Tn], device=dev)
+tidx = (tds.idx.to(dev).view(256, Tn) + base).view(-1).to(torch.int32)
+tr = FaeTrainer(ep, 4, [12, D], [20, 1], params, gen.make_dense(R, 4, device=dev), gen.make_labels(R, 4, device=dev),
+                tidx, None, 256, gen.make_dense(256, 4, device=dev, record_base=R),
+                gen.make_labels(256, 4, device=dev, record_base=R), tf32=True)
+sched = m.Scheduler(ep.n_cold_batches, ep.n_hot_batches, 50.0)
+tr.run_epoch(sched, 0.05, 0.01)
+ep.finish()
+pipe.ctx.check()
+ep.cold.ctx.check()
+torch.cuda.synchronize()
+print(f"trainer epoch: ok, swaps={sched.swaps}", flush=True)
+if os.environ.get("SANITIZE_NCCL") == "1":
+    os.environ["FAE_FORCE_MERGE"] = "1"
+    p2 = FaePipeline(cfg.rows, cfg.dim, cfg.batch, cfg.pool)
+    m.fae_comm_init(p2.ctx, m.fae_get_nccl_id(), 0, 1)
+    pr2 = p2.preprocess(ds.idx, None, R, x_pct=5.0, seed=3, t=1e-2, small_table_bytes=0)
+    Wh2 = p2.extract(W, pr2).clone()
+    p2.group(pr2)
+    nb = pr2.packed["n_hot_batches"]
+    S = cfg.batch * Tn
+    dY = gen.make_dy(nb * S, D, device=dev).view(nb, S, D)
+    p2.train(Wh2, 0, nb, dY, torch.zeros(S, D, device=dev), 0.05)
+    p2.ctx.check()
+    torch.cuda.synchronize()
+    print("exchange loop: ok", flush=True)
 print("sanitize_tiny done")
