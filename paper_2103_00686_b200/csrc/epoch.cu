@@ -27,6 +27,11 @@
 namespace fae {
 
 constexpr int kSt = kStampSlots;
+// single-lookup forward of the grouped loop: bags per lane group and pass
+#ifndef FAE_FWD_U
+#define FAE_FWD_U 4
+#endif
+constexpr int kFwdU = FAE_FWD_U;
 
 // finish a segment: emit G (a11 exchange) or W[row] -= lr * G (a10)
 template <int LPB, int NV>
@@ -735,7 +740,7 @@ k_grp_fwd_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ ru
         pdl_trigger();
     }
     if (hot_off) fwd_bags<LPB, NV, true>(W, H, D, hot_idx, hot_off + d.bag0, 0, d.n_bags, Y, err);
-    else if (P == 1) fwd_gather1<LPB, NV, true>(W, H, D, hot_idx + d.lk0, d.n_bags, Y, err);
+    else if (P == 1) fwd_gather1<LPB, NV, true, kFwdU>(W, H, D, hot_idx + d.lk0, d.n_bags, Y, err);
     else fwd_bags<LPB, NV, true>(W, H, D, hot_idx + d.lk0, nullptr, P, d.n_bags, Y, err);
     if (trig & 4) pdl_wait();       // (threads without a bag never waited above)
     if (stamps) {
@@ -996,7 +1001,7 @@ static void launch_grp_step(Ctx* c, cudaStream_t s, float* W, int64_t H, int D, 
     const int threads = 256;
     const int64_t gpb = threads / LPB;
     const int64_t maxb = (int64_t)sm_count(c) * 16;
-    const int64_t fu = g.P == 1 ? cdiv(g.max_bags, 4)
+    const int64_t fu = g.P == 1 ? cdiv(g.max_bags, kFwdU)
                      : (g.hot_off || g.P >= kWarpBagMinP) ? g.max_bags * (32 / LPB) : g.max_bags;
     const int64_t fb = std::max<int64_t>(1, std::min<int64_t>(cdiv(fu, gpb), maxb));
     k_grp_fwd<LPB, NV><<<(unsigned)fb, threads, 0, s>>>(g.desc, g.run, g.cursor, g.hot_idx, g.hot_off, g.P,
@@ -1027,7 +1032,7 @@ static fae_status launch_pdl_step(Ctx* c, cudaStream_t st, int s, float* W, int6
     cfg.numAttrs = 1;
     static const int64_t fcap = getenv("FAE_FWD_GRID") ? atoll(getenv("FAE_FWD_GRID")) : 0;
     const int64_t half = fcap > 0 ? fcap : (int64_t)sm_count(c) * 4;   // each kernel gets about half of the GPU
-    const int64_t fu = g.P == 1 ? cdiv(g.max_bags, 4)
+    const int64_t fu = g.P == 1 ? cdiv(g.max_bags, kFwdU)
                      : (g.hot_off || g.P >= kWarpBagMinP) ? g.max_bags * (32 / LPB) : g.max_bags;
     cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(fu, gpb), half)));
     FAE_CUDA(c, cudaLaunchKernelEx(&cfg, k_grp_fwd_pdl<LPB, NV>, (const BatchDesc*)g.desc, (const int64_t*)g.run,
@@ -1116,7 +1121,7 @@ static fae_status launch_x_step(Ctx* c, cudaStream_t st, int s, int last, float*
     // a slot the merge still reads
     cfg.attrs = attr;
     cfg.numAttrs = c->no_pdl ? 0 : 1;
-    const int64_t fu = g.P == 1 ? cdiv(g.max_bags, 4)
+    const int64_t fu = g.P == 1 ? cdiv(g.max_bags, kFwdU)
                      : (g.hot_off || g.P >= kWarpBagMinP) ? g.max_bags * (32 / LPB) : g.max_bags;
     cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(fu, gpb), (int64_t)sm_count(c) * 4)));
     FAE_CUDA(c, cudaLaunchKernelEx(&cfg, k_grp_fwd_pdl<LPB, NV>, (const BatchDesc*)g.desc, (const int64_t*)g.run,
@@ -1184,7 +1189,7 @@ static fae_status fwd_pdl_one(Ctx* c, cudaStream_t st, int s, float* W, int64_t 
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = c->no_pdl ? 0 : 1;
-    const int64_t fu = g.P == 1 ? cdiv(g.max_bags, 4)
+    const int64_t fu = g.P == 1 ? cdiv(g.max_bags, kFwdU)
                      : (g.hot_off || g.P >= kWarpBagMinP) ? g.max_bags * (32 / LPB) : g.max_bags;
     cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(fu, gpb), (int64_t)sm_count(c) * 4)));
     FAE_CUDA(c, cudaLaunchKernelEx(&cfg, k_grp_fwd_pdl<LPB, NV>, (const BatchDesc*)g.desc, (const int64_t*)g.run,
