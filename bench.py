@@ -346,6 +346,13 @@ def run_fae(args):
                          "avg_launch_us": avg_s * 1e6,
                          "kernels_us": {k: (kt[k][0] / max(kt[k][1], 1)) * 1e3 for k in ("fwd", "reduce")},
                          "launches_timed": kn,
+                         # the whole a8-a10 step per batch (fwd + bwd + update) on §8(d) bytes
+                         # over the training loop's time per batch (every kernel of the step)
+                         "step": (lambda sb, su: {"bytes_per_batch": sb, "us_per_batch": su,
+                                                  "achieved": sb / (su * 1e-6) / 1e9 if su else None,
+                                                  "frac": (sb / (su * 1e-6) / 1e9) / peak if su else None})(
+                             fwd_bytes(L_b, S_b, D, expl) + bwd_bytes(L_b, S_b, U_b, D, expl),
+                             phases.get("train", 0.0) / args.steps * 1e3 / max(prep.packed["n_hot_batches"], 1)),
                          **({"batches_per_launch": kt["persist_batches"] / max(kn, 1),
                              "us_per_batch": avg_s * 1e6 * kn / max(kt["persist_batches"], 1)}
                             if persist else {"pdl": overlap})},
