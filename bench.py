@@ -190,6 +190,17 @@ def run_fae(args):
         os.environ["FAE_FORCE_MERGE"] = "1"      # read at fae_create
     pipe = FaePipeline(cfg.rows, D, B, cfg.pool, max_pool=max(cfg.pool_hi, 1), device=local,
                        max_world=world)
+    # cross-step overlap (one GPU): step k+1's preprocessing and grouping run on
+    # a second ctx / stream while step k trains; trainings stay serial (step
+    # k+1's extract waits for step k's training on the device)
+    overlap = world == 1 and not args.exchange and args.overlap
+    pipes, streams = [pipe], [None]
+    if overlap:
+        pipes.append(FaePipeline(cfg.rows, D, B, cfg.pool, max_pool=max(cfg.pool_hi, 1), device=local,
+                                 max_world=world))
+        streams = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
+        for p_, s_ in zip(pipes, streams):
+            p_.ctx.set_stream(s_)
     if world > 1:
         from paper_2103_00686_b200 import dist as fdist
         fdist.init_comm(pipe.ctx, dev)
@@ -212,7 +223,37 @@ def run_fae(args):
         phases[name] = phases.get(name, 0.0) + (t1 - t0) * 1e3
         return t1
 
+    ov = {"train_done": None, "events": []}
+
+    def one_step_ov(k):
+        i = k % len(pipes)
+        p, st = pipes[i], streams[i]
+        with torch.cuda.stream(st):
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+            e[0].record(st)
+            prep = p.preprocess(ds.idx, ds.off, R, x_pct=5.0, seed=args.seed, mode=mode,
+                                t=cfg.t, budget_bytes=cfg.budget_bytes,
+                                small_table_bytes=cfg.small_bytes, bufs=state.get(("prep", i)),
+                                times=phases, record_base=rank * R, n_records_global=world * R)
+            state[("prep", i)] = prep
+            e[1].record(st)
+            p.group(prep)
+            e[2].record(st)
+            if ov["train_done"] is not None:
+                st.wait_event(ov["train_done"])
+            W_hot = p.extract(W, prep)
+            e[3].record(st)
+            p.train(W_hot, 0, prep.packed["n_hot_batches"], dY, Y, args.lr)
+            e[4].record(st)
+            ov["train_done"] = e[4]
+            ov["events"].append(e)
+        return prep.packed["n_hot_lookups"], prep
+
     def one_step():
+        if overlap:
+            k = state.get("k", 0)
+            state["k"] = k + 1
+            return one_step_ov(k)
         t = time.perf_counter()
         prep = pipe.preprocess(ds.idx, ds.off, R, x_pct=5.0, seed=args.seed, mode=mode,
                                t=cfg.t, budget_bytes=cfg.budget_bytes,
@@ -234,42 +275,68 @@ def run_fae(args):
 
     # kernel timing on from the warm-up: the captured training graph (keyed on
     # its buffers, including the timing stamps) is built outside the timed region
-    fae.fae_set_kernel_timing(pipe.ctx, 0 if args.no_ktiming else 1)
-    for _ in range(args.warmup):
+    for p_ in pipes:
+        fae.fae_set_kernel_timing(p_.ctx, 0 if args.no_ktiming else 1)
+    for _ in range(max(args.warmup, len(pipes))):
         one_step()
     torch.cuda.synchronize()
-    pipe.ctx.check()
+    for p_ in pipes:
+        p_.ctx.check()
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
     clocks = Clocks(local)
     clocks.start()
-    l0 = pipe.ctx.launches
+    l0 = sum(p_.ctx.launches for p_ in pipes)
     phases.clear()
-    fae.fae_set_kernel_timing(pipe.ctx, 0 if args.no_ktiming else 1)
+    ov["events"].clear()
+    for p_ in pipes:
+        fae.fae_set_kernel_timing(p_.ctx, 0 if args.no_ktiming else 1)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     sev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     wall0 = time.perf_counter()
     t0.record()
     sev[0].record()
+    if overlap:               # the side streams start after t0
+        for st_ in streams:
+            st_.wait_event(t0)
     hot_lookups = 0
     prep = None
     for k in range(args.steps):
         n, prep = one_step()
-        sev[k + 1].record()
+        if not overlap:
+            sev[k + 1].record()
         hot_lookups += n
+    if overlap:               # t1 after both side streams drained
+        for st_ in streams:
+            torch.cuda.current_stream().wait_stream(st_)
     t1.record()
     torch.cuda.synchronize()
-    per_step_ms = [sev[k].elapsed_time(sev[k + 1]) for k in range(args.steps)]
+    if overlap:
+        ends = [sev[0]] + [e[4] for e in ov["events"]]
+        per_step_ms = [ends[k].elapsed_time(ends[k + 1]) for k in range(args.steps)]
+        for k, e in enumerate(ov["events"]):
+            for name, a, b in (("preprocess_total", 0, 1), ("group", 1, 2), ("extract_and_wait", 2, 3),
+                               ("train", 3, 4)):
+                phases[name] = phases.get(name, 0.0) + e[a].elapsed_time(e[b])
+    else:
+        per_step_ms = [sev[k].elapsed_time(sev[k + 1]) for k in range(args.steps)]
     wall = time.perf_counter() - wall0
     ck = clocks.stop()
-    pipe.ctx.check()
+    for p_ in pipes:
+        p_.ctx.check()
     ms = t0.elapsed_time(t1)
-    launches = pipe.ctx.launches - l0
-    kt = fae.fae_get_kernel_timing(pipe.ctx)
+    launches = sum(p_.ctx.launches for p_ in pipes) - l0
+    kts = [fae.fae_get_kernel_timing(p_.ctx) for p_ in pipes]
+    kt = dict(kts[0])
+    for k2 in ("fwd", "reduce", "overlap"):
+        kt[k2] = (sum(x[k2][0] for x in kts), sum(x[k2][1] for x in kts))
+    kt["persist_batches"] = sum(x["persist_batches"] for x in kts)
     xt = fae.fae_get_exchange_timing(pipe.ctx) if (world > 1 or args.exchange) else None
-    fae.fae_set_kernel_timing(pipe.ctx, 0)
+    for p_ in pipes:
+        fae.fae_set_kernel_timing(p_.ctx, 0)
+
     tot = torch.tensor([ms, float(hot_lookups)], dtype=torch.float64, device=dev)
     if dist is not None:
         mx = tot.clone()
@@ -327,7 +394,9 @@ def run_fae(args):
                        "distinct_rows_per_batch": U_b,
                        "l2": "inputs > L2 (dataset %.1f GB, dY pool %d MB)" % (
                            ds.idx.numel() * 4 / 1e9, n_dy * dy_bytes >> 20),
-                       "parallelism": f"dp{world}"},
+                       "parallelism": f"dp{world}",
+                       "cross_step_overlap": (("step k+1's preprocessing + grouping on a second ctx / stream "
+                                               "while step k trains; trainings serial") if overlap else None)},
             "gpu_launches": launches,
             "roofline": {"kernel": kname_full,
                          "timing": ("CUDA events around each cooperative launch on the ctx stream, every launch "
@@ -365,7 +434,7 @@ def run_fae(args):
             "train_only_lookups_per_s": (lookups_all / (phases["train"] / 1e3)
                                          if phases.get("train") else None),
         }
-    return res, (pipe, ds, W, cfg, R, dist, rank, world, dev, dY, Y)
+    return res, (pipe, ds, W, cfg, R, dist, rank, world, dev, dY, Y, pipes, streams)
 
 
 def sync_report(xt, world, D, kt):
@@ -399,7 +468,7 @@ def run_e2e(args, ctxs):
     run); the trained hot table (the step's result) is read back into pinned
     host memory every step."""
     import paper_2103_00686_b200 as fae
-    pipe, ds, W, cfg, R, dist, rank, world, dev, dY, Y = ctxs
+    pipe, ds, W, cfg, R, dist, rank, world, dev, dY, Y, pipes, streams = ctxs
     idx_h = ds.idx.cpu().pin_memory()
     off_h = ds.off.cpu().pin_memory() if ds.off is not None else None
     del ds
@@ -413,6 +482,7 @@ def run_e2e(args, ctxs):
         e.record()
     mode = fae.BUDGET_EXACT if cfg.budget_bytes else fae.FIXED_T
     st = {}
+    npipe = len(pipes)
 
     CH = 16 << 20   # elements per chunk (64 MB): the small host<->device copies of
     #                  the compute path interleave with the big input copy
@@ -427,63 +497,68 @@ def run_e2e(args, ctxs):
             ready[b].record(copy_s)
 
     trace = os.environ.get("FAE_E2E_TRACE") is not None
-    cur = torch.cuda.current_stream()
 
-    def mark(tag, t_prev):
+    def mark(tag, t_prev, s_):
         if not trace:
             return t_prev
-        cur.synchronize()
+        s_.synchronize()
         t = time.perf_counter()
         print(f"[e2e] {tag:10s} {(t - t_prev) * 1e3:8.2f} ms", file=sys.stderr)
         return t
 
     def step(k, last):
         b = k % 2
+        i = k % npipe
+        p = pipes[i]
+        s_ = streams[i] if streams[i] is not None else torch.cuda.current_stream()
         tt = time.perf_counter()
-        torch.cuda.current_stream().wait_event(ready[b])
-        tt = mark("wait-in", tt)
-        prep = pipe.preprocess(idx_d[b], off_d[b] if off_d is not None else None, R, x_pct=5.0,
-                               seed=args.seed, mode=mode, t=cfg.t, budget_bytes=cfg.budget_bytes,
-                               small_table_bytes=cfg.small_bytes, bufs=st.get("prep"),
-                               record_base=rank * R, n_records_global=world * R)
-        tt = mark("preprocess", tt)
-        free[b].record()          # the hot CSR is built: this input buffer is free
-        st["prep"] = prep
-        pipe.group(prep)
-        tt = mark("group", tt)
-        if not last:
-            # next step's input crosses PCIe during this step's extract + train
-            # (after the grouping, whose small host copies would queue behind it)
-            enqueue_copy(k + 1)
-        if "rb_done" in st:       # the previous step's readback still reads the hot table
-            torch.cuda.current_stream().wait_event(st["rb_done"])
-        W_hot = pipe.extract(W, prep)
-        nb = prep.packed["n_hot_batches"]
-        if dist is not None:
-            from paper_2103_00686_b200 import dist as fdist
-            nb = fdist.max_over_ranks(nb, dev)
-        pipe.train(W_hot, 0, nb, dY, Y, args.lr)
-        tt = mark("train", tt)
-        if "out" not in st or st["out"].numel() < W_hot.numel():
-            st["out"] = torch.empty(W_hot.numel() + W_hot.numel() // 4, dtype=W_hot.dtype).pin_memory()
-        out = st["out"][:W_hot.numel()].view_as(W_hot)
+        with torch.cuda.stream(s_):
+            s_.wait_event(ready[b])
+            tt = mark("wait-in", tt, s_)
+            prep = p.preprocess(idx_d[b], off_d[b] if off_d is not None else None, R, x_pct=5.0,
+                                seed=args.seed, mode=mode, t=cfg.t, budget_bytes=cfg.budget_bytes,
+                                small_table_bytes=cfg.small_bytes, bufs=st.get(("prep", i)),
+                                record_base=rank * R, n_records_global=world * R)
+            tt = mark("preprocess", tt, s_)
+            free[b].record(s_)          # the hot CSR is built: this input buffer is free
+            st[("prep", i)] = prep
+            p.group(prep)
+            tt = mark("group", tt, s_)
+            if not last:
+                # next step's input crosses PCIe during this step's extract + train
+                # (after the grouping, whose small host copies would queue behind it)
+                enqueue_copy(k + 1)
+            if ("rb_done", i) in st:    # this pipe's previous readback still reads its hot table
+                s_.wait_event(st[("rb_done", i)])
+            if "train_done" in st:      # trainings stay in sequence
+                s_.wait_event(st["train_done"])
+            W_hot = p.extract(W, prep)
+            nb = prep.packed["n_hot_batches"]
+            if dist is not None:
+                from paper_2103_00686_b200 import dist as fdist
+                nb = fdist.max_over_ranks(nb, dev)
+            p.train(W_hot, 0, nb, dY, Y, args.lr)
+            trained = torch.cuda.Event()
+            trained.record(s_)
+            st["train_done"] = trained
+            tt = mark("train", tt, s_)
+        if ("out", i) not in st or st[("out", i)].numel() < W_hot.numel():
+            st[("out", i)] = torch.empty(W_hot.numel() + W_hot.numel() // 4, dtype=W_hot.dtype).pin_memory()
+        out = st[("out", i)][:W_hot.numel()].view_as(W_hot)
         # the trained hot table back to host memory on its own stream, so it
-        # overlaps the next step's preprocessing (the next extract waits for it)
-        trained = torch.cuda.Event()
-        trained.record()
+        # overlaps the next steps (this pipe's next extract waits for it)
         with torch.cuda.stream(rb_s):
             rb_s.wait_event(trained)
             out.copy_(W_hot, non_blocking=True)
-            st["rb_done"] = torch.cuda.Event()
-            st["rb_done"].record(rb_s)
-        mark("readback", tt)
+            st[("rb_done", i)] = torch.cuda.Event()
+            st[("rb_done", i)].record(rb_s)
+        mark("readback", tt, rb_s)
         h2d = idx_h.numel() * 4 + (off_h.numel() * 8 if off_h is not None else 0)
         return prep.packed["n_hot_lookups"], h2d, out.numel() * 4
 
     enqueue_copy(0)
     step(0, True)             # warm-up
     torch.cuda.synchronize()
-    st.pop("rb_done", None)
     ksteps = max(5, args.steps)   # amortise the first (unoverlapped) input copy
     t0 = time.perf_counter()
     n = h2d = d2h = 0
@@ -503,7 +578,8 @@ def run_e2e(args, ctxs):
         dt, n = float(mx[0]), float(sm[1])
     return {"value": n / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": ksteps,
-            "overlap": "step k+1's input copy runs on a copy stream during step k's extract/train; step k's hot-table readback runs on its own stream during step k+1's preprocessing"}
+            "overlap": ("step k+1's input copy runs on a copy stream during step k's extract/train; the hot-table "
+                        "readback runs on its own stream during step k+1's preprocessing")}
 
 
 # ----------------------------------------------------------------------------
@@ -894,7 +970,7 @@ def run_train(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     # default: the largest single-GPU configuration (Terabyte-shaped, RMC3)
     ap.add_argument("--config", default="terabyte", choices=sorted(gen.CONFIGS))
@@ -911,6 +987,9 @@ def main():
     ap.add_argument("--no-ktiming", action="store_true", help="no in-kernel stamps (overhead check; no roofline)")
     ap.add_argument("--dy-pool-mb", type=int, default=256, help="upstream-gradient pool (> L2 by default)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--overlap", action="store_true",
+                    help="A/B: step k+1's preprocessing on a second ctx / stream during step k's training "
+                         "(measured slower on B200: the streaming preprocessing slows the latency-bound training)")
     ap.add_argument("--exchange", action="store_true",
                     help="N=1: run the multi-rank exchange loop on a 1-rank NCCL communicator (sync cost)")
     ap.add_argument("--sweep", action="store_true", help="threshold sweep (one JSON line; not the driver's bench)")

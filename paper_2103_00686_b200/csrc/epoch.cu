@@ -823,6 +823,14 @@ k_grp_reduce_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__
     }
 }
 
+// timing stamps of a call: minima (slots 0, 2, 4, 5, 10) start at ~0, the rest at 0
+__global__ void k_stamps_init(unsigned long long* st, int64_t cnt) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < cnt; e += (int64_t)gridDim.x * blockDim.x) {
+        const int q = (int)(e % kSt);
+        st[e] = (q == 0 || q == 2 || q == 4 || q == 5 || q == 10) ? ~0ull : 0ull;
+    }
+}
+
 __global__ void k_set_run(int64_t* cursor, int64_t first, int64_t n, int64_t n_total) {
     if (threadIdx.x == 0) {
         cursor[0] = 0;
@@ -1327,6 +1335,8 @@ void group_free(Ctx* c) {
                     g.seg_row, g.tile_start, g.tile_batch, g.sstatus, g.pstatus, g.ghist, g.cursor, g.done_ctr, g.pbar,
                     g.stamps};
     for (void* p : ptrs) cudaFree(p);
+    if (g.h_stamps) cudaFreeHost(g.h_stamps);
+    if (g.h_ev) cudaEventDestroy(g.h_ev);
     g = Group{};
 }
 
@@ -1370,8 +1380,72 @@ static fae_status harvest_x(Ctx* c, int64_t n, int64_t xcap) {
     return FAE_OK;
 }
 
+// Process the deferred stamps of the last timed fae_train_hot_batches call
+// (world 1): exclusive kernel shares accumulated into the ctx's totals.
+fae_status harvest_pending(Ctx* c) {
+    Group& g = c->grp;
+    if (g.h_pending_n <= 0) return FAE_OK;
+    FAE_CUDA(c, cudaEventSynchronize(g.h_ev));
+    const int64_t n = g.h_pending_n;
+    const bool fused = g.h_pending_fused;
+    g.h_pending_n = 0;
+    const unsigned long long* st = g.h_stamps;
+    if (fused) {
+        for (int64_t i = 0; i <= n; i++) {
+            // K(i)'s exclusive share: from the end of K(i-1) (its own entry
+            // for the first step) to its end; no stamp waits on the grid
+            // dependency, so the kernels run exactly as untimed
+            const unsigned long long re = st[kSt * i + 3];
+            if (re == 0) continue;
+            const unsigned long long r0 = i > 0 ? st[kSt * (i - 1) + 3] : st[kSt * i + 4];
+            if (i > 0 && st[kSt * i + 4] < st[kSt * (i - 1) + 3]) c->t_overlap_n++;
+            c->t_ms[1] += re > r0 ? (double)(re - r0) * 1e-6 : 0.0;
+            c->t_n[1]++;
+        }
+        c->t_fused = true;
+        return FAE_OK;
+    }
+    for (int64_t i = 0; i < n; i++) {
+        // exclusive shares without any stamp waiting on the grid dependency:
+        // fwd(i) from the end of reduce(i-1) (its entry for the first
+        // step), reduce(i) from the end of fwd(i)
+        const unsigned long long fs = i > 0 ? st[kSt * (i - 1) + 3] : st[kSt * i + 5];
+        const unsigned long long fe = st[kSt * i + 1], re = st[kSt * i + 3];
+        if (fe == 0 || re == 0) continue;
+        // overlap evidence: the reduce entered before the forward ended
+        if (st[kSt * i + 4] < fe) c->t_overlap_n++;
+        c->t_red_entry_lead_ms += fe > st[kSt * i + 4] ? (double)(fe - st[kSt * i + 4]) * 1e-6 : 0.0;
+        c->t_ms[0] += fe > fs ? (double)(fe - fs) * 1e-6 : 0.0;
+        c->t_ms[1] += re > fe ? (double)(re - fe) * 1e-6 : 0.0;
+        c->t_n[0]++;
+        c->t_n[1]++;
+        if (st[kSt * i + 6] > fe) c->t_tier_ms[0] += (double)(st[kSt * i + 6] - fe) * 1e-6;
+        if (st[kSt * i + 7] > fe) c->t_tier_ms[1] += (double)(st[kSt * i + 7] - fe) * 1e-6;
+    }
+    if (getenv("FAE_VERBOSE") && n > 1) {
+        double a8 = 0, a9 = 0;
+        int64_t m = 0;
+        for (int64_t i = 1; i < n; i++) {
+            const double fe = (double)st[kSt * i + 1], pe = (double)st[kSt * (i - 1) + 3];
+            if (fe == 0 || pe == 0) continue;
+            a8 += (double)st[kSt * i + 8] - fe;
+            a9 += (double)st[kSt * i + 9] - pe;
+            m++;
+        }
+        if (m)
+            fprintf(stderr, "[fae_train_hot_batches] last reduce CTA entry %+.2f us after the fwd end; last fwd "
+                            "CTA entry %+.2f us after the previous reduce end\n",
+                    a8 / m * 1e-3, a9 / m * 1e-3);
+        if (c->t_n[1] > 0)
+            fprintf(stderr, "[fae_train_hot_batches] avg after fwd end: long CTAs %.2f us, short/medium CTAs %.2f us\n",
+                    c->t_tier_ms[0] / c->t_n[1] * 1e3, c->t_tier_ms[1] / c->t_n[1] * 1e3);
+    }
+    return FAE_OK;
+}
+
 extern "C" fae_status fae_set_kernel_timing(fae_ctx* h, int32_t enable) {
     if (!h) return FAE_ERR_NOT_INIT;
+    h->c.grp.h_pending_n = 0;   // stamps of an earlier timed call are dropped with the totals
     h->c.timing = enable;
     h->c.t_ms[0] = h->c.t_ms[1] = 0.0;
     h->c.t_n[0] = h->c.t_n[1] = 0;
@@ -1402,6 +1476,10 @@ extern "C" fae_status fae_get_exchange_timing(const fae_ctx* h, double* out) {
 
 extern "C" fae_status fae_get_kernel_timing(const fae_ctx* h, double* ms, int64_t* n) {
     if (!h || !ms || !n) return FAE_ERR_INVALID_ARG;
+    {
+        fae_status hs = harvest_pending(const_cast<Ctx*>(&h->c));   // a deferred harvest
+        if (hs != FAE_OK) return hs;
+    }
     ms[0] = h->c.t_ms[0];
     ms[1] = h->c.t_ms[1];
     ms[2] = h->c.t_red_entry_lead_ms;
@@ -1441,28 +1519,19 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
     // loop never queues behind a bulk host->device transfer on the copy engine
     // timing stamps (fae_set_kernel_timing(1)): kSt slots per step, reset here
     auto stamps_init = [&](int64_t steps) -> fae_status {
+        fae_status hs = harvest_pending(c);        // the previous call's stamps first
+        if (hs != FAE_OK) return hs;
         if (g.stamp_cap < steps + 1) {
+            FAE_CUDA(c, cudaStreamSynchronize(c->stream));
             cudaFree(g.stamps);
             g.stamps = nullptr;
             g.stamp_cap = steps + steps / 4 + 64;
             FAE_CUDA(c, cudaMalloc(&g.stamps, sizeof(unsigned long long) * kSt * g.stamp_cap));
         }
-        std::vector<unsigned long long> init(kSt * (steps + 1));
-        for (int64_t i = 0; i <= steps; i++) {
-            init[kSt * i + 0] = ~0ull;
-            init[kSt * i + 1] = 0;
-            init[kSt * i + 2] = ~0ull;
-            init[kSt * i + 3] = 0;
-            init[kSt * i + 4] = ~0ull;
-            init[kSt * i + 5] = ~0ull;
-            init[kSt * i + 6] = 0;
-            init[kSt * i + 7] = 0;   // tier ends
-            for (int q = 8; q < kSt; q++) init[kSt * i + q] = 0;   // maxima
-            init[kSt * i + 10] = ~0ull;                             // merge entry (min)
-        }
-        FAE_CUDA(c, cudaMemcpyAsync(g.stamps, init.data(), sizeof(unsigned long long) * kSt * (steps + 1),
-                                    cudaMemcpyHostToDevice, c->stream));
-        FAE_CUDA(c, cudaStreamSynchronize(c->stream));
+        const int64_t cnt = kSt * (steps + 1);
+        k_stamps_init<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(cnt, 256), 1024)), 256, 0, c->stream>>>(
+            g.stamps, cnt);
+        FAE_LAUNCHED(c);
         return FAE_OK;
     };
     const bool xpath = c->world > 1 || c->force_merge;
@@ -1702,70 +1771,24 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
     }
     for (int64_t r = 0; r < reps; r++) FAE_CUDA(c, cudaGraphLaunch(g.graph, c->stream));
     c->launches += 2 * reps * g.graph_steps;
-    if (stamps && fused) {
-        // one kernel per step: K(i)'s exclusive share runs from the end of
-        // K(i-1) (same replay) to its own end; attributed to slot 1
-        std::vector<unsigned long long> st(kSt * (n + 1));
-        FAE_CUDA(c, cudaMemcpyAsync(st.data(), stamps, sizeof(unsigned long long) * kSt * (n + 1),
-                                    cudaMemcpyDeviceToHost, c->stream));
-        FAE_CUDA(c, cudaStreamSynchronize(c->stream));
-        for (int64_t i = 0; i <= n; i++) {
-            // K(i)'s exclusive share: from the end of K(i-1) (its own entry
-            // for the first step) to its end; no stamp waits on the grid
-            // dependency, so the kernels run exactly as untimed
-            const unsigned long long re = st[kSt * i + 3];
-            if (re == 0) continue;
-            const unsigned long long r0 = i > 0 ? st[kSt * (i - 1) + 3] : st[kSt * i + 4];
-            if (i > 0 && st[kSt * i + 4] < st[kSt * (i - 1) + 3]) c->t_overlap_n++;
-            c->t_ms[1] += re > r0 ? (double)(re - r0) * 1e-6 : 0.0;
-            c->t_n[1]++;
+    if (stamps) {
+        // deferred harvest: the stamps go to pinned host memory behind the
+        // graph on the ctx stream and are processed at the next timed call
+        // or fae_get_kernel_timing, so the host never waits for the
+        // training here (cross-step overlap keeps running)
+        const int64_t cnt = kSt * (n + 1);
+        if (g.h_stamps_cap < cnt) {
+            if (g.h_stamps) cudaFreeHost(g.h_stamps);
+            g.h_stamps = nullptr;
+            g.h_stamps_cap = cnt + cnt / 4 + 256;
+            FAE_CUDA(c, cudaMallocHost(&g.h_stamps, sizeof(unsigned long long) * g.h_stamps_cap));
         }
-        c->t_fused = true;
-    } else if (stamps) {
-        // exclusive critical-path share of each kernel: fwd(s) from the end of
-        // reduce(s-1) (same replay), reduce(s) from the end of fwd(s)
-        std::vector<unsigned long long> st(kSt * n);
-        FAE_CUDA(c, cudaMemcpyAsync(st.data(), stamps, sizeof(unsigned long long) * kSt * n,
-                                    cudaMemcpyDeviceToHost, c->stream));
-        FAE_CUDA(c, cudaStreamSynchronize(c->stream));
-        for (int64_t i = 0; i < n; i++) {
-            // exclusive shares without any stamp waiting on the grid dependency:
-            // fwd(i) from the end of reduce(i-1) (its entry for the first
-            // step), reduce(i) from the end of fwd(i)
-            const unsigned long long fs = i > 0 ? st[kSt * (i - 1) + 3] : st[kSt * i + 5];
-            const unsigned long long fe = st[kSt * i + 1], re = st[kSt * i + 3];
-            if (fe == 0 || re == 0) continue;
-            // overlap evidence: the reduce entered before the forward ended
-            if (st[kSt * i + 4] < fe) c->t_overlap_n++;
-            c->t_red_entry_lead_ms += fe > st[kSt * i + 4] ? (double)(fe - st[kSt * i + 4]) * 1e-6 : 0.0;
-            const unsigned long long f0 = fs, r0 = fe;
-            c->t_ms[0] += fe > f0 ? (double)(fe - f0) * 1e-6 : 0.0;
-            c->t_ms[1] += re > r0 ? (double)(re - r0) * 1e-6 : 0.0;
-            c->t_n[0]++;
-            c->t_n[1]++;
-            if (st[kSt * i + 6] > fe) c->t_tier_ms[0] += (double)(st[kSt * i + 6] - fe) * 1e-6;
-            if (st[kSt * i + 7] > fe) c->t_tier_ms[1] += (double)(st[kSt * i + 7] - fe) * 1e-6;
-        }
-        if (getenv("FAE_VERBOSE") && n > 1) {
-            double a8 = 0, a9 = 0, a11 = 0;
-            int64_t m = 0;
-            for (int64_t i = 1; i < n; i++) {
-                const double fe = (double)st[kSt * i + 1], pe = (double)st[kSt * (i - 1) + 3];
-                if (fe == 0 || pe == 0) continue;
-                a8 += (double)st[kSt * i + 8] - fe;
-                a9 += (double)st[kSt * i + 9] - pe;
-                a11 += 0.0;
-                m++;
-            }
-            if (m)
-                fprintf(stderr, "[fae_train_hot_batches] last reduce CTA entry %+.2f us after the fwd end; last fwd "
-                                "CTA entry %+.2f us after the previous reduce end\n",
-                        a8 / m * 1e-3, a9 / m * 1e-3);
-            (void)a11;
-        }
-        if (getenv("FAE_VERBOSE") && c->t_n[1] > 0)
-            fprintf(stderr, "[fae_train_hot_batches] avg after fwd end: long CTAs %.2f us, short/medium CTAs %.2f us\n",
-                    c->t_tier_ms[0] / c->t_n[1] * 1e3, c->t_tier_ms[1] / c->t_n[1] * 1e3);
+        if (!g.h_ev) FAE_CUDA(c, cudaEventCreateWithFlags(&g.h_ev, cudaEventDisableTiming));
+        FAE_CUDA(c, cudaMemcpyAsync(g.h_stamps, stamps, sizeof(unsigned long long) * cnt, cudaMemcpyDeviceToHost,
+                                    c->stream));
+        FAE_CUDA(c, cudaEventRecord(g.h_ev, c->stream));
+        g.h_pending_n = n;
+        g.h_pending_fused = fused;
     }
     return FAE_OK;
 }

@@ -204,6 +204,11 @@ struct Group {
     uint64_t tgraph_key = 0;
     unsigned long long* stamps = nullptr;
     int64_t stamp_cap = 0;
+    unsigned long long* h_stamps = nullptr;   // pinned: deferred harvest of the last timed call
+    int64_t h_stamps_cap = 0;
+    cudaEvent_t h_ev = nullptr;
+    int64_t h_pending_n = 0;
+    bool h_pending_fused = false;
 };
 
 struct Ctx {
