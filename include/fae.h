@@ -597,8 +597,13 @@ fae_status fae_dlrm_buffers(fae_dlrm* m, float** Y, float** dY,
  * int64 [n_hot], dense [n_records][n_dense], label [n_records], indexed by
  * record id), then a9 + a10 on W_hot with the model's dY (lr_emb);
  * replayed from a captured graph of 128 steps.  Sequential semantics.
- * Errors: NOT_INIT (no grouping), INVALID_ARG (shapes differ from the
- * grouping / model, world > 1). */
+ * World > 1 (data parallel, every rank the same n): the loss is averaged
+ * over the GLOBAL batch of each step (every rank's records), the MLP
+ * gradient is all-reduced in ONE collective group with the hot-gradient
+ * all-gathers of a11, then every rank applies the merged hot rows and
+ * params -= lr_mlp * (summed gradient): replicas stay identical.
+ * Errors: NOT_INIT (no grouping, or world > 1 without a comm), INVALID_ARG
+ * (shapes differ from the grouping / model). */
 fae_status fae_train_dlrm_batches(fae_ctx* ctx, fae_dlrm* m, float* params,
                                   float* W_hot, int64_t H, int32_t D,
                                   int64_t first, int64_t n,

@@ -13,8 +13,10 @@
 //    gradient exchange and its rank-ordered merge) runs in the parity tests.
 //    Only the transport differs; the calling code is the same.
 //
-// Semantics (both transports): allreduce = elementwise integer sum in place
-// (uint32 wraps mod 2^32 like ncclSum); allgather = rank r's `count`
+// Semantics (both transports): allreduce = elementwise sum in place
+// (integers: uint32 wraps mod 2^32 like ncclSum; fp32: the loopback sums in
+// rank order, NCCL in its own fixed order — identical on every rank either
+// way); allgather = rank r's `count`
 // elements land at recv + r*count on every rank.
 #include <chrono>
 #include <condition_variable>
@@ -136,8 +138,10 @@ static fae_status lb_collective(Ctx* c, const void* src, void* dst, size_t out_b
                                     c->stream));
         const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(cdiv(count, 256), 1184));
         if (count > 0) {
-            if (esz == 4) k_lb_sum<uint32_t><<<(unsigned)blocks, 256, 0, c->stream>>>(c->lb->dptrs, g.world, count,
-                                                                                     (uint32_t*)tmp);
+            if (t == CollT::F32) k_lb_sum<float><<<(unsigned)blocks, 256, 0, c->stream>>>(c->lb->dptrs, g.world, count,
+                                                                                         (float*)tmp);
+            else if (esz == 4) k_lb_sum<uint32_t><<<(unsigned)blocks, 256, 0, c->stream>>>(c->lb->dptrs, g.world, count,
+                                                                                          (uint32_t*)tmp);
             else k_lb_sum<unsigned long long><<<(unsigned)blocks, 256, 0, c->stream>>>(c->lb->dptrs, g.world, count,
                                                                                       (unsigned long long*)tmp);
             FAE_LAUNCHED(c);
@@ -174,7 +178,6 @@ void coll_free(Ctx* c) {
 // the interface
 // ---------------------------------------------------------------------------
 fae_status coll_allreduce_sum(Ctx* c, void* buf, int64_t count, CollT t, const char* who) {
-    if (t == CollT::F32) return set_err(c, FAE_ERR_INVALID_ARG, std::string(who) + ": float allreduce unsupported");
     if (c->lb) return lb_collective(c, buf, buf, (size_t)count * coll_size(t), who, true, t, count);
     if (!c->comm) return set_err(c, FAE_ERR_NOT_INIT, std::string(who) + ": no communicator");
     ncclResult_t r = ncclAllReduce(buf, buf, (size_t)count, nccl_type(t), ncclSum, c->comm, c->stream);

@@ -48,11 +48,14 @@ struct Dlrm {
     float* dY = nullptr;                  // [max_batch][Tn][D] (the a9 input)
     int16_t* pairs = nullptr;             // [P][2] (i, j), i > j, row-major
     int32_t* pidx = nullptr;              // [F][F] pair index of (max, min), -1 on the diagonal
-    int32_t* nb = nullptr;                // device: samples of the current batch
+    int32_t* nb = nullptr;                // device: [0] samples of the current batch, [1] loss divisor
+    float* gbuf = nullptr;                // [n_params] gradient (world > 1: all-reduced before SGD)
     double* acc = nullptr;                // device: [0] sum of losses, [1] samples
     void* ws = nullptr;                   // cuBLAS workspace (graph capture)
     cudaGraphExec_t graph = nullptr;
     uint64_t graph_key = 0;
+    cudaGraphExec_t xgraph = nullptr;     // world > 1 exchange loop
+    uint64_t xgraph_key = 0;
     int max_w = 0;
 };
 
@@ -252,7 +255,8 @@ __global__ void __launch_bounds__(1024) k_loss(float* __restrict__ z, const floa
                                                const float* __restrict__ y, int B, const int32_t* __restrict__ nb,
                                                float* __restrict__ dz, double* __restrict__ acc, int train) {
     __shared__ double s_w[32];
-    const int n = *nb;
+    const int n = nb[0];
+    const int ndiv = nb[1] > 0 ? nb[1] : 1;   // samples of the (global) batch the loss is the mean over
     double part = 0.0;
     for (int b = threadIdx.x; b < B; b += blockDim.x) {
         float d = 0.f;
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(1024) k_loss(float* __restrict__ z, const floa
             const float yy = y[b];
             part += (double)(fmaxf(v, 0.f) - v * yy + log1pf(expf(-fabsf(v))));
             const float s = 1.f / (1.f + expf(-v));
-            d = (s - yy) / (float)n;
+            d = (s - yy) / (float)ndiv;
         }
         if (train) dz[b] = d;
     }
@@ -282,7 +286,7 @@ __global__ void k_dlrm_stage(const BatchDesc* __restrict__ desc, const int64_t* 
                              const int64_t* __restrict__ base, int s, int Tn, const int64_t* __restrict__ hot_ids,
                              const float* __restrict__ dense, const float* __restrict__ label, int n_dense,
                              int max_batch, float* __restrict__ sdense, float* __restrict__ slabel,
-                             int32_t* __restrict__ nb) {
+                             int32_t* __restrict__ nb, const int32_t* __restrict__ rec_total) {
     const int64_t rel = *base + s;
     int n = 0;
     int64_t r0 = 0;
@@ -298,11 +302,20 @@ __global__ void k_dlrm_stage(const BatchDesc* __restrict__ desc, const int64_t* 
         if (k < n_dense) sdense[(int64_t)b * n_dense + k] = b < n ? dense[rec * n_dense + k] : 0.f;
         else slabel[b] = b < n ? label[rec] : 0.f;
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) *nb = n;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        nb[0] = n;
+        nb[1] = rec_total ? (rel < base[4] ? rec_total[rel] : 0) : n;   // world > 1: the global batch
+    }
 }
 
 __global__ void k_set_nb(int32_t* nb, int v) {
-    if (threadIdx.x == 0) *nb = v;
+    if (threadIdx.x == 0) nb[0] = nb[1] = v;
+}
+
+// p = fmaf(-lr, g, p) over the flat parameters (world > 1, after the all-reduce)
+__global__ void k_mlp_sgd(float* __restrict__ p, const float* __restrict__ g, int64_t n, float lr) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        p[e] = __fmaf_rn(-lr, g[e], p[e]);
 }
 
 // ---------------------------------------------------------------------------
@@ -324,7 +337,7 @@ static unsigned grid_for(int64_t n, Ctx* c) {
 
 // One DLRM forward (+ backward + SGD when train) on the staged buffers of
 // the dlrm (act[0] = dense, label, Y -> dY), batch size *nb <= max_batch.
-static fae_status dlrm_run(Dlrm* m, float* params, float lr, bool train, cudaStream_t st) {
+static fae_status dlrm_run(Dlrm* m, float* params, float lr, bool train, cudaStream_t st, bool grad_only = false) {
     Ctx* c = m->c;
     const int B = m->cfg.max_batch, nbot = m->cfg.n_bottom, L = m->n_layers;
     const int Tn = m->cfg.n_tables, D = m->cfg.dim;
@@ -375,9 +388,16 @@ static fae_status dlrm_run(Dlrm* m, float* params, float lr, bool train, cudaStr
         if (l > 0)
             FAE_BLAS(c, cublasSgemm(m->blas, CUBLAS_OP_N, CUBLAS_OP_N, in, B, out, &one, W, in, dC, out, &zero, dX,
                                     in));
-        // W += -lr * X^T dC ; b += -lr * dC^T 1
-        FAE_BLAS(c, cublasSgemm(m->blas, CUBLAS_OP_N, CUBLAS_OP_T, in, out, B, &mlr, X, in, dC, out, &one, W, in));
-        FAE_BLAS(c, cublasSgemv(m->blas, CUBLAS_OP_N, out, B, &mlr, dC, out, m->ones, 1, &one, bvec, 1));
+        if (grad_only) {   // world > 1: the gradient, all-reduced before the update
+            FAE_BLAS(c, cublasSgemm(m->blas, CUBLAS_OP_N, CUBLAS_OP_T, in, out, B, &one, X, in, dC, out, &zero,
+                                    m->gbuf + m->woff[l], in));
+            FAE_BLAS(c, cublasSgemv(m->blas, CUBLAS_OP_N, out, B, &one, dC, out, m->ones, 1, &zero,
+                                    m->gbuf + m->boff[l], 1));
+        } else {
+            // W += -lr * X^T dC ; b += -lr * dC^T 1
+            FAE_BLAS(c, cublasSgemm(m->blas, CUBLAS_OP_N, CUBLAS_OP_T, in, out, B, &mlr, X, in, dC, out, &one, W, in));
+            FAE_BLAS(c, cublasSgemv(m->blas, CUBLAS_OP_N, out, B, &mlr, dC, out, m->ones, 1, &one, bvec, 1));
+        }
         if (l == 0) break;
         if (l == nbot) {
             // dX = d(interaction output) -> dT: bottom output gradient (masked) and dY
@@ -446,9 +466,10 @@ extern "C" void fae_dlrm_destroy(fae_dlrm* h) {
     if (!h) return;
     Dlrm& m = h->m;
     if (m.graph) cudaGraphExecDestroy(m.graph);
+    if (m.xgraph) cudaGraphExecDestroy(m.xgraph);
     if (m.blas) cublasDestroy(m.blas);
     for (float* p : m.act) cudaFree(p);
-    void* ptrs[] = {m.grad_a, m.grad_b, m.ones, m.label, m.Y, m.dY, m.pairs, m.pidx, m.nb, m.acc, m.ws};
+    void* ptrs[] = {m.grad_a, m.grad_b, m.ones, m.label, m.Y, m.dY, m.pairs, m.pidx, m.nb, m.acc, m.ws, m.gbuf};
     for (void* p : ptrs) cudaFree(p);
     delete h;
 }
@@ -514,7 +535,8 @@ extern "C" fae_status fae_dlrm_create(fae_ctx* ctx, const fae_dlrm_cfg* g, fae_d
               cudaMalloc(&m.dY, sizeof(float) * (size_t)B * Tn * D) == cudaSuccess &&
               cudaMalloc(&m.pairs, sizeof(int16_t) * 2 * std::max(m.P, 1)) == cudaSuccess &&
               cudaMalloc(&m.pidx, sizeof(int32_t) * m.F * m.F) == cudaSuccess &&
-              cudaMalloc(&m.nb, sizeof(int32_t)) == cudaSuccess && cudaMalloc(&m.acc, sizeof(double) * 2) == cudaSuccess &&
+              cudaMalloc(&m.nb, sizeof(int32_t) * 2) == cudaSuccess && cudaMalloc(&m.acc, sizeof(double) * 2) == cudaSuccess &&
+              cudaMalloc(&m.gbuf, sizeof(float) * std::max<int64_t>(m.n_params, 1)) == cudaSuccess &&
               cudaMalloc(&m.ws, 32u << 20) == cudaSuccess;
     if (!ok) return fail(cuda_err(c, cudaGetLastError(), "fae_dlrm_create: allocation"));
     std::vector<float> ones(B, 1.f);
@@ -529,7 +551,7 @@ extern "C" fae_status fae_dlrm_create(fae_ctx* ctx, const fae_dlrm_cfg* g, fae_d
     if (cudaMemcpy(m.ones, ones.data(), sizeof(float) * B, cudaMemcpyHostToDevice) != cudaSuccess ||
         (m.P && cudaMemcpy(m.pairs, pr.data(), sizeof(int16_t) * pr.size(), cudaMemcpyHostToDevice) != cudaSuccess) ||
         cudaMemcpy(m.pidx, pidx.data(), sizeof(int32_t) * pidx.size(), cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemset(m.acc, 0, sizeof(double) * 2) != cudaSuccess || cudaMemset(m.nb, 0, sizeof(int32_t)) != cudaSuccess ||
+        cudaMemset(m.acc, 0, sizeof(double) * 2) != cudaSuccess || cudaMemset(m.nb, 0, sizeof(int32_t) * 2) != cudaSuccess ||
         cudaMemset(m.dY, 0, sizeof(float) * (size_t)B * Tn * D) != cudaSuccess)
         return fail(cuda_err(c, cudaGetLastError(), "fae_dlrm_create: upload"));
     if (cublasCreate(&m.blas) != CUBLAS_STATUS_SUCCESS)
@@ -593,6 +615,110 @@ fae_status launch_grp_reduce_any(Ctx* c, cudaStream_t st, int s, int last, float
                                  const float* dY, float lr);
 }
 
+// World > 1 (or FAE_FORCE_MERGE): data-parallel DLRM hot step.  Per step:
+// the a8 forward of this rank's batch, the DLRM forward + backward with the
+// loss averaged over the GLOBAL batch (every rank's records of the step) and
+// the MLP gradient kept in gbuf, the a9 sums emitted into this rank's slot,
+// then ONE collective group — the MLP gradient all-reduce fused with the
+// hot-gradient all-gathers — and the
+// updates: the rank-ordered hot-row merge + SGD, and params -= lr * gbuf.
+// Replicas stay identical: every rank applies the same all-reduced /
+// merged bits.
+static fae_status train_dlrm_exchange(Ctx* c, Dlrm& m, float* params, float* W_hot, int64_t H, int D, int64_t first,
+                                      int64_t n, const int64_t* hot_ids, const float* dense, const float* label,
+                                      float lr_mlp, float lr_emb) {
+    Group& g = c->grp;
+    if (!has_comm(c)) return set_err(c, FAE_ERR_NOT_INIT, "fae_train_dlrm_batches: world > 1 without a communicator");
+    XPrep xp;
+    int32_t* rtot = nullptr;
+    fae_status st0 = x_prepare(c, first, n, H, &rtot, &xp);
+    if (st0 != FAE_OK) return st0;
+    const int64_t xcap = xp.xcap;
+    auto step = [&](cudaStream_t st, int s, int last) -> fae_status {
+        fae_status r = launch_grp_fwd_x(c, st, s, W_hot, H, D, m.Y);
+        if (r != FAE_OK) return r;
+        k_dlrm_stage<<<grid_for((int64_t)m.cfg.max_batch * (m.cfg.n_dense + 1), c), 256, 0, st>>>(
+            g.desc, g.run, g.cursor, s, g.Tn, hot_ids, dense, label, m.cfg.n_dense, m.cfg.max_batch, m.act[0],
+            m.label, m.nb, rtot);
+        FAE_LAUNCHED(c);
+        r = dlrm_run(&m, params, lr_mlp, true, st, true);
+        if (r != FAE_OK) return r;
+        r = launch_xreduce_plain(c, st, s, D, m.dY, xcap);
+        if (r != FAE_OK) return r;
+        {
+            cudaStream_t keep = c->stream;
+            c->stream = st;
+            coll_group_start(c);
+            fae_status a = coll_allreduce_sum(c, m.gbuf, m.n_params, CollT::F32, "dlrm exchange: MLP gradients");
+            if (a == FAE_OK)
+                a = coll_allgather(c, c->g_rows + (int64_t)c->rank * xcap, c->g_rows, xcap, CollT::I32,
+                                   "dlrm exchange: allgather rows");
+            if (a == FAE_OK)
+                a = coll_allgather(c, c->g_vals + (int64_t)c->rank * xcap * D, c->g_vals, xcap * D, CollT::F32,
+                                   "dlrm exchange: allgather grads");
+            fae_status b = coll_group_end(c, "dlrm exchange");
+            c->stream = keep;
+            if (a != FAE_OK) return a;
+            if (b != FAE_OK) return b;
+        }
+        r = launch_xmerge_any(c, st, s, last, W_hot, H, D, lr_emb, xcap, xp.per_step, xp.table);
+        if (r != FAE_OK) return r;
+        k_mlp_sgd<<<grid_for(m.n_params, c), 256, 0, st>>>(params, m.gbuf, m.n_params, lr_mlp);
+        FAE_LAUNCHED(c);
+        return FAE_OK;
+    };
+    if (c->lb) {   // loopback (tests): host loop of the same kernels, replay-shaped steps
+        for (int64_t i = 0; i < n; i++) {
+            const int s = (int)(i % kUnroll);
+            fae_status r = step(c->stream, s, s == kUnroll - 1 ? kUnroll : 0);
+            if (r != FAE_OK) return r;
+        }
+        return coll_async_error(c, "fae_train_dlrm_batches");
+    }
+    uint64_t key = 1469598103934665603ull;
+    auto mix = [&](uint64_t v) { key = (key ^ v) * 1099511628211ull; };
+    for (uint64_t v : {(uint64_t)(uintptr_t)params, (uint64_t)(uintptr_t)W_hot, (uint64_t)H, (uint64_t)D,
+                       (uint64_t)(uintptr_t)hot_ids, (uint64_t)(uintptr_t)dense, (uint64_t)(uintptr_t)label,
+                       (uint64_t)(uintptr_t)g.desc, (uint64_t)(uintptr_t)g.perm, (uint64_t)(uintptr_t)g.rec,
+                       (uint64_t)(uintptr_t)g.lmap, (uint64_t)(uintptr_t)g.lpart, (uint64_t)(uintptr_t)g.seg_row,
+                       (uint64_t)g.max_bags, (uint64_t)g.max_lchunk, (uint64_t)g.max_long, (uint64_t)xcap,
+                       (uint64_t)(uintptr_t)xp.per_step, (uint64_t)(uintptr_t)rtot, (uint64_t)xp.table,
+                       (uint64_t)(uintptr_t)g.ptab, (uint64_t)(uintptr_t)c->comm, (uint64_t)c->rank, (uint64_t)c->world})
+        mix(v);
+    uint32_t a, b;
+    memcpy(&a, &lr_mlp, 4);
+    memcpy(&b, &lr_emb, 4);
+    mix(a);
+    mix(b);
+    if (!m.xgraph || m.xgraph_key != key) {
+        if (m.xgraph) cudaGraphExecDestroy(m.xgraph);
+        m.xgraph = nullptr;
+        cudaStream_t cs;
+        FAE_CUDA(c, cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        cudaGraph_t graph;
+        const int64_t l0 = c->launches;
+        FAE_CUDA(c, cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        fae_status st = FAE_OK;
+        for (int s = 0; s < kUnroll && st == FAE_OK; s++) st = step(cs, s, s == kUnroll - 1 ? kUnroll : 0);
+        cudaError_t e = cudaStreamEndCapture(cs, &graph);
+        c->launches = l0;
+        if (st != FAE_OK || e != cudaSuccess) {
+            if (e == cudaSuccess) cudaGraphDestroy(graph);
+            cudaStreamDestroy(cs);
+            return st != FAE_OK ? st : cuda_err(c, e, "cudaStreamEndCapture (dlrm exchange)");
+        }
+        e = cudaGraphInstantiate(&m.xgraph, graph, 0);
+        cudaGraphDestroy(graph);
+        cudaStreamDestroy(cs);
+        if (e != cudaSuccess) return cuda_err(c, e, "cudaGraphInstantiate (dlrm exchange)");
+        m.xgraph_key = key;
+    }
+    const int64_t reps = cdiv(n, kUnroll);
+    for (int64_t r = 0; r < reps; r++) FAE_CUDA(c, cudaGraphLaunch(m.xgraph, c->stream));
+    c->launches += reps * kUnroll * (int64_t)(8 + 6 * m.n_layers);
+    return coll_async_error(c, "fae_train_dlrm_batches");
+}
+
 extern "C" fae_status fae_train_dlrm_batches(fae_ctx* ctx, fae_dlrm* h, float* params, float* W_hot, int64_t H,
                                              int32_t D, int64_t first, int64_t n, const int64_t* hot_ids,
                                              const float* dense, const float* label, float lr_mlp, float lr_emb) {
@@ -601,13 +727,16 @@ extern "C" fae_status fae_train_dlrm_batches(fae_ctx* ctx, fae_dlrm* h, float* p
     Dlrm& m = h->m;
     Group& g = c->grp;
     if (!g.valid) return set_err(c, FAE_ERR_NOT_INIT, "fae_train_dlrm_batches: no grouped batches");
-    if (!params || !W_hot || !hot_ids || !dense || !label || first < 0 || n < 0 || first + n > g.n_batches ||
-        H != g.H || D != m.cfg.dim || D != g.dim || g.Tn != m.cfg.n_tables || g.B > m.cfg.max_batch ||
-        !(lr_mlp == lr_mlp) || !(lr_emb == lr_emb))
-        return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_dlrm_batches: bad arguments");
-    if (c->world > 1 || c->force_merge)
-        return set_err(c, FAE_ERR_INVALID_ARG, "fae_train_dlrm_batches: world > 1 is not supported");
+    const bool xpath = c->world > 1 || c->force_merge;
+    fae_status vst = FAE_OK;
+    if (!params || !W_hot || !hot_ids || !dense || !label || first < 0 || n < 0 ||
+        (!xpath && first + n > g.n_batches) || H != g.H || D != m.cfg.dim || D != g.dim ||
+        g.Tn != m.cfg.n_tables || g.B > m.cfg.max_batch || !(lr_mlp == lr_mlp) || !(lr_emb == lr_emb))
+        vst = set_err(c, FAE_ERR_INVALID_ARG, "fae_train_dlrm_batches: bad arguments");
+    if (xpath && has_comm(c) && c->world > 1) vst = coll_agree(c, vst, "fae_train_dlrm_batches");
+    if (vst != FAE_OK) return vst;
     if (n == 0) return FAE_OK;
+    if (xpath) return train_dlrm_exchange(c, m, params, W_hot, H, D, first, n, hot_ids, dense, label, lr_mlp, lr_emb);
     fae_status rs = launch_set_run(c, c->stream, first, n, n);
     if (rs != FAE_OK) return rs;
     uint64_t key = 1469598103934665603ull;
@@ -637,7 +766,7 @@ extern "C" fae_status fae_train_dlrm_batches(fae_ctx* ctx, fae_dlrm* h, float* p
             if (st != FAE_OK) break;
             k_dlrm_stage<<<grid_for((int64_t)m.cfg.max_batch * (m.cfg.n_dense + 1), c), 256, 0, cs>>>(
                 g.desc, g.run, g.cursor, s, g.Tn, hot_ids, dense, label, m.cfg.n_dense, m.cfg.max_batch, m.act[0],
-                m.label, m.nb);
+                m.label, m.nb, (const int32_t*)nullptr);
             if (cudaGetLastError() != cudaSuccess) {
                 st = set_err(c, FAE_ERR_CUDA, "fae_train_dlrm_batches: stage launch");
                 break;

@@ -1344,6 +1344,156 @@ void group_free(Ctx* c) {
 
 using namespace fae;
 
+namespace fae {
+// Setup of an exchange run (world > 1 or FAE_FORCE_MERGE) over grouped
+// batches [first, first + n): the run cursor, every step's per-rank segment
+// counts all-gathered once (one host read; xcap = their maximum; device
+// [n][world] per_step), optionally every step's per-rank record counts
+// (rec_total[i] = the global batch's records of step i, device int32 [n]),
+// and the row-position table at world > 2.
+fae_status x_prepare(Ctx* c, int64_t first, int64_t n, int64_t H, int32_t** rec_total, XPrep* out) {
+    Group& g = c->grp;
+    const int world = c->world;
+    const int64_t n_loc = std::max<int64_t>(0, std::min<int64_t>(n, g.n_batches - first));
+    k_set_run<<<1, 32, 0, c->stream>>>(g.cursor, first, n_loc, n);
+    FAE_LAUNCHED(c);
+    const int64_t need = 4 * n * world + 2 * n + 1024;
+    if (g.cap_xcnt < need) {
+        cudaFree(g.xcnt);
+        g.xcnt = nullptr;
+        g.cap_xcnt = need;
+        FAE_CUDA(c, cudaMalloc(&g.xcnt, sizeof(int32_t) * g.cap_xcnt));
+    }
+    // [2][world][n] segment and record counts (gathered), then per_step [n][world], then rec totals [n]
+    std::vector<int32_t> mine(2 * n, 0);
+    for (int64_t i = 0; i < n_loc; i++) {
+        const BatchDesc& d = g.hdesc[first + i];
+        mine[i] = (int32_t)(d.sb1 - d.sb0);
+        mine[n + i] = d.n_bags / std::max(g.Tn, 1);
+    }
+    int32_t* all = g.xcnt;                         // [world][2n]
+    int32_t* per_step = g.xcnt + 2 * n * world;    // [n][world]
+    int32_t* rtot = per_step + n * world;          // [n]
+    FAE_CUDA(c, cudaMemcpyAsync(all + (int64_t)c->rank * 2 * n, mine.data(), sizeof(int32_t) * 2 * n,
+                                cudaMemcpyHostToDevice, c->stream));
+    fae_status cs = coll_allgather(c, all + (int64_t)c->rank * 2 * n, all, 2 * n, CollT::I32,
+                                   "exchange: allgather per-step counts");
+    if (cs != FAE_OK) return cs;
+    std::vector<int32_t> hall((size_t)2 * n * world), ht((size_t)n * world + n);
+    FAE_CUDA(c, cudaMemcpyAsync(hall.data(), all, sizeof(int32_t) * 2 * n * world, cudaMemcpyDeviceToHost, c->stream));
+    FAE_CUDA(c, cudaStreamSynchronize(c->stream));
+    int64_t xcap = 1;
+    for (int64_t i = 0; i < n; i++) {
+        int32_t rt = 0;
+        for (int rk = 0; rk < world; rk++) {
+            const int32_t v = hall[(size_t)rk * 2 * n + i];
+            ht[(size_t)i * world + rk] = v;
+            xcap = std::max<int64_t>(xcap, v);
+            rt += hall[(size_t)rk * 2 * n + n + i];
+        }
+        ht[(size_t)n * world + i] = rt;
+    }
+    // every rank saw the same counts, so every rank takes the same exit
+    if (xcap > c->g_cap) return set_err(c, FAE_ERR_CAPACITY, "exchange: a rank's U exceeds capacity");
+    FAE_CUDA(c, cudaMemcpyAsync(per_step, ht.data(), sizeof(int32_t) * (n * world + n), cudaMemcpyHostToDevice,
+                                c->stream));
+    FAE_CUDA(c, cudaStreamSynchronize(c->stream));   // ht is pageable and goes out of scope
+    g.xcap_last = xcap;
+    const bool table = c->merge_table >= 0 ? c->merge_table == 1 : world > 2;
+    if (table && g.cap_ptab < (int64_t)world * H) {
+        cudaFree(g.ptab);
+        g.ptab = nullptr;
+        g.cap_ptab = 0;
+        FAE_CUDA(c, cudaMalloc(&g.ptab, sizeof(int32_t) * world * std::max<int64_t>(H, 1)));
+        FAE_CUDA(c, cudaMemsetAsync(g.ptab, 0xff, sizeof(int32_t) * world * std::max<int64_t>(H, 1), c->stream));
+        g.cap_ptab = (int64_t)world * H;
+    }
+    out->xcap = xcap;
+    out->per_step = per_step;
+    out->table = table;
+    if (rec_total) *rec_total = rtot;
+    return FAE_OK;
+}
+
+// The DLRM exchange step's pieces (dlrm.cu): the forward of step s in the
+// exchange chain (PDL, waits on every path), the reduce-emit with a dY just
+// produced (no PDL), and the merge (+ table) of step s.
+template <int LPB, int NV>
+static fae_status fwd_x_one(Ctx* c, cudaStream_t st, int s, float* W, int64_t H, int D, float* Y) {
+    Group& g = c->grp;
+    const int64_t gpb = 256 / LPB;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = c->no_pdl ? 0 : 1;
+    const int64_t fu = g.P == 1 ? cdiv(g.max_bags, kFwdU)
+                     : (g.hot_off || g.P >= kWarpBagMinP) ? g.max_bags * (32 / LPB) : g.max_bags;
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(fu, gpb), (int64_t)sm_count(c) * 4)));
+    FAE_CUDA(c, cudaLaunchKernelEx(&cfg, k_grp_fwd_pdl<LPB, NV>, (const BatchDesc*)g.desc, (const int64_t*)g.run,
+                                   (const int64_t*)g.cursor, s, g.hot_idx, g.hot_off, (int)g.P, (const float*)W, H, D,
+                                   Y, c->d_err, (unsigned long long*)nullptr, 4));
+    return FAE_OK;
+}
+
+template <int LPB, int NV>
+static fae_status xreduce_one(Ctx* c, cudaStream_t st, int s, int D, const float* dY, int64_t xcap) {
+    Group& g = c->grp;
+    const int64_t gpb = 256 / LPB;
+    k_grp_xreduce<LPB, NV, 4><<<(unsigned)std::max<int64_t>(1, red_grid(g, gpb)), 256, 0, st>>>(
+        (const BatchDesc*)g.desc, (const int64_t*)g.run, (const int64_t*)g.cursor, s, (const SegRec*)g.rec,
+        (const int32_t*)g.perm, (const int32_t*)g.seg_row, dY, (int64_t)1, g.max_bags * (int64_t)D, D,
+        g.lpart + (int64_t)s * std::max<int64_t>(g.max_lchunk, 1) * 8 * D,
+        g.lcnt + (int64_t)s * std::max<int64_t>(g.max_long, 1), (const int32_t*)g.lmap,
+        c->g_rows + (int64_t)c->rank * xcap, c->g_vals + (int64_t)c->rank * xcap * D, c->d_err,
+        (unsigned long long*)nullptr);
+    FAE_LAUNCHED(c);
+    return FAE_OK;
+}
+
+template <int LPB, int NV>
+static fae_status xmerge_one(Ctx* c, cudaStream_t st, int s, int last, float* W, int64_t H, int D, float lr,
+                             int64_t xcap, const int32_t* per_step, bool table) {
+    Group& g = c->grp;
+    const int world = c->world;
+    const int64_t gpb = 256 / LPB;
+    const int64_t n = xcap * world;
+    if (table) {
+        const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), (int64_t)sm_count(c) * 8));
+        k_xscatter<<<(unsigned)blocks, 256, 0, st>>>(c->g_rows, per_step, g.cursor, s, world, xcap, H, g.ptab);
+        FAE_LAUNCHED(c);
+    }
+    const int64_t mb = std::max<int64_t>(1, std::min<int64_t>(cdiv(n, gpb), (int64_t)sm_count(c) * 16));
+    if (table)
+        k_xmerge<LPB, NV, true><<<(unsigned)mb, 256, 0, st>>>(c->g_rows, c->g_vals, per_step, g.cursor, s, last,
+                                                              g.done_ctr, world, xcap, D, W, lr, g.ptab, H, c->d_err,
+                                                              (unsigned long long*)nullptr);
+    else
+        k_xmerge<LPB, NV, false><<<(unsigned)mb, 256, 0, st>>>(c->g_rows, c->g_vals, per_step, g.cursor, s, last,
+                                                               g.done_ctr, world, xcap, D, W, lr, nullptr, H, c->d_err,
+                                                               (unsigned long long*)nullptr);
+    FAE_LAUNCHED(c);
+    return FAE_OK;
+}
+
+fae_status launch_grp_fwd_x(Ctx* c, cudaStream_t st, int s, float* W, int64_t H, int D, float* Y) {
+    FAE_DISPATCH_D(D, return fwd_x_one, c, st, s, W, H, D, Y);
+    return FAE_OK;
+}
+fae_status launch_xreduce_plain(Ctx* c, cudaStream_t st, int s, int D, const float* dY, int64_t xcap) {
+    FAE_DISPATCH_D(D, return xreduce_one, c, st, s, D, dY, xcap);
+    return FAE_OK;
+}
+fae_status launch_xmerge_any(Ctx* c, cudaStream_t st, int s, int last, float* W, int64_t H, int D, float lr,
+                             int64_t xcap, const int32_t* per_step, bool table) {
+    FAE_DISPATCH_D(D, return xmerge_one, c, st, s, last, W, H, D, lr, xcap, per_step, table);
+    return FAE_OK;
+}
+}  // namespace fae
+
 // Exchange-loop stamps of one call (n steps): per step, the forward from the
 // previous merge's end, the reduce-emit from the forward's end, the exchange
 // from the reduce's end (this rank's; its own last step: the previous merge)
@@ -1551,49 +1701,12 @@ extern "C" fae_status fae_train_hot_batches(fae_ctx* h, float* W_hot, int64_t H,
         // host loop of the same kernels (loopback test transport).
         if (!has_comm(c)) return set_err(c, FAE_ERR_NOT_INIT, "fae_train_hot_batches: world > 1 without a communicator");
         const int world = c->world;
-        const int64_t n_loc = std::max<int64_t>(0, std::min<int64_t>(n, g.n_batches - first));
-        k_set_run<<<1, 32, 0, c->stream>>>(g.cursor, first, n_loc, n);
-        FAE_LAUNCHED(c);
-        if (g.cap_xcnt < 2 * n * world) {
-            cudaFree(g.xcnt);
-            g.xcnt = nullptr;
-            g.cap_xcnt = 2 * n * world + 1024;
-            FAE_CUDA(c, cudaMalloc(&g.xcnt, sizeof(int32_t) * g.cap_xcnt));
-        }
-        std::vector<int32_t> mine(n, 0);
-        for (int64_t i = 0; i < n_loc; i++) mine[i] = (int32_t)(g.hdesc[first + i].sb1 - g.hdesc[first + i].sb0);
-        int32_t* all = g.xcnt;                 // [world][n]
-        int32_t* per_step = g.xcnt + n * world;  // [n][world]
-        FAE_CUDA(c, cudaMemcpyAsync(all + (int64_t)c->rank * n, mine.data(), sizeof(int32_t) * n,
-                                    cudaMemcpyHostToDevice, c->stream));
-        fae_status cs = coll_allgather(c, all + (int64_t)c->rank * n, all, n, CollT::I32,
-                                       "fae_train_hot_batches: allgather counts");
-        if (cs != FAE_OK) return cs;
-        std::vector<int32_t> hall((size_t)n * world), ht((size_t)n * world);
-        FAE_CUDA(c, cudaMemcpyAsync(hall.data(), all, sizeof(int32_t) * n * world, cudaMemcpyDeviceToHost, c->stream));
-        FAE_CUDA(c, cudaStreamSynchronize(c->stream));
-        int64_t xcap = 1;
-        for (int64_t i = 0; i < n; i++)
-            for (int rk = 0; rk < world; rk++) {
-                const int32_t v = hall[(size_t)rk * n + i];
-                ht[(size_t)i * world + rk] = v;
-                xcap = std::max<int64_t>(xcap, v);
-            }
-        // every rank saw the same counts, so every rank takes the same exit
-        if (xcap > c->g_cap) return set_err(c, FAE_ERR_CAPACITY, "fae_train_hot_batches: a rank's U exceeds capacity");
-        FAE_CUDA(c, cudaMemcpyAsync(per_step, ht.data(), sizeof(int32_t) * n * world, cudaMemcpyHostToDevice,
-                                    c->stream));
-        FAE_CUDA(c, cudaStreamSynchronize(c->stream));   // ht is pageable and goes out of scope
-        g.xcap_last = xcap;
-        const bool table = c->merge_table >= 0 ? c->merge_table == 1 : world > 2;
-        if (table && g.cap_ptab < (int64_t)world * H) {
-            cudaFree(g.ptab);
-            g.ptab = nullptr;
-            g.cap_ptab = 0;
-            FAE_CUDA(c, cudaMalloc(&g.ptab, sizeof(int32_t) * world * std::max<int64_t>(H, 1)));
-            FAE_CUDA(c, cudaMemsetAsync(g.ptab, 0xff, sizeof(int32_t) * world * std::max<int64_t>(H, 1), c->stream));
-            g.cap_ptab = (int64_t)world * H;
-        }
+        XPrep xp;
+        fae_status xs = x_prepare(c, first, n, H, nullptr, &xp);
+        if (xs != FAE_OK) return xs;
+        const int64_t xcap = xp.xcap;
+        int32_t* per_step = xp.per_step;
+        const bool table = xp.table;
         unsigned long long* xst = nullptr;
         if (c->timing == 1) {
             fae_status sst = stamps_init(n);

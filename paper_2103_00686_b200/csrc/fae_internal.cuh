@@ -314,6 +314,17 @@ fae_status step_ws_alloc(Ctx* c);
 fae_status launch_train_persist(Ctx* c, float* W, int D, const float* dY, int64_t n_dy, float* Y, float lr,
                                 int64_t first, int64_t n, cudaEvent_t* ev);
 void group_free(Ctx* c);
+// exchange runs (epoch.cu): setup and the pieces the DLRM exchange step reuses
+struct XPrep {
+    int64_t xcap = 0;
+    int32_t* per_step = nullptr;   // device [n][world] segment counts
+    bool table = false;
+};
+fae_status x_prepare(Ctx* c, int64_t first, int64_t n, int64_t H, int32_t** rec_total, XPrep* out);
+fae_status launch_grp_fwd_x(Ctx* c, cudaStream_t st, int s, float* W, int64_t H, int D, float* Y);
+fae_status launch_xreduce_plain(Ctx* c, cudaStream_t st, int s, int D, const float* dY, int64_t xcap);
+fae_status launch_xmerge_any(Ctx* c, cudaStream_t st, int s, int last, float* W, int64_t H, int D, float lr,
+                             int64_t xcap, const int32_t* per_step, bool table);
 fae_status validate_schema(Ctx* c, const fae_tables* t, const char* who);
 void step_ws_free(Ctx* c);
 

@@ -87,19 +87,25 @@ def test_dlrm_bad_config(dev):
         m.Dlrm(ctx, 5, [16, 8], [8, 2], 1, 8, 16)          # top output != 1
 
 
-@pytest.mark.parametrize("cfgname,R,t,small", [("tiny", 10_000, 1e-2, 0)])
-def test_train_dlrm_batches_equals_oracle(dev, cfgname, R, t, small):
+@pytest.mark.parametrize("cfgname,R,t,small,exchange", [("tiny", 10_000, 1e-2, 0, False),
+                                                       ("tiny", 10_000, 1e-2, 0, True)])
+def test_train_dlrm_batches_equals_oracle(dev, cfgname, R, t, small, exchange, monkeypatch):
     """The full hot step over grouped hot batches (a8 of the grouped loop ->
     DLRM forward/backward/SGD -> a9 + a10, one captured graph) == the oracle
     sequence: emb_fwd, the fp64 DLRM, emb_bwd_sgd with its dY, batch after
-    batch (pedantic fp32 GEMMs)."""
+    batch (pedantic fp32 GEMMs).  exchange: the data-parallel path (MLP
+    gradient all-reduce fused with the hot-gradient all-gathers, captured
+    with NCCL) on a 1-rank communicator."""
     m = fae()
     from paper_2103_00686_b200.pipeline import FaePipeline
+    monkeypatch.setenv("FAE_FORCE_MERGE", "1" if exchange else "0")   # read at fae_create
     c = gen.CONFIGS[cfgname]
     ds = gen.make_dataset(c, n_records=R, seed=5)
     dd = ds.to(dev)
     Tn, D, B = c.n_tables, c.dim, c.batch
     pipe = FaePipeline(ds.rows, D, B, c.pool)
+    if exchange:
+        m.fae_comm_init(pipe.ctx, m.fae_get_nccl_id(), 0, 1)
     prep = pipe.preprocess(dd.idx, dd.off, R, x_pct=5.0, seed=3, t=t, small_table_bytes=small)
     W = gen.make_weights(sum(ds.rows), D)
     W_hot = pipe.extract(W.to(dev), prep).clone()

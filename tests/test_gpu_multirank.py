@@ -321,3 +321,73 @@ def test_train_world_equals_oracle_global_batches(world, cfgname, R, t, small, s
         assert st == 0
     ok, worst = close(res[0][0], Wr)
     assert ok, worst
+
+
+# ----------------------------------------------------------------------------
+# NEXT-2 at G > 1: the DLRM hot step with the MLP gradient all-reduce fused
+# with the hot-gradient exchange
+# ----------------------------------------------------------------------------
+@pytest.mark.parametrize("world,R", [(2, 12_000), (3, 12_000)])
+def test_train_dlrm_world_equals_oracle_global_batches(world, R):
+    """fae_train_dlrm_batches over `world` virtual ranks == the oracle's DLRM
+    trained on the GLOBAL batches (global batch i = the concatenation, in
+    rank order, of each rank's hot batch i; loss = mean over the global
+    batch), hot rows and MLP parameters identical on every rank (pedantic
+    fp32 GEMMs)."""
+    from oracle import dlrm as odlrm
+    m = fae()
+    cfg = gen.CONFIGS["tiny"]
+    x, seed, t, small = 5.0, 3, 1e-2, 0
+    Tn, D, B = cfg.n_tables, cfg.dim, cfg.batch
+    full = gen.make_dataset(cfg, n_records=R, seed=23)
+    rm, base, H = _oracle_prep(cfg, full, R, x, seed, t, small)
+    W0 = gen.make_weights(sum(cfg.rows), D)
+    per = R // world
+    n_dense, bottom, top = 4, [12, D], [20, 1]
+    dims = gen.dlrm_dims(n_dense, bottom, top, Tn, D)
+    p0 = gen.make_dlrm_params(dims, seed=41)
+    dense_all = gen.make_dense(R, n_dense)
+    label_all = gen.make_labels(R, n_dense)
+    packs = []
+    for r in range(world):
+        sl = gen.make_dataset(cfg, n_records=per, seed=23, record_base=r * per)
+        flag = oracle.classify(sl.rows, sl.idx, sl.off, sl.fixed_pool, per, rm)
+        packs.append(oracle.pack(sl.rows, sl.idx, sl.off, sl.fixed_pool, per, rm, flag))
+    nb = min(4, max(-(-p["n_hot"] // B) for p in packs))
+    assert nb >= 2
+    lr_mlp, lr_emb = 0.05, 0.01
+    dev = torch.device("cuda", 0)
+
+    def body(rank, s, key):
+        ds = gen.make_dataset(cfg, n_records=per, seed=23, device=dev, record_base=rank * per)
+        pipe = _pipe(cfg, world, rank, s, key)
+        prep = pipe.preprocess(ds.idx, ds.off, per, x_pct=x, seed=seed, t=t, small_table_bytes=small,
+                               record_base=rank * per, n_records_global=world * per)
+        W_hot = pipe.extract(W0.to(dev), prep).clone()
+        pipe.group(prep)
+        model = m.Dlrm(pipe.ctx, n_dense, bottom, top, Tn, D, B, tf32=False)
+        params = p0.to(dev).clone()
+        model.train_batches(params, W_hot, 0, nb, prep.hot_ids, dense_all[rank * per:(rank + 1) * per].to(dev),
+                            label_all[rank * per:(rank + 1) * per].to(dev), lr_mlp, lr_emb)
+        pipe.ctx.check()
+        return W_hot.cpu().numpy(), params.cpu().numpy()
+
+    res = run_ranks(world, body)
+    for r in range(1, world):
+        assert np.array_equal(res[r][0], res[0][0]), f"rank {r} hot table differs"
+        assert np.array_equal(res[r][1], res[0][1]), f"rank {r} MLP parameters differ"
+    Wr = oracle.extract(W0, rm, H)
+    p = p0.double().numpy()
+    dn, lb = dense_all.double().numpy(), label_all.double().numpy()
+    for i, (idx, off, P, nbags, segs) in enumerate(_global_batches(cfg, packs, nb)):
+        recs = np.concatenate([packs[r]["hot_ids"][i * B: i * B + n_b // Tn] + r * per for r, _, n_b in segs])
+        Yb, st = oracle.emb_fwd(Wr, idx, off, P, nbags)
+        assert st == 0
+        L, cache = odlrm.forward(p, dims, len(bottom), dn[recs], Yb.reshape(-1, Tn, D).astype(np.float64), lb[recs])
+        p, dYb, _ = odlrm.backward_sgd(p, dims, len(bottom), cache, lr_mlp)
+        Wr, st = oracle.emb_bwd_sgd(Wr, idx, off, P, nbags, dYb.reshape(nbags, D).astype(np.float32), lr_emb)
+        assert st == 0
+    got_p = res[0][1].astype(np.float64)
+    assert np.all(np.abs(got_p - p) <= 1e-6 + 1e-5 * np.abs(p)), np.abs(got_p - p).max()
+    ok, worst = close(res[0][0], Wr)
+    assert ok, worst
