@@ -902,7 +902,7 @@ def run_train(args):
     torch.cuda.synchronize()
     prep_ms = (time.perf_counter() - t0) * 1e3
     dims = gen.dlrm_dims(n_dense, bottom, top, Tn, D)
-    params = gen.make_dlrm_params(dims, device=dev)
+    params = gen.dlrm_pad(gen.make_dlrm_params(dims, device=dev), dims)
     dense = gen.make_dense(R, n_dense, device=dev)
     label = gen.make_labels(R, n_dense, device=dev)
     n_test = args.test_records

@@ -351,3 +351,31 @@ def make_dlrm_params(dims, seed: int = BASE_SEED + 5000, device="cpu") -> torch.
         parts.append((-a + 2 * a * uniform01(seed, ctr)).float())
         o += k
     return torch.cat(parts)
+
+
+def dlrm_pad(flat: torch.Tensor, dims) -> torch.Tensor:
+    """Canonical flat parameters (per layer W [out][in], b [out]) -> the
+    library's layout (W rows padded to ld = in rounded up to 4 floats, pad
+    entries 0; include/fae.h fae_dlrm)."""
+    parts, o = [], 0
+    for i, n in dims:
+        ld = (i + 3) // 4 * 4
+        W = flat[o:o + n * i].view(n, i)
+        o += n * i
+        Wp = torch.zeros(n, ld, dtype=flat.dtype, device=flat.device)
+        Wp[:, :i] = W
+        parts += [Wp.reshape(-1), flat[o:o + n]]
+        o += n
+    return torch.cat(parts)
+
+
+def dlrm_unpad(flat: torch.Tensor, dims) -> torch.Tensor:
+    """The library's padded layout -> canonical flat parameters."""
+    parts, o = [], 0
+    for i, n in dims:
+        ld = (i + 3) // 4 * 4
+        parts.append(flat[o:o + n * ld].view(n, ld)[:, :i].reshape(-1))
+        o += n * ld
+        parts.append(flat[o:o + n])
+        o += n
+    return torch.cat(parts)

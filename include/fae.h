@@ -548,7 +548,10 @@ fae_status fae_sched_new_epoch(fae_sched* s);
  * [bottom output, <T_i, T_j> for i > j in row-major (i, j) order]; loss =
  * mean over the batch of the log loss; plain SGD of every weight and bias.
  * Parameters: ONE caller-owned device fp32 buffer, per layer (bottom
- * first, then top) W [out][in] row-major followed by b [out].
+ * first, then top) W [out][ld] row-major (ld = in rounded up to a multiple
+ * of 4 floats, so every GEMM operand is 16-byte aligned; the pad entries
+ * are never read or written) followed by b [out]; fae_dlrm_param_count
+ * gives the length.
  * GEMMs through cuBLAS (tf32 = 1: TF32 on the tensor cores; 0: pedantic
  * fp32); everything else hand-written kernels; no allocation after create.
  * ========================================================================== */

@@ -35,6 +35,8 @@ struct Dlrm {
     cublasHandle_t blas = nullptr;
     int n_layers = 0;                     // bottom then top
     int in_[2 * kDlrmMaxLayers], out_[2 * kDlrmMaxLayers];
+    int ld_[2 * kDlrmMaxLayers];          // row stride of W_l and of the layer's input: in rounded up to 4
+    int ld_dense = 0, ld_top = 0;         // strides of the dense input and of the interaction output
     int64_t woff[2 * kDlrmMaxLayers], boff[2 * kDlrmMaxLayers];
     int F = 0, P = 0, top_in = 0;
     int64_t n_params = 0;
@@ -85,13 +87,12 @@ __global__ void k_relu_mask(float* __restrict__ dX, const float* __restrict__ X,
 // Y_{Tn-1}] in shared memory; out[b] = [x, <T_i, T_j> for (i, j) in pairs].
 __global__ void k_interact_fwd(const float* __restrict__ xbot, const float* __restrict__ Y, int B, int Tn, int D,
                                const int16_t* __restrict__ pairs, int P, const int32_t* __restrict__ nb,
-                               float* __restrict__ out) {
+                               float* __restrict__ out, int ld) {
     extern __shared__ float s_T[];   // [warps][F][D]
     const int F = Tn + 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int b = blockIdx.x * (blockDim.x >> 5) + warp;
     if (b >= B) return;
-    const int ld = D + P;
     float* T = s_T + (int64_t)warp * F * D;
     const bool valid = b < *nb;
     for (int e = lane; e < F * D; e += 32) {
@@ -118,13 +119,12 @@ __global__ void k_interact_fwd(const float* __restrict__ xbot, const float* __re
 //   dxbot = dx + dT_0 (then the bottom ReLU mask), dY_z = dT_{z+1}.
 __global__ void k_interact_bwd(const float* __restrict__ xbot, const float* __restrict__ Y, int B, int Tn, int D,
                                const int32_t* __restrict__ pidx, int P, const int32_t* __restrict__ nb,
-                               const float* __restrict__ din, float* __restrict__ dxbot, float* __restrict__ dY) {
+                               const float* __restrict__ din, float* __restrict__ dxbot, float* __restrict__ dY, int ld) {
     extern __shared__ float s_T[];   // [warps][F][D]
     const int F = Tn + 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int b = blockIdx.x * (blockDim.x >> 5) + warp;
     if (b >= B) return;
-    const int ld = D + P;
     float* T = s_T + (int64_t)warp * F * D;
     const bool valid = b < *nb;
     for (int e = lane; e < F * D; e += 32) {
@@ -163,7 +163,7 @@ __global__ void k_interact_bwd(const float* __restrict__ xbot, const float* __re
 template <int D>
 __global__ void __launch_bounds__(128) k_interact_fwd_reg(const float* __restrict__ xbot, const float* __restrict__ Y,
                                                           int B, int Tn, int P, const int32_t* __restrict__ nb,
-                                                          float* __restrict__ out) {
+                                                          float* __restrict__ out, int ld) {
     extern __shared__ float s_z[];   // [warps][P]
     const int F = Tn + 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(128) k_interact_fwd_reg(const float* __restric
         if (lane > j && lane < F) z[kb + j] = s;
     }
     __syncwarp();
-    float* o = out + (int64_t)b * (D + P);
+    float* o = out + (int64_t)b * ld;
     if (lane == 0) {
 #pragma unroll
         for (int d = 0; d < D; d++) o[d] = t[d];
@@ -202,7 +202,7 @@ template <int D>
 __global__ void __launch_bounds__(128) k_interact_bwd_reg(const float* __restrict__ xbot, const float* __restrict__ Y,
                                                           int B, int Tn, int P, const int32_t* __restrict__ nb,
                                                           const float* __restrict__ din, float* __restrict__ dxbot,
-                                                          float* __restrict__ dY) {
+                                                          float* __restrict__ dY, int ld) {
     extern __shared__ float s_z[];   // [warps][P]
     const int F = Tn + 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(128) k_interact_bwd_reg(const float* __restric
         t[4 * q + 3] = v.w;
         a[4 * q] = a[4 * q + 1] = a[4 * q + 2] = a[4 * q + 3] = 0.f;
     }
-    const float* g = din + (int64_t)b * (D + P);
+    const float* g = din + (int64_t)b * ld;
     float* z = s_z + (int64_t)warp * P;
     for (int k = lane; k < P; k += 32) z[k] = valid ? g[D + k] : 0.f;
     __syncwarp();
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(1024) k_loss(float* __restrict__ z, const floa
 __global__ void k_dlrm_stage(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ run,
                              const int64_t* __restrict__ base, int s, int Tn, const int64_t* __restrict__ hot_ids,
                              const float* __restrict__ dense, const float* __restrict__ label, int n_dense,
-                             int max_batch, float* __restrict__ sdense, float* __restrict__ slabel,
+                             int ld_dense, int max_batch, float* __restrict__ sdense, float* __restrict__ slabel,
                              int32_t* __restrict__ nb, const int32_t* __restrict__ rec_total) {
     const int64_t rel = *base + s;
     int n = 0;
@@ -299,7 +299,7 @@ __global__ void k_dlrm_stage(const BatchDesc* __restrict__ desc, const int64_t* 
          e += (int64_t)gridDim.x * blockDim.x) {
         const int b = (int)(e / (n_dense + 1)), k = (int)(e - (int64_t)b * (n_dense + 1));
         const int64_t rec = b < n ? hot_ids[r0 + b] : 0;
-        if (k < n_dense) sdense[(int64_t)b * n_dense + k] = b < n ? dense[rec * n_dense + k] : 0.f;
+        if (k < n_dense) sdense[(int64_t)b * ld_dense + k] = b < n ? dense[rec * n_dense + k] : 0.f;
         else slabel[b] = b < n ? label[rec] : 0.f;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -348,8 +348,8 @@ static fae_status dlrm_run(Dlrm* m, float* params, float lr, bool train, cudaStr
         const float* X = (l == nbot) ? m->act[nbot + 1] /* interaction output */ : m->act[l < nbot ? l : l + 1];
         float* C = m->act[l < nbot ? l + 1 : l + 2];
         const float* W = params + m->woff[l];
-        FAE_BLAS(c, cublasSgemm(m->blas, CUBLAS_OP_T, CUBLAS_OP_N, m->out_[l], B, m->in_[l], &one, W, m->in_[l], X,
-                                m->in_[l], &zero, C, m->out_[l]));
+        FAE_BLAS(c, cublasSgemm(m->blas, CUBLAS_OP_T, CUBLAS_OP_N, m->out_[l], B, m->in_[l], &one, W, m->ld_[l], X,
+                                m->ld_[l], &zero, C, m->out_[l]));
         if (l == L - 1) break;   // the logit: bias inside the loss kernel
         k_bias_act<<<grid_for((int64_t)B * m->out_[l], c), 256, 0, st>>>(C, params + m->boff[l], B, m->out_[l],
                                                                         m->nb, 1);
@@ -362,11 +362,11 @@ static fae_status dlrm_run(Dlrm* m, float* params, float lr, bool train, cudaStr
                 auto kf = D == 8 ? k_interact_fwd_reg<8> : D == 16 ? k_interact_fwd_reg<16>
                         : D == 32 ? k_interact_fwd_reg<32> : k_interact_fwd_reg<64>;
                 kf<<<(unsigned)cdiv(B, wpb), 32 * wpb, sm, st>>>(m->act[nbot], m->Y, B, Tn, m->P, m->nb,
-                                                                 m->act[nbot + 1]);
+                                                                 m->act[nbot + 1], m->ld_top);
             } else {
                 const size_t sm = sizeof(float) * wpb * (Tn + 1) * D;
                 k_interact_fwd<<<(unsigned)cdiv(B, wpb), 32 * wpb, sm, st>>>(m->act[nbot], m->Y, B, Tn, D, m->pairs,
-                                                                             m->P, m->nb, m->act[nbot + 1]);
+                                                                             m->P, m->nb, m->act[nbot + 1], m->ld_top);
             }
             FAE_LAUNCHED(c);
         }
@@ -383,19 +383,19 @@ static fae_status dlrm_run(Dlrm* m, float* params, float lr, bool train, cudaStr
         const float* X = top ? (l == nbot ? m->act[nbot + 1] : m->act[l + 1]) : m->act[l];
         float* W = params + m->woff[l];
         float* bvec = params + m->boff[l];
-        const int in = m->in_[l], out = m->out_[l];
+        const int in = m->in_[l], out = m->out_[l], ld = m->ld_[l];
         // dX = dC W  (old W), for every layer but the first bottom one
         if (l > 0)
-            FAE_BLAS(c, cublasSgemm(m->blas, CUBLAS_OP_N, CUBLAS_OP_N, in, B, out, &one, W, in, dC, out, &zero, dX,
-                                    in));
+            FAE_BLAS(c, cublasSgemm(m->blas, CUBLAS_OP_N, CUBLAS_OP_N, in, B, out, &one, W, ld, dC, out, &zero, dX,
+                                    ld));
         if (grad_only) {   // world > 1: the gradient, all-reduced before the update
-            FAE_BLAS(c, cublasSgemm(m->blas, CUBLAS_OP_N, CUBLAS_OP_T, in, out, B, &one, X, in, dC, out, &zero,
-                                    m->gbuf + m->woff[l], in));
+            FAE_BLAS(c, cublasSgemm(m->blas, CUBLAS_OP_N, CUBLAS_OP_T, in, out, B, &one, X, ld, dC, out, &zero,
+                                    m->gbuf + m->woff[l], ld));
             FAE_BLAS(c, cublasSgemv(m->blas, CUBLAS_OP_N, out, B, &one, dC, out, m->ones, 1, &zero,
                                     m->gbuf + m->boff[l], 1));
         } else {
             // W += -lr * X^T dC ; b += -lr * dC^T 1
-            FAE_BLAS(c, cublasSgemm(m->blas, CUBLAS_OP_N, CUBLAS_OP_T, in, out, B, &mlr, X, in, dC, out, &one, W, in));
+            FAE_BLAS(c, cublasSgemm(m->blas, CUBLAS_OP_N, CUBLAS_OP_T, in, out, B, &mlr, X, ld, dC, out, &one, W, ld));
             FAE_BLAS(c, cublasSgemv(m->blas, CUBLAS_OP_N, out, B, &mlr, dC, out, m->ones, 1, &one, bvec, 1));
         }
         if (l == 0) break;
@@ -408,17 +408,17 @@ static fae_status dlrm_run(Dlrm* m, float* params, float lr, bool train, cudaStr
                 auto kb = D == 8 ? k_interact_bwd_reg<8> : D == 16 ? k_interact_bwd_reg<16>
                         : D == 32 ? k_interact_bwd_reg<32> : k_interact_bwd_reg<64>;
                 kb<<<(unsigned)cdiv(B, wpb), 32 * wpb, sm, st>>>(m->act[nbot], m->Y, B, Tn, m->P, m->nb, dX, dC,
-                                                                 m->dY);
+                                                                 m->dY, m->ld_top);
             } else {
                 const size_t sm = sizeof(float) * wpb * (Tn + 1) * D;
                 k_interact_bwd<<<(unsigned)cdiv(B, wpb), 32 * wpb, sm, st>>>(m->act[nbot], m->Y, B, Tn, D, m->pidx,
-                                                                             m->P, m->nb, dX, dC, m->dY);
+                                                                             m->P, m->nb, dX, dC, m->dY, m->ld_top);
             }
             FAE_LAUNCHED(c);
             continue;            // dC now holds the bottom output's gradient
         }
         // ReLU of the layer below (its output is X)
-        k_relu_mask<<<grid_for((int64_t)B * in, c), 256, 0, st>>>(dX, X, (int64_t)B * in);
+        k_relu_mask<<<grid_for((int64_t)B * ld, c), 256, 0, st>>>(dX, X, (int64_t)B * ld);
         FAE_LAUNCHED(c);
         std::swap(dC, dX);
     }
@@ -448,15 +448,16 @@ struct fae_dlrm {
 
 extern "C" int64_t fae_dlrm_param_count(const fae_dlrm_cfg* g) {
     if (!cfg_ok(g)) return -1;
+    auto ld4 = [](int64_t v) { return (v + 3) / 4 * 4; };
     int64_t n = 0, prev = g->n_dense;
     for (int i = 0; i < g->n_bottom; i++) {
-        n += prev * g->bottom[i] + g->bottom[i];
+        n += ld4(prev) * g->bottom[i] + g->bottom[i];
         prev = g->bottom[i];
     }
     const int64_t F = g->n_tables + 1;
     prev = g->dim + F * (F - 1) / 2;
     for (int i = 0; i < g->n_top; i++) {
-        n += prev * g->top[i] + g->top[i];
+        n += ld4(prev) * g->top[i] + g->top[i];
         prev = g->top[i];
     }
     return n;
@@ -507,8 +508,9 @@ extern "C" fae_status fae_dlrm_create(fae_ctx* ctx, const fae_dlrm_cfg* g, fae_d
         m.n_layers++;
     }
     for (int l = 0; l < m.n_layers; l++) {
+        m.ld_[l] = (m.in_[l] + 3) / 4 * 4;
         m.woff[l] = o;
-        o += (int64_t)m.in_[l] * m.out_[l];
+        o += (int64_t)m.ld_[l] * m.out_[l];
         m.boff[l] = o;
         o += m.out_[l];
         m.max_w = std::max(m.max_w, std::max(m.in_[l], m.out_[l]));
@@ -516,17 +518,20 @@ extern "C" fae_status fae_dlrm_create(fae_ctx* ctx, const fae_dlrm_cfg* g, fae_d
     m.n_params = o;
     // act[0] dense, act[1..nbot] bottom outputs, act[nbot+1] interaction,
     // act[nbot+2..] top outputs (last: the logit)
+    m.ld_dense = (g->n_dense + 3) / 4 * 4;
+    m.ld_top = (m.top_in + 3) / 4 * 4;
     std::vector<int> widths;
-    widths.push_back(g->n_dense);
+    widths.push_back(m.ld_dense);
     for (int i = 0; i < g->n_bottom; i++) widths.push_back(g->bottom[i]);
-    widths.push_back(m.top_in);
+    widths.push_back(m.ld_top);
     for (int i = 0; i < g->n_top; i++) widths.push_back(g->top[i]);
     for (int w : widths) {
         float* p = nullptr;
         if (cudaMalloc(&p, sizeof(float) * (size_t)B * w) != cudaSuccess) return fail(cuda_err(c, cudaGetLastError(), "fae_dlrm_create"));
         m.act.push_back(p);
     }
-    m.max_w = std::max(m.max_w, m.top_in);
+    m.max_w = std::max(m.max_w, m.ld_top);
+    for (int l = 0; l < m.n_layers; l++) m.max_w = std::max(m.max_w, m.ld_[l]);
     bool ok = cudaMalloc(&m.grad_a, sizeof(float) * (size_t)B * m.max_w) == cudaSuccess &&
               cudaMalloc(&m.grad_b, sizeof(float) * (size_t)B * m.max_w) == cudaSuccess &&
               cudaMalloc(&m.ones, sizeof(float) * B) == cudaSuccess &&
@@ -580,9 +585,10 @@ extern "C" fae_status fae_dlrm_step(fae_dlrm* h, float* params, int32_t B, const
         return set_err(c, FAE_ERR_INVALID_ARG, "fae_dlrm_step: bad arguments");
     const int Tn = m.cfg.n_tables, D = m.cfg.dim;
     cudaStream_t st = c->stream;
-    FAE_CUDA(c, cudaMemsetAsync(m.act[0], 0, sizeof(float) * (size_t)m.cfg.max_batch * m.cfg.n_dense, st));
+    FAE_CUDA(c, cudaMemsetAsync(m.act[0], 0, sizeof(float) * (size_t)m.cfg.max_batch * m.ld_dense, st));
     if (B > 0) {
-        FAE_CUDA(c, cudaMemcpyAsync(m.act[0], dense, sizeof(float) * (size_t)B * m.cfg.n_dense, cudaMemcpyDeviceToDevice, st));
+        FAE_CUDA(c, cudaMemcpy2DAsync(m.act[0], sizeof(float) * m.ld_dense, dense, sizeof(float) * m.cfg.n_dense,
+                                      sizeof(float) * m.cfg.n_dense, B, cudaMemcpyDeviceToDevice, st));
         FAE_CUDA(c, cudaMemcpyAsync(m.label, label, sizeof(float) * B, cudaMemcpyDeviceToDevice, st));
         FAE_CUDA(c, cudaMemcpyAsync(m.Y, Y, sizeof(float) * (size_t)B * Tn * D, cudaMemcpyDeviceToDevice, st));
     }
@@ -638,7 +644,7 @@ static fae_status train_dlrm_exchange(Ctx* c, Dlrm& m, float* params, float* W_h
         fae_status r = launch_grp_fwd_x(c, st, s, W_hot, H, D, m.Y);
         if (r != FAE_OK) return r;
         k_dlrm_stage<<<grid_for((int64_t)m.cfg.max_batch * (m.cfg.n_dense + 1), c), 256, 0, st>>>(
-            g.desc, g.run, g.cursor, s, g.Tn, hot_ids, dense, label, m.cfg.n_dense, m.cfg.max_batch, m.act[0],
+            g.desc, g.run, g.cursor, s, g.Tn, hot_ids, dense, label, m.cfg.n_dense, m.ld_dense, m.cfg.max_batch, m.act[0],
             m.label, m.nb, rtot);
         FAE_LAUNCHED(c);
         r = dlrm_run(&m, params, lr_mlp, true, st, true);
@@ -765,7 +771,7 @@ extern "C" fae_status fae_train_dlrm_batches(fae_ctx* ctx, fae_dlrm* h, float* p
             st = launch_grp_fwd_pdl_any(c, cs, s, W_hot, H, D, m.Y);
             if (st != FAE_OK) break;
             k_dlrm_stage<<<grid_for((int64_t)m.cfg.max_batch * (m.cfg.n_dense + 1), c), 256, 0, cs>>>(
-                g.desc, g.run, g.cursor, s, g.Tn, hot_ids, dense, label, m.cfg.n_dense, m.cfg.max_batch, m.act[0],
+                g.desc, g.run, g.cursor, s, g.Tn, hot_ids, dense, label, m.cfg.n_dense, m.ld_dense, m.cfg.max_batch, m.act[0],
                 m.label, m.nb, (const int32_t*)nullptr);
             if (cudaGetLastError() != cudaSuccess) {
                 st = set_err(c, FAE_ERR_CUDA, "fae_train_dlrm_batches: stage launch");

@@ -43,13 +43,13 @@ def test_dlrm_step_equals_oracle(dev, tf32, B, maxB):
     ctx = _ctx([100] * Tn, D, 1024, 1024)
     model = m.Dlrm(ctx, n_dense, bottom, top, Tn, D, maxB, tf32=tf32)
     dims = gen.dlrm_dims(n_dense, bottom, top, Tn, D)
-    assert model.n_params == sum(i * o + o for i, o in dims)
+    assert model.n_params == sum((i + 3) // 4 * 4 * o + o for i, o in dims)
     p0 = gen.make_dlrm_params(dims, seed=11)
     dense = gen.make_dense(B, n_dense, seed=12)
     label = gen.make_labels(B, n_dense, seed=13)
     Y = (0.5 * gen.make_dy(B * Tn, D, seed=14)).view(B, Tn, D)
     lr = 0.1
-    params = p0.to(dev).clone()
+    params = gen.dlrm_pad(p0, dims).to(dev)
     dY = torch.zeros(B, Tn, D, device=dev)
     model.step(params, B, dense.to(dev), label.to(dev), Y.to(dev), dY, lr, train=True)
     s, n = model.loss()
@@ -57,7 +57,7 @@ def test_dlrm_step_equals_oracle(dev, tf32, B, maxB):
                              Y.double().numpy(), label.double().numpy())
     newp, dYr, _ = odlrm.backward_sgd(p0.double().numpy(), dims, len(bottom), cache, lr)
     assert n == B
-    got_p, got_dy = params.cpu().double().numpy(), dY.cpu().double().numpy()
+    got_p, got_dy = gen.dlrm_unpad(params.cpu(), dims).double().numpy(), dY.cpu().double().numpy()
     if not tf32:
         assert abs(s / B - L) <= 1e-5 * abs(L)
         assert np.all(np.abs(got_p - newp) <= 1e-6 + 1e-5 * np.abs(newp))
@@ -114,7 +114,7 @@ def test_train_dlrm_batches_equals_oracle(dev, cfgname, R, t, small, exchange, m
     dims = gen.dlrm_dims(n_dense, bottom, top, Tn, D)
     model = m.Dlrm(pipe.ctx, n_dense, bottom, top, Tn, D, B, tf32=False)
     p0 = gen.make_dlrm_params(dims, seed=21)
-    params = p0.to(dev).clone()
+    params = gen.dlrm_pad(p0, dims).to(dev)
     dense = gen.make_dense(R, n_dense, seed=22)
     label = gen.make_labels(R, n_dense, seed=23)
     nb = min(prep.packed["n_hot_batches"], 5)
@@ -151,7 +151,7 @@ def test_train_dlrm_batches_equals_oracle(dev, cfgname, R, t, small, exchange, m
         assert st == 0
     assert n == ntot
     assert abs(s - Ltot) <= 1e-5 * abs(Ltot)
-    got_p = params.cpu().double().numpy()
+    got_p = gen.dlrm_unpad(params.cpu(), dims).double().numpy()
     assert np.all(np.abs(got_p - p) <= 1e-6 + 1e-5 * np.abs(p)), np.abs(got_p - p).max()
     got_w = W_hot.cpu().double().numpy()
     assert np.all(np.abs(got_w - Wr) <= 1e-6 + 1e-5 * np.abs(Wr)), np.abs(got_w - Wr).max()
@@ -171,7 +171,7 @@ def _trainer(dev, R, n_test, r_start, tf32=False):
     ep = MixedEpoch(pipe, prep, W, dd.idx, dd.off, R, W_hot)
     n_dense, bottom, top = 4, [12, D], [20, 1]
     dims = gen.dlrm_dims(n_dense, bottom, top, Tn, D)
-    params = gen.make_dlrm_params(dims, seed=31).to(dev)
+    params = gen.dlrm_pad(gen.make_dlrm_params(dims, seed=31), dims).to(dev)
     dense = gen.make_dense(R, n_dense).to(dev)
     label = gen.make_labels(R, n_dense).to(dev)
     # held-out records: the next n_test records of the stream, global row ids
@@ -241,7 +241,7 @@ def test_fae_trainer_epoch_equals_oracle(dev):
         r0, r1 = i * B, min((i + 1) * B, pk["n_hot"])
         Wh, p = step(Wh, pk["hot_idx"][r0 * Tn: r1 * Tn], pk["hot_ids"][r0:r1], p)
     Wf = oracle.scatter_hot(Wf, Wh, rm)
-    got_p = tr.params.cpu().double().numpy()
+    got_p = gen.dlrm_unpad(tr.params.cpu(), t["dims"]).double().numpy()
     assert np.all(np.abs(got_p - p) <= 1e-6 + 1e-5 * np.abs(p)), np.abs(got_p - p).max()
     got_w = ep.W.cpu().double().numpy()
     assert np.all(np.abs(got_w - Wf) <= 1e-6 + 1e-5 * np.abs(Wf)), np.abs(got_w - Wf).max()

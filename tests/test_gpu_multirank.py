@@ -366,11 +366,11 @@ def test_train_dlrm_world_equals_oracle_global_batches(world, R):
         W_hot = pipe.extract(W0.to(dev), prep).clone()
         pipe.group(prep)
         model = m.Dlrm(pipe.ctx, n_dense, bottom, top, Tn, D, B, tf32=False)
-        params = p0.to(dev).clone()
+        params = gen.dlrm_pad(p0, dims).to(dev)
         model.train_batches(params, W_hot, 0, nb, prep.hot_ids, dense_all[rank * per:(rank + 1) * per].to(dev),
                             label_all[rank * per:(rank + 1) * per].to(dev), lr_mlp, lr_emb)
         pipe.ctx.check()
-        return W_hot.cpu().numpy(), params.cpu().numpy()
+        return W_hot.cpu().numpy(), gen.dlrm_unpad(params.cpu(), dims).numpy()
 
     res = run_ranks(world, body)
     for r in range(1, world):

@@ -63,7 +63,7 @@ W_hot = pipe.extract(W, prep).clone()
 ep = MixedEpoch(pipe, prep, W, ds.idx, None, R, W_hot)
 Tn, D = cfg.n_tables, cfg.dim
 dims = gen.dlrm_dims(4, [12, D], [20, 1], Tn, D)
-params = gen.make_dlrm_params(dims, device=dev)
+params = gen.dlrm_pad(gen.make_dlrm_params(dims, device=dev), dims)
 tds = gen.make_dataset(cfg, n_records=256, seed=5, record_base=R)
 base = torch.tensor(np.concatenate([[0], np.cumsum(cfg.rows)])[:Tn], device=dev)
 tidx = (tds.idx.to(dev).view(256, Tn) + base).view(-1).to(torch.int32)
