@@ -317,13 +317,20 @@ k_gs_segments(const uint32_t* __restrict__ keys, const int64_t* __restrict__ til
 //      (= lk0 + z*n + i) / seg_row written; unit z = 0 sets desc[b].sb0.
 // Same outputs as the generic path (perm, seg_start, seg_row, sb0, totals).
 // ---------------------------------------------------------------------------
+// resident unit CTAs per SM (launch bounds; measured)
+#ifndef FAE_UNITS8_MB
+#define FAE_UNITS8_MB 5
+#endif
+#ifndef FAE_UNITS16_MB
+#define FAE_UNITS16_MB 4   // 4096-lookup units: 3.92 / 3.24 / 3.17 ms at 2 / 3 / 4 (Terabyte-shaped, 24M records)
+#endif
 constexpr int kUnitThreads = 256;
 constexpr int kUnitIPT = 16;
 constexpr int kUnitMax = kUnitThreads * kUnitIPT;   // 4096 lookups per unit
 constexpr int kMaxUnitTables = 1024;                 // unit path: tables per batch
 
 template <int IPT, bool kP1>
-__global__ void __launch_bounds__(kUnitThreads, IPT <= 8 ? 5 : 2)
+__global__ void __launch_bounds__(kUnitThreads, IPT <= 8 ? FAE_UNITS8_MB : FAE_UNITS16_MB)
 k_gs_units(const int32_t* __restrict__ hot_idx, int64_t H, int Tn, int P_, const BatchDesc* __restrict__ desc,
            int32_t* __restrict__ perm, int32_t* __restrict__ useg_pos, int32_t* __restrict__ useg_row,
            uint32_t* __restrict__ ucnt, uint32_t* err) {
