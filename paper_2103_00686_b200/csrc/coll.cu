@@ -159,6 +159,11 @@ static fae_status lb_collective(Ctx* c, const void* src, void* dst, size_t out_b
 }
 
 void coll_free(Ctx* c) {
+    cudaFree(c->g_rows2);
+    cudaFree(c->g_vals2);
+    c->g_rows2 = nullptr;
+    c->g_vals2 = nullptr;
+    c->g_cap2 = 0;
     if (c->comm) ncclCommDestroy(c->comm);
     c->comm = nullptr;
     if (c->lb) {

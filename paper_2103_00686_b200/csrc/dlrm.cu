@@ -657,10 +657,10 @@ static fae_status train_dlrm_exchange(Ctx* c, Dlrm& m, float* params, float* W_h
             coll_group_start(c);
             fae_status a = coll_allreduce_sum(c, m.gbuf, m.n_params, CollT::F32, "dlrm exchange: MLP gradients");
             if (a == FAE_OK)
-                a = coll_allgather(c, c->g_rows + (int64_t)c->rank * xcap, c->g_rows, xcap, CollT::I32,
+                a = coll_allgather(c, xrows_of(c, s) + (int64_t)c->rank * xcap, xrows_of(c, s), xcap, CollT::I32,
                                    "dlrm exchange: allgather rows");
             if (a == FAE_OK)
-                a = coll_allgather(c, c->g_vals + (int64_t)c->rank * xcap * D, c->g_vals, xcap * D, CollT::F32,
+                a = coll_allgather(c, xvals_of(c, s) + (int64_t)c->rank * xcap * D, xvals_of(c, s), xcap * D, CollT::F32,
                                    "dlrm exchange: allgather grads");
             fae_status b = coll_group_end(c, "dlrm exchange");
             c->stream = keep;

@@ -874,14 +874,18 @@ k_grp_xreduce(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ ru
     const BatchDesc d = desc[run[0] + rel];
     const int64_t U = d.sb1 - d.sb0;
     const int64_t n_long = U - d.n_short - d.n_med;
-    reduce_segments<LPB, NV, true>(rec + d.sb0, d.n_tiny, d.n_short, d.n_med, n_long, d.n_lchunk, perm + d.lk0,
-                                   dY + (rel % n_dy) * dy_stride, D, nullptr, 0.f, lpart, lcnt,
-                                   lmap + lmap_base(d, run[0] + rel), 1, xvals, err);
-    // the batch's rows (static, ascending) into the slot; the previous
-    // step's readers of the slot finished before this batch's forward began
-    pdl_wait();
+    // the slot of this step's parity was last read by the merge two steps
+    // back, which finished before the previous forward ended: the sums are
+    // emitted without waiting (they need dY and the grouping only, not W)
+    reduce_segments<LPB, NV, false>(rec + d.sb0, d.n_tiny, d.n_short, d.n_med, n_long, d.n_lchunk, perm + d.lk0,
+                                    dY + (rel % n_dy) * dy_stride, D, nullptr, 0.f, lpart, lcnt,
+                                    lmap + lmap_base(d, run[0] + rel), 1, xvals, err);
+    // the batch's rows (static, ascending) into the slot
     for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < U; j += (int64_t)gridDim.x * blockDim.x)
         xrows[j] = __ldg(seg_row + d.sb0 + j);
+    // completion implies the forward's (and so the previous merge's): the
+    // all-gather launched after this kernel never races a merge
+    pdl_wait();
     if (stamps) {
         __syncthreads();
         if (threadIdx.x == 0) atomicMax(&stamps[rel * kSt + 3], (unsigned long long)gtimer());
@@ -1134,8 +1138,8 @@ static fae_status launch_x_step(Ctx* c, cudaStream_t st, int s, int last, float*
     const int threads = 256;
     const int64_t gpb = threads / LPB;
     const int world = c->world;
-    int32_t* xrows = c->g_rows;
-    float* xvals = c->g_vals;
+    int32_t* xrows = xrows_of(c, s);
+    float* xvals = xvals_of(c, s);
     int32_t* my_rows = xrows + (int64_t)c->rank * xcap;
     float* my_vals = xvals + (int64_t)c->rank * xcap * D;
     cudaLaunchAttribute attr[1];
@@ -1408,6 +1412,18 @@ fae_status x_prepare(Ctx* c, int64_t first, int64_t n, int64_t H, int32_t** rec_
         FAE_CUDA(c, cudaMemsetAsync(g.ptab, 0xff, sizeof(int32_t) * world * std::max<int64_t>(H, 1), c->stream));
         g.cap_ptab = (int64_t)world * H;
     }
+    if (c->g_cap2 < (int64_t)world * xcap) {   // the odd steps' slot set
+        FAE_CUDA(c, cudaStreamSynchronize(c->stream));
+        cudaFree(c->g_rows2);
+        cudaFree(c->g_vals2);
+        c->g_rows2 = nullptr;
+        c->g_vals2 = nullptr;
+        c->g_cap2 = 0;
+        const int64_t cap2 = (int64_t)world * xcap + ((int64_t)world * xcap) / 4 + 256;
+        FAE_CUDA(c, cudaMalloc(&c->g_rows2, sizeof(int32_t) * cap2));
+        FAE_CUDA(c, cudaMalloc(&c->g_vals2, sizeof(float) * cap2 * c->cfg.max_dim));
+        c->g_cap2 = cap2;
+    }
     out->xcap = xcap;
     out->per_step = per_step;
     out->table = table;
@@ -1448,7 +1464,7 @@ static fae_status xreduce_one(Ctx* c, cudaStream_t st, int s, int D, const float
         (const int32_t*)g.perm, (const int32_t*)g.seg_row, dY, (int64_t)1, g.max_bags * (int64_t)D, D,
         g.lpart + (int64_t)s * std::max<int64_t>(g.max_lchunk, 1) * 8 * D,
         g.lcnt + (int64_t)s * std::max<int64_t>(g.max_long, 1), (const int32_t*)g.lmap,
-        c->g_rows + (int64_t)c->rank * xcap, c->g_vals + (int64_t)c->rank * xcap * D, c->d_err,
+        xrows_of(c, s) + (int64_t)c->rank * xcap, xvals_of(c, s) + (int64_t)c->rank * xcap * D, c->d_err,
         (unsigned long long*)nullptr);
     FAE_LAUNCHED(c);
     return FAE_OK;
@@ -1463,16 +1479,16 @@ static fae_status xmerge_one(Ctx* c, cudaStream_t st, int s, int last, float* W,
     const int64_t n = xcap * world;
     if (table) {
         const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), (int64_t)sm_count(c) * 8));
-        k_xscatter<<<(unsigned)blocks, 256, 0, st>>>(c->g_rows, per_step, g.cursor, s, world, xcap, H, g.ptab);
+        k_xscatter<<<(unsigned)blocks, 256, 0, st>>>(xrows_of(c, s), per_step, g.cursor, s, world, xcap, H, g.ptab);
         FAE_LAUNCHED(c);
     }
     const int64_t mb = std::max<int64_t>(1, std::min<int64_t>(cdiv(n, gpb), (int64_t)sm_count(c) * 16));
     if (table)
-        k_xmerge<LPB, NV, true><<<(unsigned)mb, 256, 0, st>>>(c->g_rows, c->g_vals, per_step, g.cursor, s, last,
+        k_xmerge<LPB, NV, true><<<(unsigned)mb, 256, 0, st>>>(xrows_of(c, s), xvals_of(c, s), per_step, g.cursor, s, last,
                                                               g.done_ctr, world, xcap, D, W, lr, g.ptab, H, c->d_err,
                                                               (unsigned long long*)nullptr);
     else
-        k_xmerge<LPB, NV, false><<<(unsigned)mb, 256, 0, st>>>(c->g_rows, c->g_vals, per_step, g.cursor, s, last,
+        k_xmerge<LPB, NV, false><<<(unsigned)mb, 256, 0, st>>>(xrows_of(c, s), xvals_of(c, s), per_step, g.cursor, s, last,
                                                                g.done_ctr, world, xcap, D, W, lr, nullptr, H, c->d_err,
                                                                (unsigned long long*)nullptr);
     FAE_LAUNCHED(c);

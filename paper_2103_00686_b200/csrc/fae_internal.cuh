@@ -233,6 +233,11 @@ struct Ctx {
     // sync scratch
     int32_t* g_rows = nullptr;                  // [max_world * cap_L]
     float* g_vals = nullptr;                    // [max_world * cap_L * max_dim]
+    // exchange loops: odd steps use a second slot set, so a step's reduce-emit
+    // never waits for the previous step's merge (grown on demand)
+    int32_t* g_rows2 = nullptr;
+    float* g_vals2 = nullptr;
+    int64_t g_cap2 = 0;                         // entries of g_rows2 (world * xcap)
     int32_t* g_counts = nullptr;                // [max_world]
     int64_t g_cap = 0;
     Group grp;
@@ -323,6 +328,9 @@ struct XPrep {
 fae_status x_prepare(Ctx* c, int64_t first, int64_t n, int64_t H, int32_t** rec_total, XPrep* out);
 fae_status launch_grp_fwd_x(Ctx* c, cudaStream_t st, int s, float* W, int64_t H, int D, float* Y);
 fae_status launch_xreduce_plain(Ctx* c, cudaStream_t st, int s, int D, const float* dY, int64_t xcap);
+// the exchange slot set of replay step s (even: g_rows / g_vals, odd: g_rows2 / g_vals2)
+inline int32_t* xrows_of(Ctx* c, int s) { return (s & 1) ? c->g_rows2 : c->g_rows; }
+inline float* xvals_of(Ctx* c, int s) { return (s & 1) ? c->g_vals2 : c->g_vals; }
 fae_status launch_xmerge_any(Ctx* c, cudaStream_t st, int s, int last, float* W, int64_t H, int D, float lr,
                              int64_t xcap, const int32_t* per_step, bool table);
 fae_status validate_schema(Ctx* c, const fae_tables* t, const char* who);
