@@ -34,6 +34,9 @@ constexpr int kSt = kStampSlots;
 #ifndef FAE_RED_ORDER
 #define FAE_RED_ORDER 0
 #endif
+#ifndef FAE_ROWS_INFLIGHT
+#define FAE_ROWS_INFLIGHT 0   // rows a lane group keeps in flight in a 16-lookup piece (0: 16 / NV)
+#endif
 constexpr int kFwdU = FAE_FWD_U;
 
 // finish a segment: emit G (a11 exchange) or W[row] -= lr * G (a10)
@@ -68,7 +71,7 @@ template <int LPB, int NV>
 __device__ __forceinline__ void sum_rows16(const int32_t* __restrict__ perm, int32_t pos, int32_t n,
                                            const float* __restrict__ src, int D, int lane,
                                            float4 (&g)[NV]) {
-    constexpr int CH = kPiece / NV > 4 ? kPiece / NV : 4;
+    constexpr int CH = FAE_ROWS_INFLIGHT > 0 ? FAE_ROWS_INFLIGHT : (kPiece / NV > 4 ? kPiece / NV : 4);   // rows in flight
     int32_t bag[kPiece];
 #pragma unroll
     for (int u = 0; u < kPiece; u++) bag[u] = u < n ? __ldg(perm + pos + u) : -1;

@@ -265,3 +265,49 @@ def test_fae_trainer_scheduler_invariants(dev):
         assert all(1.0 <= e["rate"] <= 100.0 and np.isfinite(e["test_loss"]) for e in log)
         outs.append((tr.params.cpu(), ep.W.cpu(), [e["test_loss"] for e in log]))
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1]) and outs[0][2] == outs[1][2]
+
+
+@pytest.mark.parametrize("model,tf32", [("rmc2", False), ("rmc2", True), ("rmc3", True)])
+def test_dlrm_step_paper_shapes(dev, model, tf32):
+    """One DLRM step at the paper's shapes (tab:benchmarks P:L516-526: RMC2
+    13-512-256-64-16 / 512-256-1, D 16, B 2048; RMC3 13-512-256-64 /
+    512-512-256-1, D 64, B 4096; 26 sparse features) against the fp64
+    oracle, with the tolerances of the module docstring."""
+    m = fae()
+    n_dense, bottom, top, D, B = ((13, [512, 256, 64, 16], [512, 256, 1], 16, 2048) if model == "rmc2" else
+                                  (13, [512, 256, 64], [512, 512, 256, 1], 64, 4096))
+    Tn = 26
+    ctx = _ctx([1000] * Tn, D, B * Tn, B * Tn)
+    mdl = m.Dlrm(ctx, n_dense, bottom, top, Tn, D, B, tf32=tf32)
+    dims = gen.dlrm_dims(n_dense, bottom, top, Tn, D)
+    p0 = gen.make_dlrm_params(dims, seed=51)
+    dense = gen.make_dense(B, n_dense, seed=52)
+    label = gen.make_labels(B, n_dense, seed=53)
+    Y = (0.05 * gen.make_dy(B * Tn, D, seed=54)).view(B, Tn, D)
+    lr = 0.05
+    params = gen.dlrm_pad(p0, dims).to(dev)
+    dY = torch.zeros(B, Tn, D, device=dev)
+    mdl.step(params, B, dense.to(dev), label.to(dev), Y.to(dev), dY, lr, train=True)
+    s, n = mdl.loss()
+    L, cache = odlrm.forward(p0.double().numpy(), dims, len(bottom), dense.double().numpy(), Y.double().numpy(),
+                             label.double().numpy())
+    newp, dYr, _ = odlrm.backward_sgd(p0.double().numpy(), dims, len(bottom), cache, lr)
+    got_p = gen.dlrm_unpad(params.cpu(), dims).double().numpy()
+    got_dy = dY.cpu().double().numpy()
+    assert n == B
+    if not tf32:
+        assert abs(s / B - L) <= 1e-5 * abs(L)
+        assert np.all(np.abs(got_p - newp) <= 1e-6 + 1e-5 * np.abs(newp)), np.abs(got_p - newp).max()
+        sc = np.abs(dYr).max()
+        assert np.all(np.abs(got_dy - dYr) <= 1e-5 * sc + 1e-4 * np.abs(dYr))
+    else:
+        # TF32 (R34): inputs rounded to a 10-bit mantissa, u = 2^-11; a K-term
+        # dot product of random-sign terms errs by ~2u*sqrt(K) relative, and
+        # dY is len(top) chained GEMMs deep in the backward (K <= 512 here):
+        # len(top) * 2u * sqrt(K) of max|dY|, doubled as the bound
+        kmax = max(i for i, _ in dims)
+        tol = 4 * len(top) * 2.0 ** -11 * kmax ** 0.5
+        assert abs(s / B - L) <= 1e-3 * abs(L)
+        upd = np.abs(newp - p0.double().numpy()).max()
+        assert np.abs(got_p - newp).max() <= tol * upd + 1e-7
+        assert np.abs(got_dy - dYr).max() <= tol * np.abs(dYr).max()
