@@ -37,6 +37,9 @@ constexpr int kSt = kStampSlots;
 #ifndef FAE_ROWS_INFLIGHT
 #define FAE_ROWS_INFLIGHT 0   // rows a lane group keeps in flight in a 16-lookup piece (0: 16 / NV)
 #endif
+#ifndef FAE_LPART_SERIAL
+#define FAE_LPART_SERIAL 0    // 1: the long segment's finisher reads the chunk block sums one by one (A/B)
+#endif
 constexpr int kFwdU = FAE_FWD_U;
 
 // finish a segment: emit G (a11 exchange) or W[row] -= lr * G (a10)
@@ -257,6 +260,7 @@ __device__ __forceinline__ void long_chunk(const SegRec* __restrict__ lrec, int6
         }
         __syncthreads();
         if (!s_last) return;
+#if FAE_LPART_SERIAL
         if (grp == 0) {
             for (int32_t cc = 0; cc < r2.w; cc++) {
                 const int32_t len_c = min(CHUNK, r.y - cc * CHUNK);
@@ -268,8 +272,36 @@ __device__ __forceinline__ void long_chunk(const SegRec* __restrict__ lrec, int6
                     for (int kk = 0; kk < NV; kk++) add4(tot[kk], __ldcg(rp + kk * LPB));
                 }
             }
-            if (threadIdx.x == 0) lcnt[k] = 0u;
         }
+#else
+        // every block sum of the segment, entry e = (chunk e / nbf, block
+        // e % nbf), gathered by all groups in one round per 2G entries (one
+        // L2 trip instead of one per block), then added by group 0 in entry
+        // order — the order of the serial walk, so the bits are unchanged
+        {
+            constexpr int nbf = ((CHUNK + kPiece - 1) / kPiece + CH - 1) / CH;   // blocks of a full chunk
+            const int32_t len_l = r.y - (r2.w - 1) * CHUNK;
+            const int nbl = ((len_l + kPiece - 1) / kPiece + CH - 1) / CH;      // blocks of the last chunk
+            const int ne = (r2.w - 1) * nbf + nbl;
+            for (int e0 = 0; e0 < ne; e0 += 2 * G) {
+                const int e1 = min(ne, e0 + 2 * G);
+                for (int e = e0 + grp; e < e1; e += G) {
+                    const int cc = e / nbf, j = e - cc * nbf;
+                    const float4* rp =
+                        reinterpret_cast<const float4*>(lpart + ((int64_t)(r2.z + cc) * 8 + j) * D) + lane;
+#pragma unroll
+                    for (int kk = 0; kk < NV; kk++) s_part[e - e0][kk * LPB + lane] = __ldcg(rp + kk * LPB);
+                }
+                __syncthreads();
+                if (grp == 0)
+                    for (int e = e0; e < e1; e++)
+#pragma unroll
+                        for (int kk = 0; kk < NV; kk++) add4(tot[kk], s_part[e - e0][kk * LPB + lane]);
+                __syncthreads();
+            }
+        }
+#endif
+        if (threadIdx.x == 0) lcnt[k] = 0u;
     }
     if (kPDL) pdl_wait();
     if (grp == 0) {
@@ -305,6 +337,55 @@ __device__ __forceinline__ void long_chunk(const SegRec* __restrict__ lrec, int6
     }
 }
 
+// Medium segments (kPiece < len <= kMedium) at LPB >= 8: 8 lane groups per
+// segment (one 16-lookup piece each, one pass), PER = 32 / LPB segments per
+// CTA.  The partials combine exactly as long_chunk's single-chunk case
+// (block sums of CH pieces, added to a zero total in order), so the bits
+// are those of the one-segment-per-CTA path; only the CTA count shrinks
+// (the reduce is bound by how many waves of CTA dependent-load chains it
+// needs: Terabyte-shaped, 540 medium CTAs of ~3 busy groups each).
+template <int LPB, int NV, bool kPDL>
+__device__ __forceinline__ void medium_pack(const SegRec* __restrict__ mrec, int64_t n_med, int64_t b,
+                                            const int32_t* __restrict__ perm, const float* __restrict__ src,
+                                            int D, float* W, float lr, int emit, float* grad_out, uint32_t* err) {
+    constexpr int G = 256 / LPB;
+    constexpr int PER = med_per_cta(LPB);
+    constexpr int GS = G / PER;                 // lane groups per segment
+    static_assert(GS * kPiece >= kMedium, "a medium segment is one pass");
+    constexpr int CH = kPiece / NV > 4 ? kPiece / NV : 4;
+    __shared__ float4 s_med[G][NV * LPB];
+    const int lane = threadIdx.x % LPB;
+    const int grp = threadIdx.x / LPB;
+    const int hs = grp / GS, hg = grp % GS;
+    const int64_t m = b * PER + hs;
+    int4 r = make_int4(0, 0, 0, 0);
+    if (m < n_med) r = __ldg(reinterpret_cast<const int4*>(mrec + m));   // pos, len, row, seg
+    const int32_t p0 = hg * kPiece;
+    const int32_t n = p0 < r.y ? min(kPiece, r.y - p0) : 0;
+    float4 g[NV];
+    sum_rows16<LPB, NV>(perm, r.x + p0, n, src, D, lane, g);
+#pragma unroll
+    for (int k = 0; k < NV; k++) s_med[grp][k * LPB + lane] = g[k];
+    __syncthreads();
+    if (hg != 0 || m >= n_med) return;
+    const int np = (r.y + kPiece - 1) / kPiece;
+    float4 tot[NV];
+#pragma unroll
+    for (int k = 0; k < NV; k++) tot[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q0 = 0; q0 < np; q0 += CH) {
+        float4 sub[NV];
+#pragma unroll
+        for (int k = 0; k < NV; k++) sub[k] = s_med[hs * GS + q0][k * LPB + lane];
+        for (int q = q0 + 1; q < min(np, q0 + CH); q++)
+#pragma unroll
+            for (int k = 0; k < NV; k++) add4(sub[k], s_med[hs * GS + q][k * LPB + lane]);
+#pragma unroll
+        for (int k = 0; k < NV; k++) add4(tot[k], sub[k]);
+    }
+    if (kPDL) pdl_wait();
+    seg_finish<LPB, NV>(tot, lane, r.z, r.w, W, D, lr, emit, grad_out, err);
+}
+
 // a9 + a10 over one grouped batch, no cross-CTA communication.  Block ranges:
 //  short:  one LPB-lane group per segment of <= kPiece lookups;
 //  medium: one warp per segment of <= kMedium lookups: each of the warp's
@@ -332,8 +413,8 @@ __device__ __forceinline__ void reduce_segments(const SegRec* __restrict__ rec, 
     // must not form the tail), then medium, then short
     int64_t b = blockIdx.x;
     const int64_t short_blocks = (n_short + G - 1) / G;
-    constexpr bool kMedWarp = LPB <= 4;   // medium segments: one warp, else one CTA
-    const int64_t med_blocks = med_blocks_for(n_med, LPB);
+    constexpr bool kMedWarp = LPB <= 4;   // medium segments: one warp, else 8 lane groups each
+    const int64_t med_blocks = med_blocks_red(n_med, LPB);
 #if FAE_RED_ORDER != 0
     {   // A/B: physical launch order of the block classes (logical order below)
         const int64_t ts = (n_tiny + G * kTinySeg - 1) / (G * kTinySeg) + (n_short - n_tiny + G - 1) / G;
@@ -356,8 +437,11 @@ __device__ __forceinline__ void reduce_segments(const SegRec* __restrict__ rec, 
     if (b >= n_lchunk) {
         b -= n_lchunk;
         if (!kMedWarp && b < med_blocks) {
-            long_chunk<LPB, NV, kPDL, false>(rec + n_short, n_med, b, true, perm, nullptr, src, D, W, lr,
-                                             lpart, lcnt, lmap, emit, grad_out, nullptr, err);
+            if (med_per_cta(LPB) > 1)
+                medium_pack<LPB, NV, kPDL>(rec + n_short, n_med, b, perm, src, D, W, lr, emit, grad_out, err);
+            else
+                long_chunk<LPB, NV, kPDL, false>(rec + n_short, n_med, b, true, perm, nullptr, src, D, W, lr,
+                                                 lpart, lcnt, lmap, emit, grad_out, nullptr, err);
             return;
         }
         if (b < med_blocks) {
@@ -1026,7 +1110,7 @@ void drop_graphs(Group& g) {
 static int64_t red_grid(const Group& g, int64_t G) {
     int64_t m = 1;
     for (const BatchDesc& d : g.hdesc)
-        m = std::max<int64_t>(m, d.n_lchunk + med_blocks_for(d.n_med, (int)(256 / G)) + cdiv(d.n_tiny, G * kTinySeg) +
+        m = std::max<int64_t>(m, d.n_lchunk + med_blocks_red(d.n_med, (int)(256 / G)) + cdiv(d.n_tiny, G * kTinySeg) +
                                      cdiv(d.n_short - d.n_tiny, G));
     return m;
 }

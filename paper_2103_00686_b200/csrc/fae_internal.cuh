@@ -37,6 +37,16 @@ inline int chunk_for_dim(int D) { return chunk_of_lpb(D / 4 < 32 ? D / 4 : 32); 
 __host__ __device__ inline int64_t med_blocks_for(int64_t n_med, int lpb) {
     return lpb <= 4 ? (n_med + 7) / 8 : n_med;
 }
+// the two-kernel reduce (reduce_segments): at LPB >= 8 a medium segment
+// (<= kMedium lookups = 8 pieces) takes 8 lane groups, so a CTA holds
+// 32 / LPB of them (FAE_MED_PACK=0: one CTA each, as the fused step)
+#ifndef FAE_MED_PACK
+#define FAE_MED_PACK 1
+#endif
+__host__ __device__ constexpr int med_per_cta(int lpb) { return (FAE_MED_PACK && lpb >= 8 && lpb < 32) ? 32 / lpb : 1; }
+__host__ __device__ inline int64_t med_blocks_red(int64_t n_med, int lpb) {
+    return lpb <= 4 ? (n_med + 7) / 8 : (n_med + med_per_cta(lpb) - 1) / med_per_cta(lpb);
+}
 constexpr int kStampSlots = 16;        // timing stamps per step (epoch runner)
 constexpr int kMaxPersistCtas = 2048;  // persistent kernel: barrier flag slots
 constexpr int kTinySeg = 4;            // segments of <= kTinySeg lookups: 4 per lane group
