@@ -40,6 +40,11 @@ constexpr int kSt = kStampSlots;
 #ifndef FAE_LPART_SERIAL
 #define FAE_LPART_SERIAL 0    // 1: the long segment's finisher reads the chunk block sums one by one (A/B)
 #endif
+#ifndef FAE_TINY_PER
+#define FAE_TINY_PER 4        // tiny segments per lane group in the two-kernel reduce (rounds of kTinySeg)
+#endif
+constexpr int kTinyPer = FAE_TINY_PER;
+static_assert(kTinyPer % kTinySeg == 0, "tiny rounds");
 constexpr int kFwdU = FAE_FWD_U;
 
 // finish a segment: emit G (a11 exchange) or W[row] -= lr * G (a10)
@@ -417,7 +422,7 @@ __device__ __forceinline__ void reduce_segments(const SegRec* __restrict__ rec, 
     const int64_t med_blocks = med_blocks_red(n_med, LPB);
 #if FAE_RED_ORDER != 0
     {   // A/B: physical launch order of the block classes (logical order below)
-        const int64_t ts = (n_tiny + G * kTinySeg - 1) / (G * kTinySeg) + (n_short - n_tiny + G - 1) / G;
+        const int64_t ts = (n_tiny + G * kTinyPer - 1) / (G * kTinyPer) + (n_short - n_tiny + G - 1) / G;
 #if FAE_RED_ORDER == 1   // long, tiny + short, medium
         if (b >= n_lchunk) b = b < n_lchunk + ts ? b + med_blocks : b - ts;
 #elif FAE_RED_ORDER == 2 // tiny + short, long, medium
@@ -479,9 +484,11 @@ __device__ __forceinline__ void reduce_segments(const SegRec* __restrict__ rec, 
         b -= med_blocks;
         // tiny segments (<= kTinySeg lookups): kTinySeg per lane group
         const int64_t n_small = n_short - n_tiny;
-        const int64_t tiny_blocks = (n_tiny + G * kTinySeg - 1) / (G * kTinySeg);
+        const int64_t tiny_blocks = (n_tiny + G * kTinyPer - 1) / (G * kTinyPer);
         if (b < tiny_blocks) {
-            const int64_t q0 = (b * G + grp) * kTinySeg;
+#pragma unroll 1
+          for (int h = 0; h < kTinyPer / kTinySeg; h++) {   // kTinySeg segments per round
+            const int64_t q0 = (b * G + grp) * kTinyPer + h * kTinySeg;
             if (q0 >= n_tiny) return;
             int4 r[kTinySeg];
             int32_t bag[kTinySeg][kTinySeg];
@@ -515,6 +522,7 @@ __device__ __forceinline__ void reduce_segments(const SegRec* __restrict__ rec, 
 #pragma unroll
             for (int t = 0; t < kTinySeg; t++)
                 if (q0 + t < n_tiny) seg_finish<LPB, NV>(g[t], lane, r[t].z, r[t].w, W, D, lr, emit, grad_out, err);
+          }
             return;
         }
         b -= tiny_blocks;
@@ -1110,7 +1118,7 @@ void drop_graphs(Group& g) {
 static int64_t red_grid(const Group& g, int64_t G) {
     int64_t m = 1;
     for (const BatchDesc& d : g.hdesc)
-        m = std::max<int64_t>(m, d.n_lchunk + med_blocks_red(d.n_med, (int)(256 / G)) + cdiv(d.n_tiny, G * kTinySeg) +
+        m = std::max<int64_t>(m, d.n_lchunk + med_blocks_red(d.n_med, (int)(256 / G)) + cdiv(d.n_tiny, G * kTinyPer) +
                                      cdiv(d.n_short - d.n_tiny, G));
     return m;
 }
