@@ -824,6 +824,65 @@ k_grp_reduce(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ run
     }
 }
 
+// Single-lookup forward of the grouped loop (a8, Y[b] = W_hot[idx[b]]):
+// CTA c owns a contiguous tile of ceil(n / grid) bags; its ids are staged in
+// shared memory with coalesced loads BEFORE griddepcontrol.wait (static
+// data), so after the wait a lane group's rounds of U row gathers follow one
+// another without an id load between them (fwd_gather1 reloads the ids of
+// its second round after the first round's stores, on the critical path).
+#ifndef FAE_FWD_TILE
+#define FAE_FWD_TILE 1   // with 2 forward CTAs per SM (fwd_grid_cap); at 4 per SM it lost (19.39 vs 19.10 us per batch)
+#endif
+constexpr int kFwdTileMax = 1024;
+template <int LPB, int NV, int U>
+__device__ __forceinline__ void fwd_gather1_tile(const float* __restrict__ W, int64_t H, int D,
+                                                 const int32_t* __restrict__ idx, int64_t n_bags,
+                                                 float* __restrict__ Y, uint32_t* err) {
+    constexpr int G = 256 / LPB;
+    __shared__ int32_t s_idx[kFwdTileMax];
+    const int lane = threadIdx.x % LPB;
+    const int grp = threadIdx.x / LPB;
+    int64_t T = (n_bags + gridDim.x - 1) / gridDim.x;
+    if (T > kFwdTileMax) T = kFwdTileMax;
+    bool waited = false;
+    for (int64_t t0 = blockIdx.x * T; t0 < n_bags; t0 += (int64_t)gridDim.x * T) {
+        const int nt = (int)(n_bags - t0 < T ? n_bags - t0 : T);
+        __syncthreads();                       // the previous tile's ids are consumed
+        for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+            int32_t r = __ldg(idx + t0 + i);
+            if ((uint32_t)r >= (uint64_t)H) {
+                atomicOr(err, kErrIndex);
+                r = -2;                        // zero row, as fwd_gather1
+            }
+            s_idx[i] = r;
+        }
+        __syncthreads();
+        if (!waited) {
+            pdl_wait();
+            waited = true;
+        }
+        for (int j0 = grp; j0 < nt; j0 += G * U) {
+            float4 v[U][NV];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int j = j0 + u * G;
+                const int32_t r = j < nt ? s_idx[j] : -2;
+                const float4* row = reinterpret_cast<const float4*>(W + (int64_t)(r < 0 ? 0 : r) * D) + lane;
+#pragma unroll
+                for (int k = 0; k < NV; k++) v[u][k] = r < 0 ? make_float4(0.f, 0.f, 0.f, 0.f) : __ldg(row + k * LPB);
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int j = j0 + u * G;
+                if (j >= nt) break;
+                float4* y = reinterpret_cast<float4*>(Y + (t0 + j) * D) + lane;
+#pragma unroll
+                for (int k = 0; k < NV; k++) __stcs(y + k * LPB, v[u][k]);
+            }
+        }
+    }
+}
+
 // World-1 graph kernels: step s of the replay handles batch
 // run[0] + *base + s; *base advances by kUnroll at the end of each replay.
 // Launched with programmatic stream serialization: each kernel triggers its
@@ -857,8 +916,10 @@ k_grp_fwd_pdl(const BatchDesc* __restrict__ desc, const int64_t* __restrict__ ru
         pdl_trigger();
     }
     if (hot_off) fwd_bags<LPB, NV, true>(W, H, D, hot_idx, hot_off + d.bag0, 0, d.n_bags, Y, err);
-    else if (P == 1) fwd_gather1<LPB, NV, true, kFwdU>(W, H, D, hot_idx + d.lk0, d.n_bags, Y, err);
-    else fwd_bags<LPB, NV, true>(W, H, D, hot_idx + d.lk0, nullptr, P, d.n_bags, Y, err);
+    else if (P == 1) {
+        if (FAE_FWD_TILE) fwd_gather1_tile<LPB, NV, kFwdU>(W, H, D, hot_idx + d.lk0, d.n_bags, Y, err);
+        else fwd_gather1<LPB, NV, true, kFwdU>(W, H, D, hot_idx + d.lk0, d.n_bags, Y, err);
+    } else fwd_bags<LPB, NV, true>(W, H, D, hot_idx + d.lk0, nullptr, P, d.n_bags, Y, err);
     if (trig & 4) pdl_wait();       // (threads without a bag never waited above)
     if (stamps) {
         __syncthreads();
@@ -1114,6 +1175,20 @@ void drop_graphs(Group& g) {
     g.xgraph_key = 0;
 }
 
+// Grid cap of the grouped forward.  The single-lookup tile forward runs at 2
+// CTAs per SM, leaving the other resident slots to the reduce, whose static
+// loads and long-segment sums (no W access before griddepcontrol.wait) then
+// overlap the forward.  Measured (Terabyte-shaped, train loop per batch):
+// 592 / 444 / 370 / 296 / 222 / 148 CTAs 19.1 / 18.5 / 18.2 / 17.3 / 19.4 /
+// 23.9 us (the staged-id forward); fwd_gather1 at 592: 18.7 us.  Other
+// forwards keep 4 per SM.  FAE_FWD_GRID overrides.
+static int64_t fwd_grid_cap(Ctx* c) {
+    static const int64_t fcap = getenv("FAE_FWD_GRID") ? atoll(getenv("FAE_FWD_GRID")) : 0;
+    if (fcap > 0) return fcap;
+    const Group& g = c->grp;
+    return (int64_t)sm_count(c) * ((FAE_FWD_TILE && g.P == 1 && !g.hot_off) ? 2 : 4);
+}
+
 // blocks of the reduce kernel for the largest batch
 static int64_t red_grid(const Group& g, int64_t G) {
     int64_t m = 1;
@@ -1159,8 +1234,7 @@ static fae_status launch_pdl_step(Ctx* c, cudaStream_t st, int s, float* W, int6
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    static const int64_t fcap = getenv("FAE_FWD_GRID") ? atoll(getenv("FAE_FWD_GRID")) : 0;
-    const int64_t half = fcap > 0 ? fcap : (int64_t)sm_count(c) * 4;   // each kernel gets about half of the GPU
+    const int64_t half = fwd_grid_cap(c);
     const int64_t fu = g.P == 1 ? cdiv(g.max_bags, kFwdU)
                      : (g.hot_off || g.P >= kWarpBagMinP) ? g.max_bags * (32 / LPB) : g.max_bags;
     cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(fu, gpb), half)));
@@ -1252,7 +1326,7 @@ static fae_status launch_x_step(Ctx* c, cudaStream_t st, int s, int last, float*
     cfg.numAttrs = c->no_pdl ? 0 : 1;
     const int64_t fu = g.P == 1 ? cdiv(g.max_bags, kFwdU)
                      : (g.hot_off || g.P >= kWarpBagMinP) ? g.max_bags * (32 / LPB) : g.max_bags;
-    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(fu, gpb), (int64_t)sm_count(c) * 4)));
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(fu, gpb), fwd_grid_cap(c))));
     FAE_CUDA(c, cudaLaunchKernelEx(&cfg, k_grp_fwd_pdl<LPB, NV>, (const BatchDesc*)g.desc, (const int64_t*)g.run,
                                    (const int64_t*)g.cursor, s, g.hot_idx, g.hot_off, (int)g.P, (const float*)W, H, D,
                                    Y, c->d_err, stamps, 4));
@@ -1320,7 +1394,7 @@ static fae_status fwd_pdl_one(Ctx* c, cudaStream_t st, int s, float* W, int64_t 
     cfg.numAttrs = c->no_pdl ? 0 : 1;
     const int64_t fu = g.P == 1 ? cdiv(g.max_bags, kFwdU)
                      : (g.hot_off || g.P >= kWarpBagMinP) ? g.max_bags * (32 / LPB) : g.max_bags;
-    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(fu, gpb), (int64_t)sm_count(c) * 4)));
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(fu, gpb), fwd_grid_cap(c))));
     FAE_CUDA(c, cudaLaunchKernelEx(&cfg, k_grp_fwd_pdl<LPB, NV>, (const BatchDesc*)g.desc, (const int64_t*)g.run,
                                    (const int64_t*)g.cursor, s, g.hot_idx, g.hot_off, (int)g.P, (const float*)W, H, D,
                                    Y, c->d_err, (unsigned long long*)nullptr, 0));
@@ -1543,7 +1617,7 @@ static fae_status fwd_x_one(Ctx* c, cudaStream_t st, int s, float* W, int64_t H,
     cfg.numAttrs = c->no_pdl ? 0 : 1;
     const int64_t fu = g.P == 1 ? cdiv(g.max_bags, kFwdU)
                      : (g.hot_off || g.P >= kWarpBagMinP) ? g.max_bags * (32 / LPB) : g.max_bags;
-    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(fu, gpb), (int64_t)sm_count(c) * 4)));
+    cfg.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(fu, gpb), fwd_grid_cap(c))));
     FAE_CUDA(c, cudaLaunchKernelEx(&cfg, k_grp_fwd_pdl<LPB, NV>, (const BatchDesc*)g.desc, (const int64_t*)g.run,
                                    (const int64_t*)g.cursor, s, g.hot_idx, g.hot_off, (int)g.P, (const float*)W, H, D,
                                    Y, c->d_err, (unsigned long long*)nullptr, 4));
