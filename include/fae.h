@@ -549,8 +549,9 @@ fae_status fae_sched_new_epoch(fae_sched* s);
  * mean over the batch of the log loss; plain SGD of every weight and bias.
  * Parameters: ONE caller-owned device fp32 buffer, per layer (bottom
  * first, then top) W [out][ld] row-major (ld = in rounded up to a multiple
- * of 4 floats, so every GEMM operand is 16-byte aligned; the pad entries
- * are never read or written) followed by b [out]; fae_dlrm_param_count
+ * of 4 floats, so every GEMM operand is 16-byte aligned; the GEMMs run
+ * over the padded width, so the pad entries MUST be zero — they are read as
+ * zero weights and stay zero) followed by b [out]; fae_dlrm_param_count
  * gives the length.
  * GEMMs through cuBLAS (tf32 = 1: TF32 on the tensor cores; 0: pedantic
  * fp32); everything else hand-written kernels; no allocation after create.

@@ -77,10 +77,46 @@ __global__ void k_bias_act(float* __restrict__ C, const float* __restrict__ bias
     }
 }
 
+// the same, 4 columns per thread (cols % 4 == 0, 16-byte aligned C and
+// bias; 32-bit indices: rows * cols < 2^31): same arithmetic per element
+__global__ void k_bias_act4(float4* __restrict__ C, const float4* __restrict__ bias, int rows, int cols4,
+                            const int32_t* __restrict__ nb, int relu) {
+    const int n = *nb;
+    const int tot = rows * cols4;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += gridDim.x * blockDim.x) {
+        const int b = e / cols4, j = e - b * cols4;
+        float4 v = C[e];
+        const float4 w = __ldg(bias + j);
+        v.x += w.x;
+        v.y += w.y;
+        v.z += w.z;
+        v.w += w.w;
+        if (relu) {
+            v.x = fmaxf(v.x, 0.f);
+            v.y = fmaxf(v.y, 0.f);
+            v.z = fmaxf(v.z, 0.f);
+            v.w = fmaxf(v.w, 0.f);
+        }
+        C[e] = b < n ? v : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
 // dX *= (X > 0)   (X: the ReLU output that fed the layer)
 __global__ void k_relu_mask(float* __restrict__ dX, const float* __restrict__ X, int64_t n) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
         if (!(X[e] > 0.f)) dX[e] = 0.f;
+}
+
+__global__ void k_relu_mask4(float4* __restrict__ dX, const float4* __restrict__ X, int n4) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n4; e += gridDim.x * blockDim.x) {
+        const float4 x = X[e];
+        float4 d = dX[e];
+        if (!(x.x > 0.f)) d.x = 0.f;
+        if (!(x.y > 0.f)) d.y = 0.f;
+        if (!(x.z > 0.f)) d.z = 0.f;
+        if (!(x.w > 0.f)) d.w = 0.f;
+        dX[e] = d;
+    }
 }
 
 // Interaction forward: one warp per sample.  T = [x (bottom output), Y_0 ..
@@ -154,47 +190,106 @@ __global__ void k_interact_bwd(const float* __restrict__ xbot, const float* __re
 }
 
 // Register versions (F <= 32, D in {8, 16, 32, 64}): lane i holds the row
-// T_i of its sample; row j is broadcast by shuffles, so there is no shared-
-// memory bank traffic on the rows.  Forward: lane i computes <T_i, T_j> for
+// T_i of its sample (forward) or its gradient dT_i (backward); row j is
+// broadcast from a per-warp shared-memory copy of the sample's rows (one
+// wavefront per float4, no bank conflicts; it replaced per-element shuffles,
+// D shuffles per row: RMC3 interaction forward 45.6 -> see DESIGN §8).  Forward: lane i computes <T_i, T_j> for
 // every j < i (pair index i(i-1)/2 + j), staged in shared memory and stored
 // coalesced.  Backward: lane i accumulates dT_i = sum_{j != i} dZ_(i,j) T_j
 // in ascending j (dZ staged in shared memory).  Same arithmetic and order as
 // the shared-memory kernels above.
+// stage the F = Tn + 1 rows of sample b (row 0 = bottom output, rows 1..Tn
+// = its Tn contiguous embedding rows) into the warp's shared rows [F][RS]
+// with coalesced float4 loads; invalid samples stage zeros
+template <int D, int RS>
+__device__ __forceinline__ void stage_rows(float* rows, const float* __restrict__ xbot, const float* __restrict__ Y,
+                                           int64_t b, int Tn, bool valid, int lane) {
+    constexpr int Q = D / 4;
+    const int nq = (Tn + 1) * Q;
+    const float4* x4 = reinterpret_cast<const float4*>(xbot + b * D);
+    const float4* y4 = reinterpret_cast<const float4*>(Y + b * Tn * D);
+    for (int e = lane; e < nq; e += 32) {
+        const int r = e / Q, q = e - r * Q;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid) v = r == 0 ? __ldg(x4 + q) : __ldg(y4 + (e - Q));
+        *reinterpret_cast<float4*>(rows + r * RS + 4 * q) = v;
+    }
+}
+
 template <int D>
 __global__ void __launch_bounds__(128) k_interact_fwd_reg(const float* __restrict__ xbot, const float* __restrict__ Y,
                                                           int B, int Tn, int P, const int32_t* __restrict__ nb,
                                                           float* __restrict__ out, int ld) {
-    extern __shared__ float s_z[];   // [warps][P]
+    extern __shared__ float s_dyn[];   // [warps][32][D + 4] rows, then [warps][P] pair dots
+    constexpr int RS = D + 4;          // padded row stride: a lane's own-row reads hit distinct banks
     const int F = Tn + 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int b = blockIdx.x * (blockDim.x >> 5) + warp;
+    const int nw = blockDim.x >> 5;
+    const int b = blockIdx.x * nw + warp;
     if (b >= B) return;
     const bool valid = b < *nb;
-    float t[D];
-    const float* src = lane == 0 ? xbot + (int64_t)b * D : Y + ((int64_t)b * Tn + (lane - 1)) * D;
-#pragma unroll
-    for (int q = 0; q < D / 4; q++) {
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid && lane < F) v = __ldg(reinterpret_cast<const float4*>(src) + q);
-        t[4 * q] = v.x;
-        t[4 * q + 1] = v.y;
-        t[4 * q + 2] = v.z;
-        t[4 * q + 3] = v.w;
-    }
-    float* z = s_z + (int64_t)warp * P;
+    float* rows = s_dyn + (int64_t)warp * 32 * RS;
+    stage_rows<D, RS>(rows, xbot, Y, b, Tn, valid, lane);
+    __syncwarp();
+    float* z = s_dyn + (int64_t)nw * 32 * RS + (int64_t)warp * P;
     const int kb = lane * (lane - 1) / 2;
-    for (int j = 0; j < F - 1; j++) {
+    // <T_lane, T_j>, d ascending; four rows j at a time (four independent
+    // chains, each in the order of a single one); the lane's own row is
+    // re-read from shared memory (conflict-free: padded stride), so no row
+    // lives in registers and the loads are not hoisted into spills
+    const float4* own = reinterpret_cast<const float4*>(rows + (lane < F ? lane : 0) * RS);
+    int j = 0;
+    for (; j + 4 <= F - 1; j += 4) {
+        const float4* r0 = reinterpret_cast<const float4*>(rows + j * RS);
+        const float4* r1 = r0 + RS / 4;
+        const float4* r2 = r1 + RS / 4;
+        const float4* r3 = r2 + RS / 4;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll 2
+        for (int q = 0; q < D / 4; q++) {
+            const float4 t = own[q];
+            const float4 a0 = r0[q], a1 = r1[q], a2 = r2[q], a3 = r3[q];
+            s0 = fmaf(t.x, a0.x, s0);
+            s1 = fmaf(t.x, a1.x, s1);
+            s2 = fmaf(t.x, a2.x, s2);
+            s3 = fmaf(t.x, a3.x, s3);
+            s0 = fmaf(t.y, a0.y, s0);
+            s1 = fmaf(t.y, a1.y, s1);
+            s2 = fmaf(t.y, a2.y, s2);
+            s3 = fmaf(t.y, a3.y, s3);
+            s0 = fmaf(t.z, a0.z, s0);
+            s1 = fmaf(t.z, a1.z, s1);
+            s2 = fmaf(t.z, a2.z, s2);
+            s3 = fmaf(t.z, a3.z, s3);
+            s0 = fmaf(t.w, a0.w, s0);
+            s1 = fmaf(t.w, a1.w, s1);
+            s2 = fmaf(t.w, a2.w, s2);
+            s3 = fmaf(t.w, a3.w, s3);
+        }
+        if (lane < F) {
+            if (lane > j) z[kb + j] = s0;
+            if (lane > j + 1) z[kb + j + 1] = s1;
+            if (lane > j + 2) z[kb + j + 2] = s2;
+            if (lane > j + 3) z[kb + j + 3] = s3;
+        }
+    }
+    for (; j < F - 1; j++) {
+        const float4* rj = reinterpret_cast<const float4*>(rows + j * RS);
         float s = 0.f;
-#pragma unroll
-        for (int d = 0; d < D; d++) s = fmaf(t[d], __shfl_sync(0xffffffffu, t[d], j), s);
+#pragma unroll 2
+        for (int q = 0; q < D / 4; q++) {
+            const float4 t = own[q];
+            const float4 r = rj[q];
+            s = fmaf(t.x, r.x, s);
+            s = fmaf(t.y, r.y, s);
+            s = fmaf(t.z, r.z, s);
+            s = fmaf(t.w, r.w, s);
+        }
         if (lane > j && lane < F) z[kb + j] = s;
     }
     __syncwarp();
     float* o = out + (int64_t)b * ld;
-    if (lane == 0) {
-#pragma unroll
-        for (int d = 0; d < D; d++) o[d] = t[d];
-    }
+    for (int d = lane; d < D; d += 32) o[d] = rows[d];
     for (int k = lane; k < P; k += 32) o[D + k] = z[k];
 }
 
@@ -203,48 +298,70 @@ __global__ void __launch_bounds__(128) k_interact_bwd_reg(const float* __restric
                                                           int B, int Tn, int P, const int32_t* __restrict__ nb,
                                                           const float* __restrict__ din, float* __restrict__ dxbot,
                                                           float* __restrict__ dY, int ld) {
-    extern __shared__ float s_z[];   // [warps][P]
+    extern __shared__ float s_dyn[];   // [warps][32][D + 4] rows, then [warps][P] pair gradients
+    constexpr int RS = D + 4;
+    constexpr int Q = D / 4;
     const int F = Tn + 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int b = blockIdx.x * (blockDim.x >> 5) + warp;
+    const int nw = blockDim.x >> 5;
+    const int b = blockIdx.x * nw + warp;
     if (b >= B) return;
     const bool valid = b < *nb;
-    float t[D], a[D];
-    const float* src = lane == 0 ? xbot + (int64_t)b * D : Y + ((int64_t)b * Tn + (lane - 1)) * D;
-#pragma unroll
-    for (int q = 0; q < D / 4; q++) {
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (valid && lane < F) v = __ldg(reinterpret_cast<const float4*>(src) + q);
-        t[4 * q] = v.x;
-        t[4 * q + 1] = v.y;
-        t[4 * q + 2] = v.z;
-        t[4 * q + 3] = v.w;
-        a[4 * q] = a[4 * q + 1] = a[4 * q + 2] = a[4 * q + 3] = 0.f;
-    }
+    float* rows = s_dyn + (int64_t)warp * 32 * RS;
+    stage_rows<D, RS>(rows, xbot, Y, b, Tn, valid, lane);
     const float* g = din + (int64_t)b * ld;
-    float* z = s_z + (int64_t)warp * P;
+    float* z = s_dyn + (int64_t)nw * 32 * RS + (int64_t)warp * P;
     for (int k = lane; k < P; k += 32) z[k] = valid ? g[D + k] : 0.f;
     __syncwarp();
-    for (int j = 0; j < F; j++) {
-        const int ii = lane > j ? lane : j, jj = lane > j ? j : lane;
-        const float w = (lane != j && lane < F) ? z[ii * (ii - 1) / 2 + jj] : 0.f;
+    // dT_lane[d] = sum_{j != lane} dZ(lane, j) T_j[d], j ascending for every
+    // d; columns in chunks of CW (the j loop stays rolled: no hoisted rows)
+    constexpr int CW = D < 16 ? D : 16;
+    float a[D];
 #pragma unroll
-        for (int d = 0; d < D; d++) {
-            const float tj = __shfl_sync(0xffffffffu, t[d], j);
-            if (lane != j) a[d] = fmaf(w, tj, a[d]);
+    for (int c = 0; c < D / CW; c++) {
+#pragma unroll
+        for (int k = 0; k < CW; k++) a[c * CW + k] = 0.f;
+#pragma unroll 1
+        for (int j = 0; j < F; j++) {
+            if (lane == j) continue;
+            const int ii = lane > j ? lane : j, jj = lane > j ? j : lane;
+            const float w = lane < F ? z[ii * (ii - 1) / 2 + jj] : 0.f;
+            const float4* rj = reinterpret_cast<const float4*>(rows + j * RS + c * CW);
+#pragma unroll
+            for (int q = 0; q < CW / 4; q++) {
+                const float4 r = rj[q];
+                a[c * CW + 4 * q] = fmaf(w, r.x, a[c * CW + 4 * q]);
+                a[c * CW + 4 * q + 1] = fmaf(w, r.y, a[c * CW + 4 * q + 1]);
+                a[c * CW + 4 * q + 2] = fmaf(w, r.z, a[c * CW + 4 * q + 2]);
+                a[c * CW + 4 * q + 3] = fmaf(w, r.w, a[c * CW + 4 * q + 3]);
+            }
         }
     }
+    __syncwarp();   // every lane is done reading the rows: each overwrites its own with dT
     if (lane == 0) {
-        float* o = dxbot + (int64_t)b * D;
 #pragma unroll
-        for (int d = 0; d < D; d++) {
-            const float v = valid ? g[d] + a[d] : 0.f;
-            o[d] = t[d] > 0.f ? v : 0.f;   // bottom ReLU mask
+        for (int q = 0; q < Q; q++) {   // dxbot = dx + dT_0, then the bottom ReLU mask (row 0 = bottom output)
+            float4 x = *reinterpret_cast<const float4*>(rows + 4 * q);
+            float4 v;
+            v.x = x.x > 0.f ? (valid ? g[4 * q] + a[4 * q] : 0.f) : 0.f;
+            v.y = x.y > 0.f ? (valid ? g[4 * q + 1] + a[4 * q + 1] : 0.f) : 0.f;
+            v.z = x.z > 0.f ? (valid ? g[4 * q + 2] + a[4 * q + 2] : 0.f) : 0.f;
+            v.w = x.w > 0.f ? (valid ? g[4 * q + 3] + a[4 * q + 3] : 0.f) : 0.f;
+            *reinterpret_cast<float4*>(rows + 4 * q) = v;
         }
     } else if (lane < F) {
-        float4* o = reinterpret_cast<float4*>(dY + ((int64_t)b * Tn + (lane - 1)) * D);
 #pragma unroll
-        for (int q = 0; q < D / 4; q++) o[q] = make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
+        for (int q = 0; q < Q; q++)
+            *reinterpret_cast<float4*>(rows + lane * RS + 4 * q) =
+                make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
+    }
+    __syncwarp();
+    float4* ox = reinterpret_cast<float4*>(dxbot + (int64_t)b * D);
+    for (int q = lane; q < Q; q += 32) ox[q] = *reinterpret_cast<const float4*>(rows + 4 * q);
+    float4* oy = reinterpret_cast<float4*>(dY + (int64_t)b * Tn * D);
+    for (int e = lane; e < Tn * Q; e += 32) {
+        const int r = e / Q + 1, q = e - (r - 1) * Q;
+        oy[e] = *reinterpret_cast<const float4*>(rows + r * RS + 4 * q);
     }
 }
 
@@ -348,17 +465,26 @@ static fae_status dlrm_run(Dlrm* m, float* params, float lr, bool train, cudaStr
         const float* X = (l == nbot) ? m->act[nbot + 1] /* interaction output */ : m->act[l < nbot ? l : l + 1];
         float* C = m->act[l < nbot ? l + 1 : l + 2];
         const float* W = params + m->woff[l];
-        FAE_BLAS(c, cublasSgemm(m->blas, CUBLAS_OP_T, CUBLAS_OP_N, m->out_[l], B, m->in_[l], &one, W, m->ld_[l], X,
+        // K over the padded width (pad entries of W and X are zero): every
+        // GEMM dimension but B / out a multiple of 4, so cuBLAS takes its
+        // 16-byte-aligned sm100 kernels (an odd K = 13 or 415 fell back to
+        // align-1 sm80 kernels)
+        FAE_BLAS(c, cublasSgemm(m->blas, CUBLAS_OP_T, CUBLAS_OP_N, m->out_[l], B, m->ld_[l], &one, W, m->ld_[l], X,
                                 m->ld_[l], &zero, C, m->out_[l]));
         if (l == L - 1) break;   // the logit: bias inside the loss kernel
-        k_bias_act<<<grid_for((int64_t)B * m->out_[l], c), 256, 0, st>>>(C, params + m->boff[l], B, m->out_[l],
-                                                                        m->nb, 1);
+        const float* bvec = params + m->boff[l];
+        if (m->out_[l] % 4 == 0 && ((uintptr_t)bvec & 15) == 0 && ((uintptr_t)C & 15) == 0 &&
+            (int64_t)B * m->out_[l] < (1ll << 31))
+            k_bias_act4<<<grid_for((int64_t)B * m->out_[l] / 4, c), 256, 0, st>>>(
+                reinterpret_cast<float4*>(C), reinterpret_cast<const float4*>(bvec), B, m->out_[l] / 4, m->nb, 1);
+        else
+            k_bias_act<<<grid_for((int64_t)B * m->out_[l], c), 256, 0, st>>>(C, bvec, B, m->out_[l], m->nb, 1);
         FAE_LAUNCHED(c);
         if (l == nbot - 1) {     // interaction: act[nbot] = bottom output -> act[nbot + 1]
             const int wpb = 4;
             const bool reg = Tn + 1 <= 32 && (D == 8 || D == 16 || D == 32 || D == 64);
             if (reg) {
-                const size_t sm = sizeof(float) * wpb * m->P;
+                const size_t sm = sizeof(float) * wpb * (32 * (D + 4) + m->P);
                 auto kf = D == 8 ? k_interact_fwd_reg<8> : D == 16 ? k_interact_fwd_reg<16>
                         : D == 32 ? k_interact_fwd_reg<32> : k_interact_fwd_reg<64>;
                 kf<<<(unsigned)cdiv(B, wpb), 32 * wpb, sm, st>>>(m->act[nbot], m->Y, B, Tn, m->P, m->nb,
@@ -383,7 +509,8 @@ static fae_status dlrm_run(Dlrm* m, float* params, float lr, bool train, cudaStr
         const float* X = top ? (l == nbot ? m->act[nbot + 1] : m->act[l + 1]) : m->act[l];
         float* W = params + m->woff[l];
         float* bvec = params + m->boff[l];
-        const int in = m->in_[l], out = m->out_[l], ld = m->ld_[l];
+        const int out = m->out_[l], ld = m->ld_[l];
+        const int in = ld;   // padded width: the pad rows of dX / dW come out zero (zero pads of W and X)
         // dX = dC W  (old W), for every layer but the first bottom one
         if (l > 0)
             FAE_BLAS(c, cublasSgemm(m->blas, CUBLAS_OP_N, CUBLAS_OP_N, in, B, out, &one, W, ld, dC, out, &zero, dX,
@@ -404,7 +531,7 @@ static fae_status dlrm_run(Dlrm* m, float* params, float lr, bool train, cudaStr
             const int wpb = 4;
             const bool reg = Tn + 1 <= 32 && (D == 8 || D == 16 || D == 32 || D == 64);
             if (reg) {
-                const size_t sm = sizeof(float) * wpb * m->P;
+                const size_t sm = sizeof(float) * wpb * (32 * (D + 4) + m->P);
                 auto kb = D == 8 ? k_interact_bwd_reg<8> : D == 16 ? k_interact_bwd_reg<16>
                         : D == 32 ? k_interact_bwd_reg<32> : k_interact_bwd_reg<64>;
                 kb<<<(unsigned)cdiv(B, wpb), 32 * wpb, sm, st>>>(m->act[nbot], m->Y, B, Tn, m->P, m->nb, dX, dC,
@@ -418,7 +545,11 @@ static fae_status dlrm_run(Dlrm* m, float* params, float lr, bool train, cudaStr
             continue;            // dC now holds the bottom output's gradient
         }
         // ReLU of the layer below (its output is X)
-        k_relu_mask<<<grid_for((int64_t)B * ld, c), 256, 0, st>>>(dX, X, (int64_t)B * ld);
+        if (((uintptr_t)dX & 15) == 0 && ((uintptr_t)X & 15) == 0 && (int64_t)B * ld < (1ll << 31))
+            k_relu_mask4<<<grid_for((int64_t)B * ld / 4, c), 256, 0, st>>>(
+                reinterpret_cast<float4*>(dX), reinterpret_cast<const float4*>(X), B * ld / 4);
+        else
+            k_relu_mask<<<grid_for((int64_t)B * ld, c), 256, 0, st>>>(dX, X, (int64_t)B * ld);
         FAE_LAUNCHED(c);
         std::swap(dC, dX);
     }
@@ -529,6 +660,10 @@ extern "C" fae_status fae_dlrm_create(fae_ctx* ctx, const fae_dlrm_cfg* g, fae_d
         float* p = nullptr;
         if (cudaMalloc(&p, sizeof(float) * (size_t)B * w) != cudaSuccess) return fail(cuda_err(c, cudaGetLastError(), "fae_dlrm_create"));
         m.act.push_back(p);
+        // the pad columns (beyond the layer width) are never written: zero
+        // once, so the padded-width GEMMs multiply zeros
+        if (cudaMemset(p, 0, sizeof(float) * (size_t)B * w) != cudaSuccess)
+            return fail(cuda_err(c, cudaGetLastError(), "fae_dlrm_create"));
     }
     m.max_w = std::max(m.max_w, m.ld_top);
     for (int l = 0; l < m.n_layers; l++) m.max_w = std::max(m.max_w, m.ld_[l]);
