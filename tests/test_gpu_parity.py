@@ -792,3 +792,64 @@ def test_bwd_oversized_offsets_batch_latches_capacity(dev):
         ctx.check()
     assert e.value.name == "CAPACITY"
     assert torch.equal(W, W0)
+
+
+# Two-kernel step at other row widths and a batch whose forward needs several
+# bag tiles per CTA: medium segments packed 4 per CTA (D = 32, 8-lane groups),
+# one per CTA (D = 128), and the staged-id forward past its 1024-bag tile
+# (B * Tn > 2 * SMs * 1024 bags).  All tables are small (all hot), so every
+# record is a hot record and the Zipf heads give segments in every tier.
+@pytest.mark.parametrize("name,dim,batch,R", [("d32", 32, 512, 6_000), ("d128", 128, 256, 3_000),
+                                              ("d64-big", 64, 12_288, 26_000)])
+def test_grouped_two_kernel_dims(dev, name, dim, batch, R, monkeypatch):
+    """fae_train_hot_batches (graph, two-kernel step) == the standalone calls
+    bit for bit and == the oracle's sequential SGD within tolerance."""
+    from paper_2103_00686_b200 import fae_group_info
+    from paper_2103_00686_b200.pipeline import FaePipeline
+    monkeypatch.setenv("FAE_FUSED", "0")
+    monkeypatch.setenv("FAE_PERSIST", "0")
+    rows = [max(3, r // 20_000) for r in gen.TERABYTE_ROWS]
+    c = gen.Config(name, rows, dim, batch, 1, records=R, t=1e-6)
+    small = 1 << 40                                  # every table all-hot (P:L386-387 rule)
+    ds = gen.make_dataset(c, n_records=R, seed=11)
+    dd = ds.to(dev)
+    pipe = FaePipeline(ds.rows, c.dim, c.batch, 1)
+    prep = pipe.preprocess(dd.idx, None, R, x_pct=5.0, seed=3, t=c.t, small_table_bytes=small)
+    assert prep.packed["n_hot"] == R
+    W = gen.make_weights(sum(ds.rows), c.dim)
+    W_hot = pipe.extract(W.to(dev), prep).clone()
+    W_std = W_hot.clone()
+    nbt = prep.packed["n_hot_batches"]
+    nb = min(3, nbt)
+    first = nbt - nb                                   # includes the ragged last batch
+    S = c.batch * c.n_tables
+    dY = gen.make_dy(nb * S, c.dim, seed=13).view(nb, S, c.dim).to(dev)
+    lr = 0.05
+    pipe.group(prep)
+    assert fae_group_info(pipe.ctx)["fused"] == 0
+    Y = torch.zeros(S, c.dim, device=dev)
+    pipe.train(W_hot, first, nb, dY, Y, lr)
+    pipe.ctx.check()
+    Y2 = torch.zeros(S, c.dim, device=dev)
+    for i in range(nb):
+        _, _, n_bags = pipe.batch_args(prep, first + i)
+        pipe.step(W_std, prep, first + i, Y2[:n_bags], dY[i, :n_bags], lr)
+    pipe.ctx.check()
+    assert torch.equal(W_hot, W_std)
+    assert torch.equal(Y, Y2)
+    ref = _prep_ref(ds, 5.0, 3, "t", t=c.t, small=small, dim=c.dim)
+    Wr = oracle.extract(W, ref["remap"], ref["H"])
+    pk = ref["pack"]
+    Tn = c.n_tables
+    for i in range(nb):
+        b = first + i
+        r0, r1 = b * c.batch, min((b + 1) * c.batch, pk["n_hot"])
+        n_bags = (r1 - r0) * Tn
+        bi = pk["hot_idx"][r0 * Tn: r1 * Tn]
+        if i == nb - 1:   # the last trained batch's forward output
+            Yref, _ = oracle.emb_fwd(Wr, bi, None, 1, n_bags)
+            ok, worst = close(Y[:n_bags].cpu().numpy(), Yref)
+            assert ok, worst
+        Wr, _ = oracle.emb_bwd_sgd(Wr, bi, None, 1, n_bags, dY[i, :n_bags].cpu(), lr)
+    ok, worst = close(W_hot.cpu().numpy(), Wr)
+    assert ok, worst
