@@ -16,10 +16,15 @@ from paper_2103_00686_b200.pipeline import FaePipeline  # noqa: E402
 dev = torch.device("cuda", 0)
 for fused in ("1", "0"):
     os.environ["FAE_FUSED"] = fused
-    for name in ("tiny", "ali"):
+    for name in ("tiny", "ali", "tb64"):
+        if name == "tb64" and fused == "1":
+            continue
         if name == "tiny":
             cfg = gen.CONFIGS["tiny"]
             R, t, small = 6_000, 1e-2, 0
+        elif name == "tb64":   # D = 64: medium segments packed per CTA, staged-id forward at 2 CTAs / SM
+            cfg = gen.Config("tb64", [max(3, r // 20_000) for r in gen.TERABYTE_ROWS], 64, 256, 1, records=3_000)
+            R, t, small = 3_000, 1e-6, 1 << 40
         else:
             cfg = gen.Config("ali-s", [500, 2000, 90], 16, 32, 0, 3, 12, records=2_000)
             R, t, small = 2_000, 1e-3, 0
