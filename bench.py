@@ -34,6 +34,9 @@ METRIC = "hot-batch lookups/sec (fwd+bwd+update) and % of HBM peak at 1/2/4/8 B2
 UNIT = "lookups/s"
 
 
+NOMINAL_HBM_GBS = 8000.0   # B200 HBM3e nominal (north_star's "~8 TB/s"); frac uses the measured peak
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -412,6 +415,8 @@ def run_fae(args):
                          "bound": "hbm", "achieved": achieved,
                          "peak": peak, "peak_kind": kind, "unit": "GB/s",
                          "frac": achieved / peak,
+                         # report the nominal-basis fraction too (north_star's ~8 TB/s)
+                         "frac_nominal": achieved / NOMINAL_HBM_GBS, "peak_nominal": NOMINAL_HBM_GBS,
                          "traffic": ncu_traffic(kname_full, f"{cfg.name}-shaped"),
                          "bytes_per_launch": kb,
                          "bytes_formula": ("SURVEY §8(d): fwd 4L+4DL+4DS [+4(S+1)], bwd+update "
