@@ -674,6 +674,7 @@ k_gs_records(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __r
     constexpr int NC = 4;
     __shared__ uint32_t s_w[NC][8];
     __shared__ uint32_t s_n[NC];
+    __shared__ uint64_t s_w64[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int64_t b = blockIdx.x; b < n_batches; b += gridDim.x) {
         const BatchDesc d = desc[b];
@@ -702,15 +703,23 @@ k_gs_records(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __r
             }
             return r.len <= kTinySeg ? 0 : (r.len <= kPiece ? 1 : (r.len <= kMedium ? 2 : 3));
         };
-        // pass 1: class sizes (the class depends on the length only)
+        // pass 1: class sizes (the class depends on the length only); each
+        // thread takes IPT consecutive segments per round
+        constexpr int IPT = 4;
+        constexpr int CHK = 256 * IPT;
         uint32_t nn[NC] = {0u, 0u, 0u, 0u};
-        for (int64_t q = tid; q < S; q += 256) {
-            const int64_t s = d.sb0 + q;
-            const int64_t len = (q + 1 < S ? seg_start[s + 1] : d.lk1) - seg_start[s];
-            nn[0] += len <= kTinySeg;
-            nn[1] += len > kTinySeg && len <= kPiece;
-            nn[2] += len > kPiece && len <= kMedium;
-            nn[3] += len > kMedium;
+        for (int64_t q0 = (int64_t)tid * IPT; q0 < S; q0 += CHK) {
+#pragma unroll
+            for (int i = 0; i < IPT; i++) {
+                const int64_t q = q0 + i;
+                if (q >= S) break;
+                const int64_t s = d.sb0 + q;
+                const int64_t len = (q + 1 < S ? seg_start[s + 1] : d.lk1) - seg_start[s];
+                nn[0] += len <= kTinySeg;
+                nn[1] += len > kTinySeg && len <= kPiece;
+                nn[2] += len > kPiece && len <= kMedium;
+                nn[3] += len > kMedium;
+            }
         }
 #pragma unroll
         for (int c = 0; c < NC; c++) {
@@ -732,30 +741,46 @@ k_gs_records(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __r
         const uint32_t base[NC] = {0u, s_n[0], s_n[0] + s_n[1], s_n[0] + s_n[1] + s_n[2]};
         uint32_t run[NC] = {0u, 0u, 0u, 0u};
         __syncthreads();
-        // pass 2: stable partition, chunks of 256 segments
-        for (int64_t q0 = 0; q0 < S; q0 += 256) {
-            const int64_t q = q0 + tid;
-            const bool valid = q < S;
-            SegRec r{};
-            const int k = valid ? cls(q, r) : -1;
-            uint32_t bal[NC];
+        // pass 2: stable partition, rounds of CHK segments, IPT consecutive
+        // segments per thread (blocked): the per-thread class counts (four
+        // 16-bit fields, <= CHK each) are scanned across the block in thread
+        // order, so the order inside a class is the segment order
+        for (int64_t c0 = 0; c0 < S; c0 += CHK) {
+            SegRec r[IPT];
+            int k[IPT];
+            uint64_t my = 0;
 #pragma unroll
-            for (int c = 0; c < NC; c++) bal[c] = __ballot_sync(0xffffffffu, k == c);
+            for (int i = 0; i < IPT; i++) {
+                const int64_t q = c0 + (int64_t)tid * IPT + i;
+                k[i] = q < S ? cls(q, r[i]) : -1;
+                if (k[i] >= 0) my += 1ull << (16 * k[i]);
+            }
+            uint64_t x = my;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) s_w64[warp] = x;
             __syncthreads();
-            if (lane == 0)
+            uint64_t wp = 0, tot = 0;
 #pragma unroll
-                for (int c = 0; c < NC; c++) s_w[c][warp] = __popc(bal[c]);
-            __syncthreads();
-            uint32_t pre[NC] = {0u, 0u, 0u, 0u}, tot[NC] = {0u, 0u, 0u, 0u};
-            for (int w = 0; w < 8; w++)
+            for (int w = 0; w < 8; w++) {
+                const uint64_t v = s_w64[w];
+                if (w < warp) wp += v;
+                tot += v;
+            }
+            const uint64_t ex = wp + x - my;
+            uint32_t seen[NC] = {0u, 0u, 0u, 0u};
 #pragma unroll
-                for (int c = 0; c < NC; c++) {
-                    if (w < warp) pre[c] += s_w[c][w];
-                    tot[c] += s_w[c][w];
-                }
-            if (valid) rec[d.sb0 + base[k] + run[k] + pre[k] + __popc(bal[k] & lanemask_lt())] = r;
+            for (int i = 0; i < IPT; i++) {
+                if (k[i] < 0) continue;
+                const int c = k[i];
+                const uint32_t pos = base[c] + run[c] + (uint32_t)((ex >> (16 * c)) & 0xFFFFu) + seen[c]++;
+                rec[d.sb0 + pos] = r[i];
+            }
 #pragma unroll
-            for (int c = 0; c < NC; c++) run[c] += tot[c];
+            for (int c = 0; c < NC; c++) run[c] += (uint32_t)((tot >> (16 * c)) & 0xFFFFu);
+            __syncthreads();   // s_w64 is rewritten by the next round
         }
         __syncthreads();
         {   // chunks of the long segments, in record order: block scan of nc
