@@ -621,40 +621,78 @@ k_gs_links(BatchDesc* __restrict__ desc, int64_t n_batches, const int64_t* __res
         if (staged)
             for (int64_t i = tid; i < ps1 - ps0; i += 256) s_prev[i] = seg_row[ps0 + i];
         __syncthreads();
-        for (int64_t q0 = 0; q0 < S; q0 += 256) {
-            const int64_t q = q0 + tid;
-            bool fr = false;
-            int32_t row = 0;
-            if (q < S) {
-                row = seg_row[d.sb0 + q];
-                int64_t lo = 0, hi = ps1 - ps0;   // first position with row >= row
-                while (lo < hi) {
-                    const int64_t mid = (lo + hi) >> 1;
-                    if ((staged ? s_prev[mid] : seg_row[ps0 + mid]) < row) lo = mid + 1;
-                    else hi = mid;
+        // IPT consecutive segments per thread (blocked): one binary search for
+        // the first, then a forward walk (both lists ascend); free segments
+        // compacted in segment order by a block scan of the per-thread counts
+        constexpr int IPT = 4;
+        const int64_t np = ps1 - ps0;
+        auto prow = [&](int64_t i) -> int32_t { return staged ? s_prev[i] : seg_row[ps0 + i]; };
+        for (int64_t c0 = 0; c0 < S; c0 += 256 * IPT) {
+            const int64_t q0 = c0 + (int64_t)tid * IPT;
+            bool fr[IPT];
+            int32_t row[IPT];
+            uint32_t nf = 0;
+            int64_t lo = 0;
+#pragma unroll
+            for (int i = 0; i < IPT; i++) {
+                const int64_t q = q0 + i;
+                fr[i] = false;
+                row[i] = 0;
+                if (q >= S) continue;
+                row[i] = seg_row[d.sb0 + q];
+                if (i == 0) {   // first position with prev row >= row
+                    int64_t hi = np;
+                    while (lo < hi) {
+                        const int64_t mid = (lo + hi) >> 1;
+                        if (prow(mid) < row[i]) lo = mid + 1;
+                        else hi = mid;
+                    }
+                } else {   // a short walk, then a binary search over the rest
+                    int steps = 0;
+                    while (lo < np && steps < 8 && prow(lo) < row[i]) {
+                        lo++;
+                        steps++;
+                    }
+                    if (steps == 8 && lo < np && prow(lo) < row[i]) {
+                        int64_t hi = np;
+                        while (lo < hi) {
+                            const int64_t mid = (lo + hi) >> 1;
+                            if (prow(mid) < row[i]) lo = mid + 1;
+                            else hi = mid;
+                        }
+                    }
                 }
-                if (lo < ps1 - ps0 && (staged ? s_prev[lo] : seg_row[ps0 + lo]) == row) nxt[ps0 + lo] = (int32_t)q;
-                else fr = true;
+                if (lo < np && prow(lo) == row[i]) nxt[ps0 + lo] = (int32_t)q;
+                else fr[i] = true;
+                nf += fr[i];
             }
-            const uint32_t bal = __ballot_sync(0xffffffffu, fr);
+            uint32_t x = nf;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
             __syncthreads();
-            if (lane == 0) s_w[warp] = __popc(bal);
+            if (lane == 31) s_w[warp] = x;
             __syncthreads();
             uint32_t pre = 0, tot = 0;
             for (int w = 0; w < 8; w++) {
                 if (w < warp) pre += s_w[w];
                 tot += s_w[w];
             }
-            if (fr) {
+            uint32_t at = run + pre + x - nf;
+#pragma unroll
+            for (int i = 0; i < IPT; i++) {
+                if (!fr[i]) continue;
+                const int64_t q = q0 + i;
                 const int64_t s = d.sb0 + q;
                 const int64_t st = seg_start[s];
                 const int64_t e = q + 1 < S ? seg_start[s + 1] : d.lk1;
                 FreeRec f;
                 f.pos = (int32_t)(st - d.lk0);
                 f.len = (int32_t)(e - st);
-                f.row = row;
+                f.row = row[i];
                 f.pad = 0;
-                freer[d.sb0 + run + pre + __popc(bal & lanemask_lt())] = f;
+                freer[d.sb0 + at++] = f;
             }
             run += tot;
         }
