@@ -573,7 +573,19 @@ k_gs_ucompact(const BatchDesc* __restrict__ desc, int64_t nb, int Tn, int P, con
         const BatchDesc d = desc[b];
         const int n = (d.n_bags / Tn) * P;
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (Tn <= 32) {   // the unit offsets by one warp scan (parallel count loads)
+            if (threadIdx.x < 32) {
+                const int z = threadIdx.x;
+                const uint32_t v = z < Tn ? ucnt[b * Tn + z] : 0u;
+                uint32_t x = v;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (z >= o) x += y;
+                }
+                if (z < Tn) s_off[z] = x - v;
+                if (z == Tn - 1) s_off[Tn] = x;
+            }
+        } else if (threadIdx.x == 0) {
             uint32_t acc = 0;
             for (int z = 0; z < Tn; z++) {
                 s_off[z] = acc;
@@ -582,14 +594,20 @@ k_gs_ucompact(const BatchDesc* __restrict__ desc, int64_t nb, int Tn, int P, con
             s_off[Tn] = acc;
         }
         __syncthreads();
-        for (int z = 0; z < Tn; z++) {
-            const uint32_t cnt = s_off[z + 1] - s_off[z];
-            const int64_t src = d.lk0 + (int64_t)z * n;
-            const int64_t dst = d.sb0 + s_off[z];
-            for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
-                seg_start[dst + i] = d.lk0 + useg_pos[src + i];
-                seg_row[dst + i] = useg_row[src + i];
+        // all the batch's segments in one flat loop (unit of segment e: the
+        // last z with s_off[z] <= e, a shared-memory binary search; empty
+        // units share their offset with the next one and are skipped)
+        const uint32_t total = s_off[Tn];
+        for (uint32_t e = threadIdx.x; e < total; e += blockDim.x) {
+            int lo = 0, hi = Tn - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (s_off[mid] <= e) lo = mid;
+                else hi = mid - 1;
             }
+            const int64_t src = d.lk0 + (int64_t)lo * n + (e - s_off[lo]);
+            seg_start[d.sb0 + e] = d.lk0 + useg_pos[src];
+            seg_row[d.sb0 + e] = useg_row[src];
         }
     }
 }
