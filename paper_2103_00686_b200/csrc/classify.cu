@@ -164,6 +164,9 @@ k_classify_fixed(const int32_t* __restrict__ idx, int64_t n_rec, int Tn, int P, 
 // stalling the CTA; then its hot_ids / cold_ids and hot CSR are written with
 // coalesced stores.
 constexpr int kBulkRec = 256;          // threads per CTA (>= records per tile)
+#ifndef FAE_CLS_L2HINT
+#define FAE_CLS_L2HINT 1     // dataset tiles evict-first, rank directory evict-last, outputs streamed
+#endif
 constexpr int kBulkSlots = 3;
 #ifndef FAE_CLS_MINB
 #define FAE_CLS_MINB 4      // CTAs per SM (registers capped at 64)
@@ -195,6 +198,9 @@ k_classify_bulk(const int32_t* __restrict__ idx, int64_t n_rec, int Tn, int P, i
     __shared__ int s_wsum[kBulkRec / 32];
     __shared__ uint64_t s_ex;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#if FAE_CLS_L2HINT
+    const uint64_t pol_dir = l2_policy_evict_last();
+#endif
     for (int z = tid; z < Tn; z += blockDim.x) {
         s_rb[z] = rowbase[z];
         s_rows[z] = (int32_t)rows[z];
@@ -212,7 +218,12 @@ k_classify_bulk(const int32_t* __restrict__ idx, int64_t n_rec, int Tn, int P, i
         s_tile[slot] = t;
         if (t < last_full) {
             fence_proxy_async_smem();
+#if FAE_CLS_L2HINT
+            bulk_load_hint(bufs + slot * tile_items, idx + t * tile_items, (uint32_t)tile_items * 4u, &s_bar[slot],
+                           l2_policy_evict_first());
+#else
             bulk_load(bufs + slot * tile_items, idx + t * tile_items, (uint32_t)tile_items * 4u, &s_bar[slot]);
+#endif
         }
     };
     if (tid == 0) {
@@ -274,7 +285,11 @@ k_classify_bulk(const int32_t* __restrict__ idx, int64_t n_rec, int Tn, int P, i
                                 cold = true;
                             } else {
                                 gv[u] = s_rb[z] + j;
+#if FAE_CLS_L2HINT
+                                e[u] = ldg_hint_u4(dir + (gv[u] >> 6), pol_dir);
+#else
                                 e[u] = __ldg(dir + (gv[u] >> 6));
+#endif
                             }
                         }
                     }
@@ -328,15 +343,15 @@ k_classify_bulk(const int32_t* __restrict__ idx, int64_t n_rec, int Tn, int P, i
             const int nrec = (int)(n_rec - r0 < (int64_t)TR ? n_rec - r0 : (int64_t)TR);
             if (tid < nrec) {
                 const int rk = s_rk[prev][tid];
-                if (rk >= 0) hot_ids[ex + rk] = r0 + tid;
-                else cold_ids[(r0 - ex) + (-1 - rk)] = r0 + tid;
+                if (rk >= 0) __stcs(hot_ids + ex + rk, (int64_t)(r0 + tid));
+                else __stcs(cold_ids + (r0 - ex) + (-1 - rk), (int64_t)(r0 + tid));
             }
             const int32_t* pbuf = bufs + prev * tile_items;
             int32_t* dst = hot_idx + ex * (int64_t)TnP;
             const int nout = ptot * TnP;
             for (int jx = tid; jx < nout; jx += blockDim.x) {
                 const int k = (int)__umulhi((uint32_t)jx, div_magic);   // jx / TnP
-                dst[jx] = pbuf[s_list[prev][k] * TnP + (jx - k * TnP)];
+                __stcs(dst + jx, pbuf[s_list[prev][k] * TnP + (jx - k * TnP)]);
             }
             __syncthreads();   // slot `prev` is free again
         }
