@@ -461,6 +461,11 @@ __device__ __forceinline__ uint4 ldg_hint_u4(const uint4* p, uint64_t policy) {
                  : "l"(p), "l"(policy));
     return v;
 }
+__device__ __forceinline__ int32_t ldg_hint_i32(const int32_t* p, uint64_t policy) {
+    int32_t v;
+    asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(policy));
+    return v;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     uint32_t done = 0;
     while (!done) {

@@ -202,6 +202,9 @@ k_histogram_fixed(const int64_t* __restrict__ sampled, int64_t n_s, const int32_
     const int TnP = Tn * P;
     const int64_t n = n_s * TnP;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * 8;
+    // the sampled records are read once (evict-first): L2 keeps the counters
+    // of the Zipf heads that the atomics hit again and again
+    const uint64_t pol = l2_policy_evict_first();
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x * 8; i0 < n; i0 += stride) {
         int32_t jv[8];
         int zv[8];
@@ -214,7 +217,7 @@ k_histogram_fixed(const int64_t* __restrict__ sampled, int64_t n_s, const int32_
                 const int64_t rs = i / TnP;
                 const int qq = (int)(i - rs * TnP);
                 zv[u] = qq / P;
-                jv[u] = __ldg(idx + __ldg(sampled + rs) * TnP + qq);
+                jv[u] = ldg_hint_i32(idx + __ldg(sampled + rs) * TnP + qq, pol);
             }
         }
 #pragma unroll
